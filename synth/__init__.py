@@ -1,0 +1,335 @@
+"""Seeded synthetic inputs for the AGIPC coarsening path.
+
+This module is the ONLY code shared by the CPU oracle (``oracle/``) and the
+CUDA path (``paper_2605_04773_b200``).  It holds none of the method's
+arithmetic: no Green strain, no tags derived from strain, no hashing, no
+Galerkin products, no PCG.  It only builds the *inputs* the paper's problem
+statement takes (Alg 1 lines 8-10):
+
+* a static tetrahedral fine mesh (Kuhn 6-tet subdivision of an n^3 grid,
+  centred on the origin, nodes in Morton order -- a stand-in for the METIS
+  ordering of P:226), its symmetric CSR adjacency and the tet->directed-slot
+  table ("the edge-element adjacency can be precomputed");
+* iterates x_{i-1}, x_i (twist, walls) for the strain criterion;
+* the fine Hessian H_f = M (x) I_3 + dt^2 K_lin in full-storage BSR and a
+  gradient g_f (the paper's H(x), grad E(x) of Eq. 2; H is SPD);
+* Bernoulli edge tags for map-only workloads.
+
+Recipe: side 1 m, rho = 1000,
+nu = 0.3, dt = 0.01, E per config, g_f ~ N(0,1).
+"""
+from __future__ import annotations
+
+import dataclasses
+import numpy as np
+
+__all__ = [
+    "Mesh", "kuhn_grid", "mesh_from_tets", "stiffness_blocks", "fine_hessian",
+    "fine_gradient", "twist", "walls", "random_tags", "edge_tags_to_slots",
+    "config_c1", "config_c2", "config_c3",
+]
+
+# Local edge order of a tet (a,b,c,d) = nodes 0..3.  tet_slots[t, 2e] is the
+# CSR slot of the directed edge (u->v), tet_slots[t, 2e+1] that of (v->u).
+TET_EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+
+
+@dataclasses.dataclass
+class Mesh:
+    """Static fine mesh.  All index arrays are C-contiguous numpy arrays."""
+    X: np.ndarray            # float64 [N,3] rest positions
+    tets: np.ndarray         # int32  [T,4]
+    adj_ptr: np.ndarray      # int64  [N+1]  symmetric adjacency, ascending
+    adj_nbr: np.ndarray      # int32  [2E]
+    tet_slots: np.ndarray    # int32  [T,12] directed CSR slot per tet edge
+    edges: np.ndarray        # int32  [E,2] canonical (min,max), ascending
+    edge_of_slot: np.ndarray  # int64 [2E] undirected edge id of each slot
+    bsr_ptr: np.ndarray      # int64  [N+1] fine Hessian pattern (adjacency + diagonal)
+    bsr_col: np.ndarray      # int32  [N+2E]
+    diag_slot: np.ndarray    # int64  [N] BSR slot of the diagonal block of each row
+    ijk: np.ndarray | None = None  # int32 [N,3] grid coordinates (grid meshes)
+    n_side: int = 0
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.X.shape[0])
+
+    @property
+    def n_tets(self) -> int:
+        return int(self.tets.shape[0])
+
+    @property
+    def n_edges(self) -> int:
+        return int(self.edges.shape[0])
+
+
+def _morton_key(ijk: np.ndarray) -> np.ndarray:
+    """3-D bit interleave of non-negative grid coordinates (x bit lowest)."""
+    key = np.zeros(ijk.shape[0], dtype=np.int64)
+    for bit in range(21):
+        for d in range(3):
+            key |= ((ijk[:, d].astype(np.int64) >> bit) & 1) << (3 * bit + d)
+    return key
+
+
+def mesh_from_tets(X: np.ndarray, tets: np.ndarray, ijk=None, n_side=0) -> Mesh:
+    """Build adjacency, tet->slot table and the fine BSR pattern from tets."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    tets = np.ascontiguousarray(tets, dtype=np.int32)
+    N = X.shape[0]
+    T = tets.shape[0]
+    t64 = tets.astype(np.int64)
+    if T:
+        u = np.concatenate([t64[:, a] for a, b in TET_EDGES])
+        v = np.concatenate([t64[:, b] for a, b in TET_EDGES])
+    else:
+        u = v = np.zeros(0, np.int64)
+    lo = np.minimum(u, v)
+    hi = np.maximum(u, v)
+    ekey, inv = np.unique(lo * N + hi, return_inverse=True)
+    inv = inv.reshape(-1)
+    E = ekey.shape[0]
+    edges = np.stack([ekey // N, ekey % N], axis=1).astype(np.int32)
+    allk = np.concatenate([ekey, (ekey % N) * N + ekey // N])
+    order = np.argsort(allk, kind="stable")
+    dkey = allk[order]
+    pos = np.empty(2 * E, np.int64)
+    pos[order] = np.arange(2 * E)
+    rows = dkey // N
+    adj_nbr = (dkey % N).astype(np.int32)
+    adj_ptr = np.zeros(N + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=N), out=adj_ptr[1:])
+    # tet edge -> both directed slots
+    fwd = pos[inv]            # slot of (lo -> hi)
+    bwd = pos[E + inv]        # slot of (hi -> lo)
+    s_uv = np.where(u < v, fwd, bwd).reshape(6, T)
+    s_vu = np.where(u < v, bwd, fwd).reshape(6, T)
+    ts = np.empty((T, 12), np.int32)
+    ts[:, 0::2] = s_uv.T
+    ts[:, 1::2] = s_vu.T
+    edge_of_slot = np.where(order < E, order, order - E).astype(np.int64)
+    # fine Hessian pattern: adjacency + diagonal, ascending columns
+    gt = (adj_nbr > rows).astype(np.int64)
+    nbelow = np.bincount(rows[adj_nbr < rows], minlength=N)
+    bsr_ptr = adj_ptr + np.arange(N + 1, dtype=np.int64)
+    bsr_col = np.empty(N + 2 * E, np.int32)
+    bsr_col[np.arange(2 * E, dtype=np.int64) + rows + gt] = adj_nbr
+    diag_slot = adj_ptr[:-1] + np.arange(N, dtype=np.int64) + nbelow
+    bsr_col[diag_slot] = np.arange(N, dtype=np.int32)
+    return Mesh(X=X, tets=tets, adj_ptr=adj_ptr, adj_nbr=adj_nbr, tet_slots=ts,
+                edges=edges, edge_of_slot=edge_of_slot, bsr_ptr=bsr_ptr, bsr_col=bsr_col,
+                diag_slot=diag_slot,
+                ijk=None if ijk is None else np.ascontiguousarray(ijk, np.int32), n_side=n_side)
+
+
+def kuhn_grid(n: int, order: str = "morton", side: float = 1.0, origin=(0.0, 0.0, 0.0)) -> Mesh:
+    """Kuhn/Freudenthal 6-tet subdivision of an n^3 node grid on a cube of the
+    given side centred on ``origin``.  Each cube is split along its
+    (0,0,0)-(1,1,1) diagonal into the 6 path tets.  Nodes are renumbered in
+    Morton order (``order='morton'``) or kept lexicographic (``'lex'``); tets
+    are sorted by their smallest node id (stable)."""
+    assert n >= 2
+    g = np.arange(n)
+    I, J, K = np.meshgrid(g, g, g, indexing="ij")
+    ijk = np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.int64)
+    lex = (ijk[:, 0] * n + ijk[:, 1]) * n + ijk[:, 2]
+    if order == "morton":
+        perm = np.argsort(_morton_key(ijk), kind="stable")  # new id -> lex id
+    elif order == "lex":
+        perm = np.arange(n ** 3)
+    else:
+        raise ValueError(order)
+    new_of_lex = np.empty(n ** 3, np.int64)
+    new_of_lex[lex[perm]] = np.arange(n ** 3)
+    ijk_new = ijk[perm]
+    X = ijk_new.astype(np.float64) * (side / (n - 1)) - 0.5 * side + np.asarray(origin, np.float64)
+    # tets
+    c = np.arange(n - 1)
+    CI, CJ, CK = np.meshgrid(c, c, c, indexing="ij")
+    cubes = np.stack([CI.ravel(), CJ.ravel(), CK.ravel()], axis=1)
+    unit = np.eye(3, dtype=np.int64)
+    tl = []
+    for s0, s1, s2 in ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)):
+        v0 = cubes
+        v1 = v0 + unit[s0]
+        v2 = v1 + unit[s1]
+        v3 = v2 + unit[s2]
+        tl.append(np.stack([(v[:, 0] * n + v[:, 1]) * n + v[:, 2] for v in (v0, v1, v2, v3)], axis=1))
+    tets = new_of_lex[np.concatenate(tl, axis=0)]
+    tets = tets[np.argsort(tets.min(axis=1), kind="stable")].astype(np.int32)
+    return mesh_from_tets(X, tets, ijk=ijk_new, n_side=n)
+
+
+# ----------------------------------------------------------------------------
+# Fine Hessian input: H_f = M_lumped (x) I_3 + dt^2 K_lin   (SPD)
+# ----------------------------------------------------------------------------
+
+def lame(E: float, nu: float):
+    mu = E / (2.0 * (1.0 + nu))
+    lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+    return mu, lam
+
+
+def stiffness_blocks(X: np.ndarray, tets: np.ndarray, E: float, nu: float):
+    """Per-tet linear-elastic (StVK at rest) stiffness blocks K_ab [T,4,4,3,3]
+    and volumes [T]: K_ab = V (mu (g_a.g_b) I + mu g_b g_a^T + lam g_a g_b^T),
+    g_a the P1 shape-function gradients.  Symmetrised so that K_ba = K_ab^T
+    holds bit-exactly.  Input generation only (torch CPU ops for speed)."""
+    import torch
+    mu, lam = lame(E, nu)
+    Xt = torch.from_numpy(np.ascontiguousarray(X, np.float64))
+    tt = torch.from_numpy(np.ascontiguousarray(tets, np.int64))
+    Xa = Xt[tt[:, 0]]
+    Dm = torch.stack([Xt[tt[:, 1]] - Xa, Xt[tt[:, 2]] - Xa, Xt[tt[:, 3]] - Xa], dim=2)
+    V = torch.linalg.det(Dm).abs() / 6.0
+    Minv = torch.linalg.inv(Dm)            # rows = grad N_1..3
+    g = torch.empty((tets.shape[0], 4, 3), dtype=torch.float64)
+    g[:, 1:, :] = Minv
+    g[:, 0, :] = -Minv.sum(dim=1)
+    g *= V.sqrt()[:, None, None]           # fold V into both gradients
+    gg = torch.matmul(g, g.transpose(1, 2))  # [T,a,b] = g_a . g_b
+    K = g[:, None, :, :, None] * (mu * g[:, :, None, None, :])   # mu g_b g_a^T
+    K += (lam * g[:, :, None, :, None]) * g[:, None, :, None, :]  # lam g_a g_b^T
+    d = mu * gg
+    for i in range(3):
+        K[:, :, :, i, i] += d
+    K = 0.5 * (K + K.permute(0, 2, 1, 4, 3))
+    return K.numpy(), V.numpy()
+
+
+def _slot_index(mesh: Mesh, t0: int, t1: int) -> np.ndarray:
+    """BSR slot of every (tet, a, b) pair -> int64 [t1-t0,4,4].  A row of the
+    BSR pattern is the adjacency row with the diagonal inserted, so
+    bsr_slot(u->v) = adj_slot(u->v) + u + [v > u]."""
+    tets = mesh.tets[t0:t1].astype(np.int64)
+    ts = mesh.tet_slots[t0:t1].astype(np.int64)
+    S = np.empty((tets.shape[0], 4, 4), np.int64)
+    for k in range(4):
+        S[:, k, k] = mesh.diag_slot[tets[:, k]]
+    for e, (a, b) in enumerate(TET_EDGES):
+        u, v = tets[:, a], tets[:, b]
+        S[:, a, b] = ts[:, 2 * e] + u + (v > u)
+        S[:, b, a] = ts[:, 2 * e + 1] + v + (u > v)
+    return S
+
+
+def fine_hessian(mesh: Mesh, E: float = 1e5, nu: float = 0.3, rho: float = 1000.0,
+                 dt: float = 0.01, mass: bool = True, stiffness: bool = True,
+                 chunk: int = 1 << 18) -> np.ndarray:
+    """Values of H_f in the mesh's BSR pattern: float64 [N+2E, 3, 3] row-major
+    blocks.  ``E`` may be a per-tet array (multi-material scenes)."""
+    import torch  # index_add_ is only used as a fast scatter for input generation
+    N = mesh.n_nodes
+    nnzb = mesh.bsr_col.shape[0]
+    out = torch.zeros((nnzb, 9), dtype=torch.float64)
+    T = mesh.n_tets
+    Earr = np.broadcast_to(np.asarray(E, np.float64), (T,))
+    mnode = np.zeros(N)
+    for t0 in range(0, T, chunk):
+        tt = mesh.tets[t0:t0 + chunk]
+        Ech = Earr[t0:t0 + chunk]
+        uniq = np.unique(Ech)
+        K = np.empty((tt.shape[0], 4, 4, 3, 3))
+        V = None
+        for Ev in uniq:  # E enters linearly: compute with E=1 and scale
+            sel = Ech == Ev
+            Ks, Vs = stiffness_blocks(mesh.X, tt[sel], 1.0, nu)
+            K[sel] = Ks * Ev
+            if V is None:
+                V = np.empty(tt.shape[0])
+            V[sel] = Vs
+        mnode += np.bincount(tt.ravel(), weights=np.repeat(rho * V / 4.0, 4), minlength=N)
+        if stiffness:
+            idx = torch.from_numpy(_slot_index(mesh, t0, t0 + tt.shape[0]).reshape(-1))
+            src = torch.from_numpy((dt * dt) * K.reshape(-1, 9))
+            out.index_add_(0, idx, src)
+    if mass:
+        dslot = mesh.diag_slot
+        eye = torch.tensor([1.0, 0, 0, 0, 1.0, 0, 0, 0, 1.0], dtype=torch.float64)
+        out[torch.from_numpy(dslot)] += torch.from_numpy(mnode)[:, None] * eye[None, :]
+    return out.numpy().reshape(nnzb, 3, 3)
+
+
+def lumped_mass(mesh: Mesh, rho: float = 1000.0) -> np.ndarray:
+    Xa = mesh.X[mesh.tets[:, 0]]
+    Dm = np.stack([mesh.X[mesh.tets[:, k]] - Xa for k in (1, 2, 3)], axis=2)
+    V = np.abs(np.linalg.det(Dm)) / 6.0
+    m = np.zeros(mesh.n_nodes)
+    np.add.at(m, mesh.tets.ravel(), np.repeat(rho * V / 4.0, 4))
+    return m
+
+
+def fine_gradient(n_nodes: int, seed: int = 0) -> np.ndarray:
+    """g_f ~ N(0, 1) per component, float64 [N,3]."""
+    return np.random.default_rng([seed, 7]).standard_normal((n_nodes, 3))
+
+
+# ----------------------------------------------------------------------------
+# Iterates for the strain criterion
+# ----------------------------------------------------------------------------
+
+def _smoothstep(t):
+    t = np.clip(t, 0.0, 1.0)
+    return t * t * (3.0 - 2.0 * t)
+
+
+def twist(X: np.ndarray, alpha: float, w: float = 0.2, axis=(0.0, 0.0, 1.0), center=(0.0, 0.0, 0.0)):
+    """Rotate each node about ``axis`` through ``center`` by
+    phi(s) = alpha * S(s/w + 1/2), s = axial coordinate, S = clamped smoothstep."""
+    a = np.asarray(axis, np.float64)
+    a = a / np.linalg.norm(a)
+    c = np.asarray(center, np.float64)
+    r = X - c
+    s = r @ a
+    phi = alpha * _smoothstep(s / w + 0.5)
+    cos, sin = np.cos(phi)[:, None], np.sin(phi)[:, None]
+    # Rodrigues: r cos + (a x r) sin + a (a.r)(1-cos)
+    axr = np.cross(a[None, :], r)
+    return c + r * cos + axr * sin + a[None, :] * s[:, None] * (1.0 - cos)
+
+
+def walls(mesh: Mesh, k: int, period: int = 16, rel_amp: float = 1e-2, seed: int = 0):
+    """x_prev = X; x_cur = X + delta*xi on wall nodes (any grid coordinate
+    = k mod period), delta = rel_amp * h, xi ~ N(0, I3)."""
+    assert mesh.ijk is not None
+    h = 1.0 / (mesh.n_side - 1)
+    wall = np.any(mesh.ijk % period == (k % period), axis=1)
+    xi = np.random.default_rng([seed, 11, k]).standard_normal((mesh.n_nodes, 3))
+    x_cur = mesh.X + (rel_amp * h) * xi * wall[:, None]
+    return mesh.X.copy(), x_cur
+
+
+def random_tags(mesh: Mesh, p: float, seed: int = 0) -> np.ndarray:
+    """tau_e ~ Bernoulli(p) per undirected edge in canonical (min,max) order,
+    returned per directed CSR slot (uint8 [2E], both directions equal)."""
+    tau = (np.random.default_rng([seed, 3]).random(mesh.n_edges) < p).astype(np.uint8)
+    return edge_tags_to_slots(mesh, tau)
+
+
+def edge_tags_to_slots(mesh: Mesh, tau_edge: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(tau_edge, np.uint8)[mesh.edge_of_slot])
+
+
+# ----------------------------------------------------------------------------
+# Named configurations (BASELINE.json configs)
+# ----------------------------------------------------------------------------
+
+def config_c1(seed: int = 0, p: float = 0.2):
+    """C1: 10^3 grid, random tags p, gs=32, E=1e5 (one Newton step)."""
+    m = kuhn_grid(10)
+    return dict(mesh=m, slot_tags=random_tags(m, p, seed), E=1e5, group_size=32,
+                x_prev=twist(m.X, 0.5), x_cur=twist(m.X, 0.501), theta=5e-5)
+
+
+def config_c2(n: int = 47):
+    """C2: 47^3 = 103,823 nodes, twist 0.5 -> 0.501, theta = 5e-5, E=1e5."""
+    m = kuhn_grid(n)
+    return dict(mesh=m, x_prev=twist(m.X, 0.5), x_cur=twist(m.X, 0.501), theta=5e-5,
+                E=1e5, group_size=32)
+
+
+def config_c3(n: int = 100, k: int = 0):
+    """C3: 100^3 = 1,000,000 nodes, strain walls with phase k, theta = 5e-5."""
+    m = kuhn_grid(n)
+    xp, xc = walls(m, k)
+    return dict(mesh=m, x_prev=xp, x_cur=xc, theta=5e-5, E=1e5, group_size=32)
