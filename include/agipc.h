@@ -1,0 +1,197 @@
+/*
+ * agipc.h -- C ABI of the B200-native AGIPC coarsening path (arXiv 2605.04773).
+ *
+ * One Newton iteration of AGIPC (main Alg 1 lines 8-10):
+ *   1. agipc_tag_edges        edge tags tau_e from the Green-strain increment (Eq 3)
+ *   2. agipc_build_map        fine->coarse map by group bit-hashing, prefix sum and
+ *                             level-wise recursion (supp Alg S1/S2)
+ *   3. agipc_assemble_coarse  DoF classification + reorder (supp Alg S3) and the
+ *                             Galerkin coarse Hessian / gradient H_c = U H U^T, g_c = U g
+ *                             with affine 12-DoF nodes (supp Alg S4, Eq S2/S3, P:258-319;
+ *                             main Eq 4)
+ *   4. agipc_pcg_solve        block-Jacobi PCG on the coarse system
+ *
+ * Conventions (all entry points):
+ *  - Array arguments are DEVICE pointers owned by the caller (e.g. PyTorch CUDA tensors,
+ *    C-contiguous) unless marked [host].  Inputs are never written.  The library keeps no
+ *    caller pointer between calls.
+ *  - Every kernel is enqueued on the handle's stream (agipc_set_stream; default: the
+ *    legacy default stream).  Calls that return a data-dependent size in a [host] argument
+ *    synchronise that stream before returning; the others are asynchronous.
+ *  - Errors are returned as agipc_status, never thrown or aborted; agipc_last_error()
+ *    returns a human-readable message for the last failing call on that handle.
+ *  - Index types: node, slot and column ids are int32 (sizes >= 2^31-1 return
+ *    AGIPC_ERANGE); row pointers are int64.
+ *  - Thread safety: one handle per host thread / stream.  Handles on different devices
+ *    are independent.
+ *  - Precision: all floating point is IEEE fp64 ("double-precision").
+ */
+#ifndef AGIPC_H_
+#define AGIPC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define AGIPC_API __attribute__((visibility("default")))
+#else
+#define AGIPC_API
+#endif
+
+#define AGIPC_VERSION_MAJOR 0
+#define AGIPC_VERSION_MINOR 1
+
+typedef struct agipc_handle_s *agipc_handle;
+
+typedef enum {
+  AGIPC_OK = 0,
+  AGIPC_EINVAL = 1,       /* null pointer, group_size outside [1,32], negative size, bad map  */
+  AGIPC_ERANGE = 2,       /* an index does not fit in int32                                   */
+  AGIPC_ENOSPACE = 3,     /* output capacity too small; required sizes were written back     */
+  AGIPC_ECUDA = 4,        /* a CUDA runtime call failed (message in agipc_last_error)         */
+  AGIPC_ENCCL = 5,        /* reserved for the multi-GPU path                                  */
+  AGIPC_EDEGENERATE = 6,  /* a tet with det(D_m) == 0 at rest                    */
+  AGIPC_ESINGULAR = 7,    /* a block-Jacobi diagonal block is missing or singular     */
+  AGIPC_EINDEFINITE = 8,  /* p^T A p <= 0 in PCG                                      */
+  AGIPC_EBREAKDOWN = 9,   /* NaN/Inf in PCG                                           */
+  AGIPC_NOT_CONVERGED = 10 /* max_iters reached; x holds the last iterate (not fatal)         */
+} agipc_status;
+
+/* ---- handle ------------------------------------------------------------------------- */
+AGIPC_API agipc_status agipc_create(agipc_handle *h, int cuda_device);
+AGIPC_API agipc_status agipc_destroy(agipc_handle h);
+/* stream: a cudaStream_t passed as void* (e.g. torch.cuda.current_stream().cuda_stream). */
+AGIPC_API agipc_status agipc_set_stream(agipc_handle h, void *stream);
+AGIPC_API const char *agipc_last_error(agipc_handle h);
+AGIPC_API const char *agipc_status_string(agipc_status s);
+AGIPC_API void agipc_version(int *major /*[host]*/, int *minor /*[host]*/);
+/* Number of kernels this handle has enqueued since creation ([host] counter). */
+AGIPC_API int64_t agipc_kernel_launches(agipc_handle h);
+
+/* ---- static fine mesh ("static underlying topology"; P:838 precomputed adjacency) -- */
+typedef struct {
+  int64_t n_nodes;          /* N                                                              */
+  int64_t n_tets;           /* T                                                              */
+  int64_t nnz_adj;          /* 2E: directed adjacency slots                                   */
+  const int32_t *tets;      /* [T][4] node ids; D_m = [X_b-X_a | X_c-X_a | X_d-X_a]           */
+  const int64_t *adj_ptr;   /* [N+1] symmetric adjacency, no self loops                       */
+  const int32_t *adj_nbr;   /* [2E] neighbours, ascending within a row                        */
+  const int32_t *tet_slots; /* [T][12] for local edge e in (01,02,03,12,13,23): the adjacency
+                               slot of (u->v) at 2e and of (v->u) at 2e+1                    */
+  const double *x_rest;     /* [N][3] rest positions X; also X_bar = (x,y,z,1) of Eq 4        */
+} agipc_mesh;
+
+/* Block sparse row matrix with 3x3 blocks (full storage, ascending columns per row). */
+typedef struct {
+  int64_t n_rows;           /* block rows (nodes or slots)                                    */
+  int64_t nnzb;             /* stored blocks                                                  */
+  const int64_t *row_ptr;   /* [n_rows+1]                                                     */
+  const int32_t *col;       /* [nnzb] ascending within a row                                  */
+  const double *val;        /* [nnzb][3][3] row-major blocks                                  */
+} agipc_bsr;
+
+/* ---- step 1: edge tags ----------------------------------------------------------------
+ * main Sec 4.2 Eq 3, supp Sec 1.1.  For every tet t:
+ *   F = D_s D_m^-1 (D_m^-1 = adj(D_m) * (1/det D_m)), G = 1/2 (F^T F - I) at x_prev and x_cur,
+ *   n_t = ||G(x_cur) - G(x_prev)||_F, flagged iff n_t > threshold (strict).
+ * slot_tags[s] = 0 if the edge of adjacency slot s belongs to a flagged tet, else 1
+ * (both directed slots of an edge agree).  Fixed fp64 operation order without FMA
+ * contraction (R12), so tags are reproducible bit for bit.
+ *   x_prev, x_cur : [N][3] iterates x_{i-1}, x_i (at the first Newton iteration pass x^t twice)
+ *   slot_tags     : out [nnz_adj] uint8
+ *   tet_norm      : out [T] n_t, nullable
+ *   n_flagged     : [host] out number of flagged tets, nullable (non-null => synchronises)
+ * Errors: EINVAL (null inputs); EDEGENERATE (a tet has det D_m == 0) is reported only when
+ * n_flagged is non-null (the call then synchronises); an asynchronous call treats such a
+ * tet as flagged (its edges are protected). */
+AGIPC_API agipc_status agipc_tag_edges(agipc_handle h, const agipc_mesh *mesh, const double *x_prev,
+                             const double *x_cur, double threshold, uint8_t *slot_tags,
+                             double *tet_norm, int64_t *n_flagged);
+
+/* ---- step 2: fine -> coarse map -------------------------------------------------------
+ * supp Alg S1/S2 applied level-wise, readings R1-R8:
+ * nodes are split into contiguous groups of group_size; inside a group the tagged edges
+ * are OR-propagated into 32-bit connectivity hashes; a component's local index is the
+ * rank of its first set bit among the group's elected lanes; an exclusive prefix sum of
+ * per-group counts gives global ids.  The surviving tagged edges mapped through the level
+ * map form the next level's graph; repeat until a level merges nothing or max_levels
+ * levels ran.  Result: map[f] = rank of f's aggregate ordered by its minimum fine node.
+ *   slot_tags  : [nnz_adj] 1 collapsible / 0 protected; must be symmetric
+ *   group_size : 1..32 (32 = one warp per group)
+ *   max_levels : 0 = until no merge
+ *   map        : out [N] int32 coarse id in [0, n_coarse)
+ *   agg_size   : out [N] capacity, first n_coarse entries = fine nodes per aggregate; nullable
+ *   info       : [host] out; synchronises the stream. */
+typedef struct {
+  int64_t n_coarse;
+  int32_t n_levels;          /* passes run, including the final no-merge pass               */
+  int32_t reserved;
+  int64_t level_n[64];       /* node count after each of the first 64 levels               */
+  int64_t n_cross_edges;     /* tagged fine edges between level-0 groups                    */
+} agipc_map_info;
+
+AGIPC_API agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, const uint8_t *slot_tags,
+                             int group_size, int max_levels, int32_t *map, int32_t *agg_size,
+                             agipc_map_info *info);
+
+/* ---- step 3: classification + Galerkin assembly ----------------------------------------
+ * supp Alg S3: a coarse node is 12-DoF iff it aggregates more than
+ * affine_threshold fine nodes (32); stable reorder, 3-DoF nodes first.
+ * Expanded slots (Eq S2/S3, reading R14): slot(c) = c for c < n3,
+ * slot(c,p) = n3 + 4(c-n3) + p for a 12-DoF node, p = 0..3 (rows of X_bar (x) I3).
+ * H_c[slot(a,p), slot(b,q)] = sum over stored fine blocks (i,j) with new_map(i)=a,
+ * new_map(j)=b of w_i[p] w_j[q] B_ij, w = X_bar for 12-DoF parents, 1 otherwise
+ * (Alg S4 + Eq 4; == U H_f U^T).  g_c[slot(a,p)] = sum w_f[p] g_f[f].
+ * Output is canonical BSR over n_slots block rows with ascending columns and a
+ * structural pattern (a block exists iff at least one fine block maps to it, R17).
+ *   H_fine : fine BSR over N rows; must be symmetric (B_ji = B_ij^T, as the SPD proxy H of
+ *            P:786 is): a mixed 3-DoF/12-DoF block pair is computed once and mirrored.
+ *   g_fine : [N][3], nullable (then out->g_c is not written)
+ *   out    : sizes are written back; if cap_slots < n_slots or cap_nnzb < nnzb the call
+ *            returns AGIPC_ENOSPACE with n3/n12/n_slots/nnzb filled and nothing else
+ *            written.  new_map is always written.  Synchronises the stream. */
+typedef struct {
+  int64_t n3, n12, n_slots, nnzb; /* [host] out                                             */
+  int64_t cap_slots, cap_nnzb;    /* [host] in: capacities of row_ptr/g_c and col/val       */
+  int32_t *new_map;               /* out [N] reordered coarse id of every fine node          */
+  int64_t *row_ptr;               /* out [cap_slots+1]                                       */
+  int32_t *col;                   /* out [cap_nnzb]                                          */
+  double *val;                    /* out [cap_nnzb][3][3]                                    */
+  double *g_c;                    /* out [cap_slots][3], nullable                            */
+} agipc_coarse;
+
+AGIPC_API agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *mesh, const int32_t *map,
+                                   int64_t n_coarse, int64_t affine_threshold,
+                                   const agipc_bsr *H_fine, const double *g_fine,
+                                   agipc_coarse *out);
+
+/* ---- step 4: block-Jacobi PCG ----------------------------------------------------------
+ * Preconditioned CG (textbook, reading R20) on A x = b with D^-1 = inverse of each row's
+ * 3x3 diagonal block ("3x3 block Jacobi").  Stops when ||r_k||_2 <= rel_tol ||b||_2
+ * on the recurrence residual or after max_iters iterations.  Convergence is
+ * tested on the device every iteration; the host polls every check_every iterations
+ * (the iterations in between are captured in one CUDA graph).
+ *   A       : SPD BSR (n_rows slots)
+ *   b       : [n_rows][3];  x : [n_rows][3] in: x0 (ignored if zero_x0), out: solution
+ *   zero_x0 : nonzero = start from x0 = 0 (the coarse solve of each Newton step)
+ *   stats   : [host] out; synchronises the stream.
+ * The coarse Newton direction of P:752 is d_c = -x for b = g_c (CG is linear in b). */
+typedef struct {
+  int32_t iters;
+  int32_t status;             /* agipc_status of the solve                                  */
+  double rel_residual;        /* ||r||_2 / ||b||_2 at exit (recurrence residual)            */
+  double b_norm;
+} agipc_pcg_stats;
+
+AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const double *b, double *x,
+                                       int zero_x0, double rel_tol, int max_iters, int check_every,
+                                       agipc_pcg_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGIPC_H_ */

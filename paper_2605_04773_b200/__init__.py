@@ -1,0 +1,285 @@
+"""Thin Python binding of libagipc -- the B200-native AGIPC coarsening path.
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+``libagipc.so`` (built from ``csrc/`` for sm_100a).  PyTorch provides device
+memory and streams.  There is no CPU fallback: if the library is missing or no
+CUDA device is present the calls raise.
+
+Entry points (same names as the C ABI, include/agipc.h):
+  tag_edges        step 1, Eq 3
+  build_map        step 2, supp Alg S1/S2 + recursion
+  assemble_coarse  step 3, supp Alg S3/S4 + Eq 4
+  pcg_solve        step 4, block-Jacobi PCG
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libagipc.so")
+_lib = None
+
+OK, EINVAL, ERANGE, ENOSPACE, ECUDA, ENCCL = 0, 1, 2, 3, 4, 5
+EDEGENERATE, ESINGULAR, EINDEFINITE, EBREAKDOWN, NOT_CONVERGED = 6, 7, 8, 9, 10
+
+
+class AgipcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_status_name(status)}: {msg}")
+        self.status = status
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("n_tets", C.c_int64), ("nnz_adj", C.c_int64),
+                ("tets", C.c_void_p), ("adj_ptr", C.c_void_p), ("adj_nbr", C.c_void_p),
+                ("tet_slots", C.c_void_p), ("x_rest", C.c_void_p)]
+
+
+class _Bsr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("nnzb", C.c_int64), ("row_ptr", C.c_void_p),
+                ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
+class _MapInfo(C.Structure):
+    _fields_ = [("n_coarse", C.c_int64), ("n_levels", C.c_int32), ("reserved", C.c_int32),
+                ("level_n", C.c_int64 * 64), ("n_cross_edges", C.c_int64)]
+
+
+class _Coarse(C.Structure):
+    _fields_ = [("n3", C.c_int64), ("n12", C.c_int64), ("n_slots", C.c_int64), ("nnzb", C.c_int64),
+                ("cap_slots", C.c_int64), ("cap_nnzb", C.c_int64), ("new_map", C.c_void_p),
+                ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("g_c", C.c_void_p)]
+
+
+class _PcgStats(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("rel_residual", C.c_double),
+                ("b_norm", C.c_double)]
+
+
+EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_error", "agipc_status_string",
+           "agipc_version", "agipc_kernel_launches", "agipc_tag_edges", "agipc_build_map",
+           "agipc_assemble_coarse", "agipc_pcg_solve"]
+
+
+def lib():
+    """Load libagipc.so (raises if it has not been built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                               "(nvcc, sm_100a); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        P, i64, i32, f64 = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        L.agipc_create.argtypes = [C.POINTER(C.c_void_p), i32]
+        L.agipc_destroy.argtypes = [P]
+        L.agipc_set_stream.argtypes = [P, P]
+        L.agipc_last_error.argtypes = [P]
+        L.agipc_last_error.restype = C.c_char_p
+        L.agipc_status_string.argtypes = [i32]
+        L.agipc_status_string.restype = C.c_char_p
+        L.agipc_version.argtypes = [C.POINTER(i32), C.POINTER(i32)]
+        L.agipc_version.restype = None
+        L.agipc_kernel_launches.argtypes = [P]
+        L.agipc_kernel_launches.restype = i64
+        L.agipc_tag_edges.argtypes = [P, C.POINTER(_Mesh), P, P, f64, P, P, C.POINTER(i64)]
+        L.agipc_build_map.argtypes = [P, C.POINTER(_Mesh), P, i32, i32, P, P, C.POINTER(_MapInfo)]
+        L.agipc_assemble_coarse.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), P,
+                                            C.POINTER(_Coarse)]
+        L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
+        for name in ("agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_tag_edges", "agipc_build_map",
+                     "agipc_assemble_coarse", "agipc_pcg_solve"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def _status_name(s):
+    try:
+        return lib().agipc_status_string(int(s)).decode()
+    except Exception:  # noqa: BLE001 - only used for messages
+        return f"status {s}"
+
+
+def version():
+    a, b = C.c_int(), C.c_int()
+    lib().agipc_version(C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("libagipc takes contiguous CUDA tensors")
+    return C.c_void_p(t.data_ptr())
+
+
+class Handle:
+    """One libagipc handle bound to a CUDA device; kernels go on the current torch stream."""
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libagipc needs a CUDA device (no CPU fallback)")
+        self.device = int(device)
+        self._h = C.c_void_p()
+        st = lib().agipc_create(C.byref(self._h), self.device)
+        if st != OK:
+            raise AgipcError(st, f"agipc_create(device={device}) failed")
+        self.sync_stream()
+
+    def sync_stream(self, stream: torch.cuda.Stream | None = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._check(lib().agipc_set_stream(self._h, C.c_void_p(s.cuda_stream)))
+
+    def _check(self, st, allow=()):
+        if st != OK and st not in allow:
+            raise AgipcError(st, lib().agipc_last_error(self._h).decode())
+        return st
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().agipc_kernel_launches(self._h))
+
+    def close(self):
+        if self._h:
+            lib().agipc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+@dataclasses.dataclass
+class DeviceMesh:
+    """Static fine mesh resident on the GPU (layouts of include/agipc.h: agipc_mesh)."""
+    tets: torch.Tensor       # int32 [T,4]
+    adj_ptr: torch.Tensor    # int64 [N+1]
+    adj_nbr: torch.Tensor    # int32 [2E]
+    tet_slots: torch.Tensor  # int32 [T,12]
+    x_rest: torch.Tensor     # float64 [N,3]
+
+    @property
+    def n_nodes(self):
+        return self.x_rest.shape[0]
+
+    def c_struct(self):
+        return _Mesh(self.n_nodes, self.tets.shape[0], self.adj_nbr.shape[0], _p(self.tets), _p(self.adj_ptr),
+                     _p(self.adj_nbr), _p(self.tet_slots), _p(self.x_rest))
+
+    @staticmethod
+    def from_arrays(tets, adj_ptr, adj_nbr, tet_slots, x_rest, device="cuda"):
+        t = lambda a, dt: torch.as_tensor(a).to(device=device, dtype=dt).contiguous()  # noqa: E731
+        return DeviceMesh(t(tets, torch.int32), t(adj_ptr, torch.int64), t(adj_nbr, torch.int32),
+                          t(tet_slots, torch.int32), t(x_rest, torch.float64))
+
+
+# ---------------------------------------------------------------------------------------
+# the four entry points
+# ---------------------------------------------------------------------------------------
+def tag_edges(h: Handle, mesh: DeviceMesh, x_prev, x_cur, threshold: float, slot_tags=None, tet_norm=None,
+              count: bool = False):
+    """Step 1 (Eq 3).  Returns (slot_tags uint8 [2E], n_flagged or None)."""
+    if slot_tags is None:
+        slot_tags = torch.empty(mesh.adj_nbr.shape[0], dtype=torch.uint8, device=mesh.x_rest.device)
+    ms = mesh.c_struct()
+    nf = C.c_int64(0)
+    h._check(lib().agipc_tag_edges(h._h, C.byref(ms), _p(x_prev), _p(x_cur), float(threshold), _p(slot_tags),
+                                   _p(tet_norm), C.byref(nf) if count else None))
+    return slot_tags, (int(nf.value) if count else None)
+
+
+def build_map(h: Handle, mesh: DeviceMesh, slot_tags, group_size: int = 32, max_levels: int = 0, map=None,
+              agg_size=None):
+    """Step 2 (Alg S1/S2 + P:217).  Returns (map int32 [N], info dict)."""
+    N = mesh.n_nodes
+    if map is None:
+        map = torch.empty(N, dtype=torch.int32, device=mesh.x_rest.device)
+    ms = mesh.c_struct()
+    info = _MapInfo()
+    h._check(lib().agipc_build_map(h._h, C.byref(ms), _p(slot_tags), int(group_size), int(max_levels), _p(map),
+                                   _p(agg_size), C.byref(info)))
+    L = info.n_levels
+    return map, dict(n_coarse=int(info.n_coarse), n_levels=int(L),
+                     level_n=[int(info.level_n[i]) for i in range(min(L, 64))],
+                     n_cross_edges=int(info.n_cross_edges))
+
+
+@dataclasses.dataclass
+class CoarseSystem:
+    n3: int
+    n12: int
+    n_slots: int
+    nnzb: int
+    new_map: torch.Tensor
+    row_ptr: torch.Tensor     # int64 [n_slots+1] (view)
+    col: torch.Tensor         # int32 [nnzb] (view)
+    val: torch.Tensor         # float64 [nnzb,3,3] (view)
+    g_c: torch.Tensor | None  # float64 [n_slots,3] (view)
+
+
+class CoarseBuffers:
+    """Grow-only output buffers for assemble_coarse (capacity-retry convention)."""
+
+    def __init__(self, device, n_nodes, cap_slots=0, cap_nnzb=0):
+        self.device = device
+        self.new_map = torch.empty(n_nodes, dtype=torch.int32, device=device)
+        self.cap_slots = 0
+        self.cap_nnzb = 0
+        self.grow(cap_slots, cap_nnzb)
+
+    def grow(self, slots, nnzb):
+        if slots > self.cap_slots or not hasattr(self, "row_ptr"):
+            self.cap_slots = max(int(slots * 1.25) + 16, self.cap_slots)
+            self.row_ptr = torch.empty(self.cap_slots + 1, dtype=torch.int64, device=self.device)
+            self.g_c = torch.empty((self.cap_slots, 3), dtype=torch.float64, device=self.device)
+        if nnzb > self.cap_nnzb or not hasattr(self, "col"):
+            self.cap_nnzb = max(int(nnzb * 1.25) + 64, self.cap_nnzb)
+            self.col = torch.empty(self.cap_nnzb, dtype=torch.int32, device=self.device)
+            self.val = torch.empty((self.cap_nnzb, 3, 3), dtype=torch.float64, device=self.device)
+
+
+def assemble_coarse(h: Handle, mesh: DeviceMesh, map, n_coarse: int, affine_threshold: int, H_row_ptr, H_col,
+                    H_val, g_fine=None, bufs: CoarseBuffers | None = None) -> CoarseSystem:
+    """Step 3 (Alg S3/S4 + Eq 4).  Retries once with grown buffers on AGIPC_ENOSPACE."""
+    N = mesh.n_nodes
+    if bufs is None:
+        bufs = CoarseBuffers(mesh.x_rest.device, N, 4 * n_coarse, H_col.shape[0])
+    ms = mesh.c_struct()
+    bsr = _Bsr(N, H_col.shape[0], _p(H_row_ptr), _p(H_col), _p(H_val))
+    for attempt in range(2):
+        out = _Coarse(0, 0, 0, 0, bufs.cap_slots, bufs.cap_nnzb, _p(bufs.new_map), _p(bufs.row_ptr),
+                      _p(bufs.col), _p(bufs.val), _p(bufs.g_c) if g_fine is not None else None)
+        st = lib().agipc_assemble_coarse(h._h, C.byref(ms), _p(map), int(n_coarse), int(affine_threshold),
+                                         C.byref(bsr), _p(g_fine), C.byref(out))
+        if st == ENOSPACE and attempt == 0:
+            bufs.grow(out.n_slots, out.nnzb)
+            continue
+        h._check(st)
+        break
+    ns, nb = int(out.n_slots), int(out.nnzb)
+    return CoarseSystem(int(out.n3), int(out.n12), ns, nb, bufs.new_map, bufs.row_ptr[:ns + 1], bufs.col[:nb],
+                        bufs.val[:nb], bufs.g_c[:ns] if g_fine is not None else None)
+
+
+def pcg_solve(h: Handle, row_ptr, col, val, b, x=None, rel_tol: float = 1e-3, max_iters: int = 10000,
+              check_every: int = 16, zero_x0: bool = False):
+    """Step 4 (block-Jacobi PCG).  x is the initial guess; if None (or zero_x0) the solve starts
+    from x0 = 0 in the kernels.  x is overwritten.  Returns (x, stats dict).  NOT_CONVERGED is
+    reported in stats, not raised."""
+    n = row_ptr.shape[0] - 1
+    zero_x0 = x is None or zero_x0
+    if x is None:
+        x = torch.empty((n, 3), dtype=torch.float64, device=b.device)
+    bsr = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), _p(val))
+    stats = _PcgStats()
+    h._check(lib().agipc_pcg_solve(h._h, C.byref(bsr), _p(b), _p(x), int(bool(zero_x0)), float(rel_tol),
+                                   int(max_iters), int(check_every), C.byref(stats)), allow=(NOT_CONVERGED,))
+    return x, dict(iters=int(stats.iters), status=int(stats.status), rel_residual=float(stats.rel_residual),
+                   b_norm=float(stats.b_norm))

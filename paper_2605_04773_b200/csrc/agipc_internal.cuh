@@ -1,0 +1,152 @@
+// Internal definitions of libagipc (B200 / sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <unordered_map>
+
+#include "agipc.h"
+
+#define AGIPC_WARP 32
+#define FULL_MASK 0xffffffffu
+
+// ------------------------------------------------------------------------------------
+// Handle: device, stream, error text, grow-only workspace, pinned host scratch.
+// ------------------------------------------------------------------------------------
+struct WsBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct PcgGraph;  // pcg.cu
+
+struct agipc_handle_s {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  std::unordered_map<std::string, WsBuf> ws;
+  void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
+  size_t pinned_bytes = 0;
+  PcgGraph *pcg = nullptr;
+};
+
+agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...);
+
+// Grow-only named device workspace (cudaMalloc only when a buffer must grow).
+void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st);
+// Pinned host scratch of at least `bytes`.
+void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
+
+#define CU_TRY(h, call)                                                                      \
+  do {                                                                                       \
+    cudaError_t _e = (call);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return set_err((h), AGIPC_ECUDA, "%s failed at %s:%d: %s", #call, __FILE__, __LINE__,  \
+                     cudaGetErrorString(_e));                                                \
+  } while (0)
+
+// Every kernel launch goes through LAUNCH so that the handle counts it and errors surface.
+#define LAUNCH(h, kernel, grid, block, smem, ...)                                            \
+  do {                                                                                       \
+    if ((grid) > 0) {                                                                        \
+      kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);                         \
+      (h)->launches += 1;                                                                    \
+      cudaError_t _e = cudaGetLastError();                                                   \
+      if (_e != cudaSuccess)                                                                 \
+        return set_err((h), AGIPC_ECUDA, "launch %s failed: %s", #kernel,                    \
+                       cudaGetErrorString(_e));                                              \
+    }                                                                                        \
+  } while (0)
+
+#define WS(h, var, type, name, count)                                                        \
+  type *var = nullptr;                                                                       \
+  do {                                                                                       \
+    agipc_status _st = AGIPC_OK;                                                             \
+    var = (type *)ws_get((h), (name), sizeof(type) * (size_t)((count) > 0 ? (count) : 1), &_st); \
+    if (_st != AGIPC_OK) return _st;                                                         \
+  } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------------------------
+// Device helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+
+// Inclusive warp scan (Kogge-Stone with shuffles).
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T t = __shfl_up_sync(FULL_MASK, v, o);
+    if (l >= o) v += t;
+  }
+  return v;
+}
+
+// ---- single-pass decoupled look-back (chained scan) --------------------------------
+// Status word per tile: bits 63..62 = flag (0 empty, 1 aggregate, 2 inclusive prefix),
+// bits 61..0 = value (non-negative).  Tiles are claimed in order from a counter so that
+// every predecessor tile belongs to a CTA that is already resident (forward progress).
+#define LB_AGG 1ull
+#define LB_PFX 2ull
+__device__ __forceinline__ void lb_publish(unsigned long long *status, int tile, unsigned long long flag,
+                                           long long value) {
+  unsigned long long w = (flag << 62) | (unsigned long long)value;
+  __threadfence();
+  atomicExch(status + tile, w);
+}
+
+__device__ __forceinline__ unsigned long long lb_read(const unsigned long long *status, int idx) {
+  return *((volatile const unsigned long long *)(status + idx));
+}
+
+// Called by ALL 32 lanes of one warp.  Returns the exclusive prefix of `tile`
+// (to every lane) and publishes the inclusive prefix.
+__device__ __forceinline__ long long lb_exclusive(unsigned long long *status, int tile, long long aggregate) {
+  const int l = lane_id();
+  if (tile == 0) {
+    if (l == 0) lb_publish(status, 0, LB_PFX, aggregate);
+    return 0;
+  }
+  if (l == 0) lb_publish(status, tile, LB_AGG, aggregate);
+  long long excl = 0;
+  int pred = tile - 1;
+  while (true) {
+    int idx = pred - l;
+    unsigned long long s = idx >= 0 ? lb_read(status, idx) : (LB_PFX << 62);
+    unsigned long long flag = s >> 62;
+    if (__any_sync(FULL_MASK, flag == 0)) continue;  // a predecessor has not published yet
+    unsigned pmask = __ballot_sync(FULL_MASK, flag == LB_PFX);
+    long long v = (long long)(s & ((1ull << 62) - 1));
+    int stop = pmask ? __ffs(pmask) - 1 : 31;
+    long long part = (l <= stop) ? v : 0;
+    excl += warp_sum(part);
+    if (pmask) break;
+    pred -= 32;
+  }
+  if (l == 0) lb_publish(status, tile, LB_PFX, excl + aggregate);
+  return excl;
+}
+
+// Device-wide exclusive scan of int64 values given by a functor: out[i] = sum_{k<i} f(k),
+// out[n] = total (out must hold n+1 entries).  Workspace: status[n_tiles] zeroed + counter.
+agipc_status scan_exclusive_i64(agipc_handle h, int kind, const void *src, int64_t n, int64_t *out,
+                                int64_t mul = 1, int64_t add = 0);
+// kinds of source for scan_exclusive_i64: value(i) = mul * src[i] + add  (int32 or int64 source)
+#define SCAN_SRC_I32 0
+#define SCAN_SRC_I64 1

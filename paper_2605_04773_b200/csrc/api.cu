@@ -1,0 +1,200 @@
+// Handle management, errors, workspace and the generic device-wide scan of libagipc.
+#include "agipc_internal.cuh"
+
+agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...) {
+  if (h) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return st;
+}
+
+void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st) {
+  WsBuf &b = h->ws[name];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      cudaStreamSynchronize(h->stream);  // the old buffer may still be in use
+      cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    size_t want = bytes + bytes / 8 + 256;  // headroom: sizes vary between Newton steps
+    cudaError_t e = cudaMalloc(&b.ptr, want);
+    if (e != cudaSuccess) {
+      b.ptr = nullptr;
+      *st = set_err(h, AGIPC_ECUDA, "workspace '%s' (%zu bytes): %s", name, want, cudaGetErrorString(e));
+      return nullptr;
+    }
+    b.bytes = want;
+  }
+  *st = AGIPC_OK;
+  return b.ptr;
+}
+
+void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st) {
+  if (h->pinned_bytes < bytes) {
+    if (h->pinned) {
+      cudaStreamSynchronize(h->stream);
+      cudaFreeHost(h->pinned);
+    }
+    size_t want = bytes < 4096 ? 4096 : bytes;
+    cudaError_t e = cudaMallocHost(&h->pinned, want);
+    if (e != cudaSuccess) {
+      h->pinned = nullptr;
+      h->pinned_bytes = 0;
+      *st = set_err(h, AGIPC_ECUDA, "pinned host buffer: %s", cudaGetErrorString(e));
+      return nullptr;
+    }
+    h->pinned_bytes = want;
+  }
+  *st = AGIPC_OK;
+  return h->pinned;
+}
+
+void pcg_graph_free(PcgGraph *g);  // pcg.cu
+
+extern "C" {
+
+agipc_status agipc_create(agipc_handle *out, int cuda_device) {
+  if (!out) return AGIPC_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return AGIPC_ECUDA;
+  if (cuda_device < 0 || cuda_device >= n) return AGIPC_EINVAL;
+  e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) return AGIPC_ECUDA;
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, cuda_device);
+  if (e != cudaSuccess) return AGIPC_ECUDA;
+  if (prop.major != 10) return AGIPC_ECUDA;  // built for sm_100a only
+  agipc_handle h = new agipc_handle_s();
+  h->device = cuda_device;
+  h->sm_count = prop.multiProcessorCount;
+  *out = h;
+  return AGIPC_OK;
+}
+
+agipc_status agipc_destroy(agipc_handle h) {
+  if (!h) return AGIPC_EINVAL;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  for (auto &kv : h->ws)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->pcg) pcg_graph_free(h->pcg);
+  delete h;
+  return AGIPC_OK;
+}
+
+agipc_status agipc_set_stream(agipc_handle h, void *stream) {
+  if (!h) return AGIPC_EINVAL;
+  h->stream = (cudaStream_t)stream;
+  return AGIPC_OK;
+}
+
+const char *agipc_last_error(agipc_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+const char *agipc_status_string(agipc_status s) {
+  switch (s) {
+    case AGIPC_OK: return "AGIPC_OK";
+    case AGIPC_EINVAL: return "AGIPC_EINVAL";
+    case AGIPC_ERANGE: return "AGIPC_ERANGE";
+    case AGIPC_ENOSPACE: return "AGIPC_ENOSPACE";
+    case AGIPC_ECUDA: return "AGIPC_ECUDA";
+    case AGIPC_ENCCL: return "AGIPC_ENCCL";
+    case AGIPC_EDEGENERATE: return "AGIPC_EDEGENERATE";
+    case AGIPC_ESINGULAR: return "AGIPC_ESINGULAR";
+    case AGIPC_EINDEFINITE: return "AGIPC_EINDEFINITE";
+    case AGIPC_EBREAKDOWN: return "AGIPC_EBREAKDOWN";
+    case AGIPC_NOT_CONVERGED: return "AGIPC_NOT_CONVERGED";
+  }
+  return "unknown agipc_status";
+}
+
+void agipc_version(int *major, int *minor) {
+  if (major) *major = AGIPC_VERSION_MAJOR;
+  if (minor) *minor = AGIPC_VERSION_MINOR;
+}
+
+int64_t agipc_kernel_launches(agipc_handle h) { return h ? h->launches : -1; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// Generic single-pass exclusive scan (decoupled look-back), 2048 items per CTA tile.
+// ------------------------------------------------------------------------------------
+#define SCAN_THREADS 256
+#define SCAN_ITEMS 8
+#define SCAN_TILE (SCAN_THREADS * SCAN_ITEMS)
+
+template <typename TS>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(const TS *__restrict__ src, int64_t n, int64_t mul,
+                                                        int64_t add, int64_t *__restrict__ out,
+                                                        unsigned long long *status, int *counter) {
+  __shared__ int s_tile;
+  __shared__ long long s_warp[SCAN_THREADS / 32];
+  __shared__ long long s_prefix;
+  __shared__ long long s_items[SCAN_TILE];
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * SCAN_TILE;
+  // striped coalesced load into shared memory
+  for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_THREADS) {
+    int64_t i = base + k;
+    s_items[k] = i < n ? (long long)(mul * (int64_t)src[i] + add) : 0;
+  }
+  __syncthreads();
+  long long v[SCAN_ITEMS];
+  long long tsum = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = s_items[threadIdx.x * SCAN_ITEMS + k];
+    tsum += v[k];
+  }
+  long long incl = warp_incl_scan(tsum);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long ws = l < SCAN_THREADS / 32 ? s_warp[l] : 0;
+    long long wi = warp_incl_scan(ws);
+    long long agg = __shfl_sync(FULL_MASK, wi, SCAN_THREADS / 32 - 1);
+    if (l < SCAN_THREADS / 32) s_warp[l] = wi - ws;  // exclusive warp offsets
+    long long pfx = lb_exclusive(status, tile, agg);
+    if (l == 0) s_prefix = pfx;
+  }
+  __syncthreads();
+  long long run = s_prefix + s_warp[w] + incl - tsum;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    s_items[threadIdx.x * SCAN_ITEMS + k] = run;
+    run += v[k];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_THREADS) {
+    int64_t i = base + k;
+    if (i < n) out[i] = s_items[k];
+    if (i == n) out[n] = s_items[k];  // exclusive value at n == total
+  }
+}
+
+agipc_status scan_exclusive_i64(agipc_handle h, int kind, const void *src, int64_t n, int64_t *out,
+                                int64_t mul, int64_t add) {
+  if (n < 0) return set_err(h, AGIPC_EINVAL, "scan of negative size");
+  // one extra item so that out[n] (the total) is produced by the tile containing index n
+  int64_t tiles = cdiv(n + 1, SCAN_TILE);
+  WS(h, status, unsigned long long, "scan_status", tiles + 1);
+  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), h->stream));
+  int *counter = (int *)(status + tiles);
+  if (kind == SCAN_SRC_I32)
+    LAUNCH(h, k_scan<int32_t>, (int)tiles, SCAN_THREADS, 0, (const int32_t *)src, n, mul, add, out, status, counter);
+  else
+    LAUNCH(h, k_scan<int64_t>, (int)tiles, SCAN_THREADS, 0, (const int64_t *)src, n, mul, add, out, status, counter);
+  return AGIPC_OK;
+}

@@ -1,0 +1,164 @@
+// Step 1 -- edge tags from the Green-strain increment (main Sec 4.2 Eq 3, PAPER.md P:834-838;
+// supp Sec 1.1).
+//
+// One thread per tet.  The fp64 arithmetic follows ONE fixed operation order with explicit
+// round-to-nearest intrinsics (no FMA contraction, reading R12) so that the norm --
+// and therefore the integer tag decision -- is reproducible bit for bit:
+//   D_m^-1 = adj(D_m) * (1/det D_m),  F = D_s D_m^-1,  G = 0.5 (F^T F - I),
+//   n_t = sqrt(sum_rc (G_cur - G_prev)_rc^2) (row-major order),  flag = n_t > theta (strict).
+// tau_e = 0 iff some tet containing e is flagged: the slots are pre-filled with 1 and every
+// flagged tet stores 0 into the 12 directed slots of its 6 edges (idempotent, race-free).
+#include "agipc_internal.cuh"
+
+#define TAG_THREADS 256
+
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ void load3(const double *__restrict__ P, int v, double out[3]) {
+  const double *p = P + 3 * (int64_t)v;
+  out[0] = __ldg(p);
+  out[1] = __ldg(p + 1);
+  out[2] = __ldg(p + 2);
+}
+
+// D[r][c] = P_{n_{c+1}}[r] - P_{n_0}[r]
+__device__ __forceinline__ void edge_matrix(const double *__restrict__ P, int4 t, double D[3][3]) {
+  double a[3], b[3], c[3], d[3];
+  load3(P, t.x, a);
+  load3(P, t.y, b);
+  load3(P, t.z, c);
+  load3(P, t.w, d);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    D[r][0] = ds(b[r], a[r]);
+    D[r][1] = ds(c[r], a[r]);
+    D[r][2] = ds(d[r], a[r]);
+  }
+}
+
+__device__ __forceinline__ bool inverse3(const double D[3][3], double M[3][3]) {
+  double c00 = ds(dm(D[1][1], D[2][2]), dm(D[1][2], D[2][1]));
+  double c01 = ds(dm(D[1][2], D[2][0]), dm(D[1][0], D[2][2]));
+  double c02 = ds(dm(D[1][0], D[2][1]), dm(D[1][1], D[2][0]));
+  double c10 = ds(dm(D[0][2], D[2][1]), dm(D[0][1], D[2][2]));
+  double c11 = ds(dm(D[0][0], D[2][2]), dm(D[0][2], D[2][0]));
+  double c12 = ds(dm(D[0][1], D[2][0]), dm(D[0][0], D[2][1]));
+  double c20 = ds(dm(D[0][1], D[1][2]), dm(D[0][2], D[1][1]));
+  double c21 = ds(dm(D[0][2], D[1][0]), dm(D[0][0], D[1][2]));
+  double c22 = ds(dm(D[0][0], D[1][1]), dm(D[0][1], D[1][0]));
+  double det = da(da(dm(D[0][0], c00), dm(D[0][1], c01)), dm(D[0][2], c02));
+  if (det == 0.0 || !isfinite(det)) return false;
+  double inv = __ddiv_rn(1.0, det);
+  // M[r][c] = cof[c][r] * inv
+  M[0][0] = dm(c00, inv); M[0][1] = dm(c10, inv); M[0][2] = dm(c20, inv);
+  M[1][0] = dm(c01, inv); M[1][1] = dm(c11, inv); M[1][2] = dm(c21, inv);
+  M[2][0] = dm(c02, inv); M[2][1] = dm(c12, inv); M[2][2] = dm(c22, inv);
+  return true;
+}
+
+__device__ __forceinline__ void green(const double Ds[3][3], const double M[3][3], double G[3][3]) {
+  double F[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      F[r][c] = da(da(dm(Ds[r][0], M[0][c]), dm(Ds[r][1], M[1][c])), dm(Ds[r][2], M[2][c]));
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double C = da(da(dm(F[0][r], F[0][c]), dm(F[1][r], F[1][c])), dm(F[2][r], F[2][c]));
+      G[r][c] = dm(0.5, ds(C, r == c ? 1.0 : 0.0));
+    }
+}
+
+__global__ void __launch_bounds__(TAG_THREADS) k_tag(int64_t n_tets, const int4 *__restrict__ tets,
+                                                     const int4 *__restrict__ tet_slots,
+                                                     const double *__restrict__ X,
+                                                     const double *__restrict__ xp,
+                                                     const double *__restrict__ xc, double theta,
+                                                     uint8_t *__restrict__ slot_tags,
+                                                     double *__restrict__ tet_norm,
+                                                     unsigned long long *__restrict__ counters) {
+  int64_t t = (int64_t)blockIdx.x * TAG_THREADS + threadIdx.x;
+  bool flag = false, degenerate = false;
+  if (t < n_tets) {
+    int4 q = __ldg(tets + t);
+    double Dm[3][3], M[3][3], Dp[3][3], Dc[3][3], Gp[3][3], Gc[3][3];
+    edge_matrix(X, q, Dm);
+    if (!inverse3(Dm, M)) {
+      degenerate = true;
+      flag = true;
+      if (tet_norm) tet_norm[t] = __longlong_as_double(0x7ff8000000000000ll);  // NaN
+    } else {
+      edge_matrix(xp, q, Dp);
+      edge_matrix(xc, q, Dc);
+      green(Dp, M, Gp);
+      green(Dc, M, Gc);
+      double s2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double d = ds(Gc[r][c], Gp[r][c]);
+          s2 = da(s2, dm(d, d));
+        }
+      double n = __dsqrt_rn(s2);
+      flag = n > theta;
+      if (tet_norm) tet_norm[t] = n;
+    }
+    if (flag) {
+      const int4 *s = tet_slots + 3 * t;
+      int4 s0 = __ldg(s), s1 = __ldg(s + 1), s2v = __ldg(s + 2);
+      slot_tags[s0.x] = 0; slot_tags[s0.y] = 0; slot_tags[s0.z] = 0; slot_tags[s0.w] = 0;
+      slot_tags[s1.x] = 0; slot_tags[s1.y] = 0; slot_tags[s1.z] = 0; slot_tags[s1.w] = 0;
+      slot_tags[s2v.x] = 0; slot_tags[s2v.y] = 0; slot_tags[s2v.z] = 0; slot_tags[s2v.w] = 0;
+    }
+  }
+  if (counters) {
+    unsigned fb = __ballot_sync(FULL_MASK, flag);
+    unsigned db = __ballot_sync(FULL_MASK, degenerate);
+    if (lane_id() == 0) {
+      if (fb) atomicAdd(counters, (unsigned long long)__popc(fb));
+      if (db) atomicAdd(counters + 1, (unsigned long long)__popc(db));
+    }
+  }
+}
+
+extern "C" agipc_status agipc_tag_edges(agipc_handle h, const agipc_mesh *mesh, const double *x_prev,
+                                        const double *x_cur, double threshold, uint8_t *slot_tags,
+                                        double *tet_norm, int64_t *n_flagged) {
+  if (!h) return AGIPC_EINVAL;
+  if (!mesh || mesh->n_tets < 0 || mesh->nnz_adj < 0 || mesh->n_nodes < 0)
+    return set_err(h, AGIPC_EINVAL, "tag_edges: bad mesh");
+  if (mesh->n_tets > 0 && (!mesh->tets || !mesh->tet_slots || !mesh->x_rest || !x_prev || !x_cur))
+    return set_err(h, AGIPC_EINVAL, "tag_edges: null input");
+  if (mesh->nnz_adj > 0 && !slot_tags) return set_err(h, AGIPC_EINVAL, "tag_edges: null slot_tags");
+  if (((uintptr_t)mesh->tets & 15) || ((uintptr_t)mesh->tet_slots & 15))
+    return set_err(h, AGIPC_EINVAL, "tag_edges: tets/tet_slots must be 16-byte aligned");
+  if (mesh->n_nodes >= INT32_MAX || mesh->nnz_adj >= INT32_MAX)
+    return set_err(h, AGIPC_ERANGE, "tag_edges: index exceeds int32");
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (mesh->nnz_adj > 0) CU_TRY(h, cudaMemsetAsync(slot_tags, 1, (size_t)mesh->nnz_adj, h->stream));
+  unsigned long long *counters = nullptr;
+  if (n_flagged) {
+    WS(h, c, unsigned long long, "tag_counters", 2);
+    counters = c;
+    CU_TRY(h, cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), h->stream));
+  }
+  int64_t blocks = cdiv(mesh->n_tets, TAG_THREADS);
+  LAUNCH(h, k_tag, (unsigned)blocks, TAG_THREADS, 0, mesh->n_tets, (const int4 *)mesh->tets,
+         (const int4 *)mesh->tet_slots, mesh->x_rest, x_prev, x_cur, threshold, slot_tags, tet_norm, counters);
+  if (n_flagged) {
+    agipc_status st;
+    unsigned long long *hc = (unsigned long long *)pinned_get(h, 16, &st);
+    if (st != AGIPC_OK) return st;
+    CU_TRY(h, cudaMemcpyAsync(hc, counters, 16, cudaMemcpyDeviceToHost, h->stream));
+    CU_TRY(h, cudaStreamSynchronize(h->stream));
+    *n_flagged = (int64_t)hc[0];
+    if (hc[1]) return set_err(h, AGIPC_EDEGENERATE, "tag_edges: %llu tets with det(D_m) == 0", hc[1]);
+  }
+  return AGIPC_OK;
+}

@@ -1,0 +1,58 @@
+"""One Newton iteration of the coarsening path (main Alg 1 lines 8-10):
+tag -> map -> assemble -> coarse PCG, composed from the four C-ABI calls.  Plumbing only:
+all arithmetic runs in libagipc's kernels."""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from . import (CoarseBuffers, DeviceMesh, Handle, assemble_coarse, build_map, pcg_solve, tag_edges)
+
+
+@dataclasses.dataclass
+class StepResult:
+    n_flagged: int | None
+    map_info: dict
+    coarse: object
+    x: torch.Tensor
+    pcg: dict
+
+
+class CoarseningStep:
+    """Holds the device-resident static inputs and grow-only buffers of the path."""
+
+    def __init__(self, h: Handle, mesh: DeviceMesh, H_row_ptr, H_col, H_val, group_size=32,
+                 affine_threshold=32, theta=5e-5, rel_tol=1e-3, max_iters=10000, check_every=16):
+        self.h, self.mesh = h, mesh
+        self.H = (H_row_ptr, H_col, H_val)
+        self.group_size, self.affine_threshold, self.theta = group_size, affine_threshold, theta
+        self.rel_tol, self.max_iters, self.check_every = rel_tol, max_iters, check_every
+        dev = mesh.x_rest.device
+        self.slot_tags = torch.empty(mesh.adj_nbr.shape[0], dtype=torch.uint8, device=dev)
+        self.map = torch.empty(mesh.n_nodes, dtype=torch.int32, device=dev)
+        self.bufs = CoarseBuffers(dev, mesh.n_nodes, 4 * mesh.n_nodes // 8 + 16, H_col.shape[0] // 2 + 64)
+        self.x = None
+
+    def coarsen(self, x_prev, x_cur, g_fine, count=False):
+        """Steps 1-3.  Returns (n_flagged, map_info, CoarseSystem)."""
+        _, nf = tag_edges(self.h, self.mesh, x_prev, x_cur, self.theta, self.slot_tags, count=count)
+        _, info = build_map(self.h, self.mesh, self.slot_tags, self.group_size, 0, self.map)
+        cs = assemble_coarse(self.h, self.mesh, self.map, info["n_coarse"], self.affine_threshold, *self.H,
+                             g_fine, self.bufs)
+        return nf, info, cs
+
+    def solve(self, cs):
+        """Step 4: H_c y = g_c from y0 = 0; the coarse direction of P:752 is d_c = -y."""
+        n = cs.n_slots
+        if self.x is None or self.x.shape[0] < n:
+            self.x = torch.empty((int(n * 1.25) + 16, 3), dtype=torch.float64, device=cs.val.device)
+        x = self.x[:n]
+        _, st = pcg_solve(self.h, cs.row_ptr, cs.col, cs.val, cs.g_c, x, self.rel_tol, self.max_iters,
+                          self.check_every, zero_x0=True)
+        return x, st
+
+    def __call__(self, x_prev, x_cur, g_fine, count=False) -> StepResult:
+        nf, info, cs = self.coarsen(x_prev, x_cur, g_fine, count)
+        x, st = self.solve(cs)
+        return StepResult(nf, info, cs, x, st)

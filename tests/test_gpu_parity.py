@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Contracts: tags, map, n_coarse, levels, new_map, n3, n12,
+row_ptr and col bit-exact; coarse values and g_c within 1e-12 of the oracle's |.|-Galerkin
+bound (entrywise); PCG solutions with an oracle-evaluated relative residual <= 1e-8 and
+iteration counts at the paper's tolerance within 2% of the oracle's."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_04773_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def h(P, gpu):
+    return P.Handle(0)
+
+
+def dev(a, dt):
+    return torch.as_tensor(np.ascontiguousarray(a)).to("cuda:0", dt)
+
+
+def dmesh(P, m):
+    return P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device="cuda:0")
+
+
+def check_map(P, h, m, dm, tags_np, gs, max_levels=0):
+    mp, info = P.build_map(h, dm, dev(tags_np, torch.uint8), gs, max_levels,
+                           agg_size=torch.empty(m.n_nodes, dtype=torch.int32, device="cuda:0"))
+    om = oracle.build_map(m.adj_ptr, m.adj_nbr, tags_np, gs, max_levels)
+    assert np.array_equal(mp.cpu().numpy(), om["map"]), (gs, max_levels)
+    assert info["n_coarse"] == om["n_coarse"] and info["n_levels"] == om["n_levels"]
+    L = min(om["n_levels"], 64)
+    assert info["level_n"][:L] == om["level_n"][:L].tolist()
+    return mp, info, om
+
+
+def check_assemble(P, h, m, dm, om, H, g, thr):
+    cs = P.assemble_coarse(h, dm, dev(om["map"], torch.int32), om["n_coarse"], thr, dev(m.bsr_ptr, torch.int64),
+                           dev(m.bsr_col, torch.int32), dev(H, torch.float64),
+                           None if g is None else dev(g, torch.float64))
+    oa = oracle.assemble(om["map"], om["n_coarse"], thr, m.X, m.bsr_ptr, m.bsr_col, H, g)
+    assert (cs.n3, cs.n12, cs.n_slots, cs.nnzb) == (oa["n3"], oa["n12"], oa["n_slots"], oa["nnzb"])
+    assert np.array_equal(cs.new_map.cpu().numpy(), oa["new_map"])
+    assert np.array_equal(cs.row_ptr.cpu().numpy(), oa["row_ptr"])
+    assert np.array_equal(cs.col.cpu().numpy(), oa["col"])
+    dv = np.abs(cs.val.cpu().numpy() - oa["val"])
+    bad = dv > 1e-12 * oa["bound"]
+    assert not bad.any(), f"{bad.sum()} coarse entries outside 1e-12 * bound (max diff {dv.max():.3e})"
+    if g is not None:
+        dg = np.abs(cs.g_c.cpu().numpy() - oa["g_c"])
+        assert np.all(dg <= 1e-12 * oa["g_bound"])
+    return cs, oa
+
+
+# ------------------------------------------------------------------------------------------
+# step 1
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,kind", [(2, "twist"), (5, "random"), (10, "twist"), (10, "random"), (10, "scale")])
+def test_tags_bit_exact(P, h, n, kind):
+    m = synth.kuhn_grid(n)
+    rng = np.random.default_rng(n)
+    if kind == "twist":
+        xp, xc = synth.twist(m.X, 0.5), synth.twist(m.X, 0.501)
+        theta = 5e-5
+    elif kind == "random":
+        xp = m.X + 1e-3 * rng.standard_normal(m.X.shape)
+        xc = xp + 1e-4 * rng.standard_normal(m.X.shape)
+        theta = float(np.median(oracle.tag_edges(m.tets, m.tet_slots, m.X, xp, xc, 1.0, m.adj_nbr.shape[0])[1]))
+    else:  # every tet exactly at the threshold band edges (strictness)
+        theta = 5e-5
+        xp, xc = m.X, np.sqrt(1.0 + 2.0 * theta * (1 + 1e-9) / np.sqrt(3)) * m.X
+    dm = dmesh(P, m)
+    norm = torch.empty(m.n_tets, dtype=torch.float64, device="cuda:0")
+    tags, nf = P.tag_edges(h, dm, dev(xp, torch.float64), dev(xc, torch.float64), theta, tet_norm=norm, count=True)
+    ot, on, of = oracle.tag_edges(m.tets, m.tet_slots, m.X, xp, xc, theta, m.adj_nbr.shape[0])
+    assert np.array_equal(tags.cpu().numpy(), ot)
+    assert np.array_equal(norm.cpu().numpy(), on)  # same operation order: bit-identical norms
+    assert nf == int(of.sum())
+
+
+def test_tags_degenerate_tet_reported(P, h):
+    X = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0], [0, 0, 1]], float)
+    m = synth.mesh_from_tets(X, np.array([[0, 1, 2, 3]]))
+    dm = dmesh(P, m)
+    x = dev(X, torch.float64)
+    with pytest.raises(P.AgipcError) as e:
+        P.tag_edges(h, dm, x, x, 1.0, count=True)
+    assert e.value.status == P.EDEGENERATE
+
+
+# ------------------------------------------------------------------------------------------
+# step 2
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("gs", [1, 2, 3, 4, 5, 7, 8, 16, 31, 32])
+@pytest.mark.parametrize("p", [0.0, 0.2, 0.5, 1.0])
+def test_map_bit_exact_c1_group_sizes(P, h, gs, p):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    for seed in range(2):
+        tags = synth.random_tags(m, p, seed)
+        for ml in (0, 1, 2):
+            check_map(P, h, m, dm, tags, gs, ml)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 7])
+def test_map_ragged_tails(P, h, n):
+    """n^3 not a multiple of the group size: the last group is partial."""
+    m = synth.kuhn_grid(n)
+    dm = dmesh(P, m)
+    for p in (0.3, 0.8, 1.0):
+        for gs in (3, 32):
+            check_map(P, h, m, dm, synth.random_tags(m, p, 1), gs)
+
+
+def test_map_brute_force_kuhn_cube(P, h):
+    m = synth.kuhn_grid(2)
+    dm = dmesh(P, m)
+    for pat in np.random.default_rng(0).integers(0, 1 << m.n_edges, 300):
+        tau = np.array([(int(pat) >> e) & 1 for e in range(m.n_edges)], np.uint8)
+        for gs in (2, 3, 8):
+            check_map(P, h, m, dm, synth.edge_tags_to_slots(m, tau), gs)
+
+
+def test_map_seeds_c1(P, h):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    for p in (0.1, 0.2, 0.3):
+        for seed in range(20):
+            check_map(P, h, m, dm, synth.random_tags(m, p, seed), 32)
+
+
+def test_map_errors(P, h):
+    m = synth.kuhn_grid(3)
+    dm = dmesh(P, m)
+    tags = dev(np.ones(m.adj_nbr.shape[0], np.uint8), torch.uint8)
+    for gs in (0, 33, -1):
+        with pytest.raises(P.AgipcError) as e:
+            P.build_map(h, dm, tags, gs)
+        assert e.value.status == P.EINVAL
+
+
+# ------------------------------------------------------------------------------------------
+# step 3
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("p", [0.0, 0.2, 0.5, 0.8, 1.0])
+@pytest.mark.parametrize("thr", [32, 0, 2, 5, 10 ** 9])
+def test_assemble_c1(P, h, p, thr):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    _, _, om = check_map(P, h, m, dm, synth.random_tags(m, p, 0), 32)
+    check_assemble(P, h, m, dm, om, H, g, thr)
+
+
+def test_assemble_identity_map_exact(P, h):
+    m = synth.kuhn_grid(6)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    om = dict(map=np.arange(m.n_nodes, dtype=np.int32), n_coarse=m.n_nodes)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, 32)
+    assert np.array_equal(cs.val.cpu().numpy(), H) and np.array_equal(cs.g_c.cpu().numpy(), g)
+
+
+@pytest.mark.parametrize("gs,n", [(32, 10), (8, 10), (32, 13)])
+def test_assemble_random_maps_and_groups(P, h, gs, n):
+    m = synth.kuhn_grid(n)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m, E=1e7)
+    g = synth.fine_gradient(m.n_nodes, 4)
+    for seed in range(3):
+        _, _, om = check_map(P, h, m, dm, synth.random_tags(m, 0.35, seed), gs)
+        for thr in (32, 4):
+            check_assemble(P, h, m, dm, om, H, g, thr)
+
+
+def test_assemble_enospace_then_retry(P, h):
+    m = synth.kuhn_grid(8)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    om = oracle.build_map(m.adj_ptr, m.adj_nbr, synth.random_tags(m, 0.2, 0), 32)
+    bufs = P.CoarseBuffers("cuda:0", m.n_nodes, 1, 1)
+    cs = P.assemble_coarse(h, dm, dev(om["map"], torch.int32), om["n_coarse"], 32, dev(m.bsr_ptr, torch.int64),
+                           dev(m.bsr_col, torch.int32), dev(H, torch.float64), None, bufs)
+    oa = oracle.assemble(om["map"], om["n_coarse"], 32, m.X, m.bsr_ptr, m.bsr_col, H)
+    assert cs.nnzb == oa["nnzb"] and np.array_equal(cs.col.cpu().numpy(), oa["col"])
+
+
+def test_assemble_bad_map_is_einval(P, h):
+    m = synth.kuhn_grid(3)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    mp = np.zeros(m.n_nodes, np.int32); mp[5] = 7
+    with pytest.raises(P.AgipcError) as e:
+        P.assemble_coarse(h, dm, dev(mp, torch.int32), 3, 32, dev(m.bsr_ptr, torch.int64),
+                          dev(m.bsr_col, torch.int32), dev(H, torch.float64))
+    assert e.value.status == P.EINVAL
+
+
+# ------------------------------------------------------------------------------------------
+# step 4
+# ------------------------------------------------------------------------------------------
+def test_pcg_c1_matches_oracle(P, h):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    _, _, om = check_map(P, h, m, dm, synth.random_tags(m, 0.2, 0), 32)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, 32)
+    for tol in (1e-3, 1e-10):
+        x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=tol, max_iters=10000, zero_x0=True)
+        ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=tol, max_iters=10000)
+        assert s["status"] == P.OK
+        assert abs(s["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"]))
+        rr = oracle.rel_residual(oa["row_ptr"], oa["col"], oa["val"], x.cpu().numpy(), oa["g_c"])
+        assert rr <= max(tol, 1e-8) * 1.01
+    x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-12, max_iters=20000, zero_x0=True)
+    xr = ref["x"]
+    assert np.linalg.norm(x.cpu().numpy() - xr) <= 1e-6 * np.linalg.norm(xr)
+
+
+def test_pcg_special_cases(P, h):
+    n = 10
+    rp = dev(np.arange(n + 1, dtype=np.int64), torch.int64)
+    cl = dev(np.arange(n, dtype=np.int32), torch.int32)
+    I = dev(np.tile(np.eye(3), (n, 1, 1)), torch.float64)
+    b = dev(np.random.default_rng(0).standard_normal((n, 3)), torch.float64)
+    x, s = P.pcg_solve(h, rp, cl, I, b, rel_tol=1e-12, zero_x0=True)
+    assert s["iters"] == 1 and torch.allclose(x, b, rtol=1e-15, atol=0)
+    x, s = P.pcg_solve(h, rp, cl, I, torch.zeros_like(b), rel_tol=1e-3, zero_x0=True)
+    assert s["iters"] == 0 and torch.all(x == 0)
+    with pytest.raises(P.AgipcError) as e:
+        P.pcg_solve(h, rp, cl, -I, b, rel_tol=1e-3, zero_x0=True)
+    assert e.value.status == P.EINDEFINITE
+    Z = I.clone(); Z[3] = 0
+    with pytest.raises(P.AgipcError) as e:
+        P.pcg_solve(h, rp, cl, Z, b, rel_tol=1e-3, zero_x0=True)
+    assert e.value.status == P.ESINGULAR
+    x, s = P.pcg_solve(h, rp, cl, 2 * I, b, x=b.clone(), rel_tol=1e-12)   # nonzero x0
+    assert torch.allclose(x, b / 2, rtol=1e-14)
+
+
+def test_pcg_not_converged_reports_last_iterate(P, h):
+    m = synth.kuhn_grid(8)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    x, s = P.pcg_solve(h, dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32), dev(H, torch.float64),
+                       dev(g, torch.float64), rel_tol=1e-14, max_iters=7, check_every=3, zero_x0=True)
+    assert s["status"] == P.NOT_CONVERGED and s["iters"] == 7
+    ref = oracle.pcg(m.bsr_ptr, m.bsr_col, H, g, rel_tol=1e-14, max_iters=7)
+    assert np.allclose(x.cpu().numpy(), ref["x"], rtol=1e-9, atol=1e-12 * np.abs(ref["x"]).max())
+
+
+# ------------------------------------------------------------------------------------------
+# full sizes (C2, C3) in the launch configuration bench.py times
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_full_size_path(P, h, cfg):
+    c = synth.config_c2() if cfg == "c2" else synth.config_c3()
+    m = c["mesh"]
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m, E=c["E"])
+    g = synth.fine_gradient(m.n_nodes)
+    tags, nf = P.tag_edges(h, dm, dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64), c["theta"],
+                           count=True)
+    ot, _, of = oracle.tag_edges(m.tets, m.tet_slots, m.X, c["x_prev"], c["x_cur"], c["theta"], m.adj_nbr.shape[0])
+    assert np.array_equal(tags.cpu().numpy(), ot) and nf == int(of.sum())
+    _, info, om = check_map(P, h, m, dm, ot, 32)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, 32)
+    # PCG to 1e-8: residual evaluated by the oracle (compensated)
+    x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-8, max_iters=50000, zero_x0=True)
+    rr = oracle.rel_residual(oa["row_ptr"], oa["col"], oa["val"], x.cpu().numpy(), oa["g_c"])
+    assert s["status"] == P.OK and rr <= 1.01e-8, rr
+    if cfg == "c2":  # iteration count at the paper's tolerance
+        _, s3 = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-3, zero_x0=True)
+        ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=1e-3, max_iters=10000)
+        assert abs(s3["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"]))
