@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the AGIPC coarsening path on B200.
+
+Workload (N=1): C3 of BASELINE.json -- a 1,000,000-node Kuhn tet mesh (100^3, Morton order),
+H_f = M + dt^2 K (E = 1e5), "strain walls" iterates with the wall phase k = step mod 10,
+theta = 5e-5, group size 32, affine threshold 32, coarse PCG to 1e-3 from x0 = 0.
+A step = one Newton iteration of the path: tag -> map -> assemble -> PCG (all of SURVEY §8(a)).
+
+  value      = coarsen+assemble (tag + map + assemble) ms per Newton step, device-resident inputs
+  e2e        = the same through the public API with HOST inputs: the step's H2D copies
+               (x_prev, x_cur, H_f values, g_f from pinned memory) and the D2H read of the
+               step's result (the coarse right-hand side g_c) are inside the timed region
+  roofline   = the dominant kernel (PCG SpMV, k_spmv_pq): algorithmic bytes per launch
+               / average launch duration measured with CUDA events on its launch stream
+  cpu_baseline = the C oracle on the host cores (rank 0, N=1), bounded sample
+
+Multi-GPU (torchrun, N>1): every rank runs its own C3 problem (weak scaling, no data-path
+collective; the partitioned 20M-node path with NCCL halos is not built yet -- DESIGN.md).
+`--impl reference` times the CPU oracle (the tier's reference arm) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "coarsen+assemble ms/Newton step and coarse PCG iters/s at 1M nodes; HBM GB/s % peak"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="agipc", choices=["agipc", "reference"])
+    ap.add_argument("--n", type=int, default=100, help="grid side (100 = C3, 1M nodes)")
+    ap.add_argument("--check-every", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_inputs(n):
+    import synth
+    t0 = time.time()
+    m = synth.kuhn_grid(n)
+    H = synth.fine_hessian(m, E=1e5)
+    g = synth.fine_gradient(m.n_nodes)
+    xcs = [synth.walls(m, k)[1] for k in range(10)]
+    return m, H, g, xcs, time.time() - t0
+
+
+def workload_config(m, n_gpus):
+    return {"workload": f"C3: {m.n_nodes:,}-node Kuhn tet mesh ({m.n_side}^3, Morton order), strain walls "
+                        "k = step mod 10, theta=5e-5, E=1e5, group_size=32, affine_threshold=32, "
+                        "PCG block-Jacobi to 1e-3 from x0=0",
+            "nodes": m.n_nodes, "tets": m.n_tets, "fine_blocks": int(m.bsr_col.shape[0]),
+            "l2": "flushed between steps (256 MB write, outside the timed events); fine BSR 1.12 GB > L2",
+            "parallelism": f"{n_gpus} independent ranks" if n_gpus > 1 else "1 GPU"}
+
+
+# --------------------------------------------------------------------------------------
+def cpu_baseline(m, H, g, xc, steps=1, pcg_iters=20):
+    """The oracle as it stands (single-threaded C) on one Newton step's coarsen+assemble."""
+    import oracle
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        tags, _, _ = oracle.tag_edges(m.tets, m.tet_slots, m.X, m.X, xc, 5e-5, m.adj_nbr.shape[0])
+        om = oracle.build_map(m.adj_ptr, m.adj_nbr, tags, 32)
+        oa = oracle.assemble(om["map"], om["n_coarse"], 32, m.X, m.bsr_ptr, m.bsr_col, H, g)
+    t1 = time.perf_counter()
+    oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=0.0, max_iters=pcg_iters)
+    t2 = time.perf_counter()
+    return {"coarsen_ms": 1e3 * (t1 - t0) / steps, "pcg_iters_per_s": pcg_iters / (t2 - t1),
+            "cores": 1, "sample": f"{steps} full C3 Newton step(s) of tag+map+assemble (k=0) and "
+                                  f"{pcg_iters} PCG iterations on its coarse system; single-threaded C oracle"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    m, H, g, xcs, gen_s = build_inputs(args.n)
+    times = []
+    import oracle
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        tags, _, _ = oracle.tag_edges(m.tets, m.tet_slots, m.X, m.X, xcs[s % 10], 5e-5, m.adj_nbr.shape[0])
+        om = oracle.build_map(m.adj_ptr, m.adj_nbr, tags, 32)
+        oracle.assemble(om["map"], om["n_coarse"], 32, m.X, m.bsr_ptr, m.bsr_col, H, g)
+        if s >= args.warmup:
+            times.append(1e3 * (time.perf_counter() - t0))
+    v = statistics.mean(times)
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 3), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(m, 1),
+           "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": 1, "kind": "oracle",
+                            "sample": f"each step = one full C3 Newton step of tag+map+assemble (k = step mod 10), "
+                                      "single-threaded C oracle"},
+           "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "input_generation_s": round(gen_s, 1)}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------------------
+def run_agipc(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_04773_b200 as P
+    from paper_2605_04773_b200.step import CoarseningStep
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    m, H, g, xcs, gen_s = build_inputs(args.n)
+    h = P.Handle(local_rank)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    dm = P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device=dev)
+    Hrp, Hcol, Hval = t(m.bsr_ptr, torch.int64), t(m.bsr_col, torch.int32), t(H, torch.float64)
+    gd = t(g, torch.float64)
+    xp = t(m.X, torch.float64)
+    xcd = [t(x, torch.float64) for x in xcs]
+    step = CoarseningStep(h, dm, Hrp, Hcol, Hval, check_every=args.check_every)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also sizes every workspace and captures the PCG graph)
+    for s in range(args.warmup):
+        cs = step.coarsen(xp, xcd[s % 10], gd)[2]
+        step.solve(cs)
+    torch.cuda.synchronize()
+
+    h.profile(True)
+    launches0 = h.kernel_launches
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sizes = []
+    clocks = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    wall0 = time.perf_counter()
+    for s in range(args.steps):
+        flush.zero_()
+        k = (args.warmup + s) % 10
+        ev[s][0].record()
+        nf, info, cs = step.coarsen(xp, xcd[k], gd)
+        ev[s][1].record()
+        x, st = step.solve(cs)
+        ev[s][2].record()
+        sizes.append((cs.n_slots, cs.nnzb, st["iters"], info["n_coarse"], info["n_levels"], cs.n3, cs.n12))
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    launches = h.kernel_launches - launches0
+    prof = h.profile_read()
+    h.profile(False)
+    coarsen = [ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)]
+    pcg = [ev[s][1].elapsed_time(ev[s][2]) for s in range(args.steps)]
+    total = [a + b for a, b in zip(coarsen, pcg)]
+    iters = sum(z[2] for z in sizes)
+    # max over ranks
+    vec = torch.tensor([statistics.mean(coarsen), statistics.mean(total), sum(pcg)], dtype=torch.float64,
+                       device=dev)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    coarsen_ms, step_ms, pcg_ms_sum = vec.tolist()
+
+    # ---- roofline of the dominant kernel: PCG SpMV (k_spmv_pq) ----
+    hbm, peak_src = peaks()
+    n_spmv, ms_spmv = prof.get("pcg_spmv", (0, 0.0))
+    # algorithmic bytes per SpMV launch: 72 B values + 4 B col per block, 8 B row_ptr per row,
+    # p read once (24 B/row), q written once (24 B/row)
+    bytes_spmv = sum(z[2] * (76 * z[1] + 8 * (z[0] + 1) + 48 * z[0]) for z in sizes)
+    achieved = bytes_spmv / (ms_spmv * 1e-3) / 1e9 if ms_spmv > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("k_spmv_pq")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    # coarsen+assemble algorithmic bytes (SURVEY §8(d) model) for context
+    N, T, E2, nnzb_f = m.n_nodes, m.n_tets, m.adj_nbr.shape[0], m.bsr_col.shape[0]
+    ns_mean = statistics.mean(z[0] for z in sizes)
+    nb_mean = statistics.mean(z[1] for z in sizes)
+    b_coarsen = (16 * T + 72 * N + E2) + (8 * (N + 1) + 5 * E2 + 4 * N) + \
+        (76 * nnzb_f + 8 * N + 4 * N + 24 * N + 24 * N + 76 * nb_mean + 8 * ns_mean + 24 * ns_mean)
+
+    # ---- e2e through the public API with host inputs ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        hx = pin(m.X)
+        hxc = [pin(x) for x in xcs]
+        hH = pin(H)
+        hg = pin(g)
+        hgc = torch.empty((int(ns_mean * 1.5) + 16, 3), dtype=torch.float64).pin_memory()
+        dxp = torch.empty_like(xp); dxc = torch.empty_like(xp); dH = torch.empty_like(Hval); dg = torch.empty_like(gd)
+        step2 = CoarseningStep(h, dm, Hrp, Hcol, dH, check_every=args.check_every)
+        ne = args.e2e_steps or args.steps
+        e2e_t = []
+        bi = bo = 0
+        for s in range(ne + 1):
+            flush.zero_()
+            k = s % 10
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dxp.copy_(hx, non_blocking=True); dxc.copy_(hxc[k], non_blocking=True)
+            dH.copy_(hH, non_blocking=True); dg.copy_(hg, non_blocking=True)
+            _, _, cs = step2.coarsen(dxp, dxc, dg)
+            if hgc.shape[0] < cs.n_slots:
+                hgc = torch.empty((cs.n_slots, 3), dtype=torch.float64).pin_memory()
+            hgc[:cs.n_slots].copy_(cs.g_c, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            if s > 0:  # the first e2e step re-sizes step2's buffers
+                e2e_t.append(e0.elapsed_time(e1))
+                bi = (hx.numel() + hxc[k].numel() + hH.numel() + hg.numel()) * 8
+                bo = cs.n_slots * 24
+        ev2 = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ev2, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(float(ev2.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo),
+               "scope": "H2D(x_prev, x_cur, H_f, g_f) + tag + map + assemble + D2H(g_c), pinned host memory"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(m, H, g, xcs[0])
+        cpu = {"value": round(cb["coarsen_ms"], 1), "unit": "ms", "cores": cb["cores"], "kind": "oracle",
+               "sample": cb["sample"], "pcg_iters_per_s": round(cb["pcg_iters_per_s"], 2)}
+
+    if rank != 0:
+        return
+    out = {
+        "metric": METRIC, "value": round(coarsen_ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(m, world),
+        "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,
+        "pcg_iters_per_step": round(iters / args.steps, 1),
+        "coarsen_assemble_gbs": round(b_coarsen / (coarsen_ms * 1e-3) / 1e9, 1),
+        "roofline": {"kernel": "k_spmv_pq (PCG SpMV + p.q)", "bound": "hbm",
+                     "achieved": None if achieved is None else round(achieved, 1), "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": None if achieved is None else round(achieved / hbm, 4),
+                     "traffic": traffic, "launches": n_spmv,
+                     "avg_launch_us": round(1e3 * ms_spmv / n_spmv, 2) if n_spmv else None,
+                     "algorithmic_bytes_per_launch": int(bytes_spmv / max(1, iters))},
+        "phase_ms_per_step": {k: round(v[1] / args.steps, 4) for k, v in prof.items()},
+        "coarse": {"n_coarse": sizes[-1][3], "levels": sizes[-1][4], "n3": sizes[-1][5], "n12": sizes[-1][6],
+                   "n_slots": sizes[-1][0], "nnzb": sizes[-1][1]},
+        "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_agipc(args, world, rank, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,20 @@ AGIPC_API void agipc_version(int *major /*[host]*/, int *minor /*[host]*/);
 /* Number of kernels this handle has enqueued since creation ([host] counter). */
 AGIPC_API int64_t agipc_kernel_launches(agipc_handle h);
 
+/* Profiling.  agipc_profile(h, 1) resets and enables CUDA-event timing on the streams the
+ * kernels are launched on: one interval per entry-point call (tag_edges, build_map,
+ * assemble_coarse, pcg_setup, pcg_solve) and, inside the PCG graph, one interval per kernel
+ * launch (pcg_spmv = K1, pcg_update = K2, pcg_direction = K3; early-exited launches after
+ * convergence are not counted).  agipc_profile_read synchronises pending events and fills
+ * up to cap entries; returns the number written (or the number available if out == NULL). */
+typedef struct {
+  char name[32];
+  int64_t count;     /* timed intervals */
+  double total_ms;   /* summed duration */
+} agipc_profile_entry;
+AGIPC_API agipc_status agipc_profile(agipc_handle h, int enable);
+AGIPC_API int agipc_profile_read(agipc_handle h, agipc_profile_entry *out /*[host]*/, int cap);
+
 /* ---- static fine mesh ("static underlying topology"; P:838 precomputed adjacency) -- */
 typedef struct {
   int64_t n_nodes;          /* N                                                              */

@@ -55,14 +55,18 @@ class _Coarse(C.Structure):
                 ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("g_c", C.c_void_p)]
 
 
+class _ProfEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("count", C.c_int64), ("total_ms", C.c_double)]
+
+
 class _PcgStats(C.Structure):
     _fields_ = [("iters", C.c_int32), ("status", C.c_int32), ("rel_residual", C.c_double),
                 ("b_norm", C.c_double)]
 
 
 EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_error", "agipc_status_string",
-           "agipc_version", "agipc_kernel_launches", "agipc_tag_edges", "agipc_build_map",
-           "agipc_assemble_coarse", "agipc_pcg_solve"]
+           "agipc_version", "agipc_kernel_launches", "agipc_profile", "agipc_profile_read", "agipc_tag_edges",
+           "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve"]
 
 
 def lib():
@@ -85,6 +89,10 @@ def lib():
         L.agipc_version.restype = None
         L.agipc_kernel_launches.argtypes = [P]
         L.agipc_kernel_launches.restype = i64
+        L.agipc_profile.argtypes = [P, i32]
+        L.agipc_profile.restype = i32
+        L.agipc_profile_read.argtypes = [P, C.POINTER(_ProfEntry), i32]
+        L.agipc_profile_read.restype = i32
         L.agipc_tag_edges.argtypes = [P, C.POINTER(_Mesh), P, P, f64, P, P, C.POINTER(i64)]
         L.agipc_build_map.argtypes = [P, C.POINTER(_Mesh), P, i32, i32, P, P, C.POINTER(_MapInfo)]
         L.agipc_assemble_coarse.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), P,
@@ -143,6 +151,16 @@ class Handle:
     @property
     def kernel_launches(self) -> int:
         return int(lib().agipc_kernel_launches(self._h))
+
+    def profile(self, enable: bool = True):
+        """Reset and enable/disable the library's CUDA-event timing (agipc_profile)."""
+        self._check(lib().agipc_profile(self._h, int(bool(enable))))
+
+    def profile_read(self) -> dict:
+        """{phase: (count, total_ms)} from agipc_profile_read (synchronises pending events)."""
+        buf = (_ProfEntry * 16)()
+        n = lib().agipc_profile_read(self._h, buf, 16)
+        return {buf[i].name.decode(): (int(buf[i].count), float(buf[i].total_ms)) for i in range(n)}
 
     def close(self):
         if self._h:

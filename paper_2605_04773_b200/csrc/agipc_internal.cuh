@@ -6,8 +6,10 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "agipc.h"
 
@@ -24,6 +26,24 @@ struct WsBuf {
 
 struct PcgGraph;  // pcg.cu
 
+// Profiling phases (agipc_profile_read names them)
+enum ProfPhase {
+  PROF_TAG = 0,
+  PROF_MAP,
+  PROF_ASSEMBLE,
+  PROF_PCG_SETUP,
+  PROF_PCG_SPMV,
+  PROF_PCG_UPDATE,
+  PROF_PCG_DIRECTION,
+  PROF_PCG_SOLVE,
+  PROF_N
+};
+
+struct ProfPending {
+  int phase;
+  cudaEvent_t a, b;
+};
+
 struct agipc_handle_s {
   int device = 0;
   int sm_count = 148;
@@ -34,6 +54,47 @@ struct agipc_handle_s {
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
+  // profiling (CUDA events on the launching stream; off by default)
+  bool prof = false;
+  std::vector<ProfPending> prof_pending;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_ms[PROF_N] = {0};
+  int64_t prof_n[PROF_N] = {0};
+};
+
+cudaEvent_t prof_event(agipc_handle h);             // from the pool
+void prof_push(agipc_handle h, int phase, cudaEvent_t a, cudaEvent_t b);
+void prof_add(agipc_handle h, int phase, double ms, int64_t n);
+
+// Records a start event on construction and an end event on destruction (if profiling).
+struct ProfScope {
+  agipc_handle h;
+  int phase;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  ProfScope(agipc_handle h_, int phase_, cudaStream_t s_) : h(h_), phase(phase_), s(s_) {
+    if (getenv("AGIPC_DEBUG")) {
+      cudaError_t e0 = cudaGetLastError();
+      fprintf(stderr, "libagipc[debug] enter phase %d: pending=%s\n", phase, cudaGetErrorString(e0));
+    }
+    if (h->prof) {
+      a = prof_event(h);
+      cudaError_t e = a ? cudaEventRecord(a, s) : cudaErrorInvalidValue;
+      if (e != cudaSuccess) {
+        fprintf(stderr, "libagipc: profiling disabled, cudaEventRecord: %s\n", cudaGetErrorString(e));
+        cudaGetLastError();
+        h->prof = false;
+        a = nullptr;
+      }
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(h);
+      if (b && cudaEventRecord(b, s) == cudaSuccess) prof_push(h, phase, a, b);
+      else cudaGetLastError();
+    }
+  }
 };
 
 agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...);
@@ -55,6 +116,10 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
 #define LAUNCH(h, kernel, grid, block, smem, ...)                                            \
   do {                                                                                       \
     if ((grid) > 0) {                                                                        \
+      cudaError_t _pre = cudaGetLastError();                                                 \
+      if (_pre != cudaSuccess)                                                               \
+        return set_err((h), AGIPC_ECUDA, "pending CUDA error before %s: %s", #kernel,        \
+                       cudaGetErrorString(_pre));                                            \
       kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);                         \
       (h)->launches += 1;                                                                    \
       cudaError_t _e = cudaGetLastError();                                                   \

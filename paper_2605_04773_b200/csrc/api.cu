@@ -57,6 +57,45 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st) {
 
 void pcg_graph_free(PcgGraph *g);  // pcg.cu
 
+cudaEvent_t prof_event(agipc_handle h) {
+  if (!h->prof_pool.empty()) {
+    cudaEvent_t e = h->prof_pool.back();
+    h->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaError_t err = cudaEventCreate(&e);
+  if (err != cudaSuccess) {
+    fprintf(stderr, "libagipc: cudaEventCreate: %s\n", cudaGetErrorString(err));
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+
+void prof_push(agipc_handle h, int phase, cudaEvent_t a, cudaEvent_t b) {
+  h->prof_pending.push_back(ProfPending{phase, a, b});
+}
+
+void prof_add(agipc_handle h, int phase, double ms, int64_t n) {
+  h->prof_ms[phase] += ms;
+  h->prof_n[phase] += n;
+}
+
+static void prof_flush(agipc_handle h) {
+  for (auto &p : h->prof_pending) {
+    cudaEventSynchronize(p.b);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) prof_add(h, p.phase, ms, 1);
+    h->prof_pool.push_back(p.a);
+    h->prof_pool.push_back(p.b);
+  }
+  h->prof_pending.clear();
+}
+
+static const char *kPhaseNames[PROF_N] = {"tag_edges", "build_map", "assemble_coarse", "pcg_setup",
+                                          "pcg_spmv", "pcg_update", "pcg_direction", "pcg_solve"};
+
 extern "C" {
 
 agipc_status agipc_create(agipc_handle *out, int cuda_device) {
@@ -87,6 +126,8 @@ agipc_status agipc_destroy(agipc_handle h) {
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pcg) pcg_graph_free(h->pcg);
+  prof_flush(h);
+  for (auto e : h->prof_pool) cudaEventDestroy(e);
   delete h;
   return AGIPC_OK;
 }
@@ -122,6 +163,31 @@ void agipc_version(int *major, int *minor) {
 }
 
 int64_t agipc_kernel_launches(agipc_handle h) { return h ? h->launches : -1; }
+
+agipc_status agipc_profile(agipc_handle h, int enable) {
+  if (!h) return AGIPC_EINVAL;
+  prof_flush(h);
+  for (int i = 0; i < PROF_N; ++i) {
+    h->prof_ms[i] = 0.0;
+    h->prof_n[i] = 0;
+  }
+  h->prof = enable != 0;
+  return AGIPC_OK;
+}
+
+int agipc_profile_read(agipc_handle h, agipc_profile_entry *out, int cap) {
+  if (!h) return -1;
+  prof_flush(h);
+  int n = 0;
+  for (int i = 0; i < PROF_N && n < cap; ++i) {
+    if (!out) break;
+    snprintf(out[n].name, sizeof(out[n].name), "%s", kPhaseNames[i]);
+    out[n].count = h->prof_n[i];
+    out[n].total_ms = h->prof_ms[i];
+    ++n;
+  }
+  return out ? n : PROF_N;
+}
 
 }  // extern "C"
 

@@ -797,6 +797,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (!map || !mesh->x_rest || !H->row_ptr || !H->col || !H->val || !out->new_map)
     return set_err(h, AGIPC_EINVAL, "assemble_coarse: null pointer");
   CU_TRY(h, cudaSetDevice(h->device));
+  ProfScope prof_scope(h, PROF_ASSEMBLE, h->stream);
   cudaStream_t st_ = h->stream;
   const int64_t nnzb_f = H->nnzb;
   agipc_status st;

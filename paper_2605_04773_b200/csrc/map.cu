@@ -203,6 +203,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   if (!map || !mesh->adj_ptr || (mesh->nnz_adj > 0 && (!mesh->adj_nbr || !slot_tags)))
     return set_err(h, AGIPC_EINVAL, "build_map: null pointer");
   CU_TRY(h, cudaSetDevice(h->device));
+  ProfScope prof_scope(h, PROF_MAP, h->stream);
   GroupGeom geo;
   geo.gs = group_size;
   geo.gpw = 32 / group_size;

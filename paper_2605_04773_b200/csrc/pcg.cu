@@ -11,6 +11,7 @@
 // The host enqueues check_every iterations as one CUDA graph (captured once per system on an
 // internal stream ordered after the caller's stream by events) and polls the done flag.
 #include <cmath>
+#include <vector>
 
 #include "agipc_internal.cuh"
 
@@ -33,10 +34,13 @@ struct PcgGraph {
   int64_t n = -1;
   int chunk = 0;
   int grid = 0;
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;  // profiling: 4 events per iteration of the chunk
 };
 
 void pcg_graph_free(PcgGraph *g) {
   if (!g) return;
+  for (auto e : g->ev) cudaEventDestroy(e);
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->ev_in) cudaEventDestroy(g->ev_in);
   if (g->ev_out) cudaEventDestroy(g->ev_out);
@@ -295,11 +299,15 @@ __global__ void __launch_bounds__(PCG_THREADS) k_direction(int64_t n, const doub
 
 static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int G, int64_t n, const agipc_bsr *A,
                                   double *x, double *r, double *z, double *p, double *q, const double *Dinv,
-                                  double *parts, PcgState *st) {
+                                  double *parts, PcgState *st, cudaEvent_t *ev) {
   for (int k = 0; k < iters; ++k) {
+    if (ev) cudaEventRecordWithFlags(ev[4 * k], s, cudaEventRecordExternal);
     k_spmv_pq<<<G, PCG_THREADS, 0, s>>>(n, A->row_ptr, A->col, A->val, p, q, parts, st);
+    if (ev) cudaEventRecordWithFlags(ev[4 * k + 1], s, cudaEventRecordExternal);
     k_update<<<G, PCG_THREADS, 0, s>>>(n, x, r, z, p, q, Dinv, parts, st);
+    if (ev) cudaEventRecordWithFlags(ev[4 * k + 2], s, cudaEventRecordExternal);
     k_direction<<<G, PCG_THREADS, 0, s>>>(n, z, p, st);
+    if (ev) cudaEventRecordWithFlags(ev[4 * k + 3], s, cudaEventRecordExternal);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg launch: %s", cudaGetErrorString(e));
@@ -319,6 +327,7 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   if (n >= INT32_MAX) return set_err(h, AGIPC_ERANGE, "pcg_solve: too many rows");
   if (check_every <= 0) check_every = 16;
   CU_TRY(h, cudaSetDevice(h->device));
+  ProfScope prof_setup(h, PROF_PCG_SETUP, h->stream);
   WS(h, r, double, "pcg_r", 3 * n);
   WS(h, z, double, "pcg_z", 3 * n);
   WS(h, p, double, "pcg_p", 3 * n);
@@ -354,16 +363,22 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
     }
     const int chunk = std::min(check_every, max_iters);
     const void *key[6] = {A->row_ptr, A->col, A->val, x, r, Dinv};
-    bool same = g->exec && g->n == n && g->chunk == chunk && g->grid == G;
+    bool same = g->exec && g->n == n && g->chunk == chunk && g->grid == G && g->prof == h->prof;
     for (int i = 0; i < 6 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
         cudaGraphExecDestroy(g->exec);
         g->exec = nullptr;
       }
+      while (h->prof && (int)g->ev.size() < 4 * chunk) {
+        cudaEvent_t e;
+        CU_TRY(h, cudaEventCreate(&e));
+        g->ev.push_back(e);
+      }
       cudaGraph_t graph;
       CU_TRY(h, cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
-      agipc_status es = enqueue_iters(h, g->stream, chunk, G, n, A, x, r, z, p, q, Dinv, parts, stp);
+      agipc_status es = enqueue_iters(h, g->stream, chunk, G, n, A, x, r, z, p, q, Dinv, parts, stp,
+                                      h->prof ? g->ev.data() : nullptr);
       cudaError_t ce = cudaStreamEndCapture(g->stream, &graph);
       if (es != AGIPC_OK) return es;
       if (ce != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg capture: %s", cudaGetErrorString(ce));
@@ -372,17 +387,42 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
       g->n = n;
       g->chunk = chunk;
       g->grid = G;
+      g->prof = h->prof;
       for (int i = 0; i < 6; ++i) g->key[i] = key[i];
     }
     CU_TRY(h, cudaEventRecord(g->ev_in, h->stream));
     CU_TRY(h, cudaStreamWaitEvent(g->stream, g->ev_in, 0));
+    ProfScope prof_solve(h, PROF_PCG_SOLVE, g->stream);
     int launched = 0;
+    int it_before = 0;
+    bool first = true;
     while (true) {
       CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
-      h->launches += 3 * chunk;
       launched += chunk;
       CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
       CU_TRY(h, cudaStreamSynchronize(g->stream));
+      if (first) {  // iterations already counted before this solve (none: k_init sets it = 0)
+        first = false;
+      }
+      const int ran = hst->it - it_before;  // K1/K2 launches that did work in this chunk
+      h->launches += 3 * (int64_t)ran;
+      if (h->prof) {
+        const bool conv = hst->done && hst->status == AGIPC_OK && ran > 0;
+        for (int k = 0; k < ran && k < chunk; ++k) {
+          float a = 0.f, b = 0.f, c = 0.f;
+          cudaError_t e1 = cudaEventElapsedTime(&a, g->ev[4 * k], g->ev[4 * k + 1]);
+          if (e1 != cudaSuccess && getenv("AGIPC_DEBUG"))
+            fprintf(stderr, "libagipc[debug] elapsed: %s\n", cudaGetErrorString(e1));
+          cudaEventElapsedTime(&b, g->ev[4 * k + 1], g->ev[4 * k + 2]);
+          prof_add(h, PROF_PCG_SPMV, a, 1);
+          prof_add(h, PROF_PCG_UPDATE, b, 1);
+          if (!(conv && k == ran - 1)) {  // K3 of the converged iteration exits early
+            cudaEventElapsedTime(&c, g->ev[4 * k + 2], g->ev[4 * k + 3]);
+            prof_add(h, PROF_PCG_DIRECTION, c, 1);
+          }
+        }
+      }
+      it_before = hst->it;
       if (hst->done || launched >= max_iters) break;
     }
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));

@@ -141,6 +141,7 @@ extern "C" agipc_status agipc_tag_edges(agipc_handle h, const agipc_mesh *mesh, 
   if (mesh->n_nodes >= INT32_MAX || mesh->nnz_adj >= INT32_MAX)
     return set_err(h, AGIPC_ERANGE, "tag_edges: index exceeds int32");
   CU_TRY(h, cudaSetDevice(h->device));
+  ProfScope prof_scope(h, PROF_TAG, h->stream);
   if (mesh->nnz_adj > 0) CU_TRY(h, cudaMemsetAsync(slot_tags, 1, (size_t)mesh->nnz_adj, h->stream));
   unsigned long long *counters = nullptr;
   if (n_flagged) {
