@@ -34,7 +34,6 @@ enum ProfPhase {
   PROF_PCG_SETUP,
   PROF_PCG_SPMV,
   PROF_PCG_UPDATE,
-  PROF_PCG_DIRECTION,
   PROF_PCG_SOLVE,
   PROF_N
 };

@@ -1,15 +1,22 @@
 // Step 4 -- coarse PCG with 3x3 block-Jacobi (PAPER.md P:752 d_c = -H_c^-1 g_c; P:879 relative
 // residual tolerance; "3x3 block Jacobi"; textbook preconditioned CG, reading R20).
 //
-// Per iteration three kernels, all scalars on the device (no host round trip):
-//   K1  q = A p (one warp per block row, the row's 9*nnz values streamed flat and coalesced)
-//       fused with the partial dot p.q; the last CTA reduces the partials in a fixed order
-//       (deterministic) and computes alpha = rz / pq, or flags EINDEFINITE / EBREAKDOWN;
-//   K2  x += alpha p, r -= alpha q, z = D^-1 r, partial r.z and r.r; the last CTA checks
-//       ||r|| <= tol ||b||, counts the iteration, computes beta;
-//   K3  p = z + beta p.
-// The host enqueues check_every iterations as one CUDA graph (captured once per system on an
-// internal stream ordered after the caller's stream by events) and polls the done flag.
+// B200 design:
+//  * once per solve the BSR matrix is re-laid out for streaming: rows longer than 64 blocks are
+//    split into segments ("virtual rows"), virtual rows are sorted by length inside windows of
+//    4096 and packed 32 per slice (SELL-32-sigma); a slice stores, for each block column j, a
+//    9 x 32 component-major tile of doubles and 32 column ids, so every value load of the SpMV
+//    is one fully used 256-byte line.  The conversion costs one pass over the matrix and is
+//    amortised over the hundreds of iterations of a solve;
+//  * per iteration two kernels, all scalars on the device:
+//      K1  p_new = z + beta p_old formed on the fly for every gathered column (bit-identical to
+//          the value the owner stores), q-segment = A p_new per virtual row (thread per row,
+//          ~30 independent loads in flight), partial p_new.q; the last CTA reduces the partials
+//          in a fixed order and computes alpha or flags EINDEFINITE / EBREAKDOWN;
+//      K2  q = sum of the row's segments (fixed order), x += alpha p, r -= alpha q, z = D^-1 r,
+//          partial r.z and r.r; the last CTA tests ||r|| <= tol ||b|| and computes beta;
+//  * check_every iterations are one CUDA graph on an internal stream (ordered after the caller's
+//    stream by events); the host polls the device done flag between graph launches.
 #include <cmath>
 #include <vector>
 
@@ -17,6 +24,8 @@
 
 #define PCG_THREADS 256
 #define PCG_WARPS (PCG_THREADS / 32)
+#define SEG_MAX 64          // blocks per virtual row
+#define SORT_WIN 4096       // virtual rows per sorting window (sigma = 128 slices)
 
 struct PcgState {
   double rz, alpha, beta, bn2, rr, pq;
@@ -24,18 +33,19 @@ struct PcgState {
   double tol;
   unsigned int arrive;  // last-block counter
   int pad;
+  long long nv, ns, sell_blocks;  // virtual rows, slices, stored SELL blocks (incl. padding)
 };
 
 struct PcgGraph {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  const void *key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  int64_t n = -1;
+  const void *key[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t n = -1, ns = -1;
   int chunk = 0;
-  int grid = 0;
+  int grid1 = 0, grid2 = 0;
   bool prof = false;
-  std::vector<cudaEvent_t> ev;  // profiling: 4 events per iteration of the chunk
+  std::vector<cudaEvent_t> ev;  // profiling: 3 events per iteration of the chunk
 };
 
 void pcg_graph_free(PcgGraph *g) {
@@ -85,30 +95,6 @@ __device__ __forceinline__ double reduce_parts(const double *parts, int nparts, 
   return block_sum(v, s_red);
 }
 
-// y_r = (A x)_r for the row handled by this warp (all lanes receive the 3 sums)
-__device__ __forceinline__ void row_spmv(const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                         const double *__restrict__ val, const double *__restrict__ x, int64_t r,
-                                         double &y0, double &y1, double &y2) {
-  const int l = lane_id();
-  const int64_t k0 = rp[r], k1 = rp[r + 1];
-  const int64_t ne = 9 * (k1 - k0);
-  const double *v = val + 9 * k0;
-  const int32_t *c = col + k0;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int64_t e = l; e < ne; e += 32) {
-    const int blk = (int)(e / 9);
-    const int rem = (int)(e - 9 * (int64_t)blk);
-    const int ii = rem / 3, jj = rem - 3 * ii;
-    const double prod = __ldcs(v + e) * __ldg(x + 3 * (int64_t)__ldg(c + blk) + jj);
-    a0 += ii == 0 ? prod : 0.0;
-    a1 += ii == 1 ? prod : 0.0;
-    a2 += ii == 2 ? prod : 0.0;
-  }
-  y0 = warp_sum(a0);
-  y1 = warp_sum(a1);
-  y2 = warp_sum(a2);
-}
-
 __device__ __forceinline__ void dinv_apply(const double *__restrict__ D, const double r0, const double r1,
                                            const double r2, double &z0, double &z1, double &z2) {
   z0 = D[0] * r0 + D[1] * r1 + D[2] * r2;
@@ -116,6 +102,9 @@ __device__ __forceinline__ void dinv_apply(const double *__restrict__ D, const d
   z2 = D[6] * r0 + D[7] * r1 + D[8] * r2;
 }
 
+// ------------------------------------------------------------------------------------
+// setup: block-Jacobi and the SELL layout
+// ------------------------------------------------------------------------------------
 // D^-1 of every row's 3x3 diagonal block (adjugate / determinant).
 __global__ void k_dinv(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                        const double *__restrict__ val, double *__restrict__ Dinv, PcgState *st) {
@@ -150,7 +139,136 @@ __global__ void k_dinv(int64_t n, const int64_t *__restrict__ rp, const int32_t 
   for (int i = 0; i < 9; ++i) Dinv[9 * r + i] = M[i];
 }
 
-// r = b - A x; z = D^-1 r; p = z; rz = r.z, rr = r.r, bb = b.b
+__global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rp, int32_t *__restrict__ nseg) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) {
+    int64_t len = rp[r + 1] - rp[r];
+    nseg[r] = len <= SEG_MAX ? 1 : (int32_t)((len + SEG_MAX - 1) / SEG_MAX);
+  }
+}
+
+// virtual row v = segment k of row r: blocks [rp[r] + 64k, ...) of length <= 64
+__global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ vr_ptr,
+                           int32_t *__restrict__ v_row, int32_t *__restrict__ v_len, PcgState *st) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) st->nv = vr_ptr[n];
+  if (r < n) {
+    const int64_t len = rp[r + 1] - rp[r];
+    const int64_t v0 = vr_ptr[r], nv = vr_ptr[r + 1] - v0;
+    for (int64_t k = 0; k < nv; ++k) {
+      v_row[v0 + k] = (int32_t)r;
+      v_len[v0 + k] = (int32_t)min((int64_t)SEG_MAX, len - SEG_MAX * k);
+    }
+  }
+}
+
+// sort the virtual rows of each window by decreasing length (ties: ascending id)
+__global__ void __launch_bounds__(1024) k_window_sort(const PcgState *st, const int32_t *__restrict__ v_len,
+                                                      int32_t *__restrict__ perm) {
+  __shared__ unsigned long long s_key[SORT_WIN];
+  const long long nv = st->nv;
+  const long long w0 = (long long)blockIdx.x * SORT_WIN;
+  if (w0 >= nv) return;
+  for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+    long long v = w0 + i;
+    s_key[i] = v < nv ? ((unsigned long long)(SEG_MAX - v_len[v]) << 32) | (unsigned long long)i : ~0ull;
+  }
+  __syncthreads();
+  for (int k = 2; k <= SORT_WIN; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          unsigned long long a = s_key[i], b = s_key[ixj];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            s_key[i] = b;
+            s_key[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+    long long v = w0 + i;
+    if (v < nv) perm[v] = (int32_t)(w0 + (long long)(s_key[i] & 0xffffffffull));
+  }
+}
+
+// slice length (x32, for the scan) = longest virtual row among the slice's 32
+__global__ void k_slice_len(int64_t ns_bound, const PcgState *st, const int32_t *__restrict__ perm,
+                            const int32_t *__restrict__ v_len, int32_t *__restrict__ slen) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nv = st->nv;
+  if (s < ns_bound) {
+    int L = 0;
+    for (int t = 0; t < 32 && 32 * s + t < nv; ++t) L = max(L, v_len[perm[32 * s + t]]);
+    slen[s] = 32 * L;
+  }
+}
+
+// processing order of the slices: longest first (LPT), via a counting sort over lengths 0..64
+__global__ void __launch_bounds__(1024) k_slice_order(const PcgState *st, const int32_t *__restrict__ slen,
+                                                      int32_t *__restrict__ order) {
+  __shared__ int s_cnt[SEG_MAX + 2];
+  __shared__ int s_off[SEG_MAX + 2];
+  const long long ns = st->ns;
+  for (int i = threadIdx.x; i < SEG_MAX + 2; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  for (long long s = threadIdx.x; s < ns; s += blockDim.x) atomicAdd(&s_cnt[SEG_MAX - slen[s] / 32], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < SEG_MAX + 2; ++i) {
+      s_off[i] = run;
+      run += s_cnt[i];
+    }
+  }
+  __syncthreads();
+  for (long long s = threadIdx.x; s < ns; s += blockDim.x) order[atomicAdd(&s_off[SEG_MAX - slen[s] / 32], 1)] = (int32_t)s;
+}
+
+__global__ void k_sell_scalars(int64_t ns_bound, const int64_t *__restrict__ sptr, PcgState *st) {
+  st->ns = (st->nv + 31) / 32;
+  st->sell_blocks = sptr[ns_bound];
+}
+
+// warp per slice: component-major tiles; padding = zero blocks pointing at the row itself
+__global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                            const double *__restrict__ val, const int64_t *__restrict__ vr_ptr,
+                            const int32_t *__restrict__ perm, const int32_t *__restrict__ v_row,
+                            const int32_t *__restrict__ v_len, const int64_t *__restrict__ sptr,
+                            int32_t *__restrict__ scol, double *__restrict__ sval, int32_t *__restrict__ s_vrow) {
+  const long long ns = st->ns, nv = st->nv;
+  const int l = lane_id();
+  for (long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < ns;
+       s += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long vi = 32 * s + l;
+    const int v = vi < nv ? perm[vi] : -1;
+    s_vrow[vi] = v;
+    int row = 0, len = 0;
+    long long k0 = 0;
+    if (v >= 0) {
+      row = v_row[v];
+      len = v_len[v];
+      k0 = rp[row] + (long long)SEG_MAX * (v - vr_ptr[row]);
+    }
+    const long long base = sptr[s];
+    const int L = (int)((sptr[s + 1] - base) / 32);
+    for (int j = 0; j < L; ++j) {
+      const long long t = base + 32LL * j;
+      const bool real = j < len;
+      scol[t + l] = real ? col[k0 + j] : row;
+      double *dst = sval + 9 * t + l;
+      const double *src = val + 9 * (k0 + j);
+#pragma unroll
+      for (int e = 0; e < 9; ++e) dst[32 * e] = real ? src[e] : 0.0;
+    }
+  }
+}
+
+// r = b - A x (or b); z = D^-1 r; rz = r.z, rr = r.r, bb = b.b; p_old = 0 and beta = 0, so the
+// first K1 forms p = z exactly
 __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *__restrict__ rp,
                                                       const int32_t *__restrict__ col, const double *__restrict__ val,
                                                       const double *__restrict__ b, double *__restrict__ x,
@@ -162,7 +280,19 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
   double rz = 0.0, rr = 0.0, bb = 0.0;
   for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + w; row < n; row += (int64_t)gridDim.x * PCG_WARPS) {
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    if (!zero_x0) row_spmv(rp, col, val, x, row, y0, y1, y2);
+    if (!zero_x0) {  // (A x)_row, one warp, flat over the row's values
+      const int64_t k0 = rp[row], ne = 9 * (rp[row + 1] - k0);
+      for (int64_t e = l; e < ne; e += 32) {
+        const int blk = (int)(e / 9), rem = (int)(e - 9 * (int64_t)blk), ii = rem / 3, jj = rem - 3 * ii;
+        const double prod = val[9 * k0 + e] * x[3 * (int64_t)col[k0 + blk] + jj];
+        y0 += ii == 0 ? prod : 0.0;
+        y1 += ii == 1 ? prod : 0.0;
+        y2 += ii == 2 ? prod : 0.0;
+      }
+      y0 = warp_sum(y0);
+      y1 = warp_sum(y1);
+      y2 = warp_sum(y2);
+    }
     if (l == 0) {
       if (zero_x0) {
         x[3 * row] = 0.0; x[3 * row + 1] = 0.0; x[3 * row + 2] = 0.0;
@@ -173,7 +303,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
       dinv_apply(Dinv + 9 * row, r0, r1, r2, z0, z1, z2);
       r[3 * row] = r0; r[3 * row + 1] = r1; r[3 * row + 2] = r2;
       z[3 * row] = z0; z[3 * row + 1] = z1; z[3 * row + 2] = z2;
-      p[3 * row] = z0; p[3 * row + 1] = z1; p[3 * row + 2] = z2;
+      p[3 * row] = 0.0; p[3 * row + 1] = 0.0; p[3 * row + 2] = 0.0;
       rz += r0 * z0 + r1 * z1 + r2 * z2;
       rr += r0 * r0 + r1 * r1 + r2 * r2;
       bb += b0 * b0 + b1 * b1 + b2 * b2;
@@ -197,26 +327,92 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
       st->rr = RR;
       st->bn2 = BB;
       st->it = 0;
+      st->beta = 0.0;
       if (!st->done && sqrt(RR) <= st->tol * sqrt(BB)) st->done = 1;
     }
   }
 }
 
-// K1: q = A p, pq partials; last CTA: alpha
-__global__ void __launch_bounds__(PCG_THREADS) k_spmv_pq(int64_t n, const int64_t *__restrict__ rp,
-                                                         const int32_t *__restrict__ col,
-                                                         const double *__restrict__ val, const double *__restrict__ p,
-                                                         double *__restrict__ q, double *parts, PcgState *st) {
+// ------------------------------------------------------------------------------------
+// K1: SELL SpMV, thread per virtual row, fused p update and p.q
+// ------------------------------------------------------------------------------------
+// loads of one 3x3 block column tile (9 values) and its gathered p_new = z + beta p_old entries
+struct BlkLoad {
+  double m[9], z[3], p[3];
+};
+__device__ __forceinline__ void blk_load(BlkLoad &b, const double *__restrict__ v0, int64_t c0,
+                                         const double *__restrict__ z, const double *__restrict__ pold) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) b.m[e] = __ldcs(v0 + 32 * e);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    b.z[k] = __ldg(z + c0 + k);
+    b.p[k] = __ldg(pold + c0 + k);
+  }
+}
+__device__ __forceinline__ void blk_fma(const BlkLoad &b, double beta, double &a0, double &a1, double &a2) {
+  const double x0 = b.z[0] + beta * b.p[0], x1 = b.z[1] + beta * b.p[1], x2 = b.z[2] + beta * b.p[2];
+  a0 += b.m[0] * x0 + b.m[1] * x1 + b.m[2] * x2;
+  a1 += b.m[3] * x0 + b.m[4] * x1 + b.m[5] * x2;
+  a2 += b.m[6] * x0 + b.m[7] * x1 + b.m[8] * x2;
+}
+
+// Persistent grid (resident CTAs only); every warp repeatedly claims the next slice of the
+// longest-first order from counter[parity] (reset by K2 for the next iteration).
+__global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__restrict__ sptr,
+                                                           const int32_t *__restrict__ scol,
+                                                           const double *__restrict__ sval,
+                                                           const int32_t *__restrict__ s_vrow,
+                                                           const int32_t *__restrict__ order,
+                                                           const int32_t *__restrict__ v_row,
+                                                           const int64_t *__restrict__ vr_ptr,
+                                                           const double *__restrict__ z, const double *__restrict__ pold,
+                                                           double *__restrict__ pnew, double *__restrict__ qseg,
+                                                           int *counter, double *parts, PcgState *st) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
-  const int w = threadIdx.x >> 5, l = lane_id();
+  const double beta = st->beta;
+  const long long ns = st->ns;
+  const int l = lane_id();
   double pq = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + w; row < n; row += (int64_t)gridDim.x * PCG_WARPS) {
-    double y0, y1, y2;
-    row_spmv(rp, col, val, p, row, y0, y1, y2);
-    if (l == 0) {
-      q[3 * row] = y0; q[3 * row + 1] = y1; q[3 * row + 2] = y2;
-      pq += p[3 * row] * y0 + p[3 * row + 1] * y1 + p[3 * row + 2] * y2;
+  while (true) {
+    int si = 0;
+    if (l == 0) si = atomicAdd(counter, 1);
+    si = __shfl_sync(FULL_MASK, si, 0);
+    if (si >= ns) break;
+    const long long s = order[si];
+    const long long base = sptr[s];
+    const int L = (int)((sptr[s + 1] - base) >> 5);
+    const int32_t *cp = scol + base + l;
+    const double *vp = sval + 9 * base + l;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    int64_t n0 = L > 0 ? 3 * (int64_t)__ldcs(cp) : 0, n1 = L > 1 ? 3 * (int64_t)__ldcs(cp + 32) : 0;
+    int j = 0;
+    for (; j + 1 < L; j += 2) {
+      BlkLoad b0, b1;  // all 30 loads of the pair are issued before any FMA
+      blk_load(b0, vp + 288 * (int64_t)j, n0, z, pold);
+      blk_load(b1, vp + 288 * (int64_t)(j + 1), n1, z, pold);
+      if (j + 2 < L) n0 = 3 * (int64_t)__ldcs(cp + 32 * (j + 2));  // prefetch the next pair's columns
+      if (j + 3 < L) n1 = 3 * (int64_t)__ldcs(cp + 32 * (j + 3));
+      blk_fma(b0, beta, a0, a1, a2);
+      blk_fma(b1, beta, a0, a1, a2);
+    }
+    if (j < L) {
+      BlkLoad b0;
+      blk_load(b0, vp + 288 * (int64_t)j, n0, z, pold);
+      blk_fma(b0, beta, a0, a1, a2);
+    }
+    const int v = s_vrow[32 * s + l];
+    if (v >= 0) {
+      const int64_t row = v_row[v];
+      const int64_t i = 3 * row;
+      const double pn0 = z[i] + beta * pold[i], pn1 = z[i + 1] + beta * pold[i + 1],
+                   pn2 = z[i + 2] + beta * pold[i + 2];
+      if (vr_ptr[row] == v) {  // the first segment stores the row's new direction
+        pnew[i] = pn0; pnew[i + 1] = pn1; pnew[i + 2] = pn2;
+      }
+      qseg[3 * (int64_t)v] = a0; qseg[3 * (int64_t)v + 1] = a1; qseg[3 * (int64_t)v + 2] = a2;
+      pq += pn0 * a0 + pn1 * a1 + pn2 * a2;  // p.q is linear in the segments
     }
   }
   pq = block_sum(pq, s_red);
@@ -240,24 +436,36 @@ __global__ void __launch_bounds__(PCG_THREADS) k_spmv_pq(int64_t n, const int64_
   }
 }
 
-// K2: x += alpha p; r -= alpha q; z = D^-1 r; partial rz, rr; last CTA: convergence, beta
-__global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+// K2: thread per slot; q = sum of the row's segments (fixed order); x += alpha p; r -= alpha q;
+// z = D^-1 r; last CTA: ||r|| <= tol ||b||, iteration count, beta.
+__global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t *__restrict__ vr_ptr,
+                                                        double *__restrict__ x, double *__restrict__ r,
                                                         double *__restrict__ z, const double *__restrict__ p,
-                                                        const double *__restrict__ q, const double *__restrict__ Dinv,
+                                                        const double *__restrict__ qseg,
+                                                        const double *__restrict__ Dinv, int *next_counter,
                                                         double *parts, PcgState *st) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double alpha = st->alpha;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *next_counter = 0;
   double rz = 0.0, rr = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * PCG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * PCG_THREADS) {
-    double p0 = p[3 * i], p1 = p[3 * i + 1], p2 = p[3 * i + 2];
-    double q0 = q[3 * i], q1 = q[3 * i + 1], q2 = q[3 * i + 2];
-    x[3 * i] += alpha * p0; x[3 * i + 1] += alpha * p1; x[3 * i + 2] += alpha * p2;
-    double r0 = r[3 * i] - alpha * q0, r1 = r[3 * i + 1] - alpha * q1, r2 = r[3 * i + 2] - alpha * q2;
-    r[3 * i] = r0; r[3 * i + 1] = r1; r[3 * i + 2] = r2;
+    const int64_t v0 = vr_ptr[i], v1 = vr_ptr[i + 1];
+    double q0 = qseg[3 * v0], q1 = qseg[3 * v0 + 1], q2 = qseg[3 * v0 + 2];
+    for (int64_t v = v0 + 1; v < v1; ++v) {
+      q0 += qseg[3 * v];
+      q1 += qseg[3 * v + 1];
+      q2 += qseg[3 * v + 2];
+    }
+    const int64_t k = 3 * i;
+    x[k] += alpha * p[k];
+    x[k + 1] += alpha * p[k + 1];
+    x[k + 2] += alpha * p[k + 2];
+    const double r0 = r[k] - alpha * q0, r1 = r[k + 1] - alpha * q1, r2 = r[k + 2] - alpha * q2;
+    r[k] = r0; r[k + 1] = r1; r[k + 2] = r2;
     double z0, z1, z2;
     dinv_apply(Dinv + 9 * i, r0, r1, r2, z0, z1, z2);
-    z[3 * i] = z0; z[3 * i + 1] = z1; z[3 * i + 2] = z2;
+    z[k] = z0; z[k + 1] = z1; z[k + 2] = z2;
     rz += r0 * z0 + r1 * z1 + r2 * z2;
     rr += r0 * r0 + r1 * r1 + r2 * r2;
   }
@@ -288,26 +496,33 @@ __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, double *__res
   }
 }
 
-// K3: p = z + beta p
-__global__ void __launch_bounds__(PCG_THREADS) k_direction(int64_t n, const double *__restrict__ z,
-                                                           double *__restrict__ p, const PcgState *st) {
-  if (*(volatile const int *)&st->done) return;
-  const double beta = st->beta;
-  for (int64_t i = (int64_t)blockIdx.x * PCG_THREADS + threadIdx.x; i < 3 * n; i += (int64_t)gridDim.x * PCG_THREADS)
-    p[i] = z[i] + beta * p[i];
+__global__ void k_copy_out(int64_t n3, const double *__restrict__ src, double *__restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) dst[i] = src[i];
 }
 
-static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int G, int64_t n, const agipc_bsr *A,
-                                  double *x, double *r, double *z, double *p, double *q, const double *Dinv,
-                                  double *parts, PcgState *st, cudaEvent_t *ev) {
+struct PcgBufs {
+  double *x, *r, *z, *P[2], *qseg, *Dinv, *parts, *sval;
+  int64_t *vr_ptr, *sptr;
+  int32_t *v_row, *v_len, *perm, *scol, *s_vrow, *order;
+  int *counters;  // two slice counters, used by alternate iterations
+  PcgState *st;
+  int64_t ns_bound;
+  int G1, G2;
+};
+
+// iteration j reads p_old = P[j&1] and writes p_new = P[(j+1)&1] (the chunk length is even)
+static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int64_t n, const PcgBufs &B,
+                                  cudaEvent_t *ev) {
   for (int k = 0; k < iters; ++k) {
-    if (ev) cudaEventRecordWithFlags(ev[4 * k], s, cudaEventRecordExternal);
-    k_spmv_pq<<<G, PCG_THREADS, 0, s>>>(n, A->row_ptr, A->col, A->val, p, q, parts, st);
-    if (ev) cudaEventRecordWithFlags(ev[4 * k + 1], s, cudaEventRecordExternal);
-    k_update<<<G, PCG_THREADS, 0, s>>>(n, x, r, z, p, q, Dinv, parts, st);
-    if (ev) cudaEventRecordWithFlags(ev[4 * k + 2], s, cudaEventRecordExternal);
-    k_direction<<<G, PCG_THREADS, 0, s>>>(n, z, p, st);
-    if (ev) cudaEventRecordWithFlags(ev[4 * k + 3], s, cudaEventRecordExternal);
+    double *pold = B.P[k & 1], *pnew = B.P[(k + 1) & 1];
+    if (ev) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
+    k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z, pold,
+                                             pnew, B.qseg, B.counters + (k & 1), B.parts, B.st);
+    if (ev) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
+    k_update<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
+                                          B.parts, B.st);
+    if (ev) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg launch: %s", cudaGetErrorString(e));
@@ -324,36 +539,78 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   memset(stats, 0, sizeof(*stats));
   if (n == 0) return AGIPC_OK;
   if (!A->row_ptr || !A->col || !A->val || !b || !x) return set_err(h, AGIPC_EINVAL, "pcg_solve: null pointer");
-  if (n >= INT32_MAX) return set_err(h, AGIPC_ERANGE, "pcg_solve: too many rows");
+  if (n >= INT32_MAX / 4 || A->nnzb >= ((int64_t)1 << 40)) return set_err(h, AGIPC_ERANGE, "pcg_solve: too large");
   if (check_every <= 0) check_every = 16;
   CU_TRY(h, cudaSetDevice(h->device));
-  ProfScope prof_setup(h, PROF_PCG_SETUP, h->stream);
-  WS(h, r, double, "pcg_r", 3 * n);
-  WS(h, z, double, "pcg_z", 3 * n);
-  WS(h, p, double, "pcg_p", 3 * n);
-  WS(h, q, double, "pcg_q", 3 * n);
-  WS(h, Dinv, double, "pcg_dinv", 9 * n);
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
-  WS(h, parts, double, "pcg_parts", 3 * G);
-  WS(h, stp, PcgState, "pcg_state", 1);
-  PcgState init;
-  memset(&init, 0, sizeof(init));
-  init.tol = rel_tol;
-  init.max_iters = max_iters;
-  init.status = AGIPC_OK;
+  cudaStream_t s0 = h->stream;
   agipc_status ast;
   PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
   if (ast != AGIPC_OK) return ast;
-  *hst = init;
-  CU_TRY(h, cudaMemcpyAsync(stp, hst, sizeof(PcgState), cudaMemcpyHostToDevice, h->stream));
-  LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, Dinv, stp);
-  LAUNCH(h, k_init, (unsigned)G, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, x, Dinv, r, z, p, parts, stp,
-         zero_x0);
+  PcgBufs B;
+  const int64_t nv_bound = n + A->nnzb / SEG_MAX + 1;  // virtual rows
+  B.ns_bound = cdiv(nv_bound, 32);
+  {
+    WS(h, xw, double, "pcg_x", 3 * n + 2); B.x = xw;
+    WS(h, r, double, "pcg_r", 3 * n + 2); B.r = r;
+    WS(h, z, double, "pcg_z", 3 * n + 2); B.z = z;
+    WS(h, p0, double, "pcg_p0", 3 * n + 2); B.P[0] = p0;
+    WS(h, p1, double, "pcg_p1", 3 * n + 2); B.P[1] = p1;
+    WS(h, qs, double, "pcg_qseg", 3 * nv_bound + 2); B.qseg = qs;
+    WS(h, Dinv, double, "pcg_dinv", 9 * n + 2); B.Dinv = Dinv;
+    WS(h, vr, int64_t, "pcg_vr_ptr", n + 1); B.vr_ptr = vr;
+    WS(h, nseg, int32_t, "pcg_nseg", n);
+    WS(h, vrow, int32_t, "pcg_v_row", nv_bound); B.v_row = vrow;
+    WS(h, vlen, int32_t, "pcg_v_len", nv_bound); B.v_len = vlen;
+    WS(h, perm, int32_t, "pcg_perm", nv_bound); B.perm = perm;
+    WS(h, slen, int32_t, "pcg_slen", B.ns_bound);
+    WS(h, sptr, int64_t, "pcg_sptr", B.ns_bound + 1); B.sptr = sptr;
+    WS(h, svr, int32_t, "pcg_s_vrow", 32 * B.ns_bound); B.s_vrow = svr;
+    WS(h, stp, PcgState, "pcg_state", 1); B.st = stp;
+    WS(h, order, int32_t, "pcg_order", B.ns_bound); B.order = order;
+    WS(h, ctr, int, "pcg_counters", 2); B.counters = ctr;
+    int occ = 0;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
+    B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
+    B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 4 * (int64_t)h->sm_count));
+    const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
+    const int Gp = std::max(std::max(B.G1, B.G2), Gi);
+    WS(h, parts, double, "pcg_parts", 3 * Gp); B.parts = parts;
+    PcgState init;
+    memset(&init, 0, sizeof(init));
+    init.tol = rel_tol;
+    init.max_iters = max_iters;
+    init.status = AGIPC_OK;
+    *hst = init;
+    ProfScope prof_setup(h, PROF_PCG_SETUP, s0);
+    CU_TRY(h, cudaMemcpyAsync(stp, hst, sizeof(PcgState), cudaMemcpyHostToDevice, s0));
+    if (!zero_x0) CU_TRY(h, cudaMemcpyAsync(B.x, x, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s0));
+    LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp);
+    // SELL layout (once per solve)
+    LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, nseg);
+    agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
+    if (sst != AGIPC_OK) return sst;
+    LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, B.vr_ptr, B.v_row, B.v_len, stp);
+    LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, SORT_WIN), 1024, 0, stp, B.v_len, B.perm);
+    LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
+    sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
+    if (sst != AGIPC_OK) return sst;
+    LAUNCH(h, k_sell_scalars, 1, 1, 0, B.ns_bound, B.sptr, stp);
+    LAUNCH(h, k_slice_order, 1, 1024, 0, stp, slen, B.order);
+    CU_TRY(h, cudaMemsetAsync(B.counters, 0, 2 * sizeof(int), s0));
+    CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+    CU_TRY(h, cudaStreamSynchronize(s0));
+    const long long sell_blocks = hst->sell_blocks;
+    WS(h, scol, int32_t, "pcg_scol", sell_blocks + 32); B.scol = scol;
+    WS(h, sval, double, "pcg_sval", 9 * sell_blocks + 288); B.sval = sval;
+    LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
+           0, stp, A->row_ptr, A->col, A->val, B.vr_ptr, B.perm, B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
+    LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
+           parts, stp, zero_x0);
+  }
   if (max_iters == 0) {
-    CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
-    CU_TRY(h, cudaStreamSynchronize(h->stream));
+    CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+    CU_TRY(h, cudaStreamSynchronize(s0));
   } else {
-    // chunk graph on an internal stream, ordered after the caller's stream
     PcgGraph *g = h->pcg;
     if (!g) {
       g = h->pcg = new PcgGraph();
@@ -361,73 +618,67 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
       CU_TRY(h, cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
       CU_TRY(h, cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming));
     }
-    const int chunk = std::min(check_every, max_iters);
-    const void *key[6] = {A->row_ptr, A->col, A->val, x, r, Dinv};
-    bool same = g->exec && g->n == n && g->chunk == chunk && g->grid == G && g->prof == h->prof;
-    for (int i = 0; i < 6 && same; ++i) same = g->key[i] == key[i];
+    int chunk = std::max(2, std::min(check_every, max_iters));
+    chunk += chunk & 1;  // even: the p ping-pong parity is the same at every graph launch
+    const void *key[8] = {B.sval, B.scol, B.x, B.qseg, B.Dinv, B.sptr, B.P[0], B.parts};
+    bool same = g->exec && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
+                g->grid2 == B.G2 && g->prof == h->prof;
+    for (int i = 0; i < 8 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
         cudaGraphExecDestroy(g->exec);
         g->exec = nullptr;
       }
-      while (h->prof && (int)g->ev.size() < 4 * chunk) {
+      while (h->prof && (int)g->ev.size() < 3 * chunk) {
         cudaEvent_t e;
         CU_TRY(h, cudaEventCreate(&e));
         g->ev.push_back(e);
       }
       cudaGraph_t graph;
       CU_TRY(h, cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
-      agipc_status es = enqueue_iters(h, g->stream, chunk, G, n, A, x, r, z, p, q, Dinv, parts, stp,
-                                      h->prof ? g->ev.data() : nullptr);
+      agipc_status es = enqueue_iters(h, g->stream, chunk, n, B, h->prof ? g->ev.data() : nullptr);
       cudaError_t ce = cudaStreamEndCapture(g->stream, &graph);
       if (es != AGIPC_OK) return es;
       if (ce != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg capture: %s", cudaGetErrorString(ce));
       CU_TRY(h, cudaGraphInstantiate(&g->exec, graph, 0));
       cudaGraphDestroy(graph);
       g->n = n;
+      g->ns = B.ns_bound;
       g->chunk = chunk;
-      g->grid = G;
+      g->grid1 = B.G1;
+      g->grid2 = B.G2;
       g->prof = h->prof;
-      for (int i = 0; i < 6; ++i) g->key[i] = key[i];
+      for (int i = 0; i < 8; ++i) g->key[i] = key[i];
     }
-    CU_TRY(h, cudaEventRecord(g->ev_in, h->stream));
+    CU_TRY(h, cudaEventRecord(g->ev_in, s0));
     CU_TRY(h, cudaStreamWaitEvent(g->stream, g->ev_in, 0));
-    ProfScope prof_solve(h, PROF_PCG_SOLVE, g->stream);
-    int launched = 0;
-    int it_before = 0;
-    bool first = true;
-    while (true) {
-      CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
-      launched += chunk;
-      CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
-      CU_TRY(h, cudaStreamSynchronize(g->stream));
-      if (first) {  // iterations already counted before this solve (none: k_init sets it = 0)
-        first = false;
-      }
-      const int ran = hst->it - it_before;  // K1/K2 launches that did work in this chunk
-      h->launches += 3 * (int64_t)ran;
-      if (h->prof) {
-        const bool conv = hst->done && hst->status == AGIPC_OK && ran > 0;
-        for (int k = 0; k < ran && k < chunk; ++k) {
-          float a = 0.f, b = 0.f, c = 0.f;
-          cudaError_t e1 = cudaEventElapsedTime(&a, g->ev[4 * k], g->ev[4 * k + 1]);
-          if (e1 != cudaSuccess && getenv("AGIPC_DEBUG"))
-            fprintf(stderr, "libagipc[debug] elapsed: %s\n", cudaGetErrorString(e1));
-          cudaEventElapsedTime(&b, g->ev[4 * k + 1], g->ev[4 * k + 2]);
-          prof_add(h, PROF_PCG_SPMV, a, 1);
-          prof_add(h, PROF_PCG_UPDATE, b, 1);
-          if (!(conv && k == ran - 1)) {  // K3 of the converged iteration exits early
-            cudaEventElapsedTime(&c, g->ev[4 * k + 2], g->ev[4 * k + 3]);
-            prof_add(h, PROF_PCG_DIRECTION, c, 1);
+    {
+      ProfScope prof_solve(h, PROF_PCG_SOLVE, g->stream);
+      int launched = 0, it_before = 0;
+      while (true) {
+        CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
+        launched += chunk;
+        CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
+        CU_TRY(h, cudaStreamSynchronize(g->stream));
+        const int ran = hst->it - it_before;  // iterations whose K1/K2 did work in this chunk
+        h->launches += 2 * (int64_t)ran;
+        if (h->prof) {
+          for (int k = 0; k < ran && k < chunk; ++k) {
+            float a = 0.f, b2 = 0.f;
+            if (cudaEventElapsedTime(&a, g->ev[3 * k], g->ev[3 * k + 1]) == cudaSuccess) prof_add(h, PROF_PCG_SPMV, a, 1);
+            if (cudaEventElapsedTime(&b2, g->ev[3 * k + 1], g->ev[3 * k + 2]) == cudaSuccess)
+              prof_add(h, PROF_PCG_UPDATE, b2, 1);
           }
+          cudaGetLastError();
         }
+        it_before = hst->it;
+        if (hst->done || launched >= max_iters) break;
       }
-      it_before = hst->it;
-      if (hst->done || launched >= max_iters) break;
     }
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
-    CU_TRY(h, cudaStreamWaitEvent(h->stream, g->ev_out, 0));
+    CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
   }
+  LAUNCH(h, k_copy_out, (unsigned)cdiv(3 * n, 256), 256, 0, 3 * n, B.x, x);
   stats->iters = hst->it;
   stats->status = hst->done ? hst->status : AGIPC_NOT_CONVERGED;
   stats->b_norm = sqrt(hst->bn2);
