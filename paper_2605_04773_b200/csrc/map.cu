@@ -12,40 +12,50 @@
 //    (P:86, P:222 -- reading R1, which corrects the lane_id of P:183-184);
 //  * the ExclusiveSum over per-group counts is fused into the same kernel with a
 //    single-pass decoupled look-back over CTA tiles, and map = O[g] + P;
-//  * level >= 1: the surviving tagged edges mapped through the level map (self loops
-//    dropped) are the next level's graph; their intra-group part is OR-ed into per-node
-//    hashes with atomicOr, then the same group kernel runs.  The final map composes the
-//    level maps; the recursion stops at the first level without an intra-group edge.
+//  * level >= 1 runs in ONE cooperative persistent kernel: per level, the surviving
+//    tagged edges (mapped through the previous level, self loops dropped) OR their intra-group
+//    part into per-node hashes (atomicOr), a grid barrier, the same group pass, a barrier, the
+//    edge remap + compaction and the composition of the level maps, a barrier.  No host round
+//    trip per level; the recursion stops at the first level without an intra-group edge.
+#include <cooperative_groups.h>
+
 #include "agipc_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 #define MAP_THREADS 256
 #define MAP_WARPS (MAP_THREADS / 32)
 
 struct GroupGeom {
-  int gs;         // group size 1..32
-  int gpw;        // groups per warp = 32 / gs
-  unsigned gmask; // low gs bits
+  int gs;          // group size 1..32
+  int gpw;         // groups per warp = 32 / gs
+  unsigned gmask;  // low gs bits
 };
 
-// One level of Alg S1/S2 over n nodes.  FROM_CSR: level 0 (hash from adjacency + tags, emits
-// tagged cross-group edges); otherwise the intra-group hashes come from h_mem.
+struct TileSmem {
+  int tile;
+  long long warp[MAP_WARPS];
+  long long prefix;
+};
+
+__device__ __forceinline__ int64_t tiles_of(int64_t n, const GroupGeom &geo) {
+  return (((n + geo.gs - 1) / geo.gs) + (int64_t)MAP_WARPS * geo.gpw - 1) / ((int64_t)MAP_WARPS * geo.gpw);
+}
+
+// One CTA tile of one level of Alg S1/S2 over n nodes.  FROM_CSR: level 0 (hash from adjacency
+// + tags, emits the tagged cross-group edges); otherwise the intra-group hashes come from h_mem
+// (which is cleared after it is read, ready for the next level).
 template <bool FROM_CSR>
-__global__ void __launch_bounds__(MAP_THREADS)
-    k_group_pass(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr,
-                 const int32_t *__restrict__ adj_nbr, const uint8_t *__restrict__ tags,
-                 const uint32_t *__restrict__ h_mem, int32_t *__restrict__ map_out,
-                 int2 *__restrict__ cross, unsigned long long *__restrict__ cross_count,
-                 unsigned long long *status, int *tile_counter, long long *n_out) {
-  __shared__ int s_tile;
-  __shared__ long long s_warp[MAP_WARPS];
-  __shared__ long long s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
-  __syncthreads();
-  const int tile = s_tile;
+__device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles, int64_t n, const GroupGeom &geo,
+                                           const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
+                                           const uint8_t *__restrict__ tags, uint32_t *h_mem,
+                                           int32_t *__restrict__ map_out, int2 *__restrict__ cross,
+                                           unsigned long long *__restrict__ cross_count, unsigned long long *status,
+                                           long long *n_out) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gs = geo.gs;
-  const int gin = lane / gs;                 // group index inside the warp
-  const int lig = lane - gin * gs;           // lane in group (Alg S1 lane_id)
+  const int gin = lane / gs;        // group index inside the warp
+  const int lig = lane - gin * gs;  // lane in group (Alg S1 lane_id)
   const int64_t g = ((int64_t)tile * MAP_WARPS + w) * geo.gpw + gin;
   const int64_t v = g * gs + lig;
   const bool active = (gin < geo.gpw) && (v < n);
@@ -54,11 +64,11 @@ __global__ void __launch_bounds__(MAP_THREADS)
   if (active) {
     h = 1u << lig;  // Alg S1 l.4
     if (FROM_CSR) {
-      int64_t k0 = adj_ptr[v], k1 = adj_ptr[v + 1];
+      const int64_t k0 = adj_ptr[v], k1 = adj_ptr[v + 1];
       int ncross = 0;
       for (int64_t k = k0; k < k1; ++k) {
-        if (!tags[k]) continue;                   // protected edge (Alg S1 l.6-8)
-        int64_t u = adj_nbr[k];
+        if (!tags[k]) continue;  // protected edge (Alg S1 l.6-8)
+        const int64_t u = adj_nbr[k];
         if (u / gs == g) h |= 1u << (int)(u - g * gs);  // same group (l.10-13)
         else if (u > v) ++ncross;
       }
@@ -68,18 +78,19 @@ __global__ void __launch_bounds__(MAP_THREADS)
         int o = 0;
         for (int64_t k = k0; k < k1; ++k) {
           if (!tags[k]) continue;
-          int64_t u = adj_nbr[k];
+          const int64_t u = adj_nbr[k];
           if (u / gs != g && u > v) cross[base + o++] = make_int2((int)v, (int)u);
         }
       }
     } else {
       h |= h_mem[v];
+      h_mem[v] = 0u;
     }
   }
   // Alg S2 OR-propagation == Warshall closure inside the group (registers + shuffles)
   const int base_lane = gin * gs;
   for (int k = 0; k < gs; ++k) {
-    uint32_t t = __shfl_sync(FULL_MASK, h, (base_lane + k) & 31);
+    const uint32_t t = __shfl_sync(FULL_MASK, h, (base_lane + k) & 31);
     if ((h >> k) & 1u) h |= t;
   }
   // election: lowest lane of each component
@@ -90,72 +101,250 @@ __global__ void __launch_bounds__(MAP_THREADS)
   const int first = active ? __ffs(h) - 1 : 0;
   const int local = __popc(gelect & ((1u << first) - 1u));
   const int warp_off = __popc(bal & ((1u << base_lane) - 1u));  // earlier groups of this warp
-  if (lane == 0) s_warp[w] = __popc(bal);
+  if (lane == 0) S.warp[w] = __popc(bal);
   __syncthreads();
   if (w == 0) {
-    long long c = lane < MAP_WARPS ? s_warp[lane] : 0;
-    long long ci = warp_incl_scan(c);
-    long long agg = __shfl_sync(FULL_MASK, ci, MAP_WARPS - 1);
-    if (lane < MAP_WARPS) s_warp[lane] = ci - c;
-    long long pfx = lb_exclusive(status, tile, agg);  // ExclusiveSum over groups
+    const long long c = lane < MAP_WARPS ? S.warp[lane] : 0;
+    const long long ci = warp_incl_scan(c);
+    const long long agg = __shfl_sync(FULL_MASK, ci, MAP_WARPS - 1);
+    if (lane < MAP_WARPS) S.warp[lane] = ci - c;
+    const long long pfx = lb_exclusive(status, tile, agg);  // ExclusiveSum over groups
     if (lane == 0) {
-      s_prefix = pfx;
-      if (tile == (int)gridDim.x - 1) *n_out = pfx + agg;
+      S.prefix = pfx;
+      if (tile == ntiles - 1) *n_out = pfx + agg;
     }
   }
   __syncthreads();
-  if (active) map_out[v] = (int32_t)(s_prefix + s_warp[w] + warp_off + local);  // O[g] + P
+  if (active) map_out[v] = (int32_t)(S.prefix + S.warp[w] + warp_off + local);  // O[g] + P
+  __syncthreads();  // S is reused by the next tile of a persistent CTA
 }
 
-// Level >= 1: OR the intra-group edges of the current graph into per-node hashes.
-__global__ void k_edges_intra(const int2 *__restrict__ E, const unsigned long long *__restrict__ ne_ptr,
-                              int gs, uint32_t *__restrict__ h, int *__restrict__ any) {
-  const int64_t ne = (int64_t)*ne_ptr;
-  bool hit = false;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
-    int2 uv = E[e];
-    int gu = uv.x / gs, gv = uv.y / gs;
-    if (gu == gv) {
-      atomicOr(h + uv.x, 1u << (uv.y - gv * gs));
-      atomicOr(h + uv.y, 1u << (uv.x - gu * gs));
-      hit = true;
-    }
-  }
-  if (__any_sync(FULL_MASK, hit) && lane_id() == 0) *any = 1;
+// Level 0 over the fine mesh: one tile per CTA, tiles claimed in launch order.
+__global__ void __launch_bounds__(MAP_THREADS)
+    k_level0(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
+             const uint8_t *__restrict__ tags, int32_t *__restrict__ map_out, int2 *__restrict__ cross,
+             unsigned long long *__restrict__ cross_count, unsigned long long *status, int *tile_counter,
+             long long *n_out) {
+  __shared__ TileSmem S;
+  if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  group_tile<true>(S, S.tile, gridDim.x, n, geo, adj_ptr, adj_nbr, tags, nullptr, map_out, cross, cross_count,
+                   status, n_out);
 }
 
-// Map the edge list through map_k; drop self loops; compact into E_out.
-__global__ void k_edges_remap(const int2 *__restrict__ E, const unsigned long long *__restrict__ ne_ptr,
-                              const int32_t *__restrict__ mk, int2 *__restrict__ E_out,
-                              unsigned long long *__restrict__ ne_out) {
+// Map the tagged fine cross edges through the level-0 map and de-duplicate them with an
+// open-addressing hash set (key (a << 32 | b) + 1; a < b because the level-0 map is monotone
+// across groups).  The slots a call fills are recorded and cleared again at the end.
+__global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned long long *__restrict__ ne_ptr,
+                                  const int32_t *__restrict__ m0, unsigned long long *__restrict__ table,
+                                  unsigned long long tmask, int2 *__restrict__ E_out,
+                                  unsigned long long *__restrict__ ne_out, unsigned long long *__restrict__ used) {
   const int64_t ne = (int64_t)*ne_ptr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne; base += stride) {
-    int64_t e = base + threadIdx.x;
-    int2 o = make_int2(0, 0);
+    const int64_t e = base + threadIdx.x;
     bool keep = false;
+    int2 o = make_int2(0, 0);
+    unsigned long long slot = 0;
     if (e < ne) {
-      int2 uv = E[e];
-      o.x = mk[uv.x];
-      o.y = mk[uv.y];
-      keep = o.x != o.y;
+      const int2 uv = E[e];
+      o = make_int2(m0[uv.x], m0[uv.y]);
+      const unsigned long long key = (((unsigned long long)(unsigned)o.x << 32) | (unsigned)o.y) + 1ull;
+      slot = (key * 0x9E3779B97F4A7C15ull) >> 20 & tmask;
+      while (true) {
+        const unsigned long long prev = atomicCAS(table + slot, 0ull, key);
+        if (prev == 0ull) { keep = true; break; }
+        if (prev == key) break;
+        slot = (slot + 1) & tmask;
+      }
     }
-    unsigned b = __ballot_sync(FULL_MASK, keep);
+    const unsigned b = __ballot_sync(FULL_MASK, keep);
     unsigned long long wbase = 0;
-    if (lane_id() == 0 && b) wbase = atomicAdd(ne_out, (unsigned long long)__popc(b));
+    if ((threadIdx.x & 31) == 0 && b) wbase = atomicAdd(ne_out, (unsigned long long)__popc(b));
     wbase = __shfl_sync(FULL_MASK, wbase, 0);
-    if (keep) E_out[wbase + __popc(b & ((1u << lane_id()) - 1u))] = o;
+    if (keep) {
+      const unsigned long long pos = wbase + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));
+      E_out[pos] = o;
+      used[pos] = slot;
+    }
   }
 }
 
-// comp[c] = mk[comp[c]]  (compose the level maps on the level-1 index space)
-__global__ void k_compose(int64_t n, int32_t *__restrict__ comp, const int32_t *__restrict__ mk, int first) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n) comp[c] = first ? mk[c] : mk[comp[c]];
+__global__ void k_clear_slots(const unsigned long long *__restrict__ ne_ptr, const unsigned long long *__restrict__ used,
+                              unsigned long long *__restrict__ table) {
+  const int64_t ne = (int64_t)*ne_ptr;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
+    table[used[e]] = 0ull;
 }
 
-// map[f] = comp[map[f]]
-__global__ void k_apply(int64_t n, int32_t *__restrict__ map, const int32_t *__restrict__ comp) {
+#define TAIL_THREADS 1024
+#define TAIL_WARPS (TAIL_THREADS / 32)
+
+struct TailArgs {
+  GroupGeom geo;
+  int max_levels;
+  int64_t N;
+  int tile_nodes;          // nodes per tile = TAIL_WARPS * gpw * gs
+  int2 *E[2];
+  unsigned long long *ne;  // [2] edge counts of E[0], E[1]; ne[0] = level-1 edges on entry
+  uint32_t *h;             // [>= n1], zero on entry
+  int32_t *mk;             // tile-local rank of every node at the current level
+  int32_t *comp;           // level-1 id -> current id
+  int32_t *tcount;         // per-tile coarse-node count
+  int *ctrl;               // [1] any intra edge, [2] levels run, [3] comp valid
+  long long *nvals;        // [0] n1 on entry / final n on exit
+  long long *level_n;      // [64]
+};
+
+// Levels >= 1 in one cooperative kernel, one 1024-thread CTA per SM, three grid barriers per
+// level: (P1) intra-group edges -> hashes; (P2) closure/election per tile -> tile-local rank and
+// per-tile count; (P3) every CTA scans the tile counts in shared memory, remaps + compacts the
+// edges and composes the level maps.  Stops at the first level without an intra-group edge.
+__global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ int32_t s_pref[];  // exclusive prefix of the tile counts
+  __shared__ int s_w[TAIL_WARPS];
+  __shared__ int s_red[TAIL_WARPS];
+  __shared__ int s_total;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const GroupGeom geo = A.geo;
+  const int gs = geo.gs;
+  const int TN = A.tile_nodes;
+  const int64_t n1 = A.nvals[0];
+  int64_t n = n1;
+  int level = 1, cur = 0;
+  if (gtid == 0) A.level_n[0] = n1;
+  if (n1 == A.N) {  // level 0 merged nothing: fixpoint after one pass
+    if (gtid == 0) A.ctrl[2] = 1;
+    return;
+  }
+  const int gin = lane / gs, lig = lane - gin * gs, base_lane = gin * gs;
+  while (true) {
+    ++level;
+    // ---- P1: OR the intra-group edges into the node hashes ----
+    const int64_t ne = (int64_t)*(volatile unsigned long long *)(A.ne + cur);
+    const int2 *E = A.E[cur];
+    bool hit = false;
+    for (int64_t e = gtid; e < ne; e += gstride) {
+      const int2 uv = E[e];
+      const int gu = uv.x / gs, gv = uv.y / gs;
+      if (gu == gv) {
+        atomicOr(A.h + uv.x, 1u << (uv.y - gv * gs));
+        atomicOr(A.h + uv.y, 1u << (uv.x - gu * gs));
+        hit = true;
+      }
+    }
+    if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + 1, 1);
+    grid.sync();
+    if (*(volatile int *)(A.ctrl + 1) == 0) {  // no merge possible: this pass is the fixpoint
+      if (gtid == 0) {
+        if (level <= 64) A.level_n[level - 1] = n;
+        A.ctrl[2] = level;
+        A.nvals[0] = n;
+      }
+      break;
+    }
+    // ---- P2: Alg S1/S2 per tile (closure, election, tile-local rank); clears the hashes ----
+    const int64_t ntiles = (n + TN - 1) / TN;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t v = ((t * TAIL_WARPS + w) * geo.gpw + gin) * gs + lig;
+      const bool active = (gin < geo.gpw) && (v < n);
+      uint32_t hv = 0;
+      if (active) {
+        hv = (1u << lig) | A.h[v];
+        A.h[v] = 0u;
+      }
+      for (int k = 0; k < gs; ++k) {
+        const uint32_t tt = __shfl_sync(FULL_MASK, hv, (base_lane + k) & 31);
+        if ((hv >> k) & 1u) hv |= tt;
+      }
+      const bool elected = active && ((hv & ((1u << lig) - 1u)) == 0u);
+      const unsigned bal = __ballot_sync(FULL_MASK, elected);
+      const unsigned gelect = (bal >> base_lane) & geo.gmask;
+      const int first = active ? __ffs(hv) - 1 : 0;
+      const int local = __popc(gelect & ((1u << first) - 1u)) + __popc(bal & ((1u << base_lane) - 1u));
+      if (lane == 0) s_w[w] = __popc(bal);
+      __syncthreads();
+      if (w == 0) {
+        const int c = s_w[lane];
+        const int ci = warp_incl_scan(c);
+        s_w[lane] = ci - c;
+        if (lane == 31) A.tcount[t] = ci;
+      }
+      __syncthreads();
+      if (active) A.mk[v] = s_w[w] + local;
+      __syncthreads();
+    }
+    if (gtid == 0) A.ne[1 - cur] = 0;
+    grid.sync();
+    // ---- P3: scan the tile counts (every CTA, shared memory), remap, compose, reset ----
+    {
+      const int64_t per = (ntiles + TAIL_THREADS - 1) / TAIL_THREADS;
+      const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
+      int sum = 0;
+      for (int64_t t = t0; t < t1; ++t) sum += A.tcount[t];
+      const int wi = warp_incl_scan(sum);
+      if (lane == 31) s_red[w] = wi;
+      __syncthreads();
+      if (w == 0) {
+        const int c = s_red[lane];
+        s_red[lane] = warp_incl_scan(c) - c;
+      }
+      __syncthreads();
+      int run = s_red[w] + wi - sum;
+      for (int64_t t = t0; t < t1; ++t) {
+        s_pref[t] = run;
+        run += A.tcount[t];
+      }
+      if (threadIdx.x == TAIL_THREADS - 1) s_total = run;
+      __syncthreads();
+    }
+    const int64_t n2 = s_total;
+    int2 *Eo = A.E[1 - cur];
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne; base += gstride) {
+      const int64_t e = base + threadIdx.x;
+      int2 o = make_int2(0, 0);
+      bool keep = false;
+      if (e < ne) {
+        const int2 uv = E[e];
+        o.x = s_pref[uv.x / TN] + A.mk[uv.x];
+        o.y = s_pref[uv.y / TN] + A.mk[uv.y];
+        keep = o.x != o.y;
+      }
+      const unsigned b = __ballot_sync(FULL_MASK, keep);
+      unsigned long long wbase = 0;
+      if (lane == 0 && b) wbase = atomicAdd(A.ne + (1 - cur), (unsigned long long)__popc(b));
+      wbase = __shfl_sync(FULL_MASK, wbase, 0);
+      if (keep) Eo[wbase + __popc(b & ((1u << lane) - 1u))] = o;
+    }
+    for (int64_t c = gtid; c < n1; c += gstride) {
+      const int32_t u = level == 2 ? (int32_t)c : A.comp[c];
+      A.comp[c] = s_pref[u / TN] + A.mk[u];
+    }
+    if (gtid == 0) {
+      A.ctrl[1] = 0;
+      A.ctrl[3] = 1;
+      if (level <= 64) A.level_n[level - 1] = n2;
+    }
+    grid.sync();
+    n = n2;
+    cur = 1 - cur;
+    if (A.max_levels > 0 && level >= A.max_levels) {
+      if (gtid == 0) {
+        A.ctrl[2] = level;
+        A.nvals[0] = n;
+      }
+      break;
+    }
+  }
+}
+
+// map[f] = comp[map[f]] if any tail level merged
+__global__ void k_apply(int64_t n, int32_t *__restrict__ map, const int32_t *__restrict__ comp,
+                        const int *__restrict__ ctrl) {
+  if (!ctrl[3]) return;
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f < n) map[f] = comp[map[f]];
 }
@@ -168,23 +357,13 @@ __global__ void k_histogram(int64_t n, const int32_t *__restrict__ map, int32_t 
   if (key >= 0 && (__ffs(peers) - 1) == lane_id()) atomicAdd(cnt + key, __popc(peers));
 }
 
-static agipc_status group_pass(agipc_handle h, bool from_csr, int64_t n, GroupGeom geo, const agipc_mesh *mesh,
-                               const uint8_t *tags, const uint32_t *hmem, int32_t *map_out, int2 *cross,
-                               unsigned long long *cross_count, long long *n_out) {
-  int64_t groups = cdiv(n, geo.gs);
-  int64_t tiles = cdiv(groups, (int64_t)MAP_WARPS * geo.gpw);
-  if (tiles == 0) tiles = 1;
-  WS(h, status, unsigned long long, "map_status", tiles + 1);
-  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), h->stream));
-  int *counter = (int *)(status + tiles);
-  if (from_csr)
-    LAUNCH(h, k_group_pass<true>, (unsigned)tiles, MAP_THREADS, 0, n, geo, mesh->adj_ptr, mesh->adj_nbr, tags,
-           hmem, map_out, cross, cross_count, status, counter, n_out);
-  else
-    LAUNCH(h, k_group_pass<false>, (unsigned)tiles, MAP_THREADS, 0, n, geo, nullptr, nullptr, nullptr, hmem,
-           map_out, cross, cross_count, status, counter, n_out);
-  return AGIPC_OK;
-}
+struct MapScalars {
+  long long nvals[2];
+  unsigned long long cross;  // level-0 cross edges
+  unsigned long long ne[2];
+  int ctrl[4];
+  long long level_n[64];
+};
 
 extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, const uint8_t *slot_tags,
                                         int group_size, int max_levels, int32_t *map, int32_t *agg_size,
@@ -204,79 +383,97 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     return set_err(h, AGIPC_EINVAL, "build_map: null pointer");
   CU_TRY(h, cudaSetDevice(h->device));
   ProfScope prof_scope(h, PROF_MAP, h->stream);
+  cudaStream_t s0 = h->stream;
   GroupGeom geo;
   geo.gs = group_size;
   geo.gpw = 32 / group_size;
   geo.gmask = group_size == 32 ? 0xffffffffu : ((1u << group_size) - 1u);
-
-  // scalars: [0] n_out (level), [1] cross count, [2] edge count A, [3] edge count B, [4] any-intra flag
-  WS(h, sc, long long, "map_scalars", 8);
-  agipc_status st;
-  long long *hs = (long long *)pinned_get(h, 64, &st);
-  if (st != AGIPC_OK) return st;
+  const int64_t tiles0 = std::max<int64_t>(1, cdiv(cdiv(N, geo.gs), (int64_t)MAP_WARPS * geo.gpw));
   const int64_t ecap = mesh->nnz_adj / 2 + 1;
+
+  WS(h, sc, MapScalars, "map_scalars", 1);
+  WS(h, status, unsigned long long, "map_status", tiles0 + 2);
   WS(h, cross, int2, "map_cross", ecap);
-  CU_TRY(h, cudaMemsetAsync(sc, 0, 8 * sizeof(long long), h->stream));
+  CU_TRY(h, cudaMemsetAsync(sc, 0, sizeof(MapScalars), s0));
+  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles0 + 2), s0));
+  int *tile_counter = (int *)(status + tiles0 + 1);
 
-  // ---- level 0: warp-per-group hashing over the fine mesh (fused scan) ----
-  st = group_pass(h, true, N, geo, mesh, slot_tags, nullptr, map, cross, (unsigned long long *)(sc + 1), sc + 0);
-  if (st != AGIPC_OK) return st;
-  CU_TRY(h, cudaMemcpyAsync(hs, sc, 2 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
-  CU_TRY(h, cudaStreamSynchronize(h->stream));
-  int64_t n = hs[0];
-  int64_t ncross = hs[1];
-  info->n_cross_edges = ncross;
-  info->level_n[0] = n;
-  int level = 1;
-  bool done = (n == N) || (max_levels == 1);
+  // ---- level 0: warp-per-group hashing over the fine mesh (fused look-back scan) ----
+  LAUNCH(h, k_level0, (unsigned)tiles0, MAP_THREADS, 0, N, geo, mesh->adj_ptr, mesh->adj_nbr, slot_tags, map, cross,
+         &sc->cross, status, tile_counter, &sc->nvals[0]);
 
-  if (!done) {
-    const int64_t n1 = n;
+  // ---- levels >= 1: one cooperative persistent kernel ----
+  if (max_levels != 1) {
     WS(h, EA, int2, "map_EA", ecap);
     WS(h, EB, int2, "map_EB", ecap);
-    WS(h, hh, uint32_t, "map_h", n1);
-    WS(h, mk, int32_t, "map_mk", n1);
-    WS(h, comp, int32_t, "map_comp", n1);
-    unsigned long long *neA = (unsigned long long *)(sc + 2), *neB = (unsigned long long *)(sc + 3);
-    int *any = (int *)(sc + 4);
-    // level-1 graph = tagged cross edges mapped through the level-0 map
-    CU_TRY(h, cudaMemsetAsync(neA, 0, sizeof(long long), h->stream));
-    LAUNCH(h, k_edges_remap, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ncross, 256), 8 * h->sm_count)), 256, 0,
-           cross, (const unsigned long long *)(sc + 1), map, EA, neA);
-    int first = 1;
-    while (true) {
-      ++level;
-      CU_TRY(h, cudaMemsetAsync(hh, 0, sizeof(uint32_t) * n, h->stream));
-      CU_TRY(h, cudaMemsetAsync(any, 0, sizeof(int), h->stream));
-      LAUNCH(h, k_edges_intra, (unsigned)(8 * h->sm_count), 256, 0, EA, neA, group_size, hh, any);
-      CU_TRY(h, cudaMemcpyAsync(hs, any, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-      CU_TRY(h, cudaStreamSynchronize(h->stream));
-      if (*(int *)hs == 0) {  // no intra-group edge: this pass merges nothing (fixpoint)
-        if (level <= 64) info->level_n[level - 1] = n;
-        break;
-      }
-      st = group_pass(h, false, n, geo, mesh, nullptr, hh, mk, nullptr, nullptr, sc + 0);
-      if (st != AGIPC_OK) return st;
-      CU_TRY(h, cudaMemsetAsync(neB, 0, sizeof(long long), h->stream));
-      LAUNCH(h, k_edges_remap, (unsigned)(8 * h->sm_count), 256, 0, EA, neA, mk, EB, neB);
-      LAUNCH(h, k_compose, (unsigned)cdiv(n1, 256), 256, 0, n1, comp, mk, first);
-      first = 0;
-      CU_TRY(h, cudaMemcpyAsync(hs, sc, sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
-      CU_TRY(h, cudaStreamSynchronize(h->stream));
-      n = hs[0];
-      if (level <= 64) info->level_n[level - 1] = n;
-      std::swap(EA, EB);
-      std::swap(neA, neB);
-      if (max_levels > 0 && level >= max_levels) break;
+    WS(h, used, unsigned long long, "map_used", ecap);
+    WS(h, hh, uint32_t, "map_h", N);
+    WS(h, mk, int32_t, "map_mk", N);
+    WS(h, comp, int32_t, "map_comp", N);
+    const int tile_nodes = TAIL_WARPS * geo.gpw * geo.gs;
+    const int64_t tiles_max = cdiv(N, tile_nodes) + 1;
+    WS(h, tcount, int32_t, "map_tcount", tiles_max);
+    // hash set for the level-1 edge de-duplication (zeroed once; used slots are cleared after use)
+    int64_t tsize = 1024;
+    while (tsize < 2 * ecap) tsize <<= 1;
+    {
+      WsBuf &tb = h->ws["map_hash"];
+      const bool fresh = tb.bytes < sizeof(unsigned long long) * (size_t)tsize;
+      WS(h, table_, unsigned long long, "map_hash", tsize);
+      if (fresh) CU_TRY(h, cudaMemsetAsync(table_, 0, h->ws["map_hash"].bytes, s0));
     }
-    if (!first) LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp);
+    unsigned long long *table = (unsigned long long *)h->ws["map_hash"].ptr;
+    CU_TRY(h, cudaMemsetAsync(hh, 0, sizeof(uint32_t) * N, s0));
+    const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), 8 * h->sm_count));
+    LAUNCH(h, k_cross_to_level1, gedge, 256, 0, cross, &sc->cross, map, table, (unsigned long long)(tsize - 1), EA,
+           &sc->ne[0], used);
+    LAUNCH(h, k_clear_slots, gedge, 256, 0, &sc->ne[0], used, table);
+    TailArgs A;
+    A.geo = geo;
+    A.max_levels = max_levels;
+    A.N = N;
+    A.tile_nodes = tile_nodes;
+    A.E[0] = EA;
+    A.E[1] = EB;
+    A.ne = sc->ne;
+    A.h = hh;
+    A.mk = mk;
+    A.comp = comp;
+    A.tcount = tcount;
+    A.ctrl = sc->ctrl;
+    A.nvals = sc->nvals;
+    A.level_n = sc->level_n;
+    const size_t smem = sizeof(int32_t) * (size_t)tiles_max;
+    if (smem > 200 * 1024) return set_err(h, AGIPC_ERANGE, "build_map: %lld nodes exceed the tail kernel", (long long)N);
+    CU_TRY(h, cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tail, TAIL_THREADS, smem));
+    if (occ < 1) return set_err(h, AGIPC_ECUDA, "build_map: tail kernel cannot be resident");
+    const int grid = h->sm_count;  // one CTA per SM: cheap grid barriers
+    void *args[] = {&A};
+    cudaError_t pre = cudaGetLastError();
+    if (pre != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pending CUDA error before k_tail: %s", cudaGetErrorString(pre));
+    CU_TRY(h, cudaLaunchCooperativeKernel((const void *)k_tail, grid, TAIL_THREADS, args, smem, s0));
+    h->launches += 1;
+    LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl);
   }
-  info->n_coarse = n;
-  info->n_levels = level;
   if (agg_size) {
-    CU_TRY(h, cudaMemsetAsync(agg_size, 0, sizeof(int32_t) * n, h->stream));
+    CU_TRY(h, cudaMemsetAsync(agg_size, 0, sizeof(int32_t) * N, s0));
     LAUNCH(h, k_histogram, (unsigned)cdiv(N, 256), 256, 0, N, map, agg_size);
   }
-  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  agipc_status st;
+  MapScalars *hs = (MapScalars *)pinned_get(h, sizeof(MapScalars), &st);
+  if (st != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemcpyAsync(hs, sc, sizeof(MapScalars), cudaMemcpyDeviceToHost, s0));
+  CU_TRY(h, cudaStreamSynchronize(s0));
+  info->n_cross_edges = (int64_t)hs->cross;
+  info->n_coarse = hs->nvals[0];
+  if (max_levels == 1) {
+    info->n_levels = 1;
+    info->level_n[0] = hs->nvals[0];
+  } else {
+    info->n_levels = hs->ctrl[2];
+    for (int l = 0; l < std::min(info->n_levels, 64); ++l) info->level_n[l] = hs->level_n[l];
+  }
   return AGIPC_OK;
 }
