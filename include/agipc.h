@@ -75,8 +75,8 @@ AGIPC_API int64_t agipc_kernel_launches(agipc_handle h);
 /* Profiling.  agipc_profile(h, 1) resets and enables CUDA-event timing on the streams the
  * kernels are launched on: one interval per entry-point call (tag_edges, build_map,
  * assemble_coarse, pcg_setup, pcg_solve) and, inside the PCG graph, one interval per kernel
- * launch (pcg_spmv = K1 with the fused p update, pcg_update = K2; launches that exit early after
- * convergence are not counted).  agipc_profile_read synchronises pending events and fills
+ * launch of every 8th iteration (pcg_spmv = K1 with the fused p update, pcg_update = K2;
+ * launches that exit early after convergence are not counted).  agipc_profile_read synchronises pending events and fills
  * up to cap entries; returns the number written (or the number available if out == NULL). */
 typedef struct {
   char name[32];

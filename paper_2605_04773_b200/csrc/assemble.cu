@@ -575,14 +575,25 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_small(NumArgs A) {
     const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
     const int s = A.size_new[a];
     const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);
-    for (int e = l; e < T; e += 32) {
-      int c;
-      long long k;
-      entry_of(tab, s, e, c, k);
-      const int i = tab.ci[c];
-      const int j = A.col[k];
-      const int b = A.nm[j];
-      const int idx = lower_bound_dev<int32_t>(lst, U, b);
+    // entries in batches of 32; lanes with the same target column form a peer group whose
+    // leader sums the peers' contributions (shuffles) and updates the accumulator with a plain
+    // read-modify-write -- no floating-point atomics (shared fp64 atomicAdd is a CAS loop)
+    for (int e0 = 0; e0 < T; e0 += 32) {
+      const int e = e0 + l;
+      const bool act = e < T;
+      int c = 0, i = 0, j = 0, b = 0, idx = -1;
+      long long k = 0;
+      if (act) {
+        entry_of(tab, s, e, c, k);
+        i = tab.ci[c];
+        j = A.col[k];
+        b = A.nm[j];
+        idx = lower_bound_dev<int32_t>(lst, U, b);
+      }
+      const unsigned peers = __match_any_sync(FULL_MASK, idx);
+      if (act) {
+      const int leader = __ffs(peers) - 1;
+      const bool solo = (peers & (peers - 1)) == 0;
       const int cp = colpos(idx, first12);
       const int ncb_b = ncb_of(b, n3);
       double B[9];
@@ -592,17 +603,33 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_small(NumArgs A) {
         const double wi = wgt(A.X, i, ncb_a, p);
         for (int q = 0; q < ncb_b; ++q) {
           const double coef = wi * wgt(A.X, j, ncb_b, q);
-          if (in_smem) {
-            double *dst = s_acc[w] + ((p * rl) + cp + q) * 9;
+          double v[9];
 #pragma unroll
-            for (int x = 0; x < 9; ++x) atomicAdd(dst + x, coef * B[x]);
-          } else {
-            double *dst = A.cval + 9 * (A.crp[slot_of(a, p, n3)] + cp + q);
+          for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+          if (!solo) {  // sum the peers' v into the leader (fixed lane order)
+            double sum[9];
 #pragma unroll
-            for (int x = 0; x < 9; ++x) atomicAdd(dst + x, coef * B[x]);
+            for (int x = 0; x < 9; ++x) sum[x] = 0.0;
+            unsigned m = peers;
+            while (m) {
+              const int src = __ffs(m) - 1;
+              m &= m - 1;
+#pragma unroll
+              for (int x = 0; x < 9; ++x) sum[x] += __shfl_sync(peers, v[x], src);
+            }
+#pragma unroll
+            for (int x = 0; x < 9; ++x) v[x] = sum[x];
+          }
+          if (l == leader) {
+            double *dst = in_smem ? s_acc[w] + ((p * rl) + cp + q) * 9
+                                  : A.cval + 9 * (A.crp[slot_of(a, p, n3)] + cp + q);
+#pragma unroll
+            for (int x = 0; x < 9; ++x) dst[x] += v[x];
           }
         }
       }
+      }  // act
+      __syncwarp();  // the next batch's leaders read what this batch's leaders wrote
     }
     __syncwarp();
     if (!in_smem) __threadfence();

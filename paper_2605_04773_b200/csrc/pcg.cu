@@ -26,6 +26,7 @@
 #define PCG_WARPS (PCG_THREADS / 32)
 #define SEG_MAX 64          // blocks per virtual row
 #define SORT_WIN 4096       // virtual rows per sorting window (sigma = 128 slices)
+#define PROF_EVERY 8        // profiling: time the kernels of every 8th iteration
 
 struct PcgState {
   double rz, alpha, beta, bn2, rr, pq;
@@ -516,13 +517,14 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
                                   cudaEvent_t *ev) {
   for (int k = 0; k < iters; ++k) {
     double *pold = B.P[k & 1], *pnew = B.P[(k + 1) & 1];
-    if (ev) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
+    const bool sample = ev && (k % PROF_EVERY) == 0;  // sampled kernel timing (low overhead)
+    if (sample) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
     k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z, pold,
                                              pnew, B.qseg, B.counters + (k & 1), B.parts, B.st);
-    if (ev) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
+    if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
     k_update<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
                                           B.parts, B.st);
-    if (ev) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
+    if (sample) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg launch: %s", cudaGetErrorString(e));
@@ -663,7 +665,7 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
         const int ran = hst->it - it_before;  // iterations whose K1/K2 did work in this chunk
         h->launches += 2 * (int64_t)ran;
         if (h->prof) {
-          for (int k = 0; k < ran && k < chunk; ++k) {
+          for (int k = 0; k < ran && k < chunk; k += PROF_EVERY) {
             float a = 0.f, b2 = 0.f;
             if (cudaEventElapsedTime(&a, g->ev[3 * k], g->ev[3 * k + 1]) == cudaSuccess) prof_add(h, PROF_PCG_SPMV, a, 1);
             if (cudaEventElapsedTime(&b2, g->ev[3 * k + 1], g->ev[3 * k + 2]) == cudaSuccess)
