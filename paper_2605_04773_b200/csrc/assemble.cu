@@ -31,6 +31,7 @@
 #define LIST_CAP 512
 #define ACC_CAP 1024
 #define LARGE_CHUNK 32
+#define SMALL_T 1024           // small nodes: <= 32 children and <= 1024 candidate entries
 
 struct AsmScal {
   long long n3, n12, n_slots, nnzb;
@@ -143,7 +144,7 @@ __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
                            int32_t *__restrict__ ntasks) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n_c) {
-    bool s = size_new[c] <= SMALL_CHILDREN && rowsum[c] <= SMALL_ENTRIES;
+    bool s = size_new[c] <= SMALL_CHILDREN && rowsum[c] <= SMALL_T;
     is_small[c] = s;
     ntasks[c] = s ? 0 : (int32_t)((size_new[c] + LARGE_CHUNK - 1) / LARGE_CHUNK);
   }
@@ -238,7 +239,290 @@ __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t 
 // ------------------------------------------------------------------------------------
 // B. symbolic
 // ------------------------------------------------------------------------------------
-struct SymArgs {
+// ------------------------------------------------------------------------------------
+// B. symbolic
+// ------------------------------------------------------------------------------------
+// Small coarse nodes are processed in CTA tiles of ~TILE_E consecutive candidate entries
+// (many nodes per tile): every entry (child row i, stored block k) gets the key
+// (local node, new_map[col k], entry) and one CTA-wide bitonic sort in shared memory groups
+// equal (node, column) runs.  The symbolic pass counts the runs per node (row length; 12-DoF
+// columns count 4) and emits the transposed (large column, small node) pairs; the numeric
+// pass repeats the sort and sums each run into its final position.
+#define TILE_THREADS 512
+#define TILE_E 1024            // target entries per tile
+#define TILE_CAP 2048          // max entries per tile (a small node has <= SMALL_T entries)
+
+struct TileArgs {
+  int64_t n_small;
+  const int32_t *small_list;   // small coarse node ids (ascending)
+  const int64_t *e_off;        // [n_small + 1] exclusive prefix of their candidate entries
+  const int32_t *child_list;
+  const int64_t *child_ptr;
+  const int32_t *size_new;
+  const uint8_t *is_small;
+  const int64_t *rp;
+  const int32_t *col;
+  const double *val;
+  const int32_t *nm;
+  const double *X;
+  const double *g_f;
+  const AsmScal *sc;
+  int32_t *rowlen;             // symbolic out (per coarse node)
+  int2 *pairs;                 // symbolic out: (large col, small node)
+  long long pair_cap;
+  AsmScal *scw;
+  // numeric
+  const int32_t *gbuf;         // large-node lists
+  const long long *nb_off;
+  const int32_t *nb_cnt;
+  const int64_t *crp;
+  int32_t *ccol;
+  double *cval;
+  double *g_c;
+};
+
+struct AsmTileSmem {
+  unsigned long long key[TILE_CAP];
+  int row_off[TILE_CAP + 1];   // entry offset of each child row in the tile
+  long long row_rb[TILE_CAP];  // first stored block of the row
+  int row_ci[TILE_CAP];        // fine node of the row
+  int node_row0[TILE_CAP + 1]; // first row of each local node
+  int node_e0[TILE_CAP + 1];   // first entry of each local node
+  int cp[TILE_CAP + 1];        // exclusive scan of the run weights
+  int erow[TILE_CAP];          // child row of every (unsorted) entry
+  int red[TILE_THREADS / 32];
+  int tot;
+};
+
+__device__ __forceinline__ int tile_upper(const int *a, int n, int key) {  // last i with a[i] <= key
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] <= key) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// block-wide exclusive scan of v (one value per thread); returns the exclusive prefix, total in S.tot
+__device__ __forceinline__ int block_excl_scan(AsmTileSmem &S, int v) {
+  const int w = threadIdx.x >> 5, l = lane_id();
+  const int incl = warp_incl_scan(v);
+  if (l == 31) S.red[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int c = l < TILE_THREADS / 32 ? S.red[l] : 0;
+    const int ci = warp_incl_scan(c);
+    if (l < TILE_THREADS / 32) S.red[l] = ci - c;
+    if (l == 31) S.tot = ci;
+  }
+  __syncthreads();
+  const int r = S.red[w] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(TILE_THREADS) k_tile_small(TileArgs A) {
+  extern __shared__ unsigned char smem_raw[];
+  AsmTileSmem &S = *reinterpret_cast<AsmTileSmem *>(smem_raw);
+  const long long n3 = A.sc->n3;
+  const int64_t etot = A.e_off[A.n_small];
+  const int64_t ntiles = (etot + TILE_E - 1) / TILE_E;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // nodes whose first entry falls in [t*TILE_E, (t+1)*TILE_E)
+    const int64_t s0 = lower_bound_dev<int64_t>(A.e_off, (int)A.n_small + 1, t * TILE_E);
+    const int64_t s1 = lower_bound_dev<int64_t>(A.e_off, (int)A.n_small + 1, (t + 1) * TILE_E);
+    const int nn = (int)(min(s1, A.n_small) - s0);
+    if (nn <= 0) continue;
+    const int E = (int)(A.e_off[s0 + nn] - A.e_off[s0]);
+    // local nodes: first row and first entry (children rows are contiguous per node)
+    int nrow = 0, ne = 0;
+    const int per = (nn + TILE_THREADS - 1) / TILE_THREADS;
+    {
+      int rsum = 0;
+      for (int q = threadIdx.x * per; q < min(nn, (threadIdx.x + 1) * per); ++q) rsum += A.size_new[A.small_list[s0 + q]];
+      int run = block_excl_scan(S, rsum);
+      nrow = S.tot;
+      for (int q = threadIdx.x * per; q < min(nn, (threadIdx.x + 1) * per); ++q) {
+        S.node_row0[q] = run;
+        S.node_e0[q] = (int)(A.e_off[s0 + q] - A.e_off[s0]);
+        run += A.size_new[A.small_list[s0 + q]];
+      }
+      if (threadIdx.x == 0) {
+        S.node_row0[nn] = nrow;
+        S.node_e0[nn] = E;
+      }
+    }
+    __syncthreads();
+    // child rows: fine node, first block, entry offset
+    const int rper = (nrow + TILE_THREADS - 1) / TILE_THREADS;
+    {
+      int esum = 0;
+      for (int r = threadIdx.x * rper; r < min(nrow, (threadIdx.x + 1) * rper); ++r) {
+        const int q = tile_upper(S.node_row0, nn, r);
+        const int a = A.small_list[s0 + q];
+        const int ci = A.child_list[A.child_ptr[a] + (r - S.node_row0[q])];
+        const long long rb = A.rp[ci];
+        S.row_ci[r] = ci;
+        S.row_rb[r] = rb;
+        esum += (int)(A.rp[ci + 1] - rb);
+      }
+      int run = block_excl_scan(S, esum);
+      ne = S.tot;
+      for (int r = threadIdx.x * rper; r < min(nrow, (threadIdx.x + 1) * rper); ++r) {
+        S.row_off[r] = run;
+        run += (int)(A.rp[S.row_ci[r] + 1] - S.row_rb[r]);
+      }
+      if (threadIdx.x == 0) S.row_off[nrow] = ne;
+    }
+    __syncthreads();
+    // keys: (local node, coarse column, entry)
+    const int P = next_pow2(max(E, 2));
+    for (int e = threadIdx.x; e < P; e += TILE_THREADS) {
+      unsigned long long key = ~0ull;
+      if (e < E) {
+        const int r = tile_upper(S.row_off, nrow, e);
+        S.erow[e] = r;
+        const int q = tile_upper(S.node_row0, nn, r);
+        const int b = A.nm[A.col[S.row_rb[r] + (e - S.row_off[r])]];
+        key = ((unsigned long long)q << 43) | ((unsigned long long)(unsigned)b << 12) | (unsigned long long)e;
+      }
+      S.key[e] = key;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += TILE_THREADS) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long x = S.key[i], y = S.key[ixj];
+            const bool up = (i & k) == 0;
+            if ((x > y) == up) {
+              S.key[i] = y;
+              S.key[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // column position of every run head (run = equal (node, column)) inside its node's row;
+    // 12-DoF columns take 4 slots
+    {
+      const int eper = (E + TILE_THREADS - 1) / TILE_THREADS;
+      int wsum = 0;
+      for (int e = threadIdx.x * eper; e < min(E, (threadIdx.x + 1) * eper); ++e) {
+        const unsigned long long kk = S.key[e];
+        const bool head = e == 0 || (S.key[e - 1] >> 12) != (kk >> 12);
+        const int b = (int)((kk >> 12) & 0x7fffffffull);
+        wsum += head ? (b >= n3 ? 4 : 1) : 0;
+      }
+      int run = block_excl_scan(S, wsum);
+      for (int e = threadIdx.x * eper; e < min(E, (threadIdx.x + 1) * eper); ++e) {
+        const unsigned long long kk = S.key[e];
+        const bool head = e == 0 || (S.key[e - 1] >> 12) != (kk >> 12);
+        const int b = (int)((kk >> 12) & 0x7fffffffull);
+        S.cp[e] = run;
+        run += head ? (b >= n3 ? 4 : 1) : 0;
+      }
+      if (threadIdx.x == 0) S.cp[E] = S.tot;
+      __syncthreads();
+    }
+    if (!NUMERIC) {
+      for (int q = threadIdx.x; q < nn; q += TILE_THREADS)
+        A.rowlen[A.small_list[s0 + q]] = S.cp[S.node_e0[q + 1]] - S.cp[S.node_e0[q]];
+      for (int e = threadIdx.x; e < E; e += TILE_THREADS) {
+        const unsigned long long kk = S.key[e];
+        if (e > 0 && (S.key[e - 1] >> 12) == (kk >> 12)) continue;
+        const int b = (int)((kk >> 12) & 0x7fffffffull);
+        if (!A.is_small[b]) {  // transposed pair (large column, small node)
+          const int a = A.small_list[s0 + (int)(kk >> 43)];
+          const long long pos = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, 1ull);
+          if (pos < A.pair_cap) A.pairs[pos] = make_int2(b, a);
+          else A.scw->err_overflow = 1;
+        }
+      }
+      __syncthreads();
+    } else {
+      // one thread per output block (run, q): the run head is the last entry whose weight
+      // prefix is <= o (non-head entries carry the next head's prefix)
+      const int O = S.cp[E];
+      for (int o = threadIdx.x; o < O; o += TILE_THREADS) {
+        const int e = tile_upper(S.cp, E, o);
+        const unsigned long long kk = S.key[e];
+        const int qn = (int)(kk >> 43);
+        const int b = (int)((kk >> 12) & 0x7fffffffull);
+        const int a = A.small_list[s0 + qn];
+        const int ncb_a = ncb_of(a, n3);
+        const int qq = o - S.cp[e];
+        const int colp = S.cp[e] - S.cp[S.node_e0[qn]] + qq;
+        int e_end = e + 1;
+        while (e_end < E && (S.key[e_end] >> 12) == (kk >> 12)) ++e_end;
+        const bool mirror = !A.is_small[b];
+        long long mrow = 0;
+        if (mirror) {  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
+          const int32_t *lb_ = A.gbuf + A.nb_off[b];
+          const int Ub = A.nb_cnt[b];
+          mrow = A.crp[slot_of(b, qq, n3)] +
+                 colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
+        }
+        for (int p = 0; p < ncb_a; ++p) {
+          double acc[9];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) acc[x] = 0.0;
+          for (int ee = e; ee < e_end; ++ee) {
+            const int el = (int)(S.key[ee] & 0xfffull);
+            const int r = S.erow[el];
+            const long long k = S.row_rb[r] + (el - S.row_off[r]);
+            const int i = S.row_ci[r];
+            const int j = A.col[k];
+            const double coef = wgt(A.X, i, ncb_a, p) * wgt(A.X, j, b >= n3 ? 4 : 1, qq);
+            const double *B = A.val + 9 * k;
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[x] += coef * __ldg(B + x);
+          }
+          const long long pos = A.crp[slot_of(a, p, n3)] + colp;
+          A.ccol[pos] = slot_of(b, qq, n3);
+          double *dst = A.cval + 9 * pos;
+#pragma unroll
+          for (int x = 0; x < 9; ++x) dst[x] = acc[x];
+          if (mirror) {
+            double *mt = A.cval + 9 * (mrow + p);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = acc[3 * cc + r];
+          }
+        }
+      }
+      // g_c of the tile's nodes (Eq 4): thread per node over its children
+      if (A.g_f) {
+        for (int q = threadIdx.x; q < nn; q += TILE_THREADS) {
+          const int a = A.small_list[s0 + q];
+          const int ncb_a = ncb_of(a, n3);
+          for (int p = 0; p < ncb_a; ++p) {
+            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+            for (int r = S.node_row0[q]; r < S.node_row0[q + 1]; ++r) {
+              const int i = S.row_ci[r];
+              const double wi = wgt(A.X, i, ncb_a, p);
+              g0 += wi * A.g_f[3 * (int64_t)i];
+              g1 += wi * A.g_f[3 * (int64_t)i + 1];
+              g2 += wi * A.g_f[3 * (int64_t)i + 2];
+            }
+            double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
+            gc[0] = g0;
+            gc[1] = g1;
+            gc[2] = g2;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Large nodes: 32-children chunks emit (a, b) for every large column b != a (warp de-dup with
+// __match_any_sync; duplicates across chunks are removed by the per-node sort), and (a, a).
+struct LargeArgs {
   int64_t n_c;
   const int32_t *child_list;
   const int64_t *child_ptr;
@@ -246,129 +530,62 @@ struct SymArgs {
   const uint8_t *is_small;
   const int64_t *rp;
   const int32_t *col;
+  const double *val;
   const int32_t *nm;
-  int32_t *nbs;          // neighbour lists of small nodes
-  long long nbs_cap;
-  long long *nb_off;     // per node: offset of its list (nbs for small, gbuf for large)
-  int32_t *nb_cnt;       // per node: list length
-  int32_t *rowlen;       // per node: expanded row length in blocks
-  int2 *pairs;           // (large node, neighbour) pairs
-  long long pair_cap;
+  const double *X;
+  const double *g_f;
   const int64_t *task_ptr;
-  int64_t n_tasks;
-  AsmScal *sc;
+  const AsmScal *sc;
+  int2 *pairs;
+  long long pair_cap;
+  AsmScal *scw;
+  const int32_t *gbuf;
+  const long long *nb_off;
+  const int32_t *nb_cnt;
+  const int64_t *crp;
+  double *cval;
+  double *g_c;
 };
 
-__global__ void __launch_bounds__(SYM_WARPS * 32) k_sym_small(SymArgs A) {
-  __shared__ int s_buf[SYM_WARPS][SMALL_ENTRIES];
-  __shared__ ChildTab s_tab[SYM_WARPS];
+__global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
+  __shared__ ChildTab s_tab[4];
   const int w = threadIdx.x >> 5, l = lane_id();
-  const long long n3 = A.sc->n3;
-  int *buf = s_buf[w];
-  ChildTab &tab = s_tab[w];
-  for (int64_t a = (int64_t)blockIdx.x * SYM_WARPS + w; a < A.n_c; a += (int64_t)gridDim.x * SYM_WARPS) {
-    if (!A.is_small[a]) continue;
-    const int s = A.size_new[a];
-    const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);
-    for (int e = l; e < T; e += 32) {
-      int c;
-      long long k;
-      entry_of(tab, s, e, c, k);
-      buf[e] = A.nm[A.col[k]];
-    }
-    const int P = next_pow2(T);
-    for (int e = T + l; e < P; e += 32) buf[e] = INT_MAX;
-    __syncwarp();
-    warp_bitonic_sort(buf, P);
-    // count uniques first to reserve space
-    int cnt = 0;
-    for (int e0 = 0; e0 < T; e0 += 32) {
-      int e = e0 + l;
-      cnt += __popc(__ballot_sync(FULL_MASK, e < T && (e == 0 || buf[e] != buf[e - 1])));
-    }
-    long long off = 0;
-    if (l == 0) off = atomicAdd((unsigned long long *)&A.sc->nbs_count, (unsigned long long)cnt);
-    off = __shfl_sync(FULL_MASK, off, 0);
-    if (off + cnt > A.nbs_cap) {
-      if (l == 0) A.sc->err_overflow = 1;
-      continue;
-    }
-    int u12;
-    int U = warp_unique_store(buf, T, A.nbs + off, n3, u12);
-    if (l == 0) {
-      A.nb_off[a] = off;
-      A.nb_cnt[a] = U;
-      A.rowlen[a] = U + 3 * u12;
-    }
-    __syncwarp();
-    // transposed pairs (large neighbour b, this small node a)
-    const int32_t *lst = A.nbs + off;
-    for (int t0 = 0; t0 < U; t0 += 32) {
-      int t = t0 + l;
-      int b = t < U ? lst[t] : 0;
-      bool emit = t < U && !A.is_small[b];
-      unsigned m = __ballot_sync(FULL_MASK, emit);
-      if (!m) continue;
-      long long pb = 0;
-      if (l == 0) pb = atomicAdd((unsigned long long *)&A.sc->pair_count, (unsigned long long)__popc(m));
-      pb = __shfl_sync(FULL_MASK, pb, 0);
-      if (emit) {
-        long long pos = pb + __popc(m & ((1u << l) - 1u));
-        if (pos < A.pair_cap) A.pairs[pos] = make_int2(b, (int)a);
-        else A.sc->err_overflow = 1;
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// 32-children chunks of large nodes: emit (a, b) for every large neighbour b (a itself once).
-__global__ void __launch_bounds__(SYM_WARPS * 32) k_sym_large(SymArgs A) {
-  __shared__ int s_buf[SYM_WARPS][SMALL_ENTRIES];
-  __shared__ ChildTab s_tab[SYM_WARPS];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  int *buf = s_buf[w];
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
-  for (int64_t t = (int64_t)blockIdx.x * SYM_WARPS + w; t < n_tasks; t += (int64_t)gridDim.x * SYM_WARPS) {
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
     const int a = lower_bound_dev<int64_t>(A.task_ptr, (int)A.n_c + 1, t + 1) - 1;
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
     const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
-    for (int e0 = 0; e0 < T; e0 += SMALL_ENTRIES) {
-      const int n = min(SMALL_ENTRIES, T - e0);
-      for (int e = l; e < n; e += 32) {
+    for (int e0 = 0; e0 < T; e0 += 32) {
+      const int e = e0 + l;
+      int key = -1;
+      if (e < T) {
         int c;
         long long k;
-        entry_of(tab, s, e0 + e, c, k);
-        int b = A.nm[A.col[k]];
-        buf[e] = (b == a || A.is_small[b]) ? INT_MAX : b;  // only large, off-diagonal columns
+        entry_of(tab, s, e, c, k);
+        const int b = A.nm[A.col[k]];
+        if (b != a && !A.is_small[b]) key = b;
       }
-      const int P = next_pow2(n);
-      for (int e = n + l; e < P; e += 32) buf[e] = INT_MAX;
-      __syncwarp();
-      warp_bitonic_sort(buf, P);
-      for (int e1 = 0; e1 < n; e1 += 32) {
-        int e = e1 + l;
-        bool keep = e < n && buf[e] != INT_MAX && (e == 0 || buf[e] != buf[e - 1]);
-        unsigned m = __ballot_sync(FULL_MASK, keep);
-        if (!m) continue;
-        long long pb = 0;
-        if (l == 0) pb = atomicAdd((unsigned long long *)&A.sc->pair_count, (unsigned long long)__popc(m));
-        pb = __shfl_sync(FULL_MASK, pb, 0);
-        if (keep) {
-          long long pos = pb + __popc(m & ((1u << l) - 1u));
-          if (pos < A.pair_cap) A.pairs[pos] = make_int2(a, buf[e]);
-          else A.sc->err_overflow = 1;
-        }
+      const unsigned peers = __match_any_sync(FULL_MASK, key);
+      const bool emit = key >= 0 && (__ffs(peers) - 1) == l;
+      const unsigned m = __ballot_sync(FULL_MASK, emit);
+      if (!m) continue;
+      long long pb = 0;
+      if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
+      pb = __shfl_sync(FULL_MASK, pb, 0);
+      if (emit) {
+        const long long pos = pb + __popc(m & ((1u << l) - 1u));
+        if (pos < A.pair_cap) A.pairs[pos] = make_int2(a, key);
+        else A.scw->err_overflow = 1;
       }
-      __syncwarp();
     }
     if (chunk == 0 && l == 0) {  // the diagonal block (a, a) always exists
-      long long pos = (long long)atomicAdd((unsigned long long *)&A.sc->pair_count, 1ull);
+      const long long pos = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, 1ull);
       if (pos < A.pair_cap) A.pairs[pos] = make_int2(a, a);
-      else A.sc->err_overflow = 1;
+      else A.scw->err_overflow = 1;
     }
+    __syncwarp();
   }
 }
 
@@ -488,11 +705,46 @@ __global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr
 }
 
 // ------------------------------------------------------------------------------------
-// D. numeric
+// Small nodes with <= 32 candidate entries (singletons, pairs: the bulk of the 3-DoF rows):
+// one SEG-lane segment of a warp per node (SEG = 16: two nodes per warp, interior singletons
+// have 15 entries; SEG = 32 otherwise), one entry per lane, everything in registers -- a
+// shuffle bitonic sort of (column, lane) keys, run heads by ballot, run sums by a segmented
+// shuffle scan.  No shared-memory staging of values, no barriers.
 // ------------------------------------------------------------------------------------
-struct NumArgs {
-  int64_t n_c;
-  const AsmScal *sc;
+template <int SEG>
+__device__ __forceinline__ long long seg_sort(long long key, int sl) {
+#pragma unroll
+  for (int k = 2; k <= SEG; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const long long other = __shfl_xor_sync(FULL_MASK, key, j, SEG);
+      const bool up = (sl & k) == 0, lower = (sl & j) == 0;
+      const long long mn = min(key, other), mx = max(key, other);
+      key = (lower == up) ? mn : mx;
+    }
+  return key;
+}
+
+template <int SEG>
+__device__ __forceinline__ int seg_incl_scan(int v, int sl) {
+#pragma unroll
+  for (int o = 1; o < SEG; o <<= 1) {
+    const int t = __shfl_up_sync(FULL_MASK, v, o, SEG);
+    if (sl >= o) v += t;
+  }
+  return v;
+}
+
+template <int SEG>
+__device__ __forceinline__ double seg_sum(double v) {
+#pragma unroll
+  for (int o = SEG / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o, SEG);
+  return v;
+}
+
+struct WarpArgs {
+  int64_t n_w;
+  const int32_t *wlist;        // small nodes handled by this kernel
   const int32_t *child_list;
   const int64_t *child_ptr;
   const int32_t *size_new;
@@ -503,195 +755,150 @@ struct NumArgs {
   const int32_t *nm;
   const double *X;
   const double *g_f;
-  const int32_t *nbs;
+  const AsmScal *sc;
+  int32_t *rowlen;
+  int2 *pairs;
+  long long pair_cap;
+  AsmScal *scw;
   const int32_t *gbuf;
   const long long *nb_off;
   const int32_t *nb_cnt;
-  const int32_t *rowlen;
-  const int64_t *task_ptr;
-  int64_t n_tasks;
-  const int64_t *crp;  // coarse row_ptr (slots)
+  const int64_t *crp;
   int32_t *ccol;
   double *cval;
   double *g_c;
 };
 
-__device__ __forceinline__ const int32_t *list_of(const NumArgs &A, int a) {
-  return (A.is_small[a] ? A.nbs : A.gbuf) + A.nb_off[a];
-}
-
-// Large rows: write their column ids and zero their values (blocks are then filled by the
-// mirrored writes of small rows and by the atomics of the large-row chunks).
-__global__ void k_large_rows_init(NumArgs A) {
+template <int SEG, bool NUMERIC>
+__global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
+  constexpr int NSEG = 32 / SEG;
+  __shared__ ChildTab s_tab[8 * NSEG];
   const int w = threadIdx.x >> 5, l = lane_id();
-  const int wpb = blockDim.x >> 5;
+  const int sg = l / SEG, sl = l % SEG;
+  const unsigned smask = SEG == 32 ? FULL_MASK : (((1u << SEG) - 1u) << (sg * SEG));
+  ChildTab &tab = s_tab[w * NSEG + sg];
   const long long n3 = A.sc->n3;
-  for (int64_t a = (int64_t)blockIdx.x * wpb + w; a < A.n_c; a += (int64_t)gridDim.x * wpb) {
-    if (A.is_small[a]) continue;
-    const int U = A.nb_cnt[a], rl = A.rowlen[a];
-    const int32_t *lst = list_of(A, (int)a);
-    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
-    const int ncb_a = ncb_of((int)a, n3);
-    for (int p = 0; p < ncb_a; ++p) {
-      const long long rs = A.crp[slot_of((int)a, p, n3)];
-      for (int t = l; t < U; t += 32) {
-        int b = lst[t];
-        int cp = colpos(t, first12);
-        int ncb_b = ncb_of(b, n3);
-        for (int q = 0; q < ncb_b; ++q) A.ccol[rs + cp + q] = slot_of(b, q, n3);
-      }
-      double *v = A.cval + 9 * rs;
-      for (int x = l; x < 9 * rl; x += 32) v[x] = 0.0;
+  const int64_t n_units = (A.n_w + NSEG - 1) / NSEG;
+  for (int64_t u = (int64_t)blockIdx.x * 8 + w; u < n_units; u += (int64_t)gridDim.x * 8) {
+    const int64_t wi = u * NSEG + sg;
+    const bool segv = wi < A.n_w;
+    const int a = segv ? A.wlist[wi] : 0;
+    const int s = segv ? A.size_new[a] : 0;
+    // children of the node and the offsets of their rows (segment-local scan)
+    int len = 0;
+    if (sl < s) {
+      const int ci = A.child_list[A.child_ptr[a] + sl];
+      const long long rb = A.rp[ci];
+      tab.ci[sl] = ci;
+      tab.rb[sl] = rb;
+      len = (int)(A.rp[ci + 1] - rb);
     }
-  }
-}
-
-__global__ void __launch_bounds__(NUM_WARPS * 32) k_num_small(NumArgs A) {
-  __shared__ int s_list[NUM_WARPS][LIST_CAP];
-  __shared__ double s_acc[NUM_WARPS][ACC_CAP];
-  __shared__ ChildTab s_tab[NUM_WARPS];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const long long n3 = A.sc->n3;
-  ChildTab &tab = s_tab[w];
-  for (int64_t a64 = (int64_t)blockIdx.x * NUM_WARPS + w; a64 < A.n_c; a64 += (int64_t)gridDim.x * NUM_WARPS) {
-    const int a = (int)a64;
-    if (!A.is_small[a]) continue;
-    const int ncb_a = ncb_of(a, n3);
-    const int U = A.nb_cnt[a], rl = A.rowlen[a];
-    const int32_t *glist = A.nbs + A.nb_off[a];
-    const bool in_smem = U <= LIST_CAP && ncb_a * rl * 9 <= ACC_CAP;
-    const int32_t *lst = glist;
-    if (in_smem) {
-      for (int t = l; t < U; t += 32) s_list[w][t] = glist[t];
-      for (int x = l; x < ncb_a * rl * 9; x += 32) s_acc[w][x] = 0.0;
-      lst = s_list[w];
-    } else {
-      for (int p = 0; p < ncb_a; ++p) {
-        double *v = A.cval + 9 * A.crp[slot_of(a, p, n3)];
-        for (int x = l; x < 9 * rl; x += 32) v[x] = 0.0;
-      }
-    }
+    const int incl = seg_incl_scan<SEG>(len, sl);
+    tab.off[sl + 1] = incl;
+    if (sl == 0) tab.off[0] = 0;
     __syncwarp();
-    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
-    const int s = A.size_new[a];
-    const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);
-    // entries in batches of 32; lanes with the same target column form a peer group whose
-    // leader sums the peers' contributions (shuffles) and updates the accumulator with a plain
-    // read-modify-write -- no floating-point atomics (shared fp64 atomicAdd is a CAS loop)
-    for (int e0 = 0; e0 < T; e0 += 32) {
-      const int e = e0 + l;
-      const bool act = e < T;
-      int c = 0, i = 0, j = 0, b = 0, idx = -1;
-      long long k = 0;
-      if (act) {
-        entry_of(tab, s, e, c, k);
-        i = tab.ci[c];
-        j = A.col[k];
-        b = A.nm[j];
-        idx = lower_bound_dev<int32_t>(lst, U, b);
+    const int T = __shfl_sync(FULL_MASK, incl, SEG - 1, SEG);
+    int b = INT_MAX, i = 0, j = 0;
+    long long k = 0;
+    if (sl < T) {
+      int c;
+      entry_of(tab, s, sl, c, k);
+      i = tab.ci[c];
+      j = A.col[k];
+      b = A.nm[j];
+    }
+    const long long key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
+    const int bs = (int)(key >> 5), src = (int)(key & 31);
+    const long long prevk = __shfl_up_sync(FULL_MASK, key, 1, SEG);
+    const bool valid = sl < T;
+    const bool head = valid && (sl == 0 || (prevk >> 5) != bs);
+    const unsigned hb = (__ballot_sync(FULL_MASK, head) & smask) >> (sg * SEG);  // segment-local bits
+    if (!NUMERIC) {
+      const int U = __popc(hb);
+      const int U12 = __popc((__ballot_sync(FULL_MASK, head && bs >= n3) & smask) >> (sg * SEG));
+      if (segv && sl == 0) A.rowlen[a] = U + 3 * U12;
+      const bool emit = head && !A.is_small[bs];  // transposed pair (large column, small node)
+      const unsigned m = __ballot_sync(FULL_MASK, emit);
+      if (m) {
+        long long pb = 0;
+        if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
+        pb = __shfl_sync(FULL_MASK, pb, 0);
+        if (emit) {
+          const long long pos = pb + __popc(m & ((1u << l) - 1u));
+          if (pos < A.pair_cap) A.pairs[pos] = make_int2(bs, a);
+          else A.scw->err_overflow = 1;
+        }
       }
-      const unsigned peers = __match_any_sync(FULL_MASK, idx);
-      if (act) {
-      const int leader = __ffs(peers) - 1;
-      const bool solo = (peers & (peers - 1)) == 0;
-      const int cp = colpos(idx, first12);
-      const int ncb_b = ncb_of(b, n3);
-      double B[9];
+      __syncwarp();
+      continue;
+    }
+    // numeric: column position of every run, run membership, run tails
+    const int ncb_a = segv ? ncb_of(a, n3) : 1;
+    const int wgt_b = head ? ncb_of(bs, n3) : 0;
+    const int cp_incl = seg_incl_scan<SEG>(wgt_b, sl);
+    const int hl = valid ? 31 - __clz(hb & ((2u << sl) - 1u)) : sl;  // my run's head (segment lane)
+    const int cp = __shfl_sync(FULL_MASK, cp_incl - wgt_b, hl, SEG);
+    const bool tail = valid && (sl == T - 1 || ((hb >> (sl + 1)) & 1u));
+    const int Q = __ballot_sync(FULL_MASK, valid && bs >= n3) ? 4 : 1;        // warp-uniform loop bounds
+    const int PA = __ballot_sync(FULL_MASK, segv && ncb_a == 4) ? 4 : 1;
+    const int si = __shfl_sync(FULL_MASK, i, src, SEG), sj = __shfl_sync(FULL_MASK, j, src, SEG);
+    const long long sk = __shfl_sync(FULL_MASK, k, src, SEG);
+    double B[9];
 #pragma unroll
-      for (int x = 0; x < 9; ++x) B[x] = __ldg(A.val + 9 * k + x);
-      for (int p = 0; p < ncb_a; ++p) {
-        const double wi = wgt(A.X, i, ncb_a, p);
-        for (int q = 0; q < ncb_b; ++q) {
-          const double coef = wi * wgt(A.X, j, ncb_b, q);
-          double v[9];
+    for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
+    const int ncb_b = valid ? ncb_of(bs, n3) : 1;
+    long long mbase = -1;  // position of column a in the large row bs (B_ji = B_ij^T, reading R22)
+    if (tail && !A.is_small[bs]) {
+      const int32_t *lb_ = A.gbuf + A.nb_off[bs];
+      const int Ub = A.nb_cnt[bs];
+      mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
+    }
+    for (int p = 0; p < PA; ++p) {
+      const bool pv = p < ncb_a;
+      const double wi = (valid && pv) ? wgt(A.X, si, ncb_a, p) : 0.0;
+      const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
+      for (int q = 0; q < Q; ++q) {
+        const double coef = (valid && pv && q < ncb_b) ? wi * wgt(A.X, sj, ncb_b, q) : 0.0;
+        double v[9];
 #pragma unroll
-          for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
-          if (!solo) {  // sum the peers' v into the leader (fixed lane order)
-            double sum[9];
+        for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
 #pragma unroll
-            for (int x = 0; x < 9; ++x) sum[x] = 0.0;
-            unsigned m = peers;
-            while (m) {
-              const int src = __ffs(m) - 1;
-              m &= m - 1;
+        for (int o = 1; o < SEG; o <<= 1)  // segmented inclusive scan inside runs
 #pragma unroll
-              for (int x = 0; x < 9; ++x) sum[x] += __shfl_sync(peers, v[x], src);
-            }
-#pragma unroll
-            for (int x = 0; x < 9; ++x) v[x] = sum[x];
+          for (int x = 0; x < 9; ++x) {
+            const double t = __shfl_up_sync(FULL_MASK, v[x], o, SEG);
+            if (sl - o >= hl) v[x] += t;
           }
-          if (l == leader) {
-            double *dst = in_smem ? s_acc[w] + ((p * rl) + cp + q) * 9
-                                  : A.cval + 9 * (A.crp[slot_of(a, p, n3)] + cp + q);
+        if (tail && pv && q < ncb_b) {
+          const long long pos = rs + cp + q;
+          A.ccol[pos] = slot_of(bs, q, n3);
+          double *dst = A.cval + 9 * pos;
 #pragma unroll
-            for (int x = 0; x < 9; ++x) dst[x] += v[x];
+          for (int x = 0; x < 9; ++x) dst[x] = v[x];
+          if (mbase >= 0) {
+            double *mt = A.cval + 9 * (A.crp[slot_of(bs, q, n3)] + mbase + p);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
           }
         }
       }
-      }  // act
-      __syncwarp();  // the next batch's leaders read what this batch's leaders wrote
     }
-    __syncwarp();
-    if (!in_smem) __threadfence();
-    // write the row(s): values (flat, coalesced) and column ids
-    for (int p = 0; p < ncb_a; ++p) {
-      const long long rs = A.crp[slot_of(a, p, n3)];
-      if (in_smem) {
-        double *v = A.cval + 9 * rs;
-        const double *src = s_acc[w] + p * rl * 9;
-        for (int x = l; x < 9 * rl; x += 32) v[x] = src[x];
-      }
-      for (int t = l; t < U; t += 32) {
-        int b = lst[t];
-        int cp = colpos(t, first12);
-        int ncb_b = ncb_of(b, n3);
-        for (int q = 0; q < ncb_b; ++q) A.ccol[rs + cp + q] = slot_of(b, q, n3);
-      }
-    }
-    // mirrored (large row, small column) blocks: H_c(slot(b,q), slot(a,p)) = H_c(slot(a,p), slot(b,q))^T
-    for (int t = l; t < U; t += 32) {
-      const int b = lst[t];
-      if (A.is_small[b]) continue;
-      const int cp = colpos(t, first12);
-      const int ncb_b = ncb_of(b, n3);
-      const int32_t *lb_ = A.gbuf + A.nb_off[b];
-      const int Ub = A.nb_cnt[b];
-      const int idxb = lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a);
-      const int cpb = colpos(idxb, lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
-      for (int p = 0; p < ncb_a; ++p)
-        for (int q = 0; q < ncb_b; ++q) {
-          double m[9];
-          if (in_smem) {
-            const double *src = s_acc[w] + ((p * rl) + cp + q) * 9;
-#pragma unroll
-            for (int x = 0; x < 9; ++x) m[x] = src[x];
-          } else {  // values were produced by L2 atomics: read them from L2
-            const double *src = A.cval + 9 * (A.crp[slot_of(a, p, n3)] + cp + q);
-#pragma unroll
-            for (int x = 0; x < 9; ++x) m[x] = __ldcg(src + x);
-          }
-          double *dst = A.cval + 9 * (A.crp[slot_of(b, q, n3)] + cpb + p);
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) dst[3 * r + cc] = m[3 * cc + r];
-        }
-    }
-    // g_c[slot(a,p)] = sum_children w_i[p] g_f[i]  (Eq 4)
-    if (A.g_f) {
-      for (int p = 0; p < ncb_a; ++p) {
+    if (A.g_f) {  // g_c[slot(a,p)] = sum over the children of w_i[p] g_f[i]
+      for (int p = 0; p < PA; ++p) {
         double g0 = 0, g1 = 0, g2 = 0;
-        if (l < s) {
-          int i = tab.ci[l];
-          double wi = wgt(A.X, i, ncb_a, p);
-          g0 = wi * A.g_f[3 * (int64_t)i];
-          g1 = wi * A.g_f[3 * (int64_t)i + 1];
-          g2 = wi * A.g_f[3 * (int64_t)i + 2];
+        if (sl < s && p < ncb_a) {
+          const int ci = tab.ci[sl];
+          const double wc = wgt(A.X, ci, ncb_a, p);
+          g0 = wc * A.g_f[3 * (int64_t)ci];
+          g1 = wc * A.g_f[3 * (int64_t)ci + 1];
+          g2 = wc * A.g_f[3 * (int64_t)ci + 2];
         }
-        g0 = warp_sum(g0);
-        g1 = warp_sum(g1);
-        g2 = warp_sum(g2);
-        if (l == 0) {
+        g0 = seg_sum<SEG>(g0);
+        g1 = seg_sum<SEG>(g1);
+        g2 = seg_sum<SEG>(g2);
+        if (segv && sl == 0 && p < ncb_a) {
           double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
           gc[0] = g0;
           gc[1] = g1;
@@ -703,20 +910,91 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_small(NumArgs A) {
   }
 }
 
-// Large rows, one warp per 32-children chunk.  lane = (g, p): G = 32/NCB block groups, NCB
-// lanes per fine block.  The diagonal block (a,a) accumulates in registers (NCB x 9 doubles
-// per lane) and is flushed once per chunk; (a, b) with b large and b != a uses fp64 atomics;
-// (a, b) with b small is skipped here (mirrored by the small row b).
-template <int NCB>
-__global__ void __launch_bounds__(NUM_WARPS * 32) k_num_large(NumArgs A) {
-  __shared__ ChildTab s_tab[NUM_WARPS];
+// split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
+__global__ void k_small_flags(int64_t n_c, const uint8_t *__restrict__ is_small,
+                              const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ f16,
+                              int32_t *__restrict__ f32, int32_t *__restrict__ ft) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_c) {
+    const bool sm = is_small[c];
+    f16[c] = sm && rowsum[c] <= 16;
+    f32[c] = sm && rowsum[c] > 16 && rowsum[c] <= 32;
+    ft[c] = sm && rowsum[c] > 32;
+  }
+}
+
+__global__ void k_small_lists(int64_t n_c, const int32_t *__restrict__ f16, const int32_t *__restrict__ f32,
+                              const int32_t *__restrict__ ft, const int64_t *__restrict__ i16,
+                              const int64_t *__restrict__ i32, const int64_t *__restrict__ it,
+                              const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ w16,
+                              int32_t *__restrict__ w32, int32_t *__restrict__ tlist, int64_t *__restrict__ ecount) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_c) {
+    if (f16[c]) w16[i16[c]] = (int32_t)c;
+    if (f32[c]) w32[i32[c]] = (int32_t)c;
+    if (ft[c]) {
+      tlist[it[c]] = (int32_t)c;
+      ecount[it[c]] = (int64_t)rowsum[c];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// D. numeric
+// ------------------------------------------------------------------------------------
+// ------------------------------------------------------------------------------------
+// D. numeric
+// ------------------------------------------------------------------------------------
+// Large rows: write their column ids and zero their values (blocks are then filled by the
+// mirrored writes of small rows and by the atomics of the large-row chunks).
+__global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t *__restrict__ is_small,
+                                  const int32_t *__restrict__ gbuf, const long long *__restrict__ nb_off,
+                                  const int32_t *__restrict__ nb_cnt, const int32_t *__restrict__ rowlen,
+                                  const int64_t *__restrict__ crp, int32_t *__restrict__ ccol, double *__restrict__ cval) {
   const int w = threadIdx.x >> 5, l = lane_id();
-  const int gq = l / NCB, p = l % NCB;
+  const int wpb = blockDim.x >> 5;
+  const long long n3 = sc->n3;
+  for (int64_t a = (int64_t)blockIdx.x * wpb + w; a < n_c; a += (int64_t)gridDim.x * wpb) {
+    if (is_small[a]) continue;
+    const int U = nb_cnt[a], rl = rowlen[a];
+    const int32_t *lst = gbuf + nb_off[a];
+    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
+    const int ncb_a = ncb_of((int)a, n3);
+    for (int p = 0; p < ncb_a; ++p) {
+      const long long rs = crp[slot_of((int)a, p, n3)];
+      for (int t = l; t < U; t += 32) {
+        const int b = lst[t];
+        const int cp = colpos(t, first12);
+        const int ncb_b = ncb_of(b, n3);
+        for (int q = 0; q < ncb_b; ++q) ccol[rs + cp + q] = slot_of(b, q, n3);
+      }
+      double *v = cval + 9 * rs;
+      for (int x = l; x < 9 * rl; x += 32) v[x] = 0.0;
+    }
+  }
+}
+
+// Large rows, one warp per 32-children chunk.  Phase 1 (lane per entry, coalesced): classify the
+// chunk's stored blocks into the diagonal list (new_map(j) == a, staged in shared memory),
+// large-large interface blocks (direct fp64 atomics, rare) and small columns (skipped: mirrored
+// by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
+// two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
+// registers; a final reduction over g and one fp64 atomic per entry per chunk.
+#define LSTAGE 512
+
+template <int NCB>
+__global__ void __launch_bounds__(128) k_num_large(LargeArgs A) {
+  __shared__ ChildTab s_tab[4];
+  __shared__ long long s_k[4][LSTAGE];
+  __shared__ int s_i[4][LSTAGE];
+  __shared__ int s_j[4][LSTAGE];
+  const int w = threadIdx.x >> 5, l = lane_id();
   constexpr int G = 32 / NCB;
+  const int gq = l / NCB, p = l % NCB;
   const long long n3 = A.sc->n3;
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
-  for (int64_t t = (int64_t)blockIdx.x * NUM_WARPS + w; t < n_tasks; t += (int64_t)gridDim.x * NUM_WARPS) {
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
     const int a = lower_bound_dev<int64_t>(A.task_ptr, (int)A.n_c + 1, t + 1) - 1;
     if (ncb_of(a, n3) != NCB) continue;
     const int chunk = (int)(t - A.task_ptr[a]);
@@ -725,46 +1003,81 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_large(NumArgs A) {
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
     const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
-    const long long rs_p = A.crp[slot_of(a, p, n3)];
     double acc[NCB][9];
 #pragma unroll
     for (int q = 0; q < NCB; ++q)
 #pragma unroll
       for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
-    for (int e0 = 0; e0 < T; e0 += G) {
-      const int e = e0 + gq;
-      if (e >= T) continue;
-      int c;
-      long long k;
-      entry_of(tab, s, e, c, k);
-      const int j = A.col[k];
-      const int b = A.nm[j];
-      if (b != a && A.is_small[b]) continue;
-      const int i = tab.ci[c];
-      double B[9];
-#pragma unroll
-      for (int x = 0; x < 9; ++x) B[x] = __ldg(A.val + 9 * k + x);
-      const double wi = wgt(A.X, i, NCB, p);
-      if (b == a) {
-#pragma unroll
-        for (int q = 0; q < NCB; ++q) {
-          const double coef = wi * wgt(A.X, j, NCB, q);
-#pragma unroll
-          for (int x = 0; x < 9; ++x) acc[q][x] += coef * B[x];
+    for (int base = 0; base < T; base += LSTAGE) {
+      const int n = min(LSTAGE, T - base);
+      int cnt = 0;
+      for (int e0 = 0; e0 < n; e0 += 32) {
+        const int e = base + e0 + l;
+        bool diag = false;
+        long long k = 0;
+        int i = 0, j = 0, b = -1;
+        if (e0 + l < n) {
+          int c;
+          entry_of(tab, s, e, c, k);
+          i = tab.ci[c];
+          j = A.col[k];
+          b = A.nm[j];
+          diag = b == a;
         }
-      } else {
-        const int idx = lower_bound_dev<int32_t>(lst, U, b);
-        const int cp = colpos(idx, first12);
-        const int ncb_b = ncb_of(b, n3);
-        for (int q = 0; q < ncb_b; ++q) {
-          const double coef = wi * wgt(A.X, j, ncb_b, q);
-          double *dst = A.cval + 9 * (rs_p + cp + q);
+        const unsigned m = __ballot_sync(FULL_MASK, diag);
+        if (diag) {
+          const int pos = cnt + __popc(m & ((1u << l) - 1u));
+          s_k[w][pos] = k;
+          s_i[w][pos] = i;
+          s_j[w][pos] = j;
+        }
+        cnt += __popc(m);
+        if (b >= 0 && b != a && !A.is_small[b]) {  // large-large interface block
+          const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b), first12);
+          const int ncb_b = ncb_of(b, n3);
+          double B[9];
 #pragma unroll
-          for (int x = 0; x < 9; ++x) atomicAdd(dst + x, coef * B[x]);
+          for (int x = 0; x < 9; ++x) B[x] = __ldg(A.val + 9 * k + x);
+          for (int pp = 0; pp < NCB; ++pp) {
+            const long long rs = A.crp[slot_of(a, pp, n3)];
+            const double wi = wgt(A.X, i, NCB, pp);
+            for (int q = 0; q < ncb_b; ++q) {
+              const double coef = wi * wgt(A.X, j, ncb_b, q);
+              double *dst = A.cval + 9 * (rs + cp + q);
+#pragma unroll
+              for (int x = 0; x < 9; ++x) atomicAdd(dst + x, coef * B[x]);
+            }
+          }
         }
       }
+      __syncwarp();
+      for (int d = gq; d < cnt; d += 2 * G) {
+        const bool two = d + G < cnt;
+        const long long k0 = s_k[w][d], k1 = two ? s_k[w][d + G] : k0;
+        const int i0 = s_i[w][d], i1 = two ? s_i[w][d + G] : i0;
+        const int j0 = s_j[w][d], j1 = two ? s_j[w][d + G] : j0;
+        double B0[9], B1[9], wj0[NCB], wj1[NCB];
+#pragma unroll
+        for (int x = 0; x < 9; ++x) {
+          B0[x] = __ldg(A.val + 9 * k0 + x);
+          B1[x] = __ldg(A.val + 9 * k1 + x);
+        }
+#pragma unroll
+        for (int q = 0; q < NCB; ++q) {
+          wj0[q] = wgt(A.X, j0, NCB, q);
+          wj1[q] = two ? wgt(A.X, j1, NCB, q) : 0.0;
+        }
+        const double wi0 = wgt(A.X, i0, NCB, p), wi1 = wgt(A.X, i1, NCB, p);
+#pragma unroll
+        for (int q = 0; q < NCB; ++q) {
+          const double c0 = wi0 * wj0[q], c1 = wi1 * wj1[q];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) acc[q][x] += c0 * B0[x] + c1 * B1[x];
+        }
+      }
+      __syncwarp();
     }
-    // reduce the diagonal accumulators over the block groups (lanes with the same p)
+    // reduce over the block groups (lanes with the same p) and flush the diagonal block
 #pragma unroll
     for (int o = NCB; o < 32; o <<= 1)
 #pragma unroll
@@ -772,21 +1085,19 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_large(NumArgs A) {
 #pragma unroll
         for (int x = 0; x < 9; ++x) acc[q][x] += __shfl_xor_sync(FULL_MASK, acc[q][x], o);
     if (gq == 0) {
-      const int idx = lower_bound_dev<int32_t>(lst, U, a);
-      const int cp = colpos(idx, first12);
+      const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, a), first12);
+      const long long rs = A.crp[slot_of(a, p, n3)];
 #pragma unroll
-      for (int q = 0; q < NCB; ++q) {
-        double *dst = A.cval + 9 * (rs_p + cp + q);
+      for (int q = 0; q < NCB; ++q)
 #pragma unroll
-        for (int x = 0; x < 9; ++x) atomicAdd(dst + x, acc[q][x]);
-      }
+        for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q) + x, acc[q][x]);
     }
-    if (A.g_f) {
+    if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
       for (int pp = 0; pp < NCB; ++pp) {
         double g0 = 0, g1 = 0, g2 = 0;
         if (l < s) {
-          int i = tab.ci[l];
-          double wi = wgt(A.X, i, NCB, pp);
+          const int i = tab.ci[l];
+          const double wi = wgt(A.X, i, NCB, pp);
           g0 = wi * A.g_f[3 * (int64_t)i];
           g1 = wi * A.g_f[3 * (int64_t)i + 1];
           g2 = wi * A.g_f[3 * (int64_t)i + 2];
@@ -804,6 +1115,21 @@ __global__ void __launch_bounds__(NUM_WARPS * 32) k_num_large(NumArgs A) {
     }
     __syncwarp();
   }
+}
+
+__global__ void k_small_list(int64_t n_c, const uint8_t *__restrict__ is_small, const int64_t *__restrict__ sidx,
+                             const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ small_list,
+                             int64_t *__restrict__ ecount) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_c && is_small[c]) {
+    small_list[sidx[c]] = (int32_t)c;
+    ecount[sidx[c]] = (int64_t)rowsum[c];
+  }
+}
+
+__global__ void k_is_small_i32(int64_t n_c, const uint8_t *__restrict__ is_small, int32_t *__restrict__ out) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_c) out[c] = is_small[c];
 }
 
 // ------------------------------------------------------------------------------------
@@ -844,6 +1170,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, is_small, uint8_t, "asm_is_small", n_c);
   WS(h, ntasks, int32_t, "asm_ntasks", n_c);
   WS(h, task_ptr, int64_t, "asm_task_ptr", n_c + 1);
+  WS(h, small_i32, int32_t, "asm_small_i32", n_c);
+  WS(h, sidx, int64_t, "asm_sidx", n_c + 1);
+  WS(h, small_list, int32_t, "asm_small_list", n_c);
+  WS(h, ecount, int64_t, "asm_ecount", n_c);
+  WS(h, e_off, int64_t, "asm_e_off", n_c + 1);
   CU_TRY(h, cudaMemsetAsync(size, 0, sizeof(int32_t) * n_c, st_));
   CU_TRY(h, cudaMemsetAsync(rowsum, 0, sizeof(unsigned long long) * n_c, st_));
   const unsigned gN = (unsigned)cdiv(N, 256), gC = (unsigned)cdiv(n_c, 256);
@@ -857,11 +1188,31 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_children, gN, 256, 0, N, out->new_map, H->row_ptr, cursor, child_list, rowsum);
   LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
+  // small nodes: the warp list (<= 32 candidate entries) and the tile list (> 32, with the
+  // prefix of their entries)
+  WS(h, f16, int32_t, "asm_f16", n_c);
+  WS(h, f32, int32_t, "asm_f32", n_c);
+  WS(h, i16, int64_t, "asm_i16", n_c + 1);
+  WS(h, i32, int64_t, "asm_i32", n_c + 1);
+  WS(h, w16, int32_t, "asm_w16", n_c);
+  WS(h, w32, int32_t, "asm_w32", n_c);
+  LAUNCH(h, k_small_flags, gC, 256, 0, n_c, is_small, rowsum, f16, f32, small_i32);
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f16, n_c, i16)) != AGIPC_OK) return st;
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f32, n_c, i32)) != AGIPC_OK) return st;
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, small_i32, n_c, sidx)) != AGIPC_OK) return st;
+  LAUNCH(h, k_small_lists, gC, 256, 0, n_c, f16, f32, small_i32, i16, i32, sidx, rowsum, w16, w32, small_list, ecount);
+  AsmScal *hsc = (AsmScal *)pinned_get(h, sizeof(AsmScal) + 64, &st);
+  if (st != AGIPC_OK) return st;
+  long long *h_small = (long long *)(hsc + 1);
+  CU_TRY(h, cudaMemcpyAsync(h_small, sidx + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  CU_TRY(h, cudaMemcpyAsync(h_small + 1, i16 + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  CU_TRY(h, cudaMemcpyAsync(h_small + 2, i32 + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  CU_TRY(h, cudaStreamSynchronize(st_));
+  const int64_t n_small = h_small[0], n_w16 = h_small[1], n_w32 = h_small[2];
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I64, ecount, n_small, e_off)) != AGIPC_OK) return st;
 
   // ---- B. symbolic ----
-  const long long nbs_cap = nnzb_f + 32;
   const long long pair_cap = nnzb_f + n_c + 32;
-  WS(h, nbs, int32_t, "asm_nbs", nbs_cap);
   WS(h, nb_off, long long, "asm_nb_off", n_c);
   WS(h, nb_cnt, int32_t, "asm_nb_cnt", n_c);
   WS(h, rowlen, int32_t, "asm_rowlen", n_c);
@@ -871,24 +1222,45 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, gptr, int64_t, "asm_gptr", n_c + 1);
   WS(h, gbuf, int32_t, "asm_gbuf", 2 * pair_cap);
   WS(h, big_list, int32_t, "asm_big_list", n_c);
-  // n_tasks is needed on the host for the grid only as an upper bound: sum of ceil(size/32) <= N/32 + n_c
   const int64_t task_bound = N / LARGE_CHUNK + n_c;
-  SymArgs SA;
-  SA.n_c = n_c; SA.child_list = child_list; SA.child_ptr = child_ptr; SA.size_new = size_new;
-  SA.is_small = is_small; SA.rp = H->row_ptr; SA.col = H->col; SA.nm = out->new_map;
-  SA.nbs = nbs; SA.nbs_cap = nbs_cap; SA.nb_off = nb_off; SA.nb_cnt = nb_cnt; SA.rowlen = rowlen;
-  SA.pairs = pairs; SA.pair_cap = pair_cap; SA.task_ptr = task_ptr; SA.n_tasks = task_bound; SA.sc = sc;
-  const unsigned gsym = (unsigned)std::min<int64_t>(cdiv(n_c, SYM_WARPS), 64 * h->sm_count);
-  LAUNCH(h, k_sym_small, gsym, SYM_WARPS * 32, 0, SA);
-  // the exact task count task_ptr[n_c] is read on the device; task_bound only sizes the grid
-  LAUNCH(h, k_sym_large, (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, SYM_WARPS)), 64 * h->sm_count),
-         SYM_WARPS * 32, 0, SA);
+  TileArgs TA;
+  TA.n_small = n_small; TA.small_list = small_list; TA.e_off = e_off; TA.child_list = child_list;
+  TA.child_ptr = child_ptr; TA.size_new = size_new; TA.is_small = is_small; TA.rp = H->row_ptr; TA.col = H->col;
+  TA.val = H->val; TA.nm = out->new_map; TA.X = mesh->x_rest; TA.g_f = (g_fine && out->g_c) ? g_fine : nullptr;
+  TA.sc = sc; TA.rowlen = rowlen; TA.pairs = pairs; TA.pair_cap = pair_cap; TA.scw = sc;
+  TA.gbuf = gbuf; TA.nb_off = nb_off; TA.nb_cnt = nb_cnt; TA.crp = nullptr; TA.ccol = nullptr; TA.cval = nullptr;
+  TA.g_c = out->g_c;
+  const size_t tile_smem = sizeof(AsmTileSmem);
+  CU_TRY(h, cudaFuncSetAttribute(k_tile_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+  CU_TRY(h, cudaFuncSetAttribute(k_tile_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+  const unsigned gtile = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(nnzb_f, TILE_E) + 1, 4 * h->sm_count));
+  if (n_small > 0) LAUNCH(h, k_tile_small<false>, gtile, TILE_THREADS, tile_smem, TA);
+  WarpArgs WA;
+  WA.n_w = n_w16; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
+  WA.is_small = is_small; WA.rp = H->row_ptr; WA.col = H->col; WA.val = H->val; WA.nm = out->new_map;
+  WA.X = mesh->x_rest; WA.g_f = TA.g_f; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
+  WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
+  WA.cval = nullptr; WA.g_c = out->g_c;
+  WarpArgs WB = WA;
+  WB.n_w = n_w32; WB.wlist = w32;
+  const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
+  const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
+  if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
+  if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
+  LargeArgs LA;
+  LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
+  LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
+  LA.g_f = TA.g_f; LA.task_ptr = task_ptr; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
+  LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
+  const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
+  LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
   LAUNCH(h, k_pair_count, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, gcnt);
   LAUNCH(h, k_pow2, gC, 256, 0, n_c, gcnt, gpad);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, gpad, n_c, gptr)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(cursor, gptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
   LAUNCH(h, k_pair_scatter, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, cursor, gbuf);
+  const unsigned gsym = (unsigned)std::min<int64_t>(cdiv(n_c, SYM_WARPS), 64 * h->sm_count);
   LAUNCH(h, k_group_unique, gsym, SYM_WARPS * 32, 0, n_c, is_small, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen,
          big_list, sc);
   LAUNCH(h, k_group_unique_big, (unsigned)h->sm_count, 1024, 0, sc, big_list, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen);
@@ -901,8 +1273,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_slot_rowlen, gC, 256, 0, n_c, sc, rowlen, rl);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, rl, slot_bound, crp_ws)) != AGIPC_OK) return st;
   LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws);
-  AsmScal *hsc = (AsmScal *)pinned_get(h, sizeof(AsmScal), &st);
-  if (st != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
   CU_TRY(h, cudaStreamSynchronize(st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
@@ -920,17 +1290,17 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemcpyAsync(out->row_ptr, crp_ws, sizeof(int64_t) * (out->n_slots + 1), cudaMemcpyDeviceToDevice, st_));
 
   // ---- D. numeric ----
-  NumArgs NA;
-  NA.n_c = n_c; NA.sc = sc; NA.child_list = child_list; NA.child_ptr = child_ptr; NA.size_new = size_new;
-  NA.is_small = is_small; NA.rp = H->row_ptr; NA.col = H->col; NA.val = H->val; NA.nm = out->new_map;
-  NA.X = mesh->x_rest; NA.g_f = (g_fine && out->g_c) ? g_fine : nullptr; NA.nbs = nbs; NA.gbuf = gbuf;
-  NA.nb_off = nb_off; NA.nb_cnt = nb_cnt; NA.rowlen = rowlen; NA.task_ptr = task_ptr; NA.n_tasks = task_bound;
-  NA.crp = out->row_ptr; NA.ccol = out->col; NA.cval = out->val; NA.g_c = out->g_c;
-  if (NA.g_f) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
-  LAUNCH(h, k_large_rows_init, gsym, 128, 0, NA);
-  LAUNCH(h, k_num_small, gsym, NUM_WARPS * 32, 0, NA);
-  const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, NUM_WARPS)), 64 * h->sm_count);
-  LAUNCH(h, k_num_large<4>, glarge, NUM_WARPS * 32, 0, NA);
-  LAUNCH(h, k_num_large<1>, glarge, NUM_WARPS * 32, 0, NA);
+  if (TA.g_f) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
+  LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
+         out->val);
+  TA.crp = out->row_ptr; TA.ccol = out->col; TA.cval = out->val;
+  if (n_small > 0) LAUNCH(h, k_tile_small<true>, gtile, TILE_THREADS, tile_smem, TA);
+  WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
+  WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
+  if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
+  if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
+  LA.crp = out->row_ptr; LA.cval = out->val;
+  LAUNCH(h, k_num_large<4>, glarge, 128, 0, LA);
+  LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
   return AGIPC_OK;
 }
