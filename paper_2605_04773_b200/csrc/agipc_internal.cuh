@@ -35,6 +35,9 @@ enum ProfPhase {
   PROF_PCG_SPMV,
   PROF_PCG_UPDATE,
   PROF_PCG_SOLVE,
+  PROF_ASM_CLASSIFY,
+  PROF_ASM_SYMBOLIC,
+  PROF_ASM_NUMERIC,
   PROF_N
 };
 

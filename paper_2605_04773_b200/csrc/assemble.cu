@@ -21,6 +21,7 @@
 //      chunks that keep the 12x12 diagonal block in registers (lane = (block group, p)) and
 //      flush it with one fp64 atomic per entry per chunk.
 #include <climits>
+#include <memory>
 
 #include "agipc_internal.cuh"
 
@@ -38,6 +39,7 @@ struct AsmScal {
   long long nbs_count;   // entries used in the small-node neighbour buffer
   long long pair_count;  // (large, x) pairs
   long long big_groups;  // large lists that need the CTA sort
+  long long n_large3;    // large nodes with 3 DoF (affine threshold > 32)
   int err_map;           // map value outside [0, n_c)
   int err_overflow;      // a buffer capacity was exceeded
 };
@@ -141,12 +143,13 @@ __global__ void k_children(int64_t N, const int32_t *__restrict__ nm, const int6
 
 __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
                            const unsigned long long *__restrict__ rowsum, uint8_t *__restrict__ is_small,
-                           int32_t *__restrict__ ntasks) {
+                           int32_t *__restrict__ ntasks, AsmScal *sc) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n_c) {
     bool s = size_new[c] <= SMALL_CHILDREN && rowsum[c] <= SMALL_T;
     is_small[c] = s;
     ntasks[c] = s ? 0 : (int32_t)((size_new[c] + LARGE_CHUNK - 1) / LARGE_CHUNK);
+    if (!s && c < sc->n3) atomicAdd((unsigned long long *)&sc->n_large3, 1ull);
   }
 }
 
@@ -242,284 +245,6 @@ __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t 
 // ------------------------------------------------------------------------------------
 // B. symbolic
 // ------------------------------------------------------------------------------------
-// Small coarse nodes are processed in CTA tiles of ~TILE_E consecutive candidate entries
-// (many nodes per tile): every entry (child row i, stored block k) gets the key
-// (local node, new_map[col k], entry) and one CTA-wide bitonic sort in shared memory groups
-// equal (node, column) runs.  The symbolic pass counts the runs per node (row length; 12-DoF
-// columns count 4) and emits the transposed (large column, small node) pairs; the numeric
-// pass repeats the sort and sums each run into its final position.
-#define TILE_THREADS 512
-#define TILE_E 1024            // target entries per tile
-#define TILE_CAP 2048          // max entries per tile (a small node has <= SMALL_T entries)
-
-struct TileArgs {
-  int64_t n_small;
-  const int32_t *small_list;   // small coarse node ids (ascending)
-  const int64_t *e_off;        // [n_small + 1] exclusive prefix of their candidate entries
-  const int32_t *child_list;
-  const int64_t *child_ptr;
-  const int32_t *size_new;
-  const uint8_t *is_small;
-  const int64_t *rp;
-  const int32_t *col;
-  const double *val;
-  const int32_t *nm;
-  const double *X;
-  const double *g_f;
-  const AsmScal *sc;
-  int32_t *rowlen;             // symbolic out (per coarse node)
-  int2 *pairs;                 // symbolic out: (large col, small node)
-  long long pair_cap;
-  AsmScal *scw;
-  // numeric
-  const int32_t *gbuf;         // large-node lists
-  const long long *nb_off;
-  const int32_t *nb_cnt;
-  const int64_t *crp;
-  int32_t *ccol;
-  double *cval;
-  double *g_c;
-};
-
-struct AsmTileSmem {
-  unsigned long long key[TILE_CAP];
-  int row_off[TILE_CAP + 1];   // entry offset of each child row in the tile
-  long long row_rb[TILE_CAP];  // first stored block of the row
-  int row_ci[TILE_CAP];        // fine node of the row
-  int node_row0[TILE_CAP + 1]; // first row of each local node
-  int node_e0[TILE_CAP + 1];   // first entry of each local node
-  int cp[TILE_CAP + 1];        // exclusive scan of the run weights
-  int erow[TILE_CAP];          // child row of every (unsorted) entry
-  int red[TILE_THREADS / 32];
-  int tot;
-};
-
-__device__ __forceinline__ int tile_upper(const int *a, int n, int key) {  // last i with a[i] <= key
-  int lo = 0, hi = n;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] <= key) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-// block-wide exclusive scan of v (one value per thread); returns the exclusive prefix, total in S.tot
-__device__ __forceinline__ int block_excl_scan(AsmTileSmem &S, int v) {
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int incl = warp_incl_scan(v);
-  if (l == 31) S.red[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    const int c = l < TILE_THREADS / 32 ? S.red[l] : 0;
-    const int ci = warp_incl_scan(c);
-    if (l < TILE_THREADS / 32) S.red[l] = ci - c;
-    if (l == 31) S.tot = ci;
-  }
-  __syncthreads();
-  const int r = S.red[w] + incl - v;
-  __syncthreads();
-  return r;
-}
-
-template <bool NUMERIC>
-__global__ void __launch_bounds__(TILE_THREADS) k_tile_small(TileArgs A) {
-  extern __shared__ unsigned char smem_raw[];
-  AsmTileSmem &S = *reinterpret_cast<AsmTileSmem *>(smem_raw);
-  const long long n3 = A.sc->n3;
-  const int64_t etot = A.e_off[A.n_small];
-  const int64_t ntiles = (etot + TILE_E - 1) / TILE_E;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    // nodes whose first entry falls in [t*TILE_E, (t+1)*TILE_E)
-    const int64_t s0 = lower_bound_dev<int64_t>(A.e_off, (int)A.n_small + 1, t * TILE_E);
-    const int64_t s1 = lower_bound_dev<int64_t>(A.e_off, (int)A.n_small + 1, (t + 1) * TILE_E);
-    const int nn = (int)(min(s1, A.n_small) - s0);
-    if (nn <= 0) continue;
-    const int E = (int)(A.e_off[s0 + nn] - A.e_off[s0]);
-    // local nodes: first row and first entry (children rows are contiguous per node)
-    int nrow = 0, ne = 0;
-    const int per = (nn + TILE_THREADS - 1) / TILE_THREADS;
-    {
-      int rsum = 0;
-      for (int q = threadIdx.x * per; q < min(nn, (threadIdx.x + 1) * per); ++q) rsum += A.size_new[A.small_list[s0 + q]];
-      int run = block_excl_scan(S, rsum);
-      nrow = S.tot;
-      for (int q = threadIdx.x * per; q < min(nn, (threadIdx.x + 1) * per); ++q) {
-        S.node_row0[q] = run;
-        S.node_e0[q] = (int)(A.e_off[s0 + q] - A.e_off[s0]);
-        run += A.size_new[A.small_list[s0 + q]];
-      }
-      if (threadIdx.x == 0) {
-        S.node_row0[nn] = nrow;
-        S.node_e0[nn] = E;
-      }
-    }
-    __syncthreads();
-    // child rows: fine node, first block, entry offset
-    const int rper = (nrow + TILE_THREADS - 1) / TILE_THREADS;
-    {
-      int esum = 0;
-      for (int r = threadIdx.x * rper; r < min(nrow, (threadIdx.x + 1) * rper); ++r) {
-        const int q = tile_upper(S.node_row0, nn, r);
-        const int a = A.small_list[s0 + q];
-        const int ci = A.child_list[A.child_ptr[a] + (r - S.node_row0[q])];
-        const long long rb = A.rp[ci];
-        S.row_ci[r] = ci;
-        S.row_rb[r] = rb;
-        esum += (int)(A.rp[ci + 1] - rb);
-      }
-      int run = block_excl_scan(S, esum);
-      ne = S.tot;
-      for (int r = threadIdx.x * rper; r < min(nrow, (threadIdx.x + 1) * rper); ++r) {
-        S.row_off[r] = run;
-        run += (int)(A.rp[S.row_ci[r] + 1] - S.row_rb[r]);
-      }
-      if (threadIdx.x == 0) S.row_off[nrow] = ne;
-    }
-    __syncthreads();
-    // keys: (local node, coarse column, entry)
-    const int P = next_pow2(max(E, 2));
-    for (int e = threadIdx.x; e < P; e += TILE_THREADS) {
-      unsigned long long key = ~0ull;
-      if (e < E) {
-        const int r = tile_upper(S.row_off, nrow, e);
-        S.erow[e] = r;
-        const int q = tile_upper(S.node_row0, nn, r);
-        const int b = A.nm[A.col[S.row_rb[r] + (e - S.row_off[r])]];
-        key = ((unsigned long long)q << 43) | ((unsigned long long)(unsigned)b << 12) | (unsigned long long)e;
-      }
-      S.key[e] = key;
-    }
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += TILE_THREADS) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const unsigned long long x = S.key[i], y = S.key[ixj];
-            const bool up = (i & k) == 0;
-            if ((x > y) == up) {
-              S.key[i] = y;
-              S.key[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    // column position of every run head (run = equal (node, column)) inside its node's row;
-    // 12-DoF columns take 4 slots
-    {
-      const int eper = (E + TILE_THREADS - 1) / TILE_THREADS;
-      int wsum = 0;
-      for (int e = threadIdx.x * eper; e < min(E, (threadIdx.x + 1) * eper); ++e) {
-        const unsigned long long kk = S.key[e];
-        const bool head = e == 0 || (S.key[e - 1] >> 12) != (kk >> 12);
-        const int b = (int)((kk >> 12) & 0x7fffffffull);
-        wsum += head ? (b >= n3 ? 4 : 1) : 0;
-      }
-      int run = block_excl_scan(S, wsum);
-      for (int e = threadIdx.x * eper; e < min(E, (threadIdx.x + 1) * eper); ++e) {
-        const unsigned long long kk = S.key[e];
-        const bool head = e == 0 || (S.key[e - 1] >> 12) != (kk >> 12);
-        const int b = (int)((kk >> 12) & 0x7fffffffull);
-        S.cp[e] = run;
-        run += head ? (b >= n3 ? 4 : 1) : 0;
-      }
-      if (threadIdx.x == 0) S.cp[E] = S.tot;
-      __syncthreads();
-    }
-    if (!NUMERIC) {
-      for (int q = threadIdx.x; q < nn; q += TILE_THREADS)
-        A.rowlen[A.small_list[s0 + q]] = S.cp[S.node_e0[q + 1]] - S.cp[S.node_e0[q]];
-      for (int e = threadIdx.x; e < E; e += TILE_THREADS) {
-        const unsigned long long kk = S.key[e];
-        if (e > 0 && (S.key[e - 1] >> 12) == (kk >> 12)) continue;
-        const int b = (int)((kk >> 12) & 0x7fffffffull);
-        if (!A.is_small[b]) {  // transposed pair (large column, small node)
-          const int a = A.small_list[s0 + (int)(kk >> 43)];
-          const long long pos = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, 1ull);
-          if (pos < A.pair_cap) A.pairs[pos] = make_int2(b, a);
-          else A.scw->err_overflow = 1;
-        }
-      }
-      __syncthreads();
-    } else {
-      // one thread per output block (run, q): the run head is the last entry whose weight
-      // prefix is <= o (non-head entries carry the next head's prefix)
-      const int O = S.cp[E];
-      for (int o = threadIdx.x; o < O; o += TILE_THREADS) {
-        const int e = tile_upper(S.cp, E, o);
-        const unsigned long long kk = S.key[e];
-        const int qn = (int)(kk >> 43);
-        const int b = (int)((kk >> 12) & 0x7fffffffull);
-        const int a = A.small_list[s0 + qn];
-        const int ncb_a = ncb_of(a, n3);
-        const int qq = o - S.cp[e];
-        const int colp = S.cp[e] - S.cp[S.node_e0[qn]] + qq;
-        int e_end = e + 1;
-        while (e_end < E && (S.key[e_end] >> 12) == (kk >> 12)) ++e_end;
-        const bool mirror = !A.is_small[b];
-        long long mrow = 0;
-        if (mirror) {  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
-          const int32_t *lb_ = A.gbuf + A.nb_off[b];
-          const int Ub = A.nb_cnt[b];
-          mrow = A.crp[slot_of(b, qq, n3)] +
-                 colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
-        }
-        for (int p = 0; p < ncb_a; ++p) {
-          double acc[9];
-#pragma unroll
-          for (int x = 0; x < 9; ++x) acc[x] = 0.0;
-          for (int ee = e; ee < e_end; ++ee) {
-            const int el = (int)(S.key[ee] & 0xfffull);
-            const int r = S.erow[el];
-            const long long k = S.row_rb[r] + (el - S.row_off[r]);
-            const int i = S.row_ci[r];
-            const int j = A.col[k];
-            const double coef = wgt(A.X, i, ncb_a, p) * wgt(A.X, j, b >= n3 ? 4 : 1, qq);
-            const double *B = A.val + 9 * k;
-#pragma unroll
-            for (int x = 0; x < 9; ++x) acc[x] += coef * __ldg(B + x);
-          }
-          const long long pos = A.crp[slot_of(a, p, n3)] + colp;
-          A.ccol[pos] = slot_of(b, qq, n3);
-          double *dst = A.cval + 9 * pos;
-#pragma unroll
-          for (int x = 0; x < 9; ++x) dst[x] = acc[x];
-          if (mirror) {
-            double *mt = A.cval + 9 * (mrow + p);
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = acc[3 * cc + r];
-          }
-        }
-      }
-      // g_c of the tile's nodes (Eq 4): thread per node over its children
-      if (A.g_f) {
-        for (int q = threadIdx.x; q < nn; q += TILE_THREADS) {
-          const int a = A.small_list[s0 + q];
-          const int ncb_a = ncb_of(a, n3);
-          for (int p = 0; p < ncb_a; ++p) {
-            double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-            for (int r = S.node_row0[q]; r < S.node_row0[q + 1]; ++r) {
-              const int i = S.row_ci[r];
-              const double wi = wgt(A.X, i, ncb_a, p);
-              g0 += wi * A.g_f[3 * (int64_t)i];
-              g1 += wi * A.g_f[3 * (int64_t)i + 1];
-              g2 += wi * A.g_f[3 * (int64_t)i + 2];
-            }
-            double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
-            gc[0] = g0;
-            gc[1] = g1;
-            gc[2] = g2;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // Large nodes: 32-children chunks emit (a, b) for every large column b != a (warp de-dup with
 // __match_any_sync; duplicates across chunks are removed by the per-node sort), and (a, a).
 struct LargeArgs {
@@ -910,6 +635,146 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Mid-size small nodes (> 32 and <= 1024 candidate entries, <= 32 children): one warp per
+// node; (column, entry) keys sorted in shared memory by a warp-synchronous bitonic sort; the
+// symbolic pass counts runs, the numeric pass gives each run to a lane.
+// ------------------------------------------------------------------------------------
+#define MID_WARPS 4
+#define MID_CAP 1024
+
+template <bool NUMERIC>
+__global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
+  __shared__ ChildTab s_tab[MID_WARPS];
+  __shared__ long long s_key[MID_WARPS][MID_CAP];
+  const int w = threadIdx.x >> 5, l = lane_id();
+  ChildTab &tab = s_tab[w];
+  long long *key = s_key[w];
+  const long long n3 = A.sc->n3;
+  for (int64_t wi = (int64_t)blockIdx.x * MID_WARPS + w; wi < A.n_w; wi += (int64_t)gridDim.x * MID_WARPS) {
+    const int a = A.wlist[wi];
+    const int s = A.size_new[a];
+    const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);  // T <= MID_CAP
+    const int P = next_pow2(T);
+    for (int e = l; e < P; e += 32) {
+      long long kk = LLONG_MAX;
+      if (e < T) {
+        int c;
+        long long k;
+        entry_of(tab, s, e, c, k);
+        kk = ((long long)A.nm[A.col[k]] << 10) | e;
+      }
+      key[e] = kk;
+    }
+    __syncwarp();
+    for (int kq = 2; kq <= P; kq <<= 1)
+      for (int j = kq >> 1; j > 0; j >>= 1) {
+        for (int i = l; i < P; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const long long x = key[i], y = key[ixj];
+            if ((x > y) == ((i & kq) == 0)) {
+              key[i] = y;
+              key[ixj] = x;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    // runs of equal column; colpos = prefix of the run weights (12-DoF columns count 4)
+    int run_base = 0;
+    for (int e0 = 0; e0 < T; e0 += 32) {
+      const int e = e0 + l;
+      const long long kk = e < T ? key[e] : LLONG_MAX;
+      const int b = (int)(kk >> 10);
+      const bool head = e < T && (e == 0 || (key[e - 1] >> 10) != (kk >> 10));
+      const int wgt_b = head ? ncb_of(b, n3) : 0;
+      const int incl = warp_incl_scan(wgt_b);
+      const int cp = run_base + incl - wgt_b;
+      run_base += __shfl_sync(FULL_MASK, incl, 31);
+      if (!NUMERIC) {
+        const bool emit = head && !A.is_small[b];  // transposed pair (large column, small node)
+        const unsigned m = __ballot_sync(FULL_MASK, emit);
+        if (m) {
+          long long pb = 0;
+          if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
+          pb = __shfl_sync(FULL_MASK, pb, 0);
+          if (emit) {
+            const long long pos = pb + __popc(m & ((1u << l) - 1u));
+            if (pos < A.pair_cap) A.pairs[pos] = make_int2(b, a);
+            else A.scw->err_overflow = 1;
+          }
+        }
+        continue;
+      }
+      if (!head) continue;
+      int e_end = e + 1;
+      while (e_end < T && (key[e_end] >> 10) == (kk >> 10)) ++e_end;
+      const int ncb_a = ncb_of(a, n3), ncb_b = ncb_of(b, n3);
+      long long mbase = -1;  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
+      if (!A.is_small[b]) {
+        const int32_t *lb_ = A.gbuf + A.nb_off[b];
+        const int Ub = A.nb_cnt[b];
+        mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
+      }
+      for (int p = 0; p < ncb_a; ++p) {
+        const long long rs = A.crp[slot_of(a, p, n3)];
+        for (int q = 0; q < ncb_b; ++q) {
+          double acc[9];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) acc[x] = 0.0;
+          for (int ee = e; ee < e_end; ++ee) {
+            const int el = (int)(key[ee] & 1023);
+            int c;
+            long long k;
+            entry_of(tab, s, el, c, k);
+            const double coef = wgt(A.X, tab.ci[c], ncb_a, p) * wgt(A.X, A.col[k], ncb_b, q);
+            const double *B = A.val + 9 * k;
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[x] += coef * __ldg(B + x);
+          }
+          const long long pos = rs + cp + q;
+          A.ccol[pos] = slot_of(b, q, n3);
+          double *dst = A.cval + 9 * pos;
+#pragma unroll
+          for (int x = 0; x < 9; ++x) dst[x] = acc[x];
+          if (mbase >= 0) {
+            double *mt = A.cval + 9 * (A.crp[slot_of(b, q, n3)] + mbase + p);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = acc[3 * cc + r];
+          }
+        }
+      }
+    }
+    if (NUMERIC && A.g_f) {
+      const int ncb_a = ncb_of(a, n3);
+      for (int p = 0; p < ncb_a; ++p) {
+        double g0 = 0, g1 = 0, g2 = 0;
+        if (l < s) {
+          const int ci = tab.ci[l];
+          const double wc = wgt(A.X, ci, ncb_a, p);
+          g0 = wc * A.g_f[3 * (int64_t)ci];
+          g1 = wc * A.g_f[3 * (int64_t)ci + 1];
+          g2 = wc * A.g_f[3 * (int64_t)ci + 2];
+        }
+        g0 = warp_sum(g0);
+        g1 = warp_sum(g1);
+        g2 = warp_sum(g2);
+        if (l == 0) {
+          double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
+          gc[0] = g0;
+          gc[1] = g1;
+          gc[2] = g2;
+        }
+      }
+    }
+    if (!NUMERIC && l == 0) A.rowlen[a] = run_base;
+    __syncwarp();
+  }
+}
+
 // split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
 __global__ void k_small_flags(int64_t n_c, const uint8_t *__restrict__ is_small,
                               const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ f16,
@@ -983,14 +848,15 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 #define LSTAGE 512
 
 template <int NCB>
-__global__ void __launch_bounds__(128) k_num_large(LargeArgs A) {
+__global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE];
   __shared__ int s_i[4][LSTAGE];
   __shared__ int s_j[4][LSTAGE];
   const int w = threadIdx.x >> 5, l = lane_id();
-  constexpr int G = 32 / NCB;
-  const int gq = l / NCB, p = l % NCB;
+  // lane = (block group, p, q half): NCB = 4 -> 8 lanes per block, 2 q per lane
+  constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
+  const int gq = l / LPB, p = NCB == 4 ? (l >> 1) & 3 : 0, q0 = NCB == 4 ? (l & 1) * 2 : 0;
   const long long n3 = A.sc->n3;
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
@@ -1003,9 +869,9 @@ __global__ void __launch_bounds__(128) k_num_large(LargeArgs A) {
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
     const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
-    double acc[NCB][9];
+    double acc[QN][9];
 #pragma unroll
-    for (int q = 0; q < NCB; ++q)
+    for (int q = 0; q < QN; ++q)
 #pragma unroll
       for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
     for (int base = 0; base < T; base += LSTAGE) {
@@ -1056,41 +922,36 @@ __global__ void __launch_bounds__(128) k_num_large(LargeArgs A) {
         const long long k0 = s_k[w][d], k1 = two ? s_k[w][d + G] : k0;
         const int i0 = s_i[w][d], i1 = two ? s_i[w][d + G] : i0;
         const int j0 = s_j[w][d], j1 = two ? s_j[w][d + G] : j0;
-        double B0[9], B1[9], wj0[NCB], wj1[NCB];
+        double B0[9], B1[9];
 #pragma unroll
         for (int x = 0; x < 9; ++x) {
           B0[x] = __ldg(A.val + 9 * k0 + x);
           B1[x] = __ldg(A.val + 9 * k1 + x);
         }
+        const double wi0 = wgt(A.X, i0, NCB, p), wi1 = two ? wgt(A.X, i1, NCB, p) : 0.0;
 #pragma unroll
-        for (int q = 0; q < NCB; ++q) {
-          wj0[q] = wgt(A.X, j0, NCB, q);
-          wj1[q] = two ? wgt(A.X, j1, NCB, q) : 0.0;
-        }
-        const double wi0 = wgt(A.X, i0, NCB, p), wi1 = wgt(A.X, i1, NCB, p);
+        for (int qq = 0; qq < QN; ++qq) {
+          const double c0 = wi0 * wgt(A.X, j0, NCB, q0 + qq), c1 = wi1 * wgt(A.X, j1, NCB, q0 + qq);
 #pragma unroll
-        for (int q = 0; q < NCB; ++q) {
-          const double c0 = wi0 * wj0[q], c1 = wi1 * wj1[q];
-#pragma unroll
-          for (int x = 0; x < 9; ++x) acc[q][x] += c0 * B0[x] + c1 * B1[x];
+          for (int x = 0; x < 9; ++x) acc[qq][x] += c0 * B0[x] + c1 * B1[x];
         }
       }
       __syncwarp();
     }
-    // reduce over the block groups (lanes with the same p) and flush the diagonal block
+    // reduce over the block groups (lanes with the same p, q half) and flush the diagonal block
 #pragma unroll
-    for (int o = NCB; o < 32; o <<= 1)
+    for (int o = LPB; o < 32; o <<= 1)
 #pragma unroll
-      for (int q = 0; q < NCB; ++q)
+      for (int qq = 0; qq < QN; ++qq)
 #pragma unroll
-        for (int x = 0; x < 9; ++x) acc[q][x] += __shfl_xor_sync(FULL_MASK, acc[q][x], o);
+        for (int x = 0; x < 9; ++x) acc[qq][x] += __shfl_xor_sync(FULL_MASK, acc[qq][x], o);
     if (gq == 0) {
       const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, a), first12);
       const long long rs = A.crp[slot_of(a, p, n3)];
 #pragma unroll
-      for (int q = 0; q < NCB; ++q)
+      for (int qq = 0; qq < QN; ++qq)
 #pragma unroll
-        for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q) + x, acc[q][x]);
+        for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q0 + qq) + x, acc[qq][x]);
     }
     if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
       for (int pp = 0; pp < NCB; ++pp) {
@@ -1156,6 +1017,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   agipc_status st;
 
   WS(h, sc, AsmScal, "asm_scal", 1);
+  std::unique_ptr<ProfScope> ps_classify(new ProfScope(h, PROF_ASM_CLASSIFY, st_));
   CU_TRY(h, cudaMemsetAsync(sc, 0, sizeof(AsmScal), st_));
   // ---- A. classification ----
   WS(h, size, int32_t, "asm_size", n_c);
@@ -1186,7 +1048,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, size_new, n_c, child_ptr)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(cursor, child_ptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
   LAUNCH(h, k_children, gN, 256, 0, N, out->new_map, H->row_ptr, cursor, child_list, rowsum);
-  LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks);
+  LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks, sc);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
   // small nodes: the warp list (<= 32 candidate entries) and the tile list (> 32, with the
   // prefix of their entries)
@@ -1211,6 +1073,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   const int64_t n_small = h_small[0], n_w16 = h_small[1], n_w32 = h_small[2];
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I64, ecount, n_small, e_off)) != AGIPC_OK) return st;
 
+  ps_classify.reset();
+  std::unique_ptr<ProfScope> ps_sym(new ProfScope(h, PROF_ASM_SYMBOLIC, st_));
   // ---- B. symbolic ----
   const long long pair_cap = nnzb_f + n_c + 32;
   WS(h, nb_off, long long, "asm_nb_off", n_c);
@@ -1223,34 +1087,27 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, gbuf, int32_t, "asm_gbuf", 2 * pair_cap);
   WS(h, big_list, int32_t, "asm_big_list", n_c);
   const int64_t task_bound = N / LARGE_CHUNK + n_c;
-  TileArgs TA;
-  TA.n_small = n_small; TA.small_list = small_list; TA.e_off = e_off; TA.child_list = child_list;
-  TA.child_ptr = child_ptr; TA.size_new = size_new; TA.is_small = is_small; TA.rp = H->row_ptr; TA.col = H->col;
-  TA.val = H->val; TA.nm = out->new_map; TA.X = mesh->x_rest; TA.g_f = (g_fine && out->g_c) ? g_fine : nullptr;
-  TA.sc = sc; TA.rowlen = rowlen; TA.pairs = pairs; TA.pair_cap = pair_cap; TA.scw = sc;
-  TA.gbuf = gbuf; TA.nb_off = nb_off; TA.nb_cnt = nb_cnt; TA.crp = nullptr; TA.ccol = nullptr; TA.cval = nullptr;
-  TA.g_c = out->g_c;
-  const size_t tile_smem = sizeof(AsmTileSmem);
-  CU_TRY(h, cudaFuncSetAttribute(k_tile_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
-  CU_TRY(h, cudaFuncSetAttribute(k_tile_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
-  const unsigned gtile = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(nnzb_f, TILE_E) + 1, 4 * h->sm_count));
-  if (n_small > 0) LAUNCH(h, k_tile_small<false>, gtile, TILE_THREADS, tile_smem, TA);
+  const double *gfp = (g_fine && out->g_c) ? g_fine : nullptr;
   WarpArgs WA;
   WA.n_w = n_w16; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
   WA.is_small = is_small; WA.rp = H->row_ptr; WA.col = H->col; WA.val = H->val; WA.nm = out->new_map;
-  WA.X = mesh->x_rest; WA.g_f = TA.g_f; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
+  WA.X = mesh->x_rest; WA.g_f = gfp; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
-  WarpArgs WB = WA;
+  WarpArgs WB = WA, WM;
   WB.n_w = n_w32; WB.wlist = w32;
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
   const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
+  WM = WA;
+  WM.n_w = n_small; WM.wlist = small_list;
+  const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_small, MID_WARPS), 32 * h->sm_count));
+  if (n_small > 0) LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
-  LA.g_f = TA.g_f; LA.task_ptr = task_ptr; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
+  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
   LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
@@ -1289,18 +1146,20 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     return set_err(h, AGIPC_EINVAL, "assemble_coarse: null output arrays");
   CU_TRY(h, cudaMemcpyAsync(out->row_ptr, crp_ws, sizeof(int64_t) * (out->n_slots + 1), cudaMemcpyDeviceToDevice, st_));
 
+  ps_sym.reset();
+  ProfScope ps_num(h, PROF_ASM_NUMERIC, st_);
   // ---- D. numeric ----
-  if (TA.g_f) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
+  if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
   LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
          out->val);
-  TA.crp = out->row_ptr; TA.ccol = out->col; TA.cval = out->val;
-  if (n_small > 0) LAUNCH(h, k_tile_small<true>, gtile, TILE_THREADS, tile_smem, TA);
+  WM.crp = out->row_ptr; WM.ccol = out->col; WM.cval = out->val;
+  if (n_small > 0) LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
   WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
   WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
   LAUNCH(h, k_num_large<4>, glarge, 128, 0, LA);
-  LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
+  if (hsc->n_large3 > 0) LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
   return AGIPC_OK;
 }
