@@ -10,6 +10,7 @@
  *                             with affine 12-DoF nodes (supp Alg S4, Eq S2/S3, P:258-319;
  *                             main Eq 4)
  *   4. agipc_pcg_solve        block-Jacobi PCG on the coarse system
+ *   5. agipc_prolongate       d_f = U^T d_c back to the fine nodes (NEXT#1)
  *
  * Conventions (all entry points):
  *  - Array arguments are DEVICE pointers owned by the caller (e.g. PyTorch CUDA tensors,
@@ -204,6 +205,25 @@ typedef struct {
 AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const double *b, double *x,
                                        int zero_x0, double rel_tol, int max_iters, int check_every,
                                        agipc_pcg_stats *stats);
+
+/* ---- NEXT#1: prolongation d_f = U^T d_c ------------------------------------------------
+ * "we mathematically prolongate the displacement to the fine mesh using the transpose of
+ * the restriction operator" (main Sec 4.3).  For every fine node f with parent
+ * c = new_map[f]:
+ *   c <  n3 : d_f[f] = alpha * x_c[c]
+ *   c >= n3 : d_f[f] = alpha * sum_{p<4} w_f[p] x_c[n3 + 4(c-n3) + p],  w_f = (X_bar_f, 1)
+ * (A_f^T applied to the 12 coarse DoFs, A_f = [X_bar^T 1] (x) I3).  alpha = -1 turns
+ * the coarse solution y of H_c y = g_c into the fine direction of P:752 in the same pass.
+ * The post-coarsening fine PCG (<= 10 iterations) is agipc_pcg_solve on H_f with
+ * this d_f as x0 (zero_x0 = 0).
+ *   mesh    : n_nodes, x_rest [N][3] (the X_bar of assemble) -- the other fields are unused
+ *   new_map : [N] as written by agipc_assemble_coarse; n3 = out->n3, n_slots = out->n_slots
+ *             (entries outside [0, n3 + (n_slots-n3)/4) give AGIPC_EINVAL, d_f unspecified)
+ *   x_c     : [n_slots][3] coarse vector;  d_f : [N][3] out.
+ * Asynchronous on the handle's stream except for the error check (one 4-byte D2H). */
+AGIPC_API agipc_status agipc_prolongate(agipc_handle h, const agipc_mesh *mesh, const int32_t *new_map,
+                                        int64_t n3, int64_t n_slots, const double *x_c, double alpha,
+                                        double *d_f);
 
 #ifdef __cplusplus
 }

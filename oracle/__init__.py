@@ -52,6 +52,8 @@ def lib():
         L.orc_spmv.argtypes = [i64, P, P, P, P, P]
         L.orc_block_jacobi.argtypes = [i64, P, P, P, P, P]
         L.orc_block_jacobi.restype = i32
+        L.orc_prolongate.argtypes = [i64, P, i64, P, P, P]
+        L.orc_prolongate.restype = None
         _lib = L
     return _lib
 
@@ -191,3 +193,12 @@ def block_jacobi(row_ptr, col, val):
     if st != OK:
         raise OracleError(st, f"row {int(bad[0])}")
     return D[:9 * n].reshape(n, 3, 3)
+
+
+def prolongate(new_map, n3, X, x_c):
+    """NEXT#1: d_f = U^T d_c.  Returns float64 [N,3]."""
+    nm = _c(new_map, np.int32); X = _c(X, np.float64); xc = _c(x_c, np.float64)
+    N = nm.shape[0]
+    d = np.empty((N, 3))
+    lib().orc_prolongate(N, _p(nm), int(n3), _p(X), _p(xc), _p(d))
+    return d

@@ -521,3 +521,28 @@ void orc_spmv(int64_t n, const int64_t *rp, const int32_t *col, const double *va
               double *y) {
   bsr_spmv(n, rp, col, val, x, y);
 }
+
+/* ========================================================================== */
+/* NEXT#1 -- prolongation d_f = U^T d_c (main Sec 4.3: "we mathematically */
+/* prolongate the displacement to the fine mesh using the transpose of the     */
+/* restriction operator").  For a 3-DoF parent d_f = d_c[c]; for a 12-DoF parent */
+/* d_f = sum_p X_bar_f[p] d_c[slot(c,p)] (A_f^T d_c, A_f = X_bar (x) I3). */
+/* ========================================================================== */
+void orc_prolongate(int64_t N, const int32_t *new_map, int64_t n3, const double *X, const double *x_c,
+                    double *d_f) {
+  for (int64_t f = 0; f < N; ++f) {
+    int64_t c = new_map[f];
+    for (int d = 0; d < 3; ++d) {
+      double s = 0.0;
+      if (c < n3) {
+        s = x_c[3 * c + d];
+      } else {
+        for (int p = 0; p < 4; ++p) {
+          double w = p < 3 ? X[3 * f + p] : 1.0;
+          s += w * x_c[3 * (n3 + 4 * (c - n3) + p) + d];
+        }
+      }
+      d_f[3 * f + d] = s;
+    }
+  }
+}

@@ -66,7 +66,7 @@ class _PcgStats(C.Structure):
 
 EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_error", "agipc_status_string",
            "agipc_version", "agipc_kernel_launches", "agipc_profile", "agipc_profile_read", "agipc_tag_edges",
-           "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve"]
+           "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate"]
 
 
 def lib():
@@ -98,8 +98,9 @@ def lib():
         L.agipc_assemble_coarse.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), P,
                                             C.POINTER(_Coarse)]
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
+        L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         for name in ("agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_tag_edges", "agipc_build_map",
-                     "agipc_assemble_coarse", "agipc_pcg_solve"):
+                     "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -301,3 +302,14 @@ def pcg_solve(h: Handle, row_ptr, col, val, b, x=None, rel_tol: float = 1e-3, ma
                                    int(max_iters), int(check_every), C.byref(stats)), allow=(NOT_CONVERGED,))
     return x, dict(iters=int(stats.iters), status=int(stats.status), rel_residual=float(stats.rel_residual),
                    b_norm=float(stats.b_norm))
+
+
+def prolongate(h: Handle, mesh: DeviceMesh, new_map, n3: int, n_slots: int, x_c, alpha: float = 1.0, out=None):
+    """NEXT#1: d_f = alpha * U^T x_c.  Returns out (float64 [N,3])."""
+    N = mesh.n_nodes
+    if out is None:
+        out = torch.empty((N, 3), dtype=torch.float64, device=x_c.device)
+    ms = mesh.c_struct()
+    h._check(lib().agipc_prolongate(h._h, C.byref(ms), _p(new_map), int(n3), int(n_slots), _p(x_c),
+                                    float(alpha), _p(out)))
+    return out

@@ -38,6 +38,7 @@ enum ProfPhase {
   PROF_ASM_CLASSIFY,
   PROF_ASM_SYMBOLIC,
   PROF_ASM_NUMERIC,
+  PROF_PROLONG,
   PROF_N
 };
 

@@ -95,7 +95,8 @@ static void prof_flush(agipc_handle h) {
 
 static const char *kPhaseNames[PROF_N] = {"tag_edges", "build_map", "assemble_coarse", "pcg_setup",
                                           "pcg_spmv", "pcg_update", "pcg_solve",
-                                          "asm_classify", "asm_symbolic", "asm_numeric"};
+                                          "asm_classify", "asm_symbolic", "asm_numeric",
+                                          "prolongate"};
 
 extern "C" {
 

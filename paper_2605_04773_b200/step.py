@@ -1,5 +1,6 @@
 """One Newton iteration of the coarsening path (main Alg 1 lines 8-10):
-tag -> map -> assemble -> coarse PCG, composed from the four C-ABI calls.  Plumbing only:
+tag -> map -> assemble -> coarse PCG, composed from the four C-ABI calls, optionally followed
+by NEXT#1: prolongation d_f = U^T d_c and <= refine_iters fine PCG iterations from d_f.  Plumbing only:
 all arithmetic runs in libagipc's kernels."""
 from __future__ import annotations
 
@@ -7,7 +8,7 @@ import dataclasses
 
 import torch
 
-from . import (CoarseBuffers, DeviceMesh, Handle, assemble_coarse, build_map, pcg_solve, tag_edges)
+from . import (CoarseBuffers, DeviceMesh, Handle, assemble_coarse, build_map, pcg_solve, prolongate, tag_edges)
 
 
 @dataclasses.dataclass
@@ -17,13 +18,16 @@ class StepResult:
     coarse: object
     x: torch.Tensor
     pcg: dict
+    y_f: torch.Tensor | None = None   # refined fine solution of H_f y = g_f; direction d_f = -y_f (NEXT#1)
+    refine: dict | None = None
 
 
 class CoarseningStep:
     """Holds the device-resident static inputs and grow-only buffers of the path."""
 
     def __init__(self, h: Handle, mesh: DeviceMesh, H_row_ptr, H_col, H_val, group_size=32,
-                 affine_threshold=32, theta=5e-5, rel_tol=1e-3, max_iters=10000, check_every=16):
+                 affine_threshold=32, theta=5e-5, rel_tol=1e-3, max_iters=10000, check_every=16,
+                 refine_iters=0):
         self.h, self.mesh = h, mesh
         self.H = (H_row_ptr, H_col, H_val)
         self.group_size, self.affine_threshold, self.theta = group_size, affine_threshold, theta
@@ -33,6 +37,8 @@ class CoarseningStep:
         self.map = torch.empty(mesh.n_nodes, dtype=torch.int32, device=dev)
         self.bufs = CoarseBuffers(dev, mesh.n_nodes, 4 * mesh.n_nodes // 8 + 16, H_col.shape[0] // 2 + 64)
         self.x = None
+        self.refine_iters = refine_iters
+        self.y_f = torch.empty((mesh.n_nodes, 3), dtype=torch.float64, device=dev)
 
     def coarsen(self, x_prev, x_cur, g_fine, count=False):
         """Steps 1-3.  Returns (n_flagged, map_info, CoarseSystem)."""
@@ -52,7 +58,17 @@ class CoarseningStep:
                           self.check_every, zero_x0=True)
         return x, st
 
+    def refine(self, cs, y_c, g_fine):
+        """NEXT#1: y_f = U^T y_c, then <= refine_iters block-Jacobi PCG iterations on
+        H_f y = g_f from y_f.  CG is linear in (b, x0), so the fine direction is d_f = -y_f."""
+        y = prolongate(self.h, self.mesh, cs.new_map, cs.n3, cs.n_slots, y_c, 1.0, self.y_f)
+        y, st = pcg_solve(self.h, *self.H, g_fine, y, self.rel_tol, self.refine_iters, self.check_every)
+        return y, st
+
     def __call__(self, x_prev, x_cur, g_fine, count=False) -> StepResult:
         nf, info, cs = self.coarsen(x_prev, x_cur, g_fine, count)
         x, st = self.solve(cs)
-        return StepResult(nf, info, cs, x, st)
+        if self.refine_iters <= 0:
+            return StepResult(nf, info, cs, x, st)
+        y, rst = self.refine(cs, x, g_fine)
+        return StepResult(nf, info, cs, x, st, y_f=y, refine=rst)

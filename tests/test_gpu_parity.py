@@ -262,6 +262,79 @@ def test_pcg_not_converged_reports_last_iterate(P, h):
 
 
 # ------------------------------------------------------------------------------------------
+# NEXT#1: prolongation d_f = U^T d_c and the post-coarsening fine PCG
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("thr", [32, 0, 5, 10 ** 9])
+@pytest.mark.parametrize("alpha", [1.0, -1.0, 0.5])
+def test_prolongate_bit_exact(P, h, thr, alpha):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    om = oracle.build_map(m.adj_ptr, m.adj_nbr, synth.random_tags(m, 0.5, 1), 32)
+    oa = oracle.assemble(om["map"], om["n_coarse"], thr, m.X, m.bsr_ptr, m.bsr_col, synth.fine_hessian(m))
+    xc = np.random.default_rng(thr % 97).standard_normal((oa["n_slots"], 3))
+    d = P.prolongate(h, dm, dev(oa["new_map"], torch.int32), oa["n3"], oa["n_slots"], dev(xc, torch.float64), alpha)
+    ref = oracle.prolongate(oa["new_map"], oa["n3"], m.X, xc)
+    # same operation order (w0 x0 + w1 x1 + w2 x2 + x3) on both sides; alpha*s is one rounding
+    assert np.array_equal(d.cpu().numpy(), alpha * ref)
+
+
+def test_prolongate_edge_cases_and_errors(P, h):
+    m = synth.kuhn_grid(4)
+    dm = dmesh(P, m)
+    N = m.n_nodes
+    xc = np.random.default_rng(0).standard_normal((N, 3))
+    d = P.prolongate(h, dm, dev(np.arange(N), torch.int32), N, N, dev(xc, torch.float64))
+    assert np.array_equal(d.cpu().numpy(), xc)                        # identity map: U = I
+    t = np.array([[0.0, 0, 0], [0, 0, 0], [0, 0, 0], [0.25, -1.0, 3.0]])
+    d = P.prolongate(h, dm, dev(np.zeros(N), torch.int32), 0, 4, dev(t, torch.float64))
+    assert np.array_equal(d.cpu().numpy(), np.broadcast_to(t[3], (N, 3)))   # translation
+    bad = np.zeros(N, np.int32); bad[7] = 1
+    with pytest.raises(P.AgipcError) as e:
+        P.prolongate(h, dm, dev(bad, torch.int32), 0, 4, dev(t, torch.float64))
+    assert e.value.status == P.EINVAL
+    with pytest.raises(P.AgipcError) as e:
+        P.prolongate(h, dm, dev(bad, torch.int32), 0, 5, dev(t, torch.float64))   # n_slots-n3 not 4k
+    assert e.value.status == P.EINVAL
+
+
+def test_post_coarsening_cg_matches_oracle(P, h):
+    """Coarse solve -> d_f = U^T d_c -> <= 10 fine block-Jacobi PCG iterations from d_f."""
+    c = synth.config_c1()
+    m = c["mesh"]
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    _, _, om = check_map(P, h, m, dm, c["slot_tags"], 32)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, 32)
+    yc, _ = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-13, max_iters=20000, zero_x0=True)
+    yf = P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, yc)
+    Hd = (dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32), dev(H, torch.float64))
+    y, s = P.pcg_solve(h, *Hd, dev(g, torch.float64), x=yf, rel_tol=1e-3, max_iters=10)
+    rc = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=1e-13, max_iters=20000)
+    y0 = oracle.prolongate(oa["new_map"], oa["n3"], m.X, rc["x"])
+    ref = oracle.pcg(m.bsr_ptr, m.bsr_col, H, g, x0=y0, rel_tol=1e-3, max_iters=10)
+    assert s["iters"] == ref["iters"] and s["status"] == ref["status"]
+    assert np.linalg.norm(y.cpu().numpy() - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
+    # energy of the fine quadratic model decreases from the prolongated start (CG is monotone)
+    e = lambda v: 0.5 * np.sum(v * oracle.spmv(m.bsr_ptr, m.bsr_col, H, v)) - np.sum(g * v)
+    assert e(ref["x"]) <= e(y0) <= 0.0
+
+
+def test_step_with_refinement(P, h):
+    from paper_2605_04773_b200.step import CoarseningStep
+    c = synth.config_c1()
+    m = c["mesh"]
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = dev(synth.fine_gradient(m.n_nodes), torch.float64)
+    st = CoarseningStep(h, dm, dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32), dev(H, torch.float64),
+                        refine_iters=10)
+    r = st(dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64), g)
+    assert r.y_f is not None and r.refine["iters"] <= 10
+    assert float(torch.sum(r.y_f * g)) > 0      # d_f = -y_f is a descent direction of the fine model
+
+
+# ------------------------------------------------------------------------------------------
 # full sizes (C2, C3) in the launch configuration bench.py times
 # ------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("cfg", ["c2", "c3"])
@@ -285,3 +358,7 @@ def test_full_size_path(P, h, cfg):
         _, s3 = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-3, zero_x0=True)
         ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=1e-3, max_iters=10000)
         assert abs(s3["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"]))
+    # prolongation at full size on a seeded coarse vector (bit-exact)
+    xc = np.random.default_rng(5).standard_normal((oa["n_slots"], 3))
+    d = P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, dev(xc, torch.float64), -1.0)
+    assert np.array_equal(d.cpu().numpy(), -oracle.prolongate(oa["new_map"], oa["n3"], m.X, xc))
