@@ -96,9 +96,14 @@ typedef struct {
   const int64_t *adj_ptr;   /* [N+1] symmetric adjacency, no self loops                       */
   const int32_t *adj_nbr;   /* [2E] neighbours, ascending within a row                        */
   const int32_t *tet_slots; /* [T][12] for local edge e in (01,02,03,12,13,23): the adjacency
-                               slot of (u->v) at 2e and of (v->u) at 2e+1                    */
-  const double *x_rest;     /* [N][3] rest positions X; also X_bar = (x,y,z,1) of Eq 4        */
+                               slot of (u->v) at 2e and of (v->u) at 2e+1; -1 = no slot      */
+  const double *x_rest;     /* [N(+ghosts)][3] rest positions X; also X_bar = (x,y,z,1), Eq 4 */
 } agipc_mesh;
+/* Partitioned meshes (multi-GPU): a rank passes its LOCAL mesh -- N = owned nodes
+ * 0..N-1, ghost nodes N.. (non-owned vertices of the tets that touch an owned node).  tets may
+ * reference ghosts, and x_rest / x_prev / x_cur then cover N + n_ghost rows; adjacency rows
+ * and neighbours are owned nodes only; tet_slots is -1 for an edge with a ghost end.  Every
+ * step below then works on the rank's own rows (rank-local recursion, reading R24). */
 
 /* Block sparse row matrix with 3x3 blocks (full storage, ascending columns per row). */
 typedef struct {
@@ -224,6 +229,72 @@ AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const
 AGIPC_API agipc_status agipc_prolongate(agipc_handle h, const agipc_mesh *mesh, const int32_t *new_map,
                                         int64_t n3, int64_t n_slots, const double *x_c, double alpha,
                                         double *d_f);
+
+/* ==== Multi-GPU partitioned path (north star) ==========
+ * One process per GPU; rank r owns a contiguous range of fine nodes and passes its LOCAL mesh
+ * (see agipc_mesh above).  Steps 1-3 run unchanged on the local mesh (H_fine = the rank's rows
+ * x owned columns); the caller moves the buffers below between ranks (torch.distributed /
+ * NCCL: send/recv for halos, all-gather of per-rank counts, all-reduce of the PCG sums).
+ * Global coarse numbering is rank-major: rank r's slots are [S_r, S_r + n_slots_r) with
+ * S_r = exclusive prefix sum of n_slots over ranks (the north star's all-gather exclusive scan),
+ * each rank's own slots ordered 3-DoF then 12-DoF as on one GPU.
+ *
+ * agipc_gather_rows: dst[k] = src[idx[k]] for rows of row_bytes bytes (multiple of 4) -- halo
+ *   send buffers (exchange 1: x_prev/x_cur rows of the send lists; exchange 3: column codes).
+ *
+ * agipc_coarse_halo (owner side of exchange 3): for the fine nodes send_idx[0..n_send) sent to
+ *   one peer, the coarse slots that peer needs -- aggregates in order of first appearance in
+ *   the send list, 1 or 4 consecutive slots each -- into send_slots[0..*n_slots) (this rank's
+ *   local slot ids; pack z at these slots every PCG iteration), and for every sent fine node
+ *   its column code ghost_code[k] = (offset of its aggregate's first slot in that list) |
+ *   (1<<30 if the aggregate is 12-DoF).  Capacity retry: *n_slots > cap_slots => ENOSPACE
+ *   with *n_slots set.  Synchronises.
+ *
+ * agipc_assemble_halo: the Galerkin blocks of this rank's coarse rows x ghost coarse columns
+ *   (Alg S4 + Eq 4 for fine blocks (i owned, j ghost); the off-rank part of U H U^T).
+ *   H_halo: rows = owned fine nodes, col = ghost index g (local node n_nodes + g), ascending.
+ *   ghost_code[g]: the owner's column code (above), received for every ghost.  Peer q's ghosts
+ *   are g in [peer_ghost_ptr[q], peer_ghost_ptr[q+1]) ([host], n_peers+1) and its slots start
+ *   at local column peer_slot_base[q] ([host]; >= n_slots of this rank: ghost slots follow the
+ *   owned slots in the PCG vectors).  Output: BSR over this rank's n_slots rows, columns = local
+ *   ghost-slot columns, ascending; capacity retry on col/val like agipc_assemble_coarse.
+ *   Synchronises.
+ *
+ * Distributed PCG: the 1-GPU iteration split at its reductions.  red is a device double[4]
+ * that the CALLER sums over all ranks (all-reduce) after every setup / spmv / update call:
+ *   setup(A, A_halo, n_ghost_slots, b)    -> red = [r.z, r.r, b.b] partials     (x0 = 0)
+ *   pack(send_slots) -> sendbuf; exchange; spmv(recvbuf = ghost z, red) -> red = [p.q]
+ *   update(red) -> red = [r.z, r.r];  pack + exchange; spmv; ...     status() polls (syncs);
+ *   finish(red, x) consumes the last reduced sums and copies the rank's rows of x.
+ * Every rank applies the same scalar logic to the same reduced sums, so all ranks stop at the
+ * same iteration.  Vectors: owned slots 0..n_rows-1, ghost slots n_rows..n_rows+n_ghost_slots-1
+ * (the recv buffer holds them in that order; A_halo's columns index them). */
+typedef struct {
+  int64_t n_rows, nnzb;  /* [host] out */
+  int64_t cap_nnzb;      /* [host] in  */
+  int64_t *row_ptr;      /* out [n_rows+1] (n_rows = n3 + 4 n12 of this rank) */
+  int32_t *col;          /* out [cap_nnzb] */
+  double *val;           /* out [cap_nnzb][3][3] */
+} agipc_halo_matrix;
+
+AGIPC_API agipc_status agipc_gather_rows(agipc_handle h, const void *src, const int32_t *idx, int64_t n,
+                                         int row_bytes, void *dst);
+AGIPC_API agipc_status agipc_coarse_halo(agipc_handle h, const int32_t *new_map, int64_t n3, int64_t n_coarse,
+                                         const int32_t *send_idx, int64_t n_send, int32_t *ghost_code,
+                                         int32_t *send_slots, int64_t cap_slots, int64_t *n_slots /*[host]*/);
+AGIPC_API agipc_status agipc_assemble_halo(agipc_handle h, const agipc_mesh *mesh, const int32_t *new_map,
+                                           int64_t n3, int64_t n_coarse, const agipc_bsr *H_halo, int64_t n_ghost,
+                                           const int32_t *ghost_code, int n_peers,
+                                           const int64_t *peer_ghost_ptr /*[host]*/,
+                                           const int64_t *peer_slot_base /*[host]*/, agipc_halo_matrix *out);
+AGIPC_API agipc_status agipc_dpcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *A_halo /*nullable*/,
+                                        int64_t n_ghost_slots, const double *b, double rel_tol, int max_iters,
+                                        double *red);
+AGIPC_API agipc_status agipc_dpcg_pack(agipc_handle h, const int32_t *send_slots, int64_t n_send, double *sendbuf);
+AGIPC_API agipc_status agipc_dpcg_spmv(agipc_handle h, const double *recvbuf, double *red);
+AGIPC_API agipc_status agipc_dpcg_update(agipc_handle h, double *red);
+AGIPC_API agipc_status agipc_dpcg_status(agipc_handle h, int *done /*[host]*/, agipc_pcg_stats *stats /*[host]*/);
+AGIPC_API agipc_status agipc_dpcg_finish(agipc_handle h, const double *red, double *x, agipc_pcg_stats *stats);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,9 @@ Entry points (same names as the C ABI, include/agipc.h):
   build_map        step 2, supp Alg S1/S2 + recursion
   assemble_coarse  step 3, supp Alg S3/S4 + Eq 4
   pcg_solve        step 4, block-Jacobi PCG
+  prolongate       NEXT#1, d_f = U^T d_c
+Multi-GPU: gather_rows, coarse_halo, assemble_halo, DistPcg (the rank-local
+pieces; paper_2605_04773_b200.dist drives the exchanges).
 """
 from __future__ import annotations
 
@@ -55,6 +58,11 @@ class _Coarse(C.Structure):
                 ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("g_c", C.c_void_p)]
 
 
+class _HaloMatrix(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("nnzb", C.c_int64), ("cap_nnzb", C.c_int64), ("row_ptr", C.c_void_p),
+                ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
 class _ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("count", C.c_int64), ("total_ms", C.c_double)]
 
@@ -66,7 +74,9 @@ class _PcgStats(C.Structure):
 
 EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_error", "agipc_status_string",
            "agipc_version", "agipc_kernel_launches", "agipc_profile", "agipc_profile_read", "agipc_tag_edges",
-           "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate"]
+           "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate",
+           "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
+           "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish"]
 
 
 def lib():
@@ -99,9 +109,20 @@ def lib():
                                             C.POINTER(_Coarse)]
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
-        for name in ("agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_tag_edges", "agipc_build_map",
-                     "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate"):
-            getattr(L, name).restype = i32
+        L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
+        L.agipc_coarse_halo.argtypes = [P, P, i64, i64, P, i64, P, P, i64, C.POINTER(i64)]
+        L.agipc_assemble_halo.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), i64, P, i32,
+                                          C.POINTER(i64), C.POINTER(i64), C.POINTER(_HaloMatrix)]
+        L.agipc_dpcg_setup.argtypes = [P, C.POINTER(_Bsr), C.POINTER(_Bsr), i64, P, f64, i32, P]
+        L.agipc_dpcg_pack.argtypes = [P, P, i64, P]
+        L.agipc_dpcg_spmv.argtypes = [P, P, P]
+        L.agipc_dpcg_update.argtypes = [P, P]
+        L.agipc_dpcg_status.argtypes = [P, C.POINTER(i32), C.POINTER(_PcgStats)]
+        L.agipc_dpcg_finish.argtypes = [P, P, P, C.POINTER(_PcgStats)]
+        for name in EXPORTS:
+            if name not in ("agipc_last_error", "agipc_status_string", "agipc_version", "agipc_kernel_launches",
+                            "agipc_profile_read"):
+                getattr(L, name).restype = i32
         _lib = L
     return _lib
 
@@ -182,21 +203,22 @@ class DeviceMesh:
     adj_ptr: torch.Tensor    # int64 [N+1]
     adj_nbr: torch.Tensor    # int32 [2E]
     tet_slots: torch.Tensor  # int32 [T,12]
-    x_rest: torch.Tensor     # float64 [N,3]
+    x_rest: torch.Tensor     # float64 [N(+ghosts),3]
+    n_own: int | None = None  # partitioned local mesh: owned nodes (x_rest also holds the ghosts)
 
     @property
     def n_nodes(self):
-        return self.x_rest.shape[0]
+        return self.x_rest.shape[0] if self.n_own is None else self.n_own
 
     def c_struct(self):
         return _Mesh(self.n_nodes, self.tets.shape[0], self.adj_nbr.shape[0], _p(self.tets), _p(self.adj_ptr),
                      _p(self.adj_nbr), _p(self.tet_slots), _p(self.x_rest))
 
     @staticmethod
-    def from_arrays(tets, adj_ptr, adj_nbr, tet_slots, x_rest, device="cuda"):
+    def from_arrays(tets, adj_ptr, adj_nbr, tet_slots, x_rest, device="cuda", n_own=None):
         t = lambda a, dt: torch.as_tensor(a).to(device=device, dtype=dt).contiguous()  # noqa: E731
         return DeviceMesh(t(tets, torch.int32), t(adj_ptr, torch.int64), t(adj_nbr, torch.int32),
-                          t(tet_slots, torch.int32), t(x_rest, torch.float64))
+                          t(tet_slots, torch.int32), t(x_rest, torch.float64), n_own)
 
 
 # ---------------------------------------------------------------------------------------
@@ -313,3 +335,109 @@ def prolongate(h: Handle, mesh: DeviceMesh, new_map, n3: int, n_slots: int, x_c,
     h._check(lib().agipc_prolongate(h._h, C.byref(ms), _p(new_map), int(n3), int(n_slots), _p(x_c),
                                     float(alpha), _p(out)))
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# multi-GPU pieces (include/agipc.h "Multi-GPU partitioned path")
+# ---------------------------------------------------------------------------------------
+def gather_rows(h: Handle, src, idx, out=None):
+    """out[k] = src[idx[k]] (rows of src; halo send buffers)."""
+    n = idx.shape[0]
+    if out is None:
+        out = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    rb = src[0].numel() * src.element_size() if src.shape[0] else 4
+    h._check(lib().agipc_gather_rows(h._h, _p(src), _p(idx), int(n), int(rb), _p(out)))
+    return out
+
+
+def coarse_halo(h: Handle, new_map, n3: int, n_coarse: int, send_idx, ghost_code=None, send_slots=None):
+    """Owner side of exchange 3 for one peer.  Returns (ghost_code int32 [n_send], send_slots int32 [m])."""
+    n = send_idx.shape[0]
+    dev = new_map.device
+    if ghost_code is None:
+        ghost_code = torch.empty(n, dtype=torch.int32, device=dev)
+    cap = 0 if send_slots is None else send_slots.shape[0]
+    ns = C.c_int64(0)
+    for attempt in range(2):
+        st = lib().agipc_coarse_halo(h._h, _p(new_map), int(n3), int(n_coarse), _p(send_idx), int(n), _p(ghost_code),
+                                     _p(send_slots), int(cap), C.byref(ns))
+        if st == ENOSPACE and attempt == 0:
+            cap = int(ns.value)
+            send_slots = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            continue
+        h._check(st)
+        break
+    m = int(ns.value)
+    if send_slots is None:
+        send_slots = torch.empty(0, dtype=torch.int32, device=dev)
+    return ghost_code, send_slots[:m]
+
+
+def assemble_halo(h: Handle, mesh: DeviceMesh, new_map, n3: int, n_coarse: int, H_row_ptr, H_col, H_val,
+                  ghost_code, peer_ghost_ptr, peer_slot_base, cap_nnzb: int = 0):
+    """Halo matrix of this rank's coarse rows x ghost coarse columns.  Returns (row_ptr, col, val)."""
+    n_slots = n3 + 4 * (n_coarse - n3)
+    dev = new_map.device
+    rp = torch.empty(n_slots + 1, dtype=torch.int64, device=dev)
+    col = val = None
+    P = len(peer_slot_base)
+    gp = (C.c_int64 * (P + 1))(*[int(v) for v in peer_ghost_ptr])
+    sb = (C.c_int64 * max(P, 1))(*[int(v) for v in peer_slot_base])
+    ms = mesh.c_struct()
+    bsr = _Bsr(mesh.n_nodes, H_col.shape[0], _p(H_row_ptr), _p(H_col), _p(H_val))
+    n_ghost = ghost_code.shape[0] if ghost_code is not None else 0
+    for attempt in range(2):
+        out = _HaloMatrix(0, 0, cap_nnzb, _p(rp), _p(col), _p(val))
+        st = lib().agipc_assemble_halo(h._h, C.byref(ms), _p(new_map), int(n3), int(n_coarse), C.byref(bsr),
+                                       int(n_ghost), _p(ghost_code), P, gp, sb, C.byref(out))
+        if st == ENOSPACE and attempt == 0:
+            cap_nnzb = int(out.nnzb)
+            col = torch.empty(max(cap_nnzb, 1), dtype=torch.int32, device=dev)
+            val = torch.empty((max(cap_nnzb, 1), 3, 3), dtype=torch.float64, device=dev)
+            continue
+        h._check(st)
+        break
+    nb = int(out.nnzb)
+    if col is None:
+        col = torch.empty(0, dtype=torch.int32, device=dev)
+        val = torch.empty((0, 3, 3), dtype=torch.float64, device=dev)
+    return rp, col[:nb], val[:nb]
+
+
+class DistPcg:
+    """The rank-local half of the distributed PCG (agipc_dpcg_*).  `red` (device float64[4]) must
+    be summed over the ranks after setup / spmv / update (see dist.Comm.allreduce_)."""
+
+    def __init__(self, h: Handle, row_ptr, col, val, h_row_ptr, h_col, h_val, n_ghost_slots: int, b,
+                 rel_tol: float, max_iters: int):
+        self.h = h
+        n = row_ptr.shape[0] - 1
+        self.n = n
+        self.red = torch.zeros(4, dtype=torch.float64, device=b.device)
+        self._A = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), _p(val))
+        self._Ah = None if h_row_ptr is None else _Bsr(n, h_col.shape[0], _p(h_row_ptr), _p(h_col), _p(h_val))
+        self._keep = (row_ptr, col, val, h_row_ptr, h_col, h_val, b)
+        h._check(lib().agipc_dpcg_setup(h._h, C.byref(self._A), C.byref(self._Ah) if self._Ah is not None else None,
+                                        int(n_ghost_slots), _p(b), float(rel_tol), int(max_iters), _p(self.red)))
+
+    def pack(self, send_slots, sendbuf):
+        self.h._check(lib().agipc_dpcg_pack(self.h._h, _p(send_slots), int(send_slots.shape[0]), _p(sendbuf)))
+
+    def spmv(self, recvbuf):
+        self.h._check(lib().agipc_dpcg_spmv(self.h._h, _p(recvbuf) if recvbuf is not None and recvbuf.numel() else None,
+                                            _p(self.red)))
+
+    def update(self):
+        self.h._check(lib().agipc_dpcg_update(self.h._h, _p(self.red)))
+
+    def status(self):
+        d = C.c_int(0)
+        s = _PcgStats()
+        self.h._check(lib().agipc_dpcg_status(self.h._h, C.byref(d), C.byref(s)))
+        return bool(d.value), dict(iters=int(s.iters), status=int(s.status), rel_residual=float(s.rel_residual))
+
+    def finish(self, x):
+        s = _PcgStats()
+        self.h._check(lib().agipc_dpcg_finish(self.h._h, _p(self.red), _p(x), C.byref(s)), allow=(NOT_CONVERGED,))
+        return dict(iters=int(s.iters), status=int(s.status), rel_residual=float(s.rel_residual),
+                    b_norm=float(s.b_norm))

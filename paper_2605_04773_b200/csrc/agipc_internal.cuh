@@ -39,6 +39,7 @@ enum ProfPhase {
   PROF_ASM_SYMBOLIC,
   PROF_ASM_NUMERIC,
   PROF_PROLONG,
+  PROF_DIST,
   PROF_N
 };
 
@@ -57,6 +58,7 @@ struct agipc_handle_s {
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
+  struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;
   std::vector<ProfPending> prof_pending;

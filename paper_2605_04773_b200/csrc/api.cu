@@ -56,6 +56,7 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st) {
 }
 
 void pcg_graph_free(PcgGraph *g);  // pcg.cu
+void dpcg_free(struct DPcg *d);    // pcg.cu
 
 cudaEvent_t prof_event(agipc_handle h) {
   if (!h->prof_pool.empty()) {
@@ -96,7 +97,7 @@ static void prof_flush(agipc_handle h) {
 static const char *kPhaseNames[PROF_N] = {"tag_edges", "build_map", "assemble_coarse", "pcg_setup",
                                           "pcg_spmv", "pcg_update", "pcg_solve",
                                           "asm_classify", "asm_symbolic", "asm_numeric",
-                                          "prolongate"};
+                                          "prolongate", "dist_halo"};
 
 extern "C" {
 
@@ -128,6 +129,7 @@ agipc_status agipc_destroy(agipc_handle h) {
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pcg) pcg_graph_free(h->pcg);
+  if (h->dpcg) dpcg_free(h->dpcg);
   prof_flush(h);
   for (auto e : h->prof_pool) cudaEventDestroy(e);
   delete h;

@@ -27,6 +27,8 @@
 #define SEG_MAX 64          // blocks per virtual row
 #define SORT_WIN 4096       // virtual rows per sorting window (sigma = 128 slices)
 #define PROF_EVERY 8        // profiling: time the kernels of every 8th iteration
+#define HALO_BIT (1 << 30)  // v_len flag: the virtual row is a segment of the halo matrix (8(e))
+#define VLEN(x) ((x) & (HALO_BIT - 1))
 
 struct PcgState {
   double rz, alpha, beta, bn2, rr, pq;
@@ -140,25 +142,35 @@ __global__ void k_dinv(int64_t n, const int64_t *__restrict__ rp, const int32_t 
   for (int i = 0; i < 9; ++i) Dinv[9 * r + i] = M[i];
 }
 
-__global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rp, int32_t *__restrict__ nseg) {
+// segments of row r: max(1, ceil(len/64)) of the matrix, then ceil(len_h/64) of the halo matrix
+// (distributed solve: the rank's rows x ghost columns); hrp == nullptr: none
+__device__ __forceinline__ int64_t nseg_local(int64_t len) { return len <= SEG_MAX ? 1 : (len + SEG_MAX - 1) / SEG_MAX; }
+
+__global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ hrp,
+                            int32_t *__restrict__ nseg) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) {
-    int64_t len = rp[r + 1] - rp[r];
-    nseg[r] = len <= SEG_MAX ? 1 : (int32_t)((len + SEG_MAX - 1) / SEG_MAX);
+    int64_t ns = nseg_local(rp[r + 1] - rp[r]);
+    if (hrp) ns += (hrp[r + 1] - hrp[r] + SEG_MAX - 1) / SEG_MAX;
+    nseg[r] = (int32_t)ns;
   }
 }
 
-// virtual row v = segment k of row r: blocks [rp[r] + 64k, ...) of length <= 64
-__global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ vr_ptr,
-                           int32_t *__restrict__ v_row, int32_t *__restrict__ v_len, PcgState *st) {
+// virtual row v = segment k of row r: blocks [rp[r] + 64k, ...) of length <= 64 (halo segments
+// carry HALO_BIT and index hrp)
+__global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ hrp,
+                           const int64_t *__restrict__ vr_ptr, int32_t *__restrict__ v_row,
+                           int32_t *__restrict__ v_len, PcgState *st) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r == 0) st->nv = vr_ptr[n];
   if (r < n) {
     const int64_t len = rp[r + 1] - rp[r];
+    const int64_t nl = nseg_local(len);
     const int64_t v0 = vr_ptr[r], nv = vr_ptr[r + 1] - v0;
     for (int64_t k = 0; k < nv; ++k) {
       v_row[v0 + k] = (int32_t)r;
-      v_len[v0 + k] = (int32_t)min((int64_t)SEG_MAX, len - SEG_MAX * k);
+      if (k < nl) v_len[v0 + k] = (int32_t)min((int64_t)SEG_MAX, len - SEG_MAX * k);
+      else v_len[v0 + k] = (int32_t)min((int64_t)SEG_MAX, hrp[r + 1] - hrp[r] - SEG_MAX * (k - nl)) | HALO_BIT;
     }
   }
 }
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(1024) k_window_sort(const PcgState *st, const 
   if (w0 >= nv) return;
   for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
     long long v = w0 + i;
-    s_key[i] = v < nv ? ((unsigned long long)(SEG_MAX - v_len[v]) << 32) | (unsigned long long)i : ~0ull;
+    s_key[i] = v < nv ? ((unsigned long long)(SEG_MAX - VLEN(v_len[v])) << 32) | (unsigned long long)i : ~0ull;
   }
   __syncthreads();
   for (int k = 2; k <= SORT_WIN; k <<= 1)
@@ -203,7 +215,7 @@ __global__ void k_slice_len(int64_t ns_bound, const PcgState *st, const int32_t 
   const long long nv = st->nv;
   if (s < ns_bound) {
     int L = 0;
-    for (int t = 0; t < 32 && 32 * s + t < nv; ++t) L = max(L, v_len[perm[32 * s + t]]);
+    for (int t = 0; t < 32 && 32 * s + t < nv; ++t) L = max(L, VLEN(v_len[perm[32 * s + t]]));
     slen[s] = 32 * L;
   }
 }
@@ -236,7 +248,9 @@ __global__ void k_sell_scalars(int64_t ns_bound, const int64_t *__restrict__ spt
 
 // warp per slice: component-major tiles; padding = zero blocks pointing at the row itself
 __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                            const double *__restrict__ val, const int64_t *__restrict__ vr_ptr,
+                            const double *__restrict__ val, const int64_t *__restrict__ hrp,
+                            const int32_t *__restrict__ hcol, const double *__restrict__ hval,
+                            const int64_t *__restrict__ vr_ptr,
                             const int32_t *__restrict__ perm, const int32_t *__restrict__ v_row,
                             const int32_t *__restrict__ v_len, const int64_t *__restrict__ sptr,
                             int32_t *__restrict__ scol, double *__restrict__ sval, int32_t *__restrict__ s_vrow) {
@@ -249,19 +263,26 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, 
     s_vrow[vi] = v;
     int row = 0, len = 0;
     long long k0 = 0;
+    bool halo = false;
     if (v >= 0) {
       row = v_row[v];
-      len = v_len[v];
-      k0 = rp[row] + (long long)SEG_MAX * (v - vr_ptr[row]);
+      const int vl = v_len[v];
+      len = VLEN(vl);
+      halo = (vl & HALO_BIT) != 0;
+      const long long k = v - vr_ptr[row];
+      if (!halo) k0 = rp[row] + (long long)SEG_MAX * k;
+      else k0 = hrp[row] + (long long)SEG_MAX * (k - nseg_local(rp[row + 1] - rp[row]));
     }
+    const int32_t *cs = halo ? hcol : col;
+    const double *vs = halo ? hval : val;
     const long long base = sptr[s];
     const int L = (int)((sptr[s + 1] - base) / 32);
     for (int j = 0; j < L; ++j) {
       const long long t = base + 32LL * j;
       const bool real = j < len;
-      scol[t + l] = real ? col[k0 + j] : row;
+      scol[t + l] = real ? cs[k0 + j] : row;
       double *dst = sval + 9 * t + l;
-      const double *src = val + 9 * (k0 + j);
+      const double *src = vs + 9 * (k0 + j);
 #pragma unroll
       for (int e = 0; e < 9; ++e) dst[32 * e] = real ? src[e] : 0.0;
     }
@@ -275,7 +296,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
                                                       const double *__restrict__ b, double *__restrict__ x,
                                                       const double *__restrict__ Dinv, double *__restrict__ r,
                                                       double *__restrict__ z, double *__restrict__ p, double *parts,
-                                                      PcgState *st, int zero_x0) {
+                                                      PcgState *st, int zero_x0, double *red) {
   __shared__ double s_red[PCG_WARPS];
   const int w = threadIdx.x >> 5, l = lane_id();
   double rz = 0.0, rr = 0.0, bb = 0.0;
@@ -323,7 +344,9 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
     double RZ = reduce_parts(parts, G, s_red);
     double RR = reduce_parts(parts + G, G, s_red);
     double BB = reduce_parts(parts + 2 * G, G, s_red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && red) {  // distributed: rank partials, the caller all-reduces them
+      red[0] = RZ; red[1] = RR; red[2] = BB;
+    } else if (threadIdx.x == 0) {
       st->rz = RZ;
       st->rr = RR;
       st->bn2 = BB;
@@ -369,7 +392,8 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
                                                            const int64_t *__restrict__ vr_ptr,
                                                            const double *__restrict__ z, const double *__restrict__ pold,
                                                            double *__restrict__ pnew, double *__restrict__ qseg,
-                                                           int *counter, double *parts, PcgState *st) {
+                                                           int *counter, double *parts, PcgState *st,
+                                                           double *red) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double beta = st->beta;
@@ -420,7 +444,9 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
   if (threadIdx.x == 0) parts[blockIdx.x] = pq;
   if (last_block(st)) {
     double PQ = reduce_parts(parts, gridDim.x, s_red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && red) {
+      red[0] = PQ;
+    } else if (threadIdx.x == 0) {
       st->pq = PQ;
       if (!isfinite(PQ) || !isfinite(st->rz)) {
         st->status = AGIPC_EBREAKDOWN;
@@ -444,7 +470,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t
                                                         double *__restrict__ z, const double *__restrict__ p,
                                                         const double *__restrict__ qseg,
                                                         const double *__restrict__ Dinv, int *next_counter,
-                                                        double *parts, PcgState *st) {
+                                                        double *parts, PcgState *st, double *red) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double alpha = st->alpha;
@@ -480,7 +506,9 @@ __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t
   if (last_block(st)) {
     double RZ = reduce_parts(parts + G, G, s_red);
     double RR = reduce_parts(parts + 2 * G, G, s_red);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && red) {
+      red[0] = RZ; red[1] = RR;
+    } else if (threadIdx.x == 0) {
       st->it += 1;
       st->rr = RR;
       if (sqrt(RR) <= st->tol * sqrt(st->bn2)) {
@@ -520,14 +548,91 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
     const bool sample = ev && (k % PROF_EVERY) == 0;  // sampled kernel timing (low overhead)
     if (sample) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
     k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z, pold,
-                                             pnew, B.qseg, B.counters + (k & 1), B.parts, B.st);
+                                             pnew, B.qseg, B.counters + (k & 1), B.parts, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
     k_update<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
-                                          B.parts, B.st);
+                                          B.parts, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pcg launch: %s", cudaGetErrorString(e));
+  return AGIPC_OK;
+}
+
+// Block-Jacobi + SELL layout + k_init, shared by the 1-GPU solve and the distributed solve.
+// Ah (nullable): halo matrix of the rank's rows x ghost columns (columns >= n index the ghost
+// region of the vectors, n_gs slots).  red != nullptr: k_init leaves rank partials in red.
+static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *Ah, int64_t n_gs, const double *b,
+                              const double *x, int zero_x0, double rel_tol, int max_iters, PcgBufs &B,
+                              PcgState *hst, double *red) {
+  const int64_t n = A->n_rows;
+  const int64_t nh = Ah ? Ah->nnzb : 0;
+  cudaStream_t s0 = h->stream;
+  const int64_t nv_bound = n + (A->nnzb + nh) / SEG_MAX + (Ah ? n : 0) + 1;  // virtual rows
+  const int64_t nx = n + n_gs;  // owned + ghost slots (z and p carry the ghost region)
+  B.ns_bound = cdiv(nv_bound, 32);
+  WS(h, xw, double, "pcg_x", 3 * n + 2); B.x = xw;
+  WS(h, r, double, "pcg_r", 3 * n + 2); B.r = r;
+  WS(h, z, double, "pcg_z", 3 * nx + 2); B.z = z;
+  WS(h, p0, double, "pcg_p0", 3 * nx + 2); B.P[0] = p0;
+  WS(h, p1, double, "pcg_p1", 3 * nx + 2); B.P[1] = p1;
+  WS(h, qs, double, "pcg_qseg", 3 * nv_bound + 2); B.qseg = qs;
+  WS(h, Dinv, double, "pcg_dinv", 9 * n + 2); B.Dinv = Dinv;
+  WS(h, vr, int64_t, "pcg_vr_ptr", n + 1); B.vr_ptr = vr;
+  WS(h, nseg, int32_t, "pcg_nseg", n);
+  WS(h, vrow, int32_t, "pcg_v_row", nv_bound); B.v_row = vrow;
+  WS(h, vlen, int32_t, "pcg_v_len", nv_bound); B.v_len = vlen;
+  WS(h, perm, int32_t, "pcg_perm", nv_bound); B.perm = perm;
+  WS(h, slen, int32_t, "pcg_slen", B.ns_bound);
+  WS(h, sptr, int64_t, "pcg_sptr", B.ns_bound + 1); B.sptr = sptr;
+  WS(h, svr, int32_t, "pcg_s_vrow", 32 * B.ns_bound); B.s_vrow = svr;
+  WS(h, stp, PcgState, "pcg_state", 1); B.st = stp;
+  WS(h, order, int32_t, "pcg_order", B.ns_bound); B.order = order;
+  WS(h, ctr, int, "pcg_counters", 2); B.counters = ctr;
+  int occ = 0;
+  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
+  B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
+  B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 4 * (int64_t)h->sm_count));
+  const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
+  const int Gp = std::max(std::max(B.G1, B.G2), Gi);
+  WS(h, parts, double, "pcg_parts", 3 * Gp); B.parts = parts;
+  PcgState init;
+  memset(&init, 0, sizeof(init));
+  init.tol = rel_tol;
+  init.max_iters = max_iters;
+  init.status = AGIPC_OK;
+  *hst = init;
+  ProfScope prof_setup(h, PROF_PCG_SETUP, s0);
+  CU_TRY(h, cudaMemcpyAsync(stp, hst, sizeof(PcgState), cudaMemcpyHostToDevice, s0));
+  if (!zero_x0) CU_TRY(h, cudaMemcpyAsync(B.x, x, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s0));
+  if (n_gs > 0) {  // ghost p starts at 0 like the owned p (beta = 0 in the first iteration)
+    CU_TRY(h, cudaMemsetAsync(B.P[0] + 3 * n, 0, sizeof(double) * 3 * n_gs, s0));
+    CU_TRY(h, cudaMemsetAsync(B.P[1] + 3 * n, 0, sizeof(double) * 3 * n_gs, s0));
+  }
+  LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp);
+  // SELL layout (once per solve)
+  const int64_t *hrp = Ah ? Ah->row_ptr : nullptr;
+  LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, hrp, nseg);
+  agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
+  if (sst != AGIPC_OK) return sst;
+  LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
+  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, SORT_WIN), 1024, 0, stp, B.v_len, B.perm);
+  LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
+  sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
+  if (sst != AGIPC_OK) return sst;
+  LAUNCH(h, k_sell_scalars, 1, 1, 0, B.ns_bound, B.sptr, stp);
+  LAUNCH(h, k_slice_order, 1, 1024, 0, stp, slen, B.order);
+  CU_TRY(h, cudaMemsetAsync(B.counters, 0, 2 * sizeof(int), s0));
+  CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+  CU_TRY(h, cudaStreamSynchronize(s0));
+  const long long sell_blocks = hst->sell_blocks;
+  WS(h, scol, int32_t, "pcg_scol", sell_blocks + 32); B.scol = scol;
+  WS(h, sval, double, "pcg_sval", 9 * sell_blocks + 288); B.sval = sval;
+  LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
+         0, stp, A->row_ptr, A->col, A->val, hrp, Ah ? Ah->col : nullptr, Ah ? Ah->val : nullptr, B.vr_ptr, B.perm,
+         B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
+  LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
+         parts, stp, zero_x0, red);
   return AGIPC_OK;
 }
 
@@ -549,66 +654,8 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
   if (ast != AGIPC_OK) return ast;
   PcgBufs B;
-  const int64_t nv_bound = n + A->nnzb / SEG_MAX + 1;  // virtual rows
-  B.ns_bound = cdiv(nv_bound, 32);
-  {
-    WS(h, xw, double, "pcg_x", 3 * n + 2); B.x = xw;
-    WS(h, r, double, "pcg_r", 3 * n + 2); B.r = r;
-    WS(h, z, double, "pcg_z", 3 * n + 2); B.z = z;
-    WS(h, p0, double, "pcg_p0", 3 * n + 2); B.P[0] = p0;
-    WS(h, p1, double, "pcg_p1", 3 * n + 2); B.P[1] = p1;
-    WS(h, qs, double, "pcg_qseg", 3 * nv_bound + 2); B.qseg = qs;
-    WS(h, Dinv, double, "pcg_dinv", 9 * n + 2); B.Dinv = Dinv;
-    WS(h, vr, int64_t, "pcg_vr_ptr", n + 1); B.vr_ptr = vr;
-    WS(h, nseg, int32_t, "pcg_nseg", n);
-    WS(h, vrow, int32_t, "pcg_v_row", nv_bound); B.v_row = vrow;
-    WS(h, vlen, int32_t, "pcg_v_len", nv_bound); B.v_len = vlen;
-    WS(h, perm, int32_t, "pcg_perm", nv_bound); B.perm = perm;
-    WS(h, slen, int32_t, "pcg_slen", B.ns_bound);
-    WS(h, sptr, int64_t, "pcg_sptr", B.ns_bound + 1); B.sptr = sptr;
-    WS(h, svr, int32_t, "pcg_s_vrow", 32 * B.ns_bound); B.s_vrow = svr;
-    WS(h, stp, PcgState, "pcg_state", 1); B.st = stp;
-    WS(h, order, int32_t, "pcg_order", B.ns_bound); B.order = order;
-    WS(h, ctr, int, "pcg_counters", 2); B.counters = ctr;
-    int occ = 0;
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
-    B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
-    B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 4 * (int64_t)h->sm_count));
-    const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
-    const int Gp = std::max(std::max(B.G1, B.G2), Gi);
-    WS(h, parts, double, "pcg_parts", 3 * Gp); B.parts = parts;
-    PcgState init;
-    memset(&init, 0, sizeof(init));
-    init.tol = rel_tol;
-    init.max_iters = max_iters;
-    init.status = AGIPC_OK;
-    *hst = init;
-    ProfScope prof_setup(h, PROF_PCG_SETUP, s0);
-    CU_TRY(h, cudaMemcpyAsync(stp, hst, sizeof(PcgState), cudaMemcpyHostToDevice, s0));
-    if (!zero_x0) CU_TRY(h, cudaMemcpyAsync(B.x, x, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s0));
-    LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp);
-    // SELL layout (once per solve)
-    LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, nseg);
-    agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
-    if (sst != AGIPC_OK) return sst;
-    LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, B.vr_ptr, B.v_row, B.v_len, stp);
-    LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, SORT_WIN), 1024, 0, stp, B.v_len, B.perm);
-    LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
-    sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
-    if (sst != AGIPC_OK) return sst;
-    LAUNCH(h, k_sell_scalars, 1, 1, 0, B.ns_bound, B.sptr, stp);
-    LAUNCH(h, k_slice_order, 1, 1024, 0, stp, slen, B.order);
-    CU_TRY(h, cudaMemsetAsync(B.counters, 0, 2 * sizeof(int), s0));
-    CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
-    CU_TRY(h, cudaStreamSynchronize(s0));
-    const long long sell_blocks = hst->sell_blocks;
-    WS(h, scol, int32_t, "pcg_scol", sell_blocks + 32); B.scol = scol;
-    WS(h, sval, double, "pcg_sval", 9 * sell_blocks + 288); B.sval = sval;
-    LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
-           0, stp, A->row_ptr, A->col, A->val, B.vr_ptr, B.perm, B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
-    LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
-           parts, stp, zero_x0);
-  }
+  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr);
+  if (ast != AGIPC_OK) return ast;
   if (max_iters == 0) {
     CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
     CU_TRY(h, cudaStreamSynchronize(s0));
@@ -688,6 +735,215 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   if (stats->status == AGIPC_ESINGULAR) return set_err(h, AGIPC_ESINGULAR, "pcg_solve: singular diagonal block");
   if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "pcg_solve: p^T A p <= 0");
   if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "pcg_solve: NaN/Inf");
+  if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
+  return AGIPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// Distributed PCG: the rank's rows of H_c (matrix A, columns = owned slots) and
+// of its halo matrix Ah (columns n + g = ghost slot g).  The iteration is the 1-GPU one split
+// at its three reductions; after every dpcg call the caller sums `red` over the ranks
+// (all-reduce) and, after update, exchanges the ghost slots of z (pack -> send/recv -> the
+// recv buffer of the next spmv).  The scalar logic that the last CTA runs in the 1-GPU solve
+// (alpha, convergence, beta) then runs on the reduced sums in k_dscalars, identically on every
+// rank, so all ranks take the same decisions and stop at the same iteration.
+// ------------------------------------------------------------------------------------
+enum { DP_INIT = 0, DP_ALPHA = 1, DP_UPDATE = 2, DP_NONE = 3 };
+
+struct DPcg {
+  PcgBufs B;
+  int64_t n = 0, n_gs = 0;
+  int k = 0;            // iterations launched (p ping-pong parity)
+  int pending = DP_NONE;  // which reduced sums in red the next call must consume
+  bool active = false;
+};
+
+void dpcg_free(DPcg *d) { delete d; }
+
+__global__ void k_dscalars(PcgState *st, const double *red, int phase) {
+  if (phase == DP_INIT) {
+    st->rz = red[0];
+    st->rr = red[1];
+    st->bn2 = red[2];
+    st->it = 0;
+    st->beta = 0.0;
+    if (!st->done && sqrt(red[1]) <= st->tol * sqrt(red[2])) st->done = 1;
+    return;
+  }
+  if (st->done) return;
+  if (phase == DP_ALPHA) {
+    const double PQ = red[0];
+    st->pq = PQ;
+    if (!isfinite(PQ) || !isfinite(st->rz)) {
+      st->status = AGIPC_EBREAKDOWN;
+      st->done = 1;
+      st->it += 1;
+    } else if (PQ <= 0.0) {
+      st->status = AGIPC_EINDEFINITE;
+      st->done = 1;
+      st->it += 1;
+    } else {
+      st->alpha = st->rz / PQ;
+    }
+  } else {  // DP_UPDATE
+    const double RZ = red[0], RR = red[1];
+    st->it += 1;
+    st->rr = RR;
+    if (sqrt(RR) <= st->tol * sqrt(st->bn2)) {
+      st->done = 1;
+      st->status = AGIPC_OK;
+    } else if (st->it >= st->max_iters) {
+      st->done = 1;
+      st->status = AGIPC_NOT_CONVERGED;
+    } else {
+      st->beta = RZ / st->rz;
+      st->rz = RZ;
+    }
+  }
+}
+
+// ghost slots: z from the owners; p_new = z + beta p_old (the owner's value, bit for bit)
+__global__ void k_ghost_in(int64_t n, int64_t n_gs, const double *__restrict__ recv, double *__restrict__ z,
+                           const double *__restrict__ pold, double *__restrict__ pnew, const PcgState *st) {
+  if (*(volatile int *)&st->done) return;
+  const double beta = st->beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * n_gs; i += (int64_t)gridDim.x * blockDim.x) {
+    const double zv = recv[i];
+    z[3 * n + i] = zv;
+    pnew[3 * n + i] = zv + beta * pold[3 * n + i];
+  }
+}
+
+__global__ void k_pack3(int64_t m, const int32_t *__restrict__ idx, const double *__restrict__ src,
+                        double *__restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 3 * m) {
+    const int64_t k = i / 3, c = i - 3 * k;
+    dst[i] = src[3 * (int64_t)idx[k] + c];
+  }
+}
+
+static agipc_status dpcg_get(agipc_handle h, DPcg **d, const char *who) {
+  if (!h) return AGIPC_EINVAL;
+  if (!h->dpcg || !h->dpcg->active) return set_err(h, AGIPC_EINVAL, "%s: no distributed solve in progress", who);
+  *d = h->dpcg;
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *A_halo,
+                                         int64_t n_ghost_slots, const double *b, double rel_tol, int max_iters,
+                                         double *red) {
+  if (!h) return AGIPC_EINVAL;
+  if (!A || !red || !b || max_iters < 0 || A->n_rows <= 0 || n_ghost_slots < 0 || !(rel_tol >= 0.0))
+    return set_err(h, AGIPC_EINVAL, "dpcg_setup: bad arguments");
+  if (!A->row_ptr || !A->col || !A->val) return set_err(h, AGIPC_EINVAL, "dpcg_setup: null matrix");
+  if (A_halo && (A_halo->n_rows != A->n_rows || !A_halo->row_ptr || (A_halo->nnzb > 0 && (!A_halo->col || !A_halo->val))))
+    return set_err(h, AGIPC_EINVAL, "dpcg_setup: bad halo matrix");
+  const int64_t n = A->n_rows;
+  if (n + n_ghost_slots >= INT32_MAX / 4) return set_err(h, AGIPC_ERANGE, "dpcg_setup: too large");
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (!h->dpcg) h->dpcg = new DPcg();
+  DPcg *d = h->dpcg;
+  agipc_status ast;
+  PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
+  if (ast != AGIPC_OK) return ast;
+  ast = pcg_setup(h, A, A_halo, n_ghost_slots, b, nullptr, 1, rel_tol, max_iters, d->B, hst, red);
+  if (ast != AGIPC_OK) return ast;
+  d->n = n;
+  d->n_gs = n_ghost_slots;
+  d->k = 0;
+  d->pending = DP_INIT;
+  d->active = true;
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_pack(agipc_handle h, const int32_t *send_slots, int64_t n_send, double *sendbuf) {
+  DPcg *d;
+  agipc_status st = dpcg_get(h, &d, "dpcg_pack");
+  if (st != AGIPC_OK) return st;
+  if (n_send <= 0) return AGIPC_OK;
+  if (!send_slots || !sendbuf) return set_err(h, AGIPC_EINVAL, "dpcg_pack: null pointer");
+  LAUNCH(h, k_pack3, (unsigned)cdiv(3 * n_send, 256), 256, 0, n_send, send_slots, d->B.z, sendbuf);
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_spmv(agipc_handle h, const double *recvbuf, double *red) {
+  DPcg *d;
+  agipc_status st = dpcg_get(h, &d, "dpcg_spmv");
+  if (st != AGIPC_OK) return st;
+  if (d->pending != DP_INIT && d->pending != DP_UPDATE) return set_err(h, AGIPC_EINVAL, "dpcg_spmv: out of order");
+  if (!red || (d->n_gs > 0 && !recvbuf)) return set_err(h, AGIPC_EINVAL, "dpcg_spmv: null pointer");
+  const PcgBufs &B = d->B;
+  double *pold = B.P[d->k & 1], *pnew = B.P[(d->k + 1) & 1];
+  ProfScope prof(h, PROF_PCG_SPMV, h->stream);
+  LAUNCH(h, k_dscalars, 1, 1, 0, B.st, (const double *)red, d->pending);
+  if (d->n_gs > 0)
+    LAUNCH(h, k_ghost_in, (unsigned)std::min<int64_t>(cdiv(3 * d->n_gs, 256), 4 * h->sm_count), 256, 0, d->n, d->n_gs,
+           recvbuf, B.z, (const double *)pold, pnew, (const PcgState *)B.st);
+  LAUNCH(h, k_spmv_sell, (unsigned)B.G1, PCG_THREADS, 0, B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
+         B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (d->k & 1), B.parts, B.st, red);
+  d->pending = DP_ALPHA;
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_update(agipc_handle h, double *red) {
+  DPcg *d;
+  agipc_status st = dpcg_get(h, &d, "dpcg_update");
+  if (st != AGIPC_OK) return st;
+  if (d->pending != DP_ALPHA) return set_err(h, AGIPC_EINVAL, "dpcg_update: out of order");
+  if (!red) return set_err(h, AGIPC_EINVAL, "dpcg_update: null pointer");
+  const PcgBufs &B = d->B;
+  double *pnew = B.P[(d->k + 1) & 1];
+  ProfScope prof(h, PROF_PCG_UPDATE, h->stream);
+  LAUNCH(h, k_dscalars, 1, 1, 0, B.st, (const double *)red, (int)DP_ALPHA);
+  LAUNCH(h, k_update, (unsigned)B.G2, PCG_THREADS, 0, d->n, B.vr_ptr, B.x, B.r, B.z, (const double *)pnew, B.qseg,
+         B.Dinv, B.counters + ((d->k + 1) & 1), B.parts, B.st, red);
+  d->k += 1;
+  d->pending = DP_UPDATE;
+  return AGIPC_OK;
+}
+
+static void dpcg_fill_stats(const PcgState *hst, agipc_pcg_stats *stats) {
+  stats->iters = hst->it;
+  stats->status = hst->done ? hst->status : AGIPC_NOT_CONVERGED;
+  stats->b_norm = sqrt(hst->bn2);
+  stats->rel_residual = hst->bn2 > 0 ? sqrt(hst->rr) / sqrt(hst->bn2) : sqrt(hst->rr);
+}
+
+extern "C" agipc_status agipc_dpcg_status(agipc_handle h, int *done, agipc_pcg_stats *stats) {
+  DPcg *d;
+  agipc_status st = dpcg_get(h, &d, "dpcg_status");
+  if (st != AGIPC_OK) return st;
+  PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &st);
+  if (st != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemcpyAsync(hst, d->B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  if (done) *done = hst->done;
+  if (stats) dpcg_fill_stats(hst, stats);
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_finish(agipc_handle h, const double *red, double *x, agipc_pcg_stats *stats) {
+  DPcg *d;
+  agipc_status st = dpcg_get(h, &d, "dpcg_finish");
+  if (st != AGIPC_OK) return st;
+  if (!x || !stats) return set_err(h, AGIPC_EINVAL, "dpcg_finish: null pointer");
+  if (d->pending == DP_ALPHA) return set_err(h, AGIPC_EINVAL, "dpcg_finish: out of order (after spmv)");
+  if (d->pending == DP_INIT || d->pending == DP_UPDATE) {
+    if (!red) return set_err(h, AGIPC_EINVAL, "dpcg_finish: null red");
+    LAUNCH(h, k_dscalars, 1, 1, 0, d->B.st, red, d->pending);
+  }
+  d->pending = DP_NONE;
+  d->active = false;
+  LAUNCH(h, k_copy_out, (unsigned)cdiv(3 * d->n, 256), 256, 0, 3 * d->n, d->B.x, x);
+  PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &st);
+  if (st != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemcpyAsync(hst, d->B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  dpcg_fill_stats(hst, stats);
+  if (stats->status == AGIPC_ESINGULAR) return set_err(h, AGIPC_ESINGULAR, "dpcg: singular diagonal block");
+  if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "dpcg: p^T A p <= 0");
+  if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "dpcg: NaN/Inf");
   if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
   return AGIPC_OK;
 }

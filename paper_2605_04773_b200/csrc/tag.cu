@@ -112,9 +112,11 @@ __global__ void __launch_bounds__(TAG_THREADS) k_tag(int64_t n_tets, const int4 
     if (flag) {
       const int4 *s = tet_slots + 3 * t;
       int4 s0 = __ldg(s), s1 = __ldg(s + 1), s2v = __ldg(s + 2);
-      slot_tags[s0.x] = 0; slot_tags[s0.y] = 0; slot_tags[s0.z] = 0; slot_tags[s0.w] = 0;
-      slot_tags[s1.x] = 0; slot_tags[s1.y] = 0; slot_tags[s1.z] = 0; slot_tags[s1.w] = 0;
-      slot_tags[s2v.x] = 0; slot_tags[s2v.y] = 0; slot_tags[s2v.z] = 0; slot_tags[s2v.w] = 0;
+      // slot -1: the edge is not owned at both ends on this rank (partitioned mesh, 8(e))
+      const int sl[12] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w, s2v.x, s2v.y, s2v.z, s2v.w};
+#pragma unroll
+      for (int k = 0; k < 12; ++k)
+        if (sl[k] >= 0) slot_tags[sl[k]] = 0;
     }
   }
   if (counters) {

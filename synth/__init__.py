@@ -333,3 +333,95 @@ def config_c3(n: int = 100, k: int = 0):
     m = kuhn_grid(n)
     xp, xc = walls(m, k)
     return dict(mesh=m, x_prev=xp, x_cur=xc, theta=5e-5, E=1e5, group_size=32)
+
+
+# ----------------------------------------------------------------------------
+# Partitioned workloads: a box of n x n x (R n) nodes ordered
+# slab-major (slab s = nodes with s n <= k < (s+1) n), Morton inside each slab,
+# so rank r of R owns the contiguous global range [r n^3, (r+1) n^3).  With
+# R = 1 this is exactly kuhn_grid(n).
+# ----------------------------------------------------------------------------
+
+def kuhn_box(n: int, slabs: int = 1, z_lo: int = 0, z_hi: int | None = None, side: float = 1.0):
+    """Kuhn 6-tet grid over nodes (i, j, k), 0 <= i, j < n, z_lo <= k <= z_hi (default: the
+    whole box, k < slabs*n).  Returns (mesh, gid): gid[v] = global slab-major Morton id of local
+    node v; local ids are ascending in gid (so a sub-box keeps the global order).  Spacing
+    h = side/(n-1); the whole box is centred on the origin."""
+    nz = slabs * n
+    z_hi = nz - 1 if z_hi is None else z_hi
+    assert n >= 2 and 0 <= z_lo < z_hi < nz
+    h = side / (n - 1)
+    gi = np.arange(n)
+    gk = np.arange(z_lo, z_hi + 1)
+    I, J, K = np.meshgrid(gi, gi, gk, indexing="ij")
+    ijk = np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.int64)
+    s = ijk[:, 2] // n
+    loc = ijk.copy()
+    loc[:, 2] -= s * n
+    gid_all = s * n ** 3 + _morton_rank(n)[_morton_key(loc)]
+    perm = np.argsort(gid_all, kind="stable")
+    gid = gid_all[perm]
+    ijk_new = ijk[perm]
+    nzl = z_hi - z_lo + 1
+    lex = ((ijk[:, 0] * n + ijk[:, 1]) * nzl + (ijk[:, 2] - z_lo))
+    new_of_lex = np.empty(lex.shape[0], np.int64)
+    new_of_lex[lex[perm]] = np.arange(lex.shape[0])
+    X = ijk_new.astype(np.float64) * h
+    X[:, 0:2] -= 0.5 * side
+    X[:, 2] -= 0.5 * h * (nz - 1)
+    c = np.arange(n - 1)
+    ck = np.arange(nzl - 1)
+    CI, CJ, CK = np.meshgrid(c, c, ck, indexing="ij")
+    cubes = np.stack([CI.ravel(), CJ.ravel(), CK.ravel()], axis=1)
+    unit = np.eye(3, dtype=np.int64)
+    tl = []
+    for s0, s1, s2 in ((0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)):
+        v0 = cubes
+        v1 = v0 + unit[s0]
+        v2 = v1 + unit[s1]
+        v3 = v2 + unit[s2]
+        tl.append(np.stack([(v[:, 0] * n + v[:, 1]) * nzl + v[:, 2] for v in (v0, v1, v2, v3)], axis=1))
+    tets = new_of_lex[np.concatenate(tl, axis=0)]
+    tets = tets[np.argsort(tets.min(axis=1), kind="stable")].astype(np.int32)
+    return mesh_from_tets(X, tets, ijk=ijk_new, n_side=n), gid
+
+
+_MR = {}
+
+
+def _morton_rank(n: int):
+    """Dense rank of every Morton key of the n^3 grid (lookup table, key -> rank)."""
+    if n not in _MR:
+        g = np.arange(n)
+        I, J, K = np.meshgrid(g, g, g, indexing="ij")
+        keys = _morton_key(np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.int64))
+        tab = np.full(int(keys.max()) + 1, -1, np.int64)
+        tab[np.sort(keys)] = np.arange(keys.shape[0])
+        _MR[n] = tab
+    return _MR[n]
+
+
+def slab_walls(ijk: np.ndarray, gid: np.ndarray, n: int, k: int, period: int = 16, rel_amp: float = 1e-2,
+               seed: int = 0):
+    """C3's wall displacement on a slab-ordered box, drawn per GLOBAL node id (counter-based:
+    one generator per node block of 2^16 ids) so that every rank reproduces the owner's value
+    for its ghosts.  Returns the displacement [len(gid), 3] (x_prev = X, x_cur = X + disp)."""
+    h = 1.0 / (n - 1)
+    wall = np.any(ijk % period == (k % period), axis=1)
+    disp = np.zeros((gid.shape[0], 3))
+    blk = gid >> 16
+    for b in np.unique(blk):
+        sel = blk == b
+        xi = np.random.default_rng([seed, 11, k, int(b)]).standard_normal((1 << 16, 3))
+        disp[sel] = xi[gid[sel] & 0xFFFF]
+    return (rel_amp * h) * disp * wall[:, None]
+
+
+def slab_gradient(gid: np.ndarray, seed: int = 0) -> np.ndarray:
+    """g_f ~ N(0,1) per component, drawn per global node id (counter-based like slab_walls)."""
+    g = np.empty((gid.shape[0], 3))
+    blk = gid >> 16
+    for b in np.unique(blk):
+        sel = blk == b
+        g[sel] = np.random.default_rng([seed, 7, int(b)]).standard_normal((1 << 16, 3))[gid[sel] & 0xFFFF]
+    return g
