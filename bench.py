@@ -14,8 +14,11 @@ A step = one Newton iteration of the path: tag -> map -> assemble -> PCG (all of
                / average launch duration measured with CUDA events on its launch stream
   cpu_baseline = the C oracle on the host cores (rank 0, N=1), bounded sample
 
-Multi-GPU (torchrun, N>1): every rank runs its own C3 problem (weak scaling, no data-path
-collective; the partitioned 20M-node path with NCCL halos is not built yet -- DESIGN.md).
+Multi-GPU (torchrun, N>1): the partitioned path on ONE global mesh of
+n x n x (N n) nodes (N million at n = 100), ordered slab-major, rank r owning the 1M-node slab r
+(weak scaling: fixed work per GPU).  Ranks exchange ghost positions and column codes, all-gather
+the coarse slot counts, and run one distributed PCG on the global coarse system with NCCL
+send/recv of the ghost slots and all-reduce of the PCG sums (paper_2605_04773_b200.dist).
 `--impl reference` times the CPU oracle (the tier's reference arm) on the same workload.
 """
 from __future__ import annotations
@@ -49,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--partitioned", action="store_true", help="use the partitioned path even at N=1")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: several ranks may share one GPU (correctness runs only)")
     return ap.parse_args()
 
 
@@ -333,6 +339,124 @@ def run_agipc(args, world, rank, local_rank):
     print(json.dumps(out), flush=True)
 
 
+# --------------------------------------------------------------------------------------
+def build_partition(n, world, rank):
+    """Rank r's slab of the n x n x (world n) box plus its ghost planes; H_f on the sub-box."""
+    import synth
+    from paper_2605_04773_b200 import partition as pt
+    t0 = time.time()
+    b = pt.slab_bounds(n, world)
+    S, gid = synth.kuhn_box(n, slabs=world, z_lo=max(0, rank * n - 1), z_hi=min(world * n - 1, (rank + 1) * n))
+    lm = pt.local_mesh(S, gid, b[rank], b[rank + 1], b, rank)
+    H = synth.fine_hessian(S, E=1e5)
+    Hl = np.ascontiguousarray(H[lm.loc_src])
+    Hh = np.ascontiguousarray(H[lm.halo_src])
+    del H
+    lid = np.searchsorted(gid, lm.gid)          # sub-box node of every local node
+    ijk = S.ijk[lid]
+    g = synth.slab_gradient(lm.gid[:lm.n_own])
+    disp = [synth.slab_walls(ijk, lm.gid, n, k) for k in range(10)]
+    return lm, Hl, Hh, g, disp, time.time() - t0
+
+
+def run_partitioned(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_04773_b200 as P
+    from paper_2605_04773_b200 import partition as pt
+    from paper_2605_04773_b200.dist import Comm, DistCoarseningStep
+
+    ndev = torch.cuda.device_count()
+    dev_i = local_rank % max(1, ndev)
+    torch.cuda.set_device(dev_i)
+    dev = torch.device("cuda", dev_i)
+    comm = Comm()
+    lm, Hl, Hh, g, disp, gen_s = build_partition(args.n, world, rank)
+    pt.exchange_requests(lm, world, comm.alltoall_i64)
+    h = P.Handle(dev_i)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    Hld, Hhd, gd = t(Hl, torch.float64), t(Hh, torch.float64), t(g, torch.float64)
+    xp = t(lm.X, torch.float64)
+    xcd = [t(lm.X + d, torch.float64) for d in disp]
+    step = DistCoarseningStep(h, comm, lm, dev, check_every=args.check_every)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    for s in range(args.warmup):
+        step(xp, xcd[s % 10], gd, Hld, Hhd)
+    torch.cuda.synchronize()
+    dist.barrier()
+    h.profile(True)
+    launches0 = h.kernel_launches
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sizes = []
+    clocks = ClockSampler(dev_i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks.start()
+    wall0 = time.perf_counter()
+    for s in range(args.steps):
+        flush.zero_()
+        k = (args.warmup + s) % 10
+        ev[s][0].record()
+        dc = step.coarsen(xp, xcd[k], gd, Hld, Hhd)
+        ev[s][1].record()
+        x, st = step.solve(dc)
+        ev[s][2].record()
+        sizes.append((dc.cs.n_slots, dc.cs.nnzb + dc.h_col.shape[0], st["iters"], int(dc.n_slots_all.sum()),
+                      dc.n_ghost_slots, dc.map_info["n_levels"]))
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    launches = h.kernel_launches - launches0
+    prof = h.profile_read()
+    h.profile(False)
+    coarsen = [ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)]
+    pcg = [ev[s][1].elapsed_time(ev[s][2]) for s in range(args.steps)]
+    iters = sum(z[2] for z in sizes)
+    vec = torch.tensor([statistics.mean(coarsen), statistics.mean([a + b for a, b in zip(coarsen, pcg)]), sum(pcg)],
+                       dtype=torch.float64)
+    dist.all_reduce(vec, op=dist.ReduceOp.MAX) if comm.stage else None
+    if not comm.stage:
+        vd = vec.to(dev)
+        dist.all_reduce(vd, op=dist.ReduceOp.MAX)
+        vec = vd.cpu()
+    coarsen_ms, step_ms, pcg_ms_sum = vec.tolist()
+    hbm, peak_src = peaks()
+    n_spmv, ms_spmv = prof.get("pcg_spmv", (0, 0.0))
+    bytes_spmv = sum(z[2] * (76 * z[1] + 8 * (z[0] + 1) + 48 * z[0]) for z in sizes)
+    bytes_per_launch = bytes_spmv / max(1, iters)
+    avg_spmv_s = (ms_spmv * 1e-3 / n_spmv) if n_spmv else None
+    achieved = bytes_per_launch / avg_spmv_s / 1e9 if avg_spmv_s else None
+    if rank != 0:
+        return
+    out = {
+        "metric": METRIC, "value": round(coarsen_ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"partitioned C3: one {args.n}x{args.n}x{world * args.n} Kuhn tet box "
+                               f"({world * args.n ** 3:,} nodes, slab-major Morton), rank r owns slab r "
+                               f"({args.n ** 3:,} nodes); strain walls k = step mod 10, theta=5e-5, E=1e5, "
+                               "gs=32, affine_threshold=32, distributed block-Jacobi PCG to 1e-3 from x0=0",
+                   "nodes": world * args.n ** 3, "nodes_per_rank": args.n ** 3,
+                   "l2": "flushed between steps (256 MB write); per-rank fine BSR 1.1 GB > L2",
+                   "parallelism": f"{world} ranks, partitioned ({comm.world} x {dist.get_backend()})"},
+        "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,
+        "pcg_iters_per_step": round(iters / args.steps, 1),
+        "roofline": {"kernel": "k_spmv_sell (PCG SpMV + p.q; owned + halo rows)", "bound": "hbm",
+                     "achieved": None if achieved is None else round(achieved, 1), "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": None if achieved is None else round(achieved / hbm, 4), "traffic": None,
+                     "avg_launch_us": round(1e3 * ms_spmv / n_spmv, 2) if n_spmv else None,
+                     "algorithmic_bytes_per_launch": int(bytes_per_launch), "note": "rank 0's launches"},
+        "phase_ms_per_step": {k: round(v[1] / args.steps, 4) for k, v in prof.items()},
+        "coarse": {"n_slots_global": sizes[-1][3], "n_slots_rank0": sizes[-1][0], "ghost_slots_rank0": sizes[-1][4],
+                   "levels_rank0": sizes[-1][5]},
+        "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None,
+        "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
+    }
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -341,11 +465,23 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_i = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_i)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_i))
+        else:
+            dist.init_process_group("gloo")
+        run_partitioned(args, world, rank, local_rank)
+        dist.destroy_process_group()
+        return
     run_agipc(args, world, rank, local_rank)
     if world > 1:
         import torch.distributed as dist
