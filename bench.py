@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="agipc", choices=["agipc", "reference"])
-    ap.add_argument("--n", type=int, default=100, help="grid side (100 = C3, 1M nodes)")
+    ap.add_argument("--side", type=int, default=100, help="grid side (100 = C3, 1M nodes per GPU)")
     ap.add_argument("--check-every", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -153,7 +153,7 @@ def cpu_baseline(m, H, g, xc, steps=1, pcg_iters=20):
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    m, H, g, xcs, gen_s = build_inputs(args.n)
+    m, H, g, xcs, gen_s = build_inputs(args.side)
     times = []
     import oracle
     for s in range(args.warmup + args.steps):
@@ -185,7 +185,7 @@ def run_agipc(args, world, rank, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    m, H, g, xcs, gen_s = build_inputs(args.n)
+    m, H, g, xcs, gen_s = build_inputs(args.side)
     h = P.Handle(local_rank)
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
     dm = P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device=dev)
@@ -268,7 +268,7 @@ def run_agipc(args, world, rank, local_rank):
 
     # ---- e2e through the public API with host inputs ----
     e2e = None
-    if not args.no_e2e:
+    if not args.sideo_e2e:
         pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         hx = pin(m.X)
         hxc = [pin(x) for x in xcs]
@@ -305,7 +305,7 @@ def run_agipc(args, world, rank, local_rank):
                "scope": "H2D(x_prev, x_cur, H_f, g_f) + tag + map + assemble + D2H(g_c), pinned host memory"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.sideo_cpu_baseline:
         cb = cpu_baseline(m, H, g, xcs[0])
         cpu = {"value": round(cb["coarsen_ms"], 1), "unit": "ms", "cores": cb["cores"], "kind": "oracle",
                "sample": cb["sample"], "pcg_iters_per_s": round(cb["pcg_iters_per_s"], 2)}
@@ -371,7 +371,7 @@ def run_partitioned(args, world, rank, local_rank):
     torch.cuda.set_device(dev_i)
     dev = torch.device("cuda", dev_i)
     comm = Comm()
-    lm, Hl, Hh, g, disp, gen_s = build_partition(args.n, world, rank)
+    lm, Hl, Hh, g, disp, gen_s = build_partition(args.side, world, rank)
     pt.exchange_requests(lm, world, comm.alltoall_i64)
     h = P.Handle(dev_i)
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
@@ -433,11 +433,11 @@ def run_partitioned(args, world, rank, local_rank):
         "metric": METRIC, "value": round(coarsen_ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"partitioned C3: one {args.n}x{args.n}x{world * args.n} Kuhn tet box "
-                               f"({world * args.n ** 3:,} nodes, slab-major Morton), rank r owns slab r "
-                               f"({args.n ** 3:,} nodes); strain walls k = step mod 10, theta=5e-5, E=1e5, "
+        "config": {"workload": f"partitioned C3: one {args.side}x{args.side}x{world * args.side} Kuhn tet box "
+                               f"({world * args.side ** 3:,} nodes, slab-major Morton), rank r owns slab r "
+                               f"({args.side ** 3:,} nodes); strain walls k = step mod 10, theta=5e-5, E=1e5, "
                                "gs=32, affine_threshold=32, distributed block-Jacobi PCG to 1e-3 from x0=0",
-                   "nodes": world * args.n ** 3, "nodes_per_rank": args.n ** 3,
+                   "nodes": world * args.side ** 3, "nodes_per_rank": args.side ** 3,
                    "l2": "flushed between steps (256 MB write); per-rank fine BSR 1.1 GB > L2",
                    "parallelism": f"{world} ranks, partitioned ({comm.world} x {dist.get_backend()})"},
         "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,

@@ -173,7 +173,7 @@ class DistCoarseningStep:
             base += m
         gptr.append(lm.n_ghost)
         if not self.recv_peers:
-            gptr = [0, lm.n_ghost]
+            gptr = [0]
         hrp, hcol, hval = assemble_halo(h, self.dmesh, cs.new_map, cs.n3, n_c, self.Hh_ptr, self.Hh_col, Hh_val,
                                         self.ghost_code, gptr, sbase)
         return DistCoarse(cs, hrp, hcol, hval, slot_off, coarse_off, allc[:, 0].copy(), base - cs.n_slots, send_slots,
