@@ -11,6 +11,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
 
 
 def _init(rank, world, port):
@@ -160,8 +161,10 @@ def gpu_worker(rank, world, port, out_dir, n, thr, kind):
         assert st["status"] == P.OK and rr <= 1.01e-8, (st, rr)
         step.rel_tol = 1e-3
         _, st3 = step.solve(dc)
-        ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=1e-3, max_iters=10000)
-        assert abs(st3["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"])), (st3, ref["iters"])
+        from pcg_band import oracle_iteration_band  # reading R25
+        lo, hi = oracle_iteration_band(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], 1e-3)
+        assert lo <= st3["iters"] <= hi, (st3, lo, hi)
+        ref = {"iters": (lo, hi)}
         dist.barrier()
         dist.destroy_process_group()
         open(os.path.join(out_dir, f"ok{rank}"), "w").write(f"{st} {st3['iters']} {ref['iters']} {rr}")

@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import synth
+from pcg_band import oracle_iteration_band
 
 pytestmark = pytest.mark.gpu
 
@@ -221,7 +222,8 @@ def test_pcg_c1_matches_oracle(P, h):
         x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=tol, max_iters=10000, zero_x0=True)
         ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=tol, max_iters=10000)
         assert s["status"] == P.OK
-        assert abs(s["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"]))
+        lo, hi = oracle_iteration_band(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], tol)
+        assert lo <= s["iters"] <= hi, (s["iters"], lo, hi)
         rr = oracle.rel_residual(oa["row_ptr"], oa["col"], oa["val"], x.cpu().numpy(), oa["g_c"])
         assert rr <= max(tol, 1e-8) * 1.01
     x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-12, max_iters=20000, zero_x0=True)
@@ -354,10 +356,10 @@ def test_full_size_path(P, h, cfg):
     x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-8, max_iters=50000, zero_x0=True)
     rr = oracle.rel_residual(oa["row_ptr"], oa["col"], oa["val"], x.cpu().numpy(), oa["g_c"])
     assert s["status"] == P.OK and rr <= 1.01e-8, rr
-    if cfg == "c2":  # iteration count at the paper's tolerance
+    if cfg == "c2":  # iteration count at the paper's tolerance, band of reading R25
         _, s3 = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-3, zero_x0=True)
-        ref = oracle.pcg(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], rel_tol=1e-3, max_iters=10000)
-        assert abs(s3["iters"] - ref["iters"]) <= max(2, int(0.02 * ref["iters"]))
+        lo, hi = oracle_iteration_band(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], 1e-3)
+        assert lo <= s3["iters"] <= hi, (s3["iters"], lo, hi)
     # prolongation at full size on a seeded coarse vector (bit-exact)
     xc = np.random.default_rng(5).standard_normal((oa["n_slots"], 3))
     d = P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, dev(xc, torch.float64), -1.0)
