@@ -10,7 +10,7 @@ A step = one Newton iteration of the path: tag -> map -> assemble -> PCG (all of
   e2e        = the same through the public API with HOST inputs: the step's H2D copies
                (x_prev, x_cur, H_f values, g_f from pinned memory) and the D2H read of the
                step's result (the coarse right-hand side g_c) are inside the timed region
-  roofline   = the dominant kernel (PCG SpMV, k_spmv_pq): algorithmic bytes per launch
+  roofline   = the dominant kernel (PCG SpMV, k_spmv_sell): algorithmic bytes per launch
                / average launch duration measured with CUDA events on its launch stream
   cpu_baseline = the C oracle on the host cores (rank 0, N=1), bounded sample
 
@@ -256,7 +256,7 @@ def run_agipc(args, world, rank, local_rank):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("k_spmv_pq")
+            traffic = json.load(open(tf)).get("k_spmv_sell")
         except Exception:  # noqa: BLE001
             traffic = None
     # coarsen+assemble algorithmic bytes (SURVEY §8(d) model) for context
@@ -268,7 +268,7 @@ def run_agipc(args, world, rank, local_rank):
 
     # ---- e2e through the public API with host inputs ----
     e2e = None
-    if not args.sideo_e2e:
+    if not args.no_e2e:
         pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         hx = pin(m.X)
         hxc = [pin(x) for x in xcs]
@@ -305,7 +305,7 @@ def run_agipc(args, world, rank, local_rank):
                "scope": "H2D(x_prev, x_cur, H_f, g_f) + tag + map + assemble + D2H(g_c), pinned host memory"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.sideo_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(m, H, g, xcs[0])
         cpu = {"value": round(cb["coarsen_ms"], 1), "unit": "ms", "cores": cb["cores"], "kind": "oracle",
                "sample": cb["sample"], "pcg_iters_per_s": round(cb["pcg_iters_per_s"], 2)}
@@ -320,7 +320,7 @@ def run_agipc(args, world, rank, local_rank):
         "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,
         "pcg_iters_per_step": round(iters / args.steps, 1),
         "coarsen_assemble_gbs": round(b_coarsen / (coarsen_ms * 1e-3) / 1e9, 1),
-        "roofline": {"kernel": "k_spmv_pq (PCG SpMV + p.q)", "bound": "hbm",
+        "roofline": {"kernel": "k_spmv_sell (PCG SpMV + fused p update + p.q)", "bound": "hbm",
                      "achieved": None if achieved is None else round(achieved, 1), "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),

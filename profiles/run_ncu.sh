@@ -9,8 +9,11 @@ mkdir -p $OUT
 B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   $B > $OUT/launches_bench.log 2>&1
-for K in k_spmv_sell k_num_large k_mid_warp k_small_warp k_tail k_level0 k_update k_tag; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 40 -c 1 \
+# K:skip (launches to skip: the warm-up step's, or 40 PCG iterations)
+for KS in k_spmv_sell:40 k_update:40 k_num_large:2 k_mid_warp:2 k_small_warp:4 k_tail:1 k_level0:1 k_tag:1 \
+          k_cross_to_level1:1 k_sym_large:1; do
+  K=${KS%%:*}; S=${KS##*:}
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
     -o $OUT/full_$K $B > $OUT/full_$K.log 2>&1
 done
 for f in $OUT/full_*.ncu-rep; do

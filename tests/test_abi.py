@@ -91,3 +91,23 @@ def test_product_path_does_not_import_the_oracle():
     orc = open(os.path.join(ROOT, "oracle", "agipc_oracle.c")).read()
     includes = re.findall(r"#include\s*[<\"]([^>\"]+)[>\"]", orc)
     assert includes and all(i in ("math.h", "stdint.h", "stdlib.h", "string.h") for i in includes)
+
+
+def test_bench_args_exist_and_reference_arm_runs_on_cpu(tmp_path):
+    """bench.py only reads attributes its parser defines, and the reference arm (the CPU oracle)
+    prints one JSON line with the contract keys on a tiny grid."""
+    import json
+    import re
+    import subprocess
+    import sys
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    used = set(re.findall(r"args\.(\w+)", src))
+    dests = set(re.findall(r'add_argument\("--([\w-]+)"', src))
+    dests = {d.replace("-", "_") for d in dests}
+    assert used <= dests, used - dests
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--side", "6",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "impl", "cpu_baseline", "e2e", "config"):
+        assert k in line
