@@ -119,17 +119,108 @@ __device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles
   __syncthreads();  // S is reused by the next tile of a persistent CTA
 }
 
-// Level 0 over the fine mesh: one tile per CTA, tiles claimed in launch order.
+// Level 0 over the fine mesh.  A warp handles L0_CHUNKS consecutive chunks of gpw groups
+// (<= 32 nodes); the adjacency entries of a chunk are read ENTRY-parallel (lane = entry,
+// coalesced adj_nbr / tag loads, every load independent), each entry's row found by a binary
+// search over the chunk's row pointers in shared memory; intra-group tagged edges set the row's
+// hash bit with a shared atomicOr (Alg S1 l.10-13), tagged cross-group edges (u > v) are
+// compacted warp-wide (one global atomic per 32 entries).  Then the register closure /
+// election of group_tile per chunk, and one decoupled look-back per CTA tile.
+#define L0_CHUNKS 4
+
 __global__ void __launch_bounds__(MAP_THREADS)
     k_level0(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
              const uint8_t *__restrict__ tags, int32_t *__restrict__ map_out, int2 *__restrict__ cross,
              unsigned long long *__restrict__ cross_count, unsigned long long *status, int *tile_counter,
              long long *n_out) {
   __shared__ TileSmem S;
+  __shared__ long long s_ptr[MAP_WARPS][33];
+  __shared__ uint32_t s_h[MAP_WARPS][32];
   if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1);
   __syncthreads();
-  group_tile<true>(S, S.tile, gridDim.x, n, geo, adj_ptr, adj_nbr, tags, nullptr, map_out, cross, cross_count,
-                   status, n_out);
+  const int tile = S.tile;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gs = geo.gs, cn = geo.gpw * gs;  // nodes per chunk
+  const int gin = lane / gs, lig = lane - gin * gs, base_lane = gin * gs;
+  int local[L0_CHUNKS], off[L0_CHUNKS];
+  int wcount = 0;
+#pragma unroll
+  for (int c = 0; c < L0_CHUNKS; ++c) {
+    const int64_t q = ((int64_t)tile * MAP_WARPS + w) * L0_CHUNKS + c;
+    const int64_t v0 = q * cn;
+    const int nn = v0 < n ? (int)min((int64_t)cn, n - v0) : 0;
+    const int64_t v = v0 + lane;
+    const bool active = lane < nn;
+    if (lane <= nn) s_ptr[w][lane] = adj_ptr[v0 + lane];
+    if (lane == 0 && nn == 32) s_ptr[w][32] = adj_ptr[v0 + 32];
+    s_h[w][lane] = 0u;
+    __syncwarp();
+    if (nn > 0) {
+      const long long E0 = s_ptr[w][0], E1 = s_ptr[w][nn];
+      for (long long eb = E0; eb < E1; eb += 32) {
+        const long long e = eb + lane;
+        const bool valid = e < E1;
+        int u = 0, t = 0;
+        if (valid) {
+          u = __ldg(adj_nbr + e);
+          t = __ldg(tags + e);
+        }
+        int lo = 0, hi = nn;  // row r: s_ptr[r] <= e < s_ptr[r+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_ptr[w][mid] <= e) lo = mid; else hi = mid;
+        }
+        const int64_t vv = v0 + lo;
+        const int64_t gv = vv / gs;
+        const bool tg = valid && t;
+        const bool intra = tg && (int64_t)u / gs == gv;
+        const bool cr = tg && !intra && (int64_t)u > vv;
+        if (intra) atomicOr(&s_h[w][lo], 1u << (int)(u - gv * gs));
+        const unsigned b = __ballot_sync(FULL_MASK, cr);
+        if (b) {
+          unsigned long long cb = 0;
+          if (lane == 0) cb = atomicAdd(cross_count, (unsigned long long)__popc(b));
+          cb = __shfl_sync(FULL_MASK, cb, 0);
+          if (cr) cross[cb + __popc(b & ((1u << lane) - 1u))] = make_int2((int)vv, u);
+        }
+      }
+    }
+    __syncwarp();
+    uint32_t h = active ? ((1u << lig) | s_h[w][lane]) : 0u;
+    for (int k = 0; k < gs; ++k) {  // Alg S2 OR-propagation == Warshall closure
+      const uint32_t tt = __shfl_sync(FULL_MASK, h, (base_lane + k) & 31);
+      if ((h >> k) & 1u) h |= tt;
+    }
+    const bool elected = active && gin < geo.gpw && ((h & ((1u << lig) - 1u)) == 0u);
+    const unsigned bal = __ballot_sync(FULL_MASK, elected);
+    const unsigned gelect = (bal >> base_lane) & geo.gmask;
+    const int first = active ? __ffs(h) - 1 : 0;
+    local[c] = __popc(gelect & ((1u << first) - 1u));
+    off[c] = wcount + __popc(bal & ((1u << base_lane) - 1u));
+    wcount += __popc(bal);
+    __syncwarp();
+  }
+  if (lane == 0) S.warp[w] = wcount;
+  __syncthreads();
+  if (w == 0) {
+    const long long cc = lane < MAP_WARPS ? S.warp[lane] : 0;
+    const long long ci = warp_incl_scan(cc);
+    const long long agg = __shfl_sync(FULL_MASK, ci, MAP_WARPS - 1);
+    if (lane < MAP_WARPS) S.warp[lane] = ci - cc;
+    const long long pfx = lb_exclusive(status, tile, agg);  // ExclusiveSum over groups
+    if (lane == 0) {
+      S.prefix = pfx;
+      if (tile == gridDim.x - 1) *n_out = pfx + agg;
+    }
+  }
+  __syncthreads();
+  const long long wb = S.prefix + S.warp[w];
+#pragma unroll
+  for (int c = 0; c < L0_CHUNKS; ++c) {
+    const int64_t q = ((int64_t)tile * MAP_WARPS + w) * L0_CHUNKS + c;
+    const int64_t v = q * cn + lane;
+    if (lane < cn && v < n) map_out[v] = (int32_t)(wb + off[c] + local[c]);  // O[g] + P
+  }
 }
 
 // Map the tagged fine cross edges through the level-0 map and de-duplicate them with an
@@ -146,10 +237,16 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
     bool keep = false;
     int2 o = make_int2(0, 0);
     unsigned long long slot = 0;
+    unsigned long long key = 0ull;  // 0: no edge
     if (e < ne) {
       const int2 uv = E[e];
       o = make_int2(m0[uv.x], m0[uv.y]);
-      const unsigned long long key = (((unsigned long long)(unsigned)o.x << 32) | (unsigned)o.y) + 1ull;
+      key = (((unsigned long long)(unsigned)o.x << 32) | (unsigned)o.y) + 1ull;
+    }
+    // neighbouring list entries mostly map to the same coarse pair: one probe per distinct key
+    // of the warp (the lowest lane holding it)
+    const unsigned same = __match_any_sync(FULL_MASK, key);
+    if (key && (same & ((1u << (threadIdx.x & 31)) - 1u)) == 0u) {
       slot = (key * 0x9E3779B97F4A7C15ull) >> 20 & tmask;
       while (true) {
         const unsigned long long prev = atomicCAS(table + slot, 0ull, key);
@@ -196,10 +293,12 @@ struct TailArgs {
   long long *level_n;      // [64]
 };
 
-// Levels >= 1 in one cooperative kernel, one 1024-thread CTA per SM, three grid barriers per
-// level: (P1) intra-group edges -> hashes; (P2) closure/election per tile -> tile-local rank and
-// per-tile count; (P3) every CTA scans the tile counts in shared memory, remaps + compacts the
-// edges and composes the level maps.  Stops at the first level without an intra-group edge.
+// Levels >= 1 in one cooperative kernel, one 1024-thread CTA per SM, two grid barriers per
+// level: (P2) closure/election per tile -> tile-local rank and per-tile count; (P3) every CTA
+// scans the tile counts in shared memory, remaps + compacts the edges, composes the level maps
+// and ORs the remapped intra-group edges into the next level's hashes (P1 of the next level;
+// P1 of the first tail level runs on its own).  Stops at the first level without an
+// intra-group edge.  The "any intra edge" flag alternates between ctrl[0] and ctrl[1].
 __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ int32_t s_pref[];  // exclusive prefix of the tile counts
@@ -221,24 +320,28 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
     return;
   }
   const int gin = lane / gs, lig = lane - gin * gs, base_lane = gin * gs;
+  bool first_pass = true;
   while (true) {
     ++level;
-    // ---- P1: OR the intra-group edges into the node hashes ----
+    const int fl = level & 1;
     const int64_t ne = (int64_t)*(volatile unsigned long long *)(A.ne + cur);
     const int2 *E = A.E[cur];
-    bool hit = false;
-    for (int64_t e = gtid; e < ne; e += gstride) {
-      const int2 uv = E[e];
-      const int gu = uv.x / gs, gv = uv.y / gs;
-      if (gu == gv) {
-        atomicOr(A.h + uv.x, 1u << (uv.y - gv * gs));
-        atomicOr(A.h + uv.y, 1u << (uv.x - gu * gs));
-        hit = true;
+    if (first_pass) {  // ---- P1 of the first tail level: intra-group edges -> node hashes ----
+      bool hit = false;
+      for (int64_t e = gtid; e < ne; e += gstride) {
+        const int2 uv = E[e];
+        const int gu = uv.x / gs, gv = uv.y / gs;
+        if (gu == gv) {
+          atomicOr(A.h + uv.x, 1u << (uv.y - gv * gs));
+          atomicOr(A.h + uv.y, 1u << (uv.x - gu * gs));
+          hit = true;
+        }
       }
+      if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + fl, 1);
+      grid.sync();
+      first_pass = false;
     }
-    if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + 1, 1);
-    grid.sync();
-    if (*(volatile int *)(A.ctrl + 1) == 0) {  // no merge possible: this pass is the fixpoint
+    if (*(volatile int *)(A.ctrl + fl) == 0) {  // no merge possible: this pass is the fixpoint
       if (gtid == 0) {
         if (level <= 64) A.level_n[level - 1] = n;
         A.ctrl[2] = level;
@@ -303,6 +406,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
     }
     const int64_t n2 = s_total;
     int2 *Eo = A.E[1 - cur];
+    bool hit = false;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne; base += gstride) {
       const int64_t e = base + threadIdx.x;
       int2 o = make_int2(0, 0);
@@ -312,6 +416,11 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         o.x = s_pref[uv.x / TN] + A.mk[uv.x];
         o.y = s_pref[uv.y / TN] + A.mk[uv.y];
         keep = o.x != o.y;
+        if (keep && o.x / gs == o.y / gs) {  // P1 of the next level
+          atomicOr(A.h + o.x, 1u << (o.y - (o.y / gs) * gs));
+          atomicOr(A.h + o.y, 1u << (o.x - (o.x / gs) * gs));
+          hit = true;
+        }
       }
       const unsigned b = __ballot_sync(FULL_MASK, keep);
       unsigned long long wbase = 0;
@@ -319,12 +428,13 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       wbase = __shfl_sync(FULL_MASK, wbase, 0);
       if (keep) Eo[wbase + __popc(b & ((1u << lane) - 1u))] = o;
     }
+    if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
     for (int64_t c = gtid; c < n1; c += gstride) {
       const int32_t u = level == 2 ? (int32_t)c : A.comp[c];
       A.comp[c] = s_pref[u / TN] + A.mk[u];
     }
     if (gtid == 0) {
-      A.ctrl[1] = 0;
+      A.ctrl[fl] = 0;
       A.ctrl[3] = 1;
       if (level <= 64) A.level_n[level - 1] = n2;
     }
@@ -388,7 +498,8 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   geo.gs = group_size;
   geo.gpw = 32 / group_size;
   geo.gmask = group_size == 32 ? 0xffffffffu : ((1u << group_size) - 1u);
-  const int64_t tiles0 = std::max<int64_t>(1, cdiv(cdiv(N, geo.gs), (int64_t)MAP_WARPS * geo.gpw));
+  const int64_t tiles0 =
+      std::max<int64_t>(1, cdiv(cdiv(N, (int64_t)geo.gpw * geo.gs), (int64_t)MAP_WARPS * L0_CHUNKS));
   const int64_t ecap = mesh->nnz_adj / 2 + 1;
 
   WS(h, sc, MapScalars, "map_scalars", 1);
