@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       }
     // runs of equal column; colpos = prefix of the run weights (12-DoF columns count 4)
     int run_base = 0;
-    for (int e0 = 0; e0 < T; e0 += 32) {
+    for (int e0 = 0; !NUMERIC && e0 < T; e0 += 32) {
       const int e = e0 + l;
       const long long kk = e < T ? key[e] : LLONG_MAX;
       const int b = (int)(kk >> 10);
@@ -707,45 +707,99 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
         }
         continue;
       }
-      if (!head) continue;
-      int e_end = e + 1;
-      while (e_end < T && (key[e_end] >> 10) == (kk >> 10)) ++e_end;
-      const int ncb_a = ncb_of(a, n3), ncb_b = ncb_of(b, n3);
-      long long mbase = -1;  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
-      if (!A.is_small[b]) {
-        const int32_t *lb_ = A.gbuf + A.nb_off[b];
-        const int Ub = A.nb_cnt[b];
-        mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
-      }
+    }
+    if (NUMERIC) {
+      // Lane per sorted entry, one pass per row p of the node.  Per 32-entry window: the
+      // entries' blocks are loaded in parallel, scaled by w_j[q], summed over each run of equal
+      // column with a segmented shuffle scan; the tail lane of a run writes the coarse block
+      // (and its mirror in a large row, R22).  A run that continues into the next window
+      // passes its partial sums on in `carry` (added by the lanes of the next window's first run).
+      const int ncb_a = ncb_of(a, n3);
       for (int p = 0; p < ncb_a; ++p) {
-        const long long rs = A.crp[slot_of(a, p, n3)];
-        for (int q = 0; q < ncb_b; ++q) {
-          double acc[9];
+      double carry[4][9];
 #pragma unroll
-          for (int x = 0; x < 9; ++x) acc[x] = 0.0;
-          for (int ee = e; ee < e_end; ++ee) {
-            const int el = (int)(key[ee] & 1023);
-            int c;
-            long long k;
-            entry_of(tab, s, el, c, k);
-            const double coef = wgt(A.X, tab.ci[c], ncb_a, p) * wgt(A.X, A.col[k], ncb_b, q);
-            const double *B = A.val + 9 * k;
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int x = 0; x < 9; ++x) acc[x] += coef * __ldg(B + x);
-          }
-          const long long pos = rs + cp + q;
-          A.ccol[pos] = slot_of(b, q, n3);
-          double *dst = A.cval + 9 * pos;
-#pragma unroll
-          for (int x = 0; x < 9; ++x) dst[x] = acc[x];
-          if (mbase >= 0) {
-            double *mt = A.cval + 9 * (A.crp[slot_of(b, q, n3)] + mbase + p);
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = acc[3 * cc + r];
-          }
+        for (int x = 0; x < 9; ++x) carry[q][x] = 0.0;
+      int rb = 0, carry_cp = 0;
+      const long long rs = A.crp[slot_of(a, p, n3)];
+      for (int e0 = 0; e0 < T; e0 += 32) {
+        const int e = e0 + l;
+        const bool valid = e < T;
+        const long long kk = valid ? key[e] : LLONG_MAX;
+        const int b = (int)(kk >> 10);
+        const bool head = valid && (e == 0 || (key[e - 1] >> 10) != (kk >> 10));
+        const bool tail = valid && (e == T - 1 || (key[e + 1] >> 10) != (kk >> 10));
+        const int wgt_b = head ? ncb_of(b, n3) : 0;
+        const int incl = warp_incl_scan(wgt_b);
+        const unsigned hb = __ballot_sync(FULL_MASK, head);
+        const int hl = (hb & ((2u << l) - 1u)) ? 31 - __clz(hb & ((2u << l) - 1u)) : -1;  // my run's head lane
+        const int cp_head = rb + incl - wgt_b;
+        int cp = __shfl_sync(FULL_MASK, cp_head, hl < 0 ? 0 : hl);
+        if (hl < 0) cp = carry_cp;  // the run started in an earlier window
+        const int lo = hl < 0 ? 0 : hl;
+        int el = 0, j = 0;
+        long long k = 0;
+        double wi = 0.0;
+        if (valid) {
+          el = (int)(kk & 1023);
+          int c;
+          entry_of(tab, s, el, c, k);
+          j = A.col[k];
+          wi = wgt(A.X, tab.ci[c], ncb_a, p);
         }
+        double B[9];
+#pragma unroll
+        for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * k + x) : 0.0;
+        const int ncb_b = valid ? ncb_of(b, n3) : 1;
+        const int Q = __ballot_sync(FULL_MASK, valid && ncb_b == 4) ? 4 : 1;
+        long long mbase = -1;  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
+        if (tail && !A.is_small[b]) {
+          const int32_t *lb_ = A.gbuf + A.nb_off[b];
+          const int Ub = A.nb_cnt[b];
+          mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
+        }
+        const bool cont = valid && !tail && l == 31;  // my run continues into the next window
+        const int last_cp = __shfl_sync(FULL_MASK, cp, 31);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= Q) break;
+          const double coef = (valid && q < ncb_b) ? wi * wgt(A.X, j, ncb_b, q) : 0.0;
+          double v[9];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) {
+              const double t = __shfl_up_sync(FULL_MASK, v[x], o);
+              if (l - o >= lo) v[x] += t;
+            }
+          if (hl < 0) {
+#pragma unroll
+            for (int x = 0; x < 9; ++x) v[x] += carry[q][x];
+          }
+          if (tail && q < ncb_b) {
+            const long long pos = rs + cp + q;
+            A.ccol[pos] = slot_of(b, q, n3);
+            double *dst = A.cval + 9 * pos;
+#pragma unroll
+            for (int x = 0; x < 9; ++x) dst[x] = v[x];
+            if (mbase >= 0) {
+              double *mt = A.cval + 9 * (A.crp[slot_of(b, q, n3)] + mbase + p);
+#pragma unroll
+              for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
+            }
+          }
+          const bool any_cont = __shfl_sync(FULL_MASK, cont ? 1 : 0, 31);
+#pragma unroll
+          for (int x = 0; x < 9; ++x) carry[q][x] = any_cont ? __shfl_sync(FULL_MASK, v[x], 31) : 0.0;
+        }
+        carry_cp = last_cp;
+        rb += __shfl_sync(FULL_MASK, incl, 31);
+      }
       }
     }
     if (NUMERIC && A.g_f) {
