@@ -902,11 +902,12 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 #define LSTAGE 512
 
 template <int NCB>
-__global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
+__global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE];
   __shared__ int s_i[4][LSTAGE];
   __shared__ int s_j[4][LSTAGE];
+  __shared__ int s_b[4][LSTAGE];  // interface entries (staged from the top): column aggregate
   const int w = threadIdx.x >> 5, l = lane_id();
   // lane = (block group, p, q half): NCB = 4 -> 8 lanes per block, 2 q per lane
   constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
@@ -930,7 +931,7 @@ __global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
       for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
     for (int base = 0; base < T; base += LSTAGE) {
       const int n = min(LSTAGE, T - base);
-      int cnt = 0;
+      int cnt = 0, icnt = 0;
       for (int e0 = 0; e0 < n; e0 += 32) {
         const int e = base + e0 + l;
         bool diag = false;
@@ -952,45 +953,114 @@ __global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
           s_j[w][pos] = j;
         }
         cnt += __popc(m);
-        if (b >= 0 && b != a && !A.is_small[b]) {  // large-large interface block
-          const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b), first12);
-          const int ncb_b = ncb_of(b, n3);
-          double B[9];
+        // large-large interface block: staged from the top, reduced per column aggregate below
+        const bool itf = b >= 0 && b != a && !A.is_small[b];
+        const unsigned mi = __ballot_sync(FULL_MASK, itf);
+        if (itf) {
+          const int pos = LSTAGE - 1 - (icnt + __popc(mi & ((1u << l) - 1u)));
+          s_k[w][pos] = k;
+          s_i[w][pos] = i;
+          s_j[w][pos] = j;
+          s_b[w][pos] = b;
+        }
+        icnt += __popc(mi);
+      }
+      __syncwarp();
+      for (int d = gq; d < cnt; d += 4 * G) {  // four diagonal blocks per group in flight
+        long long kk[4];
+        int ii[4], jj[4];
+        bool ok[4];
 #pragma unroll
-          for (int x = 0; x < 9; ++x) B[x] = __ldg(A.val + 9 * k + x);
-          for (int pp = 0; pp < NCB; ++pp) {
-            const long long rs = A.crp[slot_of(a, pp, n3)];
-            const double wi = wgt(A.X, i, NCB, pp);
-            for (int q = 0; q < ncb_b; ++q) {
-              const double coef = wi * wgt(A.X, j, ncb_b, q);
-              double *dst = A.cval + 9 * (rs + cp + q);
+        for (int u = 0; u < 4; ++u) {
+          ok[u] = d + u * G < cnt;
+          const int dd = ok[u] ? d + u * G : d;
+          kk[u] = s_k[w][dd];
+          ii[u] = s_i[w][dd];
+          jj[u] = s_j[w][dd];
+        }
+        double Bv[4][9];
 #pragma unroll
-              for (int x = 0; x < 9; ++x) atomicAdd(dst + x, coef * B[x]);
-            }
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int x = 0; x < 9; ++x) Bv[u][x] = __ldg(A.val + 9 * kk[u] + x);
+        double wi[4], wj[4][QN];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wi[u] = ok[u] ? wgt(A.X, ii[u], NCB, p) : 0.0;
+#pragma unroll
+          for (int qq = 0; qq < QN; ++qq) wj[u][qq] = wgt(A.X, jj[u], NCB, q0 + qq);
+        }
+#pragma unroll
+        for (int qq = 0; qq < QN; ++qq) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double c = wi[u] * wj[u][qq];
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[qq][x] += c * Bv[u][x];
           }
         }
       }
       __syncwarp();
-      for (int d = gq; d < cnt; d += 2 * G) {
-        const bool two = d + G < cnt;
-        const long long k0 = s_k[w][d], k1 = two ? s_k[w][d + G] : k0;
-        const int i0 = s_i[w][d], i1 = two ? s_i[w][d + G] : i0;
-        const int j0 = s_j[w][d], j1 = two ? s_j[w][d + G] : j0;
-        double B0[9], B1[9];
-#pragma unroll
-        for (int x = 0; x < 9; ++x) {
-          B0[x] = __ldg(A.val + 9 * k0 + x);
-          B1[x] = __ldg(A.val + 9 * k1 + x);
+      // interface entries [LSTAGE - icnt, LSTAGE): one pass per distinct column aggregate b0,
+      // lanes (block group, p, q half) accumulate its entries, one set of atomics per (a, b0)
+      const int i0 = LSTAGE - icnt;
+      int left = icnt;
+      while (left > 0) {
+        int f = -1;
+        for (int d0 = 0; d0 < icnt && f < 0; d0 += 32) {
+          const unsigned mb = __ballot_sync(FULL_MASK, d0 + l < icnt && s_b[w][i0 + d0 + l] >= 0);
+          if (mb) f = d0 + __ffs(mb) - 1;
         }
-        const double wi0 = wgt(A.X, i0, NCB, p), wi1 = two ? wgt(A.X, i1, NCB, p) : 0.0;
+        const int b0 = s_b[w][i0 + f];
+        const int ncb_b = ncb_of(b0, n3);
+        constexpr int QI = NCB == 4 ? 2 : 4;  // q values per lane (a 3-DoF row meets 12-DoF columns)
+        double ac[QI][9];
 #pragma unroll
-        for (int qq = 0; qq < QN; ++qq) {
-          const double c0 = wi0 * wgt(A.X, j0, NCB, q0 + qq), c1 = wi1 * wgt(A.X, j1, NCB, q0 + qq);
+        for (int qq = 0; qq < QI; ++qq)
 #pragma unroll
-          for (int x = 0; x < 9; ++x) acc[qq][x] += c0 * B0[x] + c1 * B1[x];
+          for (int x = 0; x < 9; ++x) ac[qq][x] = 0.0;
+        for (int d = f + gq; d < icnt; d += G) {
+          if (s_b[w][i0 + d] != b0) continue;
+          const long long kk = s_k[w][i0 + d];
+          const double wi = wgt(A.X, s_i[w][i0 + d], NCB, p);
+          const int jj = s_j[w][i0 + d];
+          double Bv[9];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * kk + x);
+#pragma unroll
+          for (int qq = 0; qq < QI; ++qq) {
+            const double c = q0 + qq < ncb_b ? wi * wgt(A.X, jj, ncb_b, q0 + qq) : 0.0;
+#pragma unroll
+            for (int x = 0; x < 9; ++x) ac[qq][x] += c * Bv[x];
+          }
+        }
+        __syncwarp();
+        int done_n = 0;
+        for (int d0 = f; d0 < icnt; d0 += 32) {
+          const bool mine = d0 + l < icnt && s_b[w][i0 + d0 + l] == b0;
+          done_n += __popc(__ballot_sync(FULL_MASK, mine));
+          if (mine) s_b[w][i0 + d0 + l] = -1;
+        }
+        __syncwarp();
+        left -= done_n;
+#pragma unroll
+        for (int o = LPB; o < 32; o <<= 1)
+#pragma unroll
+          for (int qq = 0; qq < QI; ++qq)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) ac[qq][x] += __shfl_xor_sync(FULL_MASK, ac[qq][x], o);
+        const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b0), first12);
+        if (gq == 0) {
+          const long long rs = A.crp[slot_of(a, p, n3)];
+#pragma unroll
+          for (int qq = 0; qq < QI; ++qq)
+            if (q0 + qq < ncb_b) {
+              double *dst = A.cval + 9 * (rs + cp + q0 + qq);
+#pragma unroll
+              for (int x = 0; x < 9; ++x) atomicAdd(dst + x, ac[qq][x]);
+            }
         }
       }
-      __syncwarp();
     }
     // reduce over the block groups (lanes with the same p, q half) and flush the diagonal block
 #pragma unroll
