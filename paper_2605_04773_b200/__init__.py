@@ -23,7 +23,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libagipc.so")
+LIB_PATH = os.environ.get("AGIPC_LIB") or os.path.join(_HERE, "libagipc.so")
 _lib = None
 
 OK, EINVAL, ERANGE, ENOSPACE, ECUDA, ENCCL = 0, 1, 2, 3, 4, 5
