@@ -592,7 +592,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   int occ = 0;
   CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
   B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
-  B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 4 * (int64_t)h->sm_count));
+  B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 2 * (int64_t)h->sm_count));
   const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
   const int Gp = std::max(std::max(B.G1, B.G2), Gi);
   WS(h, parts, double, "pcg_parts", 3 * Gp); B.parts = parts;
