@@ -7,6 +7,8 @@ recursion of step 2 is rank-local, reading R24).  Its LOCAL mesh numbers the own
 owned node) n_own.. in ascending global id, so the ghosts of one peer form one contiguous
 range.
 
+  * ghosts      non-owned vertices of those tets and non-owned columns of the owned rows of the
+                fine Hessian (contact couplings, C4);
   * tets        every tet with at least one owned vertex (boundary tets are evaluated on both
                 sides); tet_slots is -1 for an edge that is not owned at both ends, so tags are
                 written only into owned rows and cross-rank edges never merge;
@@ -70,6 +72,9 @@ def local_mesh(mesh, gid, lo, hi, bounds, rank) -> LocalMesh:
     used = np.zeros(Nm, bool)
     used[tets_m.ravel()] = True
     used |= own
+    # Hessian-only couplings of owned rows (contact blocks, C4) also need their columns
+    brow_all = np.repeat(np.arange(Nm), np.diff(mesh.bsr_ptr))
+    used[mesh.bsr_col[own[brow_all]]] = True
     ghost = used & ~own
     own_idx = np.nonzero(own)[0]
     ghost_idx = np.nonzero(ghost)[0]   # ascending mesh id == ascending gid

@@ -49,6 +49,7 @@ class Mesh:
     diag_slot: np.ndarray    # int64  [N] BSR slot of the diagonal block of each row
     ijk: np.ndarray | None = None  # int32 [N,3] grid coordinates (grid meshes)
     n_side: int = 0
+    n_extra: int = 0         # BSR blocks beyond adjacency + diagonal (contact pairs, C4)
 
     @property
     def n_nodes(self) -> int:
@@ -72,8 +73,10 @@ def _morton_key(ijk: np.ndarray) -> np.ndarray:
     return key
 
 
-def mesh_from_tets(X: np.ndarray, tets: np.ndarray, ijk=None, n_side=0) -> Mesh:
-    """Build adjacency, tet->slot table and the fine BSR pattern from tets."""
+def mesh_from_tets(X: np.ndarray, tets: np.ndarray, ijk=None, n_side=0, extra_pairs=None) -> Mesh:
+    """Build adjacency, tet->slot table and the fine BSR pattern from tets.  `extra_pairs`
+    (int [P,2]) adds symmetric Hessian-only blocks (contact, C4) to the BSR pattern; they are
+    not mesh edges (never tagged, not in the adjacency)."""
     X = np.ascontiguousarray(X, dtype=np.float64)
     tets = np.ascontiguousarray(tets, dtype=np.int32)
     N = X.shape[0]
@@ -116,10 +119,31 @@ def mesh_from_tets(X: np.ndarray, tets: np.ndarray, ijk=None, n_side=0) -> Mesh:
     bsr_col[np.arange(2 * E, dtype=np.int64) + rows + gt] = adj_nbr
     diag_slot = adj_ptr[:-1] + np.arange(N, dtype=np.int64) + nbelow
     bsr_col[diag_slot] = np.arange(N, dtype=np.int32)
+    n_extra = 0
+    if extra_pairs is not None and len(extra_pairs):
+        ep = np.asarray(extra_pairs, np.int64)
+        brow = np.repeat(np.arange(N, dtype=np.int64), np.diff(bsr_ptr))
+        key = np.unique(np.concatenate([brow * N + bsr_col, ep[:, 0] * N + ep[:, 1], ep[:, 1] * N + ep[:, 0]]))
+        n_extra = int(key.shape[0] - bsr_col.shape[0])
+        bsr_col = (key % N).astype(np.int32)
+        bsr_ptr = np.zeros(N + 1, np.int64)
+        np.cumsum(np.bincount(key // N, minlength=N), out=bsr_ptr[1:])
+        diag_slot = np.searchsorted(key, np.arange(N, dtype=np.int64) * (N + 1))
     return Mesh(X=X, tets=tets, adj_ptr=adj_ptr, adj_nbr=adj_nbr, tet_slots=ts,
                 edges=edges, edge_of_slot=edge_of_slot, bsr_ptr=bsr_ptr, bsr_col=bsr_col,
                 diag_slot=diag_slot,
-                ijk=None if ijk is None else np.ascontiguousarray(ijk, np.int32), n_side=n_side)
+                ijk=None if ijk is None else np.ascontiguousarray(ijk, np.int32), n_side=n_side, n_extra=n_extra)
+
+
+def bsr_slot(mesh: Mesh, u, v) -> np.ndarray:
+    """BSR slot of blocks (u, v) (general lookup; -1 if absent)."""
+    N = mesh.n_nodes
+    brow = np.repeat(np.arange(N, dtype=np.int64), np.diff(mesh.bsr_ptr))
+    key = brow * N + mesh.bsr_col
+    q = np.asarray(u, np.int64) * N + np.asarray(v, np.int64)
+    pos = np.searchsorted(key, q)
+    ok = (pos < key.shape[0]) & (key[np.minimum(pos, key.shape[0] - 1)] == q)
+    return np.where(ok, pos, -1)
 
 
 def kuhn_grid(n: int, order: str = "morton", side: float = 1.0, origin=(0.0, 0.0, 0.0)) -> Mesh:
@@ -202,6 +226,10 @@ def _slot_index(mesh: Mesh, t0: int, t1: int) -> np.ndarray:
     BSR pattern is the adjacency row with the diagonal inserted, so
     bsr_slot(u->v) = adj_slot(u->v) + u + [v > u]."""
     tets = mesh.tets[t0:t1].astype(np.int64)
+    if mesh.n_extra:  # the pattern is not adjacency + diagonal: general lookup
+        u = np.repeat(tets, 4, axis=1).reshape(-1)
+        v = np.tile(tets, (1, 4)).reshape(-1)
+        return bsr_slot(mesh, u, v).reshape(tets.shape[0], 4, 4)
     ts = mesh.tet_slots[t0:t1].astype(np.int64)
     S = np.empty((tets.shape[0], 4, 4), np.int64)
     for k in range(4):
@@ -425,3 +453,77 @@ def slab_gradient(gid: np.ndarray, seed: int = 0) -> np.ndarray:
         sel = blk == b
         g[sel] = np.random.default_rng([seed, 7, int(b)]).standard_normal((1 << 16, 3))[gid[sel] & 0xFFFF]
     return g
+
+
+# ----------------------------------------------------------------------------
+# C4: multi-object contact scene: k^3 objects of n^3 nodes on a lattice with
+# gaps, E cycling {1e5, 1e6, 1e7}, contact blocks between facing boundary nodes of adjacent
+# objects (Hessian entries, never tagged: coarsening stays inside objects)
+# ----------------------------------------------------------------------------
+
+def c4_scene(n: int = 57, k: int = 3, gap: float = 1e-3, side: float = 1.0, seed: int = 0):
+    base = kuhn_grid(n, side=side)
+    N0 = base.n_nodes
+    nobj = k ** 3
+    pitch = side + gap
+    offs = []
+    for ox in range(k):
+        for oy in range(k):
+            for oz in range(k):
+                offs.append(((ox - (k - 1) / 2) * pitch, (oy - (k - 1) / 2) * pitch, (oz - (k - 1) / 2) * pitch))
+    offs = np.asarray(offs)
+    X = np.concatenate([base.X + offs[o] for o in range(nobj)])
+    tets = np.concatenate([base.tets.astype(np.int64) + o * N0 for o in range(nobj)]).astype(np.int32)
+    ijk = np.tile(base.ijk, (nobj, 1))
+    # facing boundary nodes of lattice neighbours: (max face of o, min face of o + e_d)
+    lid = np.empty((n, n, n), np.int64)
+    lid[base.ijk[:, 0], base.ijk[:, 1], base.ijk[:, 2]] = np.arange(N0)
+    oid = np.arange(nobj).reshape(k, k, k)
+    pairs, normals = [], []
+    for d in range(3):
+        hi = np.take(lid, n - 1, axis=d).reshape(-1)
+        lo = np.take(lid, 0, axis=d).reshape(-1)
+        a_obj = np.take(oid, np.arange(k - 1), axis=d).reshape(-1)
+        b_obj = np.take(oid, np.arange(1, k), axis=d).reshape(-1)
+        for oa, ob in zip(a_obj, b_obj):
+            pairs.append(np.stack([hi + oa * N0, lo + ob * N0], axis=1))
+            nrm = np.zeros(3)
+            nrm[d] = 1.0
+            normals.append(np.broadcast_to(nrm, (hi.shape[0], 3)))
+    pairs = np.concatenate(pairs)
+    normals = np.concatenate(normals)
+    m = mesh_from_tets(X, tets, ijk=ijk, n_side=n, extra_pairs=pairs)
+    E_tet = np.repeat(np.asarray([(1e5, 1e6, 1e7)[o % 3] for o in range(nobj)]), base.n_tets)
+    rng = np.random.default_rng([seed, 41])
+    axes = rng.standard_normal((nobj, 3))
+    return dict(mesh=m, N0=N0, nobj=nobj, offs=offs, pairs=pairs, normals=normals, E_tet=E_tet, axes=axes,
+                side=side)
+
+
+def c4_hessian(sc: dict, dt: float = 0.01) -> np.ndarray:
+    """H_f = M + dt^2 K (per-object E) + contact kappa n n^T couplings, kappa = the mean
+    diagonal entry of the elastic H_f (PSD pair blocks)."""
+    m = sc["mesh"]
+    H = fine_hessian(m, E=sc["E_tet"], dt=dt)
+    kappa = float(np.mean(np.einsum("bii->b", H[m.diag_slot]) / 3.0))
+    i, j = sc["pairs"][:, 0], sc["pairs"][:, 1]
+    nn = np.einsum("pa,pb->pab", sc["normals"], sc["normals"]) * kappa
+    np.add.at(H, m.diag_slot[i], nn)
+    np.add.at(H, m.diag_slot[j], nn)
+    np.add.at(H, bsr_slot(m, i, j), -nn)
+    np.add.at(H, bsr_slot(m, j, i), -nn)
+    return H
+
+
+def c4_iterates(sc: dict, alpha0: float = 0.5, alpha1: float = 0.501, w: float = 0.2):
+    """Per object: twist about its seeded random axis through its centre, alpha0 -> alpha1."""
+    m = sc["mesh"]
+    N0 = sc["N0"]
+    xp = np.empty_like(m.X)
+    xc = np.empty_like(m.X)
+    for o in range(sc["nobj"]):
+        sl = slice(o * N0, (o + 1) * N0)
+        c = sc["offs"][o]
+        xp[sl] = twist(m.X[sl], alpha0, w=w * sc["side"], axis=sc["axes"][o], center=c)
+        xc[sl] = twist(m.X[sl], alpha1, w=w * sc["side"], axis=sc["axes"][o], center=c)
+    return xp, xc

@@ -79,13 +79,23 @@ def gpu_worker(rank, world, port, out_dir, n, thr, kind):
         torch.cuda.set_device(0)
         comm = Comm()
         h = P.Handle(0)
-        G, gid = synth.kuhn_box(n, slabs=world)
-        b = pt.slab_bounds(n, world)
+        if kind == "c4":  # multi-object contact scene split mid-object (contact blocks become halo)
+            sc = synth.c4_scene(n=n, k=2)
+            G = sc["mesh"]
+            gid = np.arange(G.n_nodes)
+            b = [int(round(r * G.n_nodes / world)) for r in range(world + 1)]
+            H = synth.c4_hessian(sc)
+        else:
+            G, gid = synth.kuhn_box(n, slabs=world)
+            b = pt.slab_bounds(n, world)
+            H = synth.fine_hessian(G)
         lm = pt.local_mesh(G, gid, b[rank], b[rank + 1], b, rank)
         pt.exchange_requests(lm, world, comm.alltoall_i64)
-        H = synth.fine_hessian(G)
         g = synth.fine_gradient(G.n_nodes, seed=1)
-        if kind == "twist":
+        if kind == "c4":
+            xp, xc = synth.c4_iterates(sc)
+            theta = 5e-5
+        elif kind == "twist":
             xp, xc, theta = synth.twist(G.X, 0.5, w=0.2 * world), synth.twist(G.X, 0.501, w=0.2 * world), 5e-5
         else:
             rng = np.random.default_rng(3)

@@ -337,6 +337,31 @@ def test_step_with_refinement(P, h):
 
 
 # ------------------------------------------------------------------------------------------
+# C4: multi-object contact scene (contact blocks in H_f, per-object stiffness 1e5/1e6/1e7)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,thr", [(5, 32), (8, 32), (8, 5)])
+def test_c4_contact_scene_path(P, h, n, thr):
+    sc = synth.c4_scene(n=n, k=3)
+    m = sc["mesh"]
+    dm = dmesh(P, m)
+    H = synth.c4_hessian(sc)
+    g = synth.fine_gradient(m.n_nodes, seed=4)
+    xp, xc = synth.c4_iterates(sc)
+    tags, nf = P.tag_edges(h, dm, dev(xp, torch.float64), dev(xc, torch.float64), 5e-5, count=True)
+    ot, _, of = oracle.tag_edges(m.tets, m.tet_slots, m.X, xp, xc, 5e-5, m.adj_nbr.shape[0])
+    assert np.array_equal(tags.cpu().numpy(), ot) and nf == int(of.sum())
+    _, info, om = check_map(P, h, m, dm, ot, 32)
+    obj = np.arange(m.n_nodes) // sc["N0"]
+    first = np.full(om["n_coarse"], -1)
+    first[om["map"]] = obj               # every aggregate lies inside one object
+    assert np.array_equal(first[om["map"]], obj)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, thr)
+    x, s = P.pcg_solve(h, cs.row_ptr, cs.col, cs.val, cs.g_c, rel_tol=1e-8, max_iters=50000, zero_x0=True)
+    rr = oracle.rel_residual(oa["row_ptr"], oa["col"], oa["val"], x.cpu().numpy(), oa["g_c"])
+    assert s["status"] == P.OK and rr <= 1.01e-8, rr
+
+
+# ------------------------------------------------------------------------------------------
 # full sizes (C2, C3) in the launch configuration bench.py times
 # ------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("cfg", ["c2", "c3"])

@@ -239,3 +239,16 @@ def test_segments_keep_aggregates_inside_segments():
     r2 = oracle.build_map(m.adj_ptr, m.adj_nbr, tags, 32, seg_begin=seg)
     assert r2["n_coarse"] == 2
     assert np.all(r2["map"][:512] == 0) and np.all(r2["map"][512:] == 1)
+
+
+def test_contact_blocks_never_merge_objects():
+    """C4: contact couplings are Hessian entries, not mesh edges -- with every edge
+    collapsible each object collapses to one aggregate and no aggregate spans two objects."""
+    sc = synth.c4_scene(n=4, k=2)
+    m = sc["mesh"]
+    tags = np.ones(m.adj_nbr.shape[0], np.uint8)
+    om = oracle.build_map(m.adj_ptr, m.adj_nbr, tags, 32)
+    assert om["n_coarse"] == sc["nobj"]
+    obj = np.arange(m.n_nodes) // sc["N0"]
+    assert np.array_equal(om["map"], obj)  # numbered by minimum member = object order
+    assert m.n_extra == 2 * len(sc["pairs"])
