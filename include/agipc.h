@@ -211,6 +211,28 @@ AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const
                                        int zero_x0, double rel_tol, int max_iters, int check_every,
                                        agipc_pcg_stats *stats);
 
+/* ---- NEXT#4: step 1 for shells and rods ------------------------------------------------
+ * "applicable to various element types (shells, volumes, rods)" (main Sec 4.2).
+ *   shells (triangles a,b,c): rest tangent basis t1 = e1/|e1|, n = e1 x e2 / |e1 x e2|,
+ *     t2 = n x t1 (e1 = X_b - X_a, e2 = X_c - X_a); D_m = [t_r . e_c] (2x2);
+ *     F = D_s D_m^-1 (3x2), D_s = [x_b - x_a | x_c - x_a]; G = 1/2 (F^T F - I_2)
+ *   rods (edges a,b): F = |x_b - x_a| / |X_b - X_a|, G = 1/2 (F^2 - 1)
+ *   n_el = ||G(x_cur) - G(x_prev)||_F, flagged iff n_el > threshold (strict); every slot listed
+ *   for a flagged element gets tag 0.  Flags ACCUMULATE into slot_tags: reset_tags = 1 first
+ *   sets all nnz_adj slots to 1; a mixed mesh calls agipc_tag_edges (which resets) and then
+ *   these with reset_tags = 0, so an edge is protected iff ANY adjacent element is flagged.
+ *   tris [T][3] / segs [S][2]: node ids; tri_slots [T][6] = slots of (01,10,02,20,12,21),
+ *   seg_slots [S][2] = slots of (ab, ba); -1 = no slot.  Fixed fp64 operation order (R12).
+ *   Errors / n_flagged / EDEGENERATE as agipc_tag_edges. */
+AGIPC_API agipc_status agipc_tag_shells(agipc_handle h, int64_t n_tris, const int32_t *tris, const int32_t *tri_slots,
+                                        const double *x_rest, const double *x_prev, const double *x_cur,
+                                        double threshold, int64_t nnz_adj, int reset_tags, uint8_t *slot_tags,
+                                        double *tri_norm, int64_t *n_flagged /*[host]*/);
+AGIPC_API agipc_status agipc_tag_rods(agipc_handle h, int64_t n_segs, const int32_t *segs, const int32_t *seg_slots,
+                                      const double *x_rest, const double *x_prev, const double *x_cur,
+                                      double threshold, int64_t nnz_adj, int reset_tags, uint8_t *slot_tags,
+                                      double *seg_norm, int64_t *n_flagged /*[host]*/);
+
 /* ---- NEXT#1: prolongation d_f = U^T d_c ------------------------------------------------
  * "we mathematically prolongate the displacement to the fine mesh using the transpose of
  * the restriction operator" (main Sec 4.3).  For every fine node f with parent

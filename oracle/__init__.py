@@ -54,6 +54,9 @@ def lib():
         L.orc_block_jacobi.restype = i32
         L.orc_prolongate.argtypes = [i64, P, i64, P, P, P]
         L.orc_prolongate.restype = None
+        for nm in ("orc_tag_shells", "orc_tag_rods"):
+            getattr(L, nm).argtypes = [i64, P, P, P, P, P, f64, i64, i32, P, P, P]
+            getattr(L, nm).restype = i32
         _lib = L
     return _lib
 
@@ -202,3 +205,29 @@ def prolongate(new_map, n3, X, x_c):
     d = np.empty((N, 3))
     lib().orc_prolongate(N, _p(nm), int(n3), _p(X), _p(xc), _p(d))
     return d
+
+
+def _tag_elems(fn, elems, slots, X, x_prev, x_cur, theta, n_slots, slot_tags=None):
+    el = _c(elems, np.int32); sl = _c(slots, np.int32)
+    X = _c(X, np.float64); xp = _c(x_prev, np.float64); xc = _c(x_cur, np.float64)
+    T = el.shape[0]
+    reset = slot_tags is None
+    tags = np.empty(n_slots, np.uint8) if reset else np.ascontiguousarray(slot_tags, np.uint8).copy()
+    norm = np.empty(T, np.float64)
+    bad = np.zeros(1, np.int64)
+    st = getattr(lib(), fn)(T, _p(el), _p(sl), _p(X), _p(xp), _p(xc), float(theta), int(n_slots), int(reset),
+                            _p(tags), _p(norm), _p(bad))
+    if st != OK:
+        raise OracleError(st, f"degenerate element {int(bad[0])}")
+    return tags, norm
+
+
+def tag_shells(tris, tri_slots, X, x_prev, x_cur, theta, n_slots, slot_tags=None):
+    """NEXT#4, triangles ("shells"): returns (slot_tags, tri_norm).  If slot_tags is given
+    the flags are accumulated into a copy of it (tets + shells + rods), else all start at 1."""
+    return _tag_elems("orc_tag_shells", tris, tri_slots, X, x_prev, x_cur, theta, n_slots, slot_tags)
+
+
+def tag_rods(segs, seg_slots, X, x_prev, x_cur, theta, n_slots, slot_tags=None):
+    """NEXT#4, edges ("rods"): G = 1/2 (F^2 - 1), F = l / L."""
+    return _tag_elems("orc_tag_rods", segs, seg_slots, X, x_prev, x_cur, theta, n_slots, slot_tags)

@@ -546,3 +546,119 @@ void orc_prolongate(int64_t N, const int32_t *new_map, int64_t n3, const double 
     }
   }
 }
+
+/* ========================================================================== */
+/* NEXT#4 -- step 1 for shells and rods (main Sec 4.2: "applicable to various  */
+/* element types (shells, volumes, rods)").       */
+/* Triangle (a,b,c): rest tangent basis t1 = e1/|e1|, n = (e1 x e2)/|e1 x e2|, */
+/* t2 = n x t1 (e1 = X_b - X_a, e2 = X_c - X_a); D_m = [t_r . e_c] (2x2);       */
+/* F = D_s D_m^-1 (3x2), D_s = [x_b - x_a | x_c - x_a]; G = 1/2 (F^T F - I_2). */
+/* Edge (a,b): F = l / L (current / rest length), G = 1/2 (F^2 - 1).           */
+/* n = ||G(x_cur) - G(x_prev)||_F (|.| for edges), flagged iff n > theta;     */
+/* every directed slot of a flagged element's edges gets tag 0.  The caller's  */
+/* slot_tags are NOT reset (tets, shells and rods accumulate; reset_tags = 1   */
+/* first sets every slot to 1).  Fixed operation order, no FMA [R12].          */
+/* ========================================================================== */
+static double dot3(const double *u, const double *v) { return u[0] * v[0] + u[1] * v[1] + u[2] * v[2]; }
+
+static void cross3(const double *u, const double *v, double *w) {
+  w[0] = u[1] * v[2] - u[2] * v[1];
+  w[1] = u[2] * v[0] - u[0] * v[2];
+  w[2] = u[0] * v[1] - u[1] * v[0];
+}
+
+/* G (2x2) of triangle t at positions P, with the rest inverse Minv */
+static void tri_green(const double *P, const int32_t *t, const double Minv[2][2], double G[2][2]) {
+  double d1[3], d2[3], F[3][2];
+  for (int r = 0; r < 3; ++r) {
+    d1[r] = P[3 * (int64_t)t[1] + r] - P[3 * (int64_t)t[0] + r];
+    d2[r] = P[3 * (int64_t)t[2] + r] - P[3 * (int64_t)t[0] + r];
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 2; ++c) F[r][c] = d1[r] * Minv[0][c] + d2[r] * Minv[1][c];
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) {
+      double C = F[0][r] * F[0][c] + F[1][r] * F[1][c] + F[2][r] * F[2][c];
+      G[r][c] = 0.5 * (C - (r == c ? 1.0 : 0.0));
+    }
+}
+
+int orc_tag_shells(int64_t n_tris, const int32_t *tris, const int32_t *tri_slots, const double *X,
+                   const double *x_prev, const double *x_cur, double theta, int64_t n_slots, int reset_tags,
+                   uint8_t *slot_tags, double *tri_norm, int64_t *bad) {
+  if (reset_tags)
+    for (int64_t s = 0; s < n_slots; ++s) slot_tags[s] = 1;
+  for (int64_t t = 0; t < n_tris; ++t) {
+    const int32_t *tt = tris + 3 * t;
+    double e1[3], e2[3], nr[3], t1[3], t2[3];
+    for (int r = 0; r < 3; ++r) {
+      e1[r] = X[3 * (int64_t)tt[1] + r] - X[3 * (int64_t)tt[0] + r];
+      e2[r] = X[3 * (int64_t)tt[2] + r] - X[3 * (int64_t)tt[0] + r];
+    }
+    double L1 = sqrt(dot3(e1, e1));
+    cross3(e1, e2, nr);
+    double Ln = sqrt(dot3(nr, nr));
+    if (L1 == 0.0 || Ln == 0.0 || !isfinite(L1) || !isfinite(Ln)) {
+      if (bad) *bad = t;
+      return ORC_EDEGENERATE;
+    }
+    double i1 = 1.0 / L1, in = 1.0 / Ln;
+    for (int r = 0; r < 3; ++r) {
+      t1[r] = e1[r] * i1;
+      nr[r] = nr[r] * in;
+    }
+    cross3(nr, t1, t2);
+    double Dm[2][2] = {{dot3(t1, e1), dot3(t1, e2)}, {dot3(t2, e1), dot3(t2, e2)}};
+    double det = Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0];
+    if (det == 0.0 || !isfinite(det)) {
+      if (bad) *bad = t;
+      return ORC_EDEGENERATE;
+    }
+    double id = 1.0 / det;
+    double Minv[2][2] = {{Dm[1][1] * id, -Dm[0][1] * id}, {-Dm[1][0] * id, Dm[0][0] * id}};
+    double Gp[2][2], Gc[2][2];
+    tri_green(x_prev, tt, Minv, Gp);
+    tri_green(x_cur, tt, Minv, Gc);
+    double s2 = 0.0;
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) {
+        double d = Gc[r][c] - Gp[r][c];
+        s2 = s2 + d * d;
+      }
+    double n = sqrt(s2);
+    if (tri_norm) tri_norm[t] = n;
+    if (n > theta)
+      for (int k = 0; k < 6; ++k)
+        if (tri_slots[6 * t + k] >= 0) slot_tags[tri_slots[6 * t + k]] = 0;
+  }
+  return ORC_OK;
+}
+
+int orc_tag_rods(int64_t n_segs, const int32_t *segs, const int32_t *seg_slots, const double *X,
+                 const double *x_prev, const double *x_cur, double theta, int64_t n_slots, int reset_tags,
+                 uint8_t *slot_tags, double *seg_norm, int64_t *bad) {
+  if (reset_tags)
+    for (int64_t s = 0; s < n_slots; ++s) slot_tags[s] = 1;
+  for (int64_t t = 0; t < n_segs; ++t) {
+    const int64_t a = segs[2 * t], b = segs[2 * t + 1];
+    double dR[3], dp[3], dc[3];
+    for (int r = 0; r < 3; ++r) {
+      dR[r] = X[3 * b + r] - X[3 * a + r];
+      dp[r] = x_prev[3 * b + r] - x_prev[3 * a + r];
+      dc[r] = x_cur[3 * b + r] - x_cur[3 * a + r];
+    }
+    double L = sqrt(dot3(dR, dR));
+    if (L == 0.0 || !isfinite(L)) {
+      if (bad) *bad = t;
+      return ORC_EDEGENERATE;
+    }
+    double Fp = sqrt(dot3(dp, dp)) / L, Fc = sqrt(dot3(dc, dc)) / L;
+    double Gp = 0.5 * (Fp * Fp - 1.0), Gc = 0.5 * (Fc * Fc - 1.0);
+    double n = fabs(Gc - Gp);
+    if (seg_norm) seg_norm[t] = n;
+    if (n > theta)
+      for (int k = 0; k < 2; ++k)
+        if (seg_slots[2 * t + k] >= 0) slot_tags[seg_slots[2 * t + k]] = 0;
+  }
+  return ORC_OK;
+}

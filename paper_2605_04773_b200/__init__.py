@@ -76,7 +76,8 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_version", "agipc_kernel_launches", "agipc_profile", "agipc_profile_read", "agipc_tag_edges",
            "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate",
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
-           "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish"]
+           "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
+           "agipc_tag_rods"]
 
 
 def lib():
@@ -110,6 +111,8 @@ def lib():
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
+        for nm in ("agipc_tag_shells", "agipc_tag_rods"):
+            getattr(L, nm).argtypes = [P, i64, P, P, P, P, P, f64, i64, i32, P, P, C.POINTER(i64)]
         L.agipc_coarse_halo.argtypes = [P, P, i64, i64, P, i64, P, P, i64, C.POINTER(i64)]
         L.agipc_assemble_halo.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), i64, P, i32,
                                           C.POINTER(i64), C.POINTER(i64), C.POINTER(_HaloMatrix)]
@@ -441,3 +444,25 @@ class DistPcg:
         self.h._check(lib().agipc_dpcg_finish(self.h._h, _p(self.red), _p(x), C.byref(s)), allow=(NOT_CONVERGED,))
         return dict(iters=int(s.iters), status=int(s.status), rel_residual=float(s.rel_residual),
                     b_norm=float(s.b_norm))
+
+
+def _tag_elems(fn, h, elems, el_slots, x_rest, x_prev, x_cur, threshold, slot_tags, reset, norm, count):
+    nf = C.c_int64(0)
+    h._check(getattr(lib(), fn)(h._h, int(elems.shape[0]), _p(elems), _p(el_slots), _p(x_rest), _p(x_prev), _p(x_cur),
+                                float(threshold), int(slot_tags.shape[0]), int(bool(reset)), _p(slot_tags), _p(norm),
+                                C.byref(nf) if count else None))
+    return slot_tags, (int(nf.value) if count else None)
+
+
+def tag_shells(h: Handle, tris, tri_slots, x_rest, x_prev, x_cur, threshold: float, slot_tags, reset: bool = False,
+               tri_norm=None, count: bool = False):
+    """NEXT#4: step 1 for triangles; flags accumulate into slot_tags unless reset."""
+    return _tag_elems("agipc_tag_shells", h, tris, tri_slots, x_rest, x_prev, x_cur, threshold, slot_tags, reset,
+                      tri_norm, count)
+
+
+def tag_rods(h: Handle, segs, seg_slots, x_rest, x_prev, x_cur, threshold: float, slot_tags, reset: bool = False,
+             seg_norm=None, count: bool = False):
+    """NEXT#4: step 1 for rods (edges); flags accumulate into slot_tags unless reset."""
+    return _tag_elems("agipc_tag_rods", h, segs, seg_slots, x_rest, x_prev, x_cur, threshold, slot_tags, reset,
+                      seg_norm, count)

@@ -527,3 +527,89 @@ def c4_iterates(sc: dict, alpha0: float = 0.5, alpha1: float = 0.501, w: float =
         xp[sl] = twist(m.X[sl], alpha0, w=w * sc["side"], axis=sc["axes"][o], center=c)
         xc[sl] = twist(m.X[sl], alpha1, w=w * sc["side"], axis=sc["axes"][o], center=c)
     return xp, xc
+
+
+# ----------------------------------------------------------------------------
+# NEXT#4: shells (triangles) and rods (edges) for step 1
+# ----------------------------------------------------------------------------
+
+def adj_slot(adj_ptr: np.ndarray, adj_nbr: np.ndarray, u, v) -> np.ndarray:
+    """Adjacency slot of the directed edge (u -> v) (-1 if absent)."""
+    N = adj_ptr.shape[0] - 1
+    rows = np.repeat(np.arange(N, dtype=np.int64), np.diff(adj_ptr))
+    key = rows * N + adj_nbr.astype(np.int64)
+    q = np.asarray(u, np.int64) * N + np.asarray(v, np.int64)
+    pos = np.searchsorted(key, q)
+    ok = (pos < key.shape[0]) & (key[np.minimum(pos, key.shape[0] - 1)] == q)
+    return np.where(ok, pos, -1)
+
+
+def element_slots(adj_ptr, adj_nbr, elems: np.ndarray, local_edges) -> np.ndarray:
+    """int32 [n_el, 2*len(local_edges)]: slots of (u->v), (v->u) for each local edge."""
+    out = np.empty((elems.shape[0], 2 * len(local_edges)), np.int32)
+    for e, (a, b) in enumerate(local_edges):
+        out[:, 2 * e] = adj_slot(adj_ptr, adj_nbr, elems[:, a], elems[:, b])
+        out[:, 2 * e + 1] = adj_slot(adj_ptr, adj_nbr, elems[:, b], elems[:, a])
+    return out
+
+
+TRI_EDGES = ((0, 1), (0, 2), (1, 2))
+
+
+def adjacency_from_edges(N: int, pairs: np.ndarray):
+    """Symmetric ascending adjacency CSR from undirected pairs."""
+    p = np.asarray(pairs, np.int64)
+    lo, hi = np.minimum(p[:, 0], p[:, 1]), np.maximum(p[:, 0], p[:, 1])
+    ek = np.unique(lo * N + hi)
+    allk = np.sort(np.concatenate([ek, (ek % N) * N + ek // N]))
+    adj_nbr = (allk % N).astype(np.int32)
+    adj_ptr = np.zeros(N + 1, np.int64)
+    np.cumsum(np.bincount(allk // N, minlength=N), out=adj_ptr[1:])
+    return adj_ptr, adj_nbr
+
+
+def sheet(n: int, side: float = 1.0, seed: int = 0, rods: bool = True):
+    """An n x n cloth sheet (2 triangles per quad) in a seeded random plane, Morton order, plus
+    (rods=True) rod strands along every third grid row sharing the sheet's nodes.  Returns
+    dict(X, tris, tri_slots, segs, seg_slots, adj_ptr, adj_nbr, ij)."""
+    g = np.arange(n)
+    I, J = np.meshgrid(g, g, indexing="ij")
+    ij = np.stack([I.ravel(), J.ravel()], axis=1).astype(np.int64)
+    key = np.zeros(ij.shape[0], np.int64)
+    for bit in range(21):
+        for d in range(2):
+            key |= ((ij[:, d] >> bit) & 1) << (2 * bit + d)
+    perm = np.argsort(key, kind="stable")
+    new_of = np.empty(n * n, np.int64)
+    new_of[perm] = np.arange(n * n)
+    ij = ij[perm]
+    q, _ = np.linalg.qr(np.random.default_rng([seed, 17]).standard_normal((3, 3)))
+    P2 = np.stack([ij[:, 0], ij[:, 1], np.zeros(n * n)], axis=1) * (side / (n - 1)) - np.array([side / 2, side / 2, 0])
+    X = P2 @ q.T
+    c = np.arange(n - 1)
+    CI, CJ = np.meshgrid(c, c, indexing="ij")
+    v00 = (CI * n + CJ).ravel()
+    v10, v01, v11 = v00 + n, v00 + 1, v00 + n + 1
+    tris = new_of[np.concatenate([np.stack([v00, v10, v11], 1), np.stack([v00, v11, v01], 1)])].astype(np.int32)
+    tris = tris[np.argsort(tris.min(axis=1), kind="stable")]
+    segs = np.zeros((0, 2), np.int32)
+    if rods:
+        rows = np.arange(0, n, 3)
+        a = (rows[:, None] * n + np.arange(n - 1)[None, :]).ravel()
+        segs = new_of[np.stack([a, a + 1], 1)].astype(np.int32)
+    pairs = np.concatenate([tris[:, [0, 1]], tris[:, [0, 2]], tris[:, [1, 2]], segs])
+    adj_ptr, adj_nbr = adjacency_from_edges(n * n, pairs)
+    return dict(X=X, tris=tris, tri_slots=element_slots(adj_ptr, adj_nbr, tris, TRI_EDGES), segs=segs,
+                seg_slots=element_slots(adj_ptr, adj_nbr, segs, ((0, 1),)), adj_ptr=adj_ptr, adj_nbr=adj_nbr,
+                ij=ij, n=n, rot=q)
+
+
+def boundary_triangles(mesh: Mesh) -> np.ndarray:
+    """Boundary faces of a tet mesh (faces used by exactly one tet), int32 [F,3]."""
+    t = mesh.tets.astype(np.int64)
+    faces = np.concatenate([t[:, [0, 1, 2]], t[:, [0, 1, 3]], t[:, [0, 2, 3]], t[:, [1, 2, 3]]])
+    fs = np.sort(faces, axis=1)
+    N = mesh.n_nodes
+    key = (fs[:, 0] * N + fs[:, 1]) * N + fs[:, 2]
+    u, idx, cnt = np.unique(key, return_index=True, return_counts=True)
+    return faces[idx[cnt == 1]].astype(np.int32)

@@ -389,3 +389,61 @@ def test_full_size_path(P, h, cfg):
     xc = np.random.default_rng(5).standard_normal((oa["n_slots"], 3))
     d = P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, dev(xc, torch.float64), -1.0)
     assert np.array_equal(d.cpu().numpy(), -oracle.prolongate(oa["new_map"], oa["n3"], m.X, xc))
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT#4: shells and rods in step 1 (bit-exact norms and tags; accumulation into tet tags)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", ["scale", "random", "rigid"])
+def test_shells_rods_bit_exact(P, h, kind):
+    sh = synth.sheet(33, seed=1)
+    X = sh["X"]
+    rng = np.random.default_rng(7)
+    if kind == "scale":
+        xp, xc = X, 1.01 * X
+    elif kind == "random":
+        xp = X + 1e-3 * rng.standard_normal(X.shape)
+        xc = xp + 1e-4 * rng.standard_normal(X.shape)
+    else:
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        xp, xc = X, X @ q.T + 0.3
+    ns = sh["adj_nbr"].shape[0]
+    ot, on = oracle.tag_shells(sh["tris"], sh["tri_slots"], X, xp, xc, 0.0, ns)
+    th = float(np.median(on)) if kind != "rigid" else 1e-12
+    ot, on = oracle.tag_shells(sh["tris"], sh["tri_slots"], X, xp, xc, th, ns)
+    ot2, on2 = oracle.tag_rods(sh["segs"], sh["seg_slots"], X, xp, xc, th, ns, slot_tags=ot)
+    d = lambda a, dt: dev(a, dt)  # noqa: E731
+    tags = torch.empty(ns, dtype=torch.uint8, device="cuda:0")
+    tn = torch.empty(sh["tris"].shape[0], dtype=torch.float64, device="cuda:0")
+    sn = torch.empty(sh["segs"].shape[0], dtype=torch.float64, device="cuda:0")
+    Xd, xpd, xcd = d(X, torch.float64), d(xp, torch.float64), d(xc, torch.float64)
+    _, nf = P.tag_shells(h, d(sh["tris"], torch.int32), d(sh["tri_slots"], torch.int32), Xd, xpd, xcd, th, tags,
+                         reset=True, tri_norm=tn, count=True)
+    assert np.array_equal(tn.cpu().numpy(), on) and np.array_equal(tags.cpu().numpy(), ot)
+    assert nf == int((on > th).sum())
+    P.tag_rods(h, d(sh["segs"], torch.int32), d(sh["seg_slots"], torch.int32), Xd, xpd, xcd, th, tags,
+               seg_norm=sn)
+    assert np.array_equal(sn.cpu().numpy(), on2) and np.array_equal(tags.cpu().numpy(), ot2)
+
+
+def test_mixed_tets_shells_rods_then_map(P, h):
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    rng = np.random.default_rng(3)
+    xp = m.X.copy()
+    xc = m.X + 2e-3 * rng.standard_normal(m.X.shape) * (rng.random(m.n_nodes) < 0.05)[:, None]
+    ns = m.adj_nbr.shape[0]
+    tris = synth.boundary_triangles(m)
+    ts = synth.element_slots(m.adj_ptr, m.adj_nbr, tris, synth.TRI_EDGES)
+    segs = m.edges[::5].astype(np.int32)
+    ss = synth.element_slots(m.adj_ptr, m.adj_nbr, segs, ((0, 1),))
+    th = 1e-4
+    t0, _, _ = oracle.tag_edges(m.tets, m.tet_slots, m.X, xp, xc, th, ns)
+    t1, _ = oracle.tag_shells(tris, ts, m.X, xp, xc, th, ns, slot_tags=t0)
+    t2, _ = oracle.tag_rods(segs, ss, m.X, xp, xc, th, ns, slot_tags=t1)
+    xpd, xcd = dev(xp, torch.float64), dev(xc, torch.float64)
+    tags, _ = P.tag_edges(h, dm, xpd, xcd, th)
+    P.tag_shells(h, dev(tris, torch.int32), dev(ts, torch.int32), dm.x_rest, xpd, xcd, th, tags)
+    P.tag_rods(h, dev(segs, torch.int32), dev(ss, torch.int32), dm.x_rest, xpd, xcd, th, tags)
+    assert np.array_equal(tags.cpu().numpy(), t2)
+    check_map(P, h, m, dm, t2, 32)
