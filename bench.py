@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--partitioned", action="store_true", help="use the partitioned path even at N=1")
+    ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: several ranks may share one GPU (correctness runs only)")
     return ap.parse_args()
@@ -266,6 +267,8 @@ def run_agipc(args, world, rank, local_rank):
     b_coarsen = (16 * T + 72 * N + E2) + (8 * (N + 1) + 5 * E2 + 4 * N) + \
         (76 * nnzb_f + 8 * N + 4 * N + 24 * N + 24 * N + 76 * nb_mean + 8 * ns_mean + 24 * ns_mean)
 
+    next_rows = None if args.no_next else measure_next_rows(P, h, step, cs, x, gd, dm, Hrp, Hcol, Hval, flush)
+
     # ---- e2e through the public API with host inputs ----
     e2e = None
     if not args.no_e2e:
@@ -334,9 +337,74 @@ def run_agipc(args, world, rank, local_rank):
         "coarse": {"n_coarse": sizes[-1][3], "levels": sizes[-1][4], "n3": sizes[-1][5], "n12": sizes[-1][6],
                    "n_slots": sizes[-1][0], "nnzb": sizes[-1][1]},
         "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "next_rows": next_rows,
         "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
     }
     print(json.dumps(out), flush=True)
+
+
+def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=5):
+    """NEXT#1 (prolongation + <= 10 post-coarsening fine PCG iterations) on the last C3
+    step's coarse solution, and NEXT#4 (shell / rod tags) on a 1000 x 1000 cloth sheet
+    with rod strands; CUDA events on the library stream, L2 flushed before each call."""
+    import torch
+    import synth
+    hbm, _ = peaks()
+    out = {}
+    N = dm.n_nodes
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_pro = []
+    yf = torch.empty((N, 3), dtype=torch.float64, device=y_c.device)
+    for _ in range(reps):
+        flush.zero_()
+        a, b = ev(), ev()
+        a.record()
+        P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, y_c, 1.0, yf)
+        b.record()
+        torch.cuda.synchronize()
+        t_pro.append(a.elapsed_time(b))
+    ms = statistics.median(t_pro)
+    byt = N * (4 + 24 + 24) + cs.n_slots * 24   # new_map, X_bar, d_f written, coarse vector
+    out["prolongate"] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
+                         "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 3), "bytes": int(byt)}
+    t_ref, its = [], 0
+    for _ in range(2):
+        flush.zero_()
+        P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, y_c, 1.0, yf)
+        a, b = ev(), ev()
+        a.record()
+        _, st = P.pcg_solve(h, Hrp, Hcol, Hval, gd, yf, 1e-3, 10, 10)
+        b.record()
+        torch.cuda.synchronize()
+        t_ref.append(a.elapsed_time(b))
+        its = st["iters"]
+    out["post_coarsening_pcg"] = {"ms_per_solve": round(min(t_ref), 3), "iters": its,
+                                  "note": "fine block-Jacobi PCG from d_f, <= 10 iterations, incl. the per-solve "
+                                          "SELL re-layout of the 1.1 GB fine matrix"}
+    sh = synth.sheet(1000, seed=3)
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(y_c.device, dt)  # noqa: E731
+    X = t(sh["X"], torch.float64)
+    rng = np.random.default_rng(4)
+    xc = t(sh["X"] + 1e-4 * rng.standard_normal(sh["X"].shape), torch.float64)
+    tris, ts = t(sh["tris"], torch.int32), t(sh["tri_slots"], torch.int32)
+    segs, ss = t(sh["segs"], torch.int32), t(sh["seg_slots"], torch.int32)
+    tags = torch.empty(sh["adj_nbr"].shape[0], dtype=torch.uint8, device=y_c.device)
+    tt = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = ev(), ev()
+        a.record()
+        P.tag_shells(h, tris, ts, X, X, xc, 1e-4, tags, reset=True)
+        P.tag_rods(h, segs, ss, X, X, xc, 1e-4, tags)
+        b.record()
+        torch.cuda.synchronize()
+        tt.append(a.elapsed_time(b))
+    ms = statistics.median(tt)
+    Nn, T, S, E2 = sh["X"].shape[0], sh["tris"].shape[0], sh["segs"].shape[0], sh["adj_nbr"].shape[0]
+    byt = Nn * 72 + T * (12 + 24) + S * (8 + 8) + E2
+    out["tag_shells_rods"] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
+                              "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 3), "nodes": Nn, "tris": T, "segs": S}
+    return out
 
 
 # --------------------------------------------------------------------------------------
