@@ -233,6 +233,31 @@ AGIPC_API agipc_status agipc_tag_rods(agipc_handle h, int64_t n_segs, const int3
                                       double threshold, int64_t nnz_adj, int reset_tags, uint8_t *slot_tags,
                                       double *seg_norm, int64_t *n_flagged /*[host]*/);
 
+/* ---- NEXT#3: fine-level hash reduction -------------------------------------------------
+ * supp Sec 2: unreduced Hessian triplets (i, j, B_ij) get the key (i << 32) | j,
+ * are sorted by key (equal keys keep their input order) and each run of equal keys is summed
+ * in that order; the unique triplets form the fine BSR (rows ascending, columns ascending).
+ * The topology is static: agipc_triplet_plan does the key sort once per mesh (caller
+ * buffers, capacity retry on col/seg_ptr: ENOSPACE with nnzb set; synchronises), and
+ * agipc_triplet_reduce streams the values of every Newton step (thread per unique block,
+ * in-order sums, bit-identical to the sequential definition).
+ *   ti, tj : [n_trip] row / column ids (0 <= ti < n_rows; EINVAL otherwise)
+ *   tval   : [n_trip][3][3];  val : out [nnzb][3][3] */
+typedef struct {
+  int64_t n_rows, n_trip;  /* [host] set by plan */
+  int64_t nnzb;            /* [host] out: unique blocks */
+  int64_t cap_nnzb;        /* [host] in: capacity of col and seg_ptr (seg_ptr holds cap_nnzb+1) */
+  int64_t *row_ptr;        /* out [n_rows+1] */
+  int32_t *col;            /* out [cap_nnzb] */
+  int64_t *seg_ptr;        /* out [cap_nnzb+1]: triplets of block u are seg_idx[seg_ptr[u]..seg_ptr[u+1]) */
+  int32_t *seg_idx;        /* out [n_trip]: triplet ids sorted by (key, id) */
+} agipc_triplet_plan_t;
+
+AGIPC_API agipc_status agipc_triplet_plan(agipc_handle h, int64_t n_rows, int64_t n_trip, const int32_t *ti,
+                                          const int32_t *tj, agipc_triplet_plan_t *plan);
+AGIPC_API agipc_status agipc_triplet_reduce(agipc_handle h, const agipc_triplet_plan_t *plan, const double *tval,
+                                            double *val);
+
 /* ---- NEXT#1: prolongation d_f = U^T d_c ------------------------------------------------
  * "we mathematically prolongate the displacement to the fine mesh using the transpose of
  * the restriction operator" (main Sec 4.3).  For every fine node f with parent

@@ -54,6 +54,8 @@ def lib():
         L.orc_block_jacobi.restype = i32
         L.orc_prolongate.argtypes = [i64, P, i64, P, P, P]
         L.orc_prolongate.restype = None
+        L.orc_reduce_triplets.argtypes = [i64, i64, P, P, P, P, P, P]
+        L.orc_reduce_triplets.restype = i64
         for nm in ("orc_tag_shells", "orc_tag_rods"):
             getattr(L, nm).argtypes = [i64, P, P, P, P, P, f64, i64, i32, P, P, P]
             getattr(L, nm).restype = i32
@@ -231,3 +233,17 @@ def tag_shells(tris, tri_slots, X, x_prev, x_cur, theta, n_slots, slot_tags=None
 def tag_rods(segs, seg_slots, X, x_prev, x_cur, theta, n_slots, slot_tags=None):
     """NEXT#4, edges ("rods"): G = 1/2 (F^2 - 1), F = l / L."""
     return _tag_elems("orc_tag_rods", segs, seg_slots, X, x_prev, x_cur, theta, n_slots, slot_tags)
+
+
+def reduce_triplets(n_rows, ti, tj, tval):
+    """NEXT#3 (supp Sec 2): stable key sort + in-order segmented sums.
+    Returns (row_ptr int64 [n_rows+1], col int32 [nnzb], val float64 [nnzb,3,3])."""
+    ti = _c(ti, np.int32); tj = _c(tj, np.int32); tv = _c(tval, np.float64)
+    n = ti.shape[0]
+    rp = np.zeros(n_rows + 1, np.int64)
+    col = np.empty(max(n, 1), np.int32)
+    val = np.empty((max(n, 1), 9))
+    nb = lib().orc_reduce_triplets(int(n_rows), n, _p(ti), _p(tj), _p(tv), _p(rp), _p(col), _p(val))
+    if nb < 0:
+        raise OracleError(-nb)
+    return rp, col[:nb].copy(), val[:nb].reshape(nb, 3, 3).copy()

@@ -662,3 +662,52 @@ int orc_tag_rods(int64_t n_segs, const int32_t *segs, const int32_t *seg_slots, 
   }
   return ORC_OK;
 }
+
+/* ========================================================================== */
+/* NEXT#3 -- fine-level hash reduction (supp Sec 2): triplets      */
+/* (i, j, B_ij) keyed by (i << 32) | j, sorted by key (stable: equal keys keep */
+/* input order), each group of equal keys summed in that order.  Output: the  */
+/* unique triplets as BSR (rows ascending, columns ascending within a row).   */
+/* ========================================================================== */
+static const uint64_t *g_trip_key;
+
+static int trip_cmp(const void *pa, const void *pb) {
+  const int64_t a = *(const int64_t *)pa, b = *(const int64_t *)pb;
+  if (g_trip_key[a] != g_trip_key[b]) return g_trip_key[a] < g_trip_key[b] ? -1 : 1;
+  return a < b ? -1 : (a > b ? 1 : 0); /* stable */
+}
+
+/* returns nnzb (>= 0) or -ORC_EINVAL; row_ptr[n_rows+1], col/val sized n (worst case) */
+int64_t orc_reduce_triplets(int64_t n_rows, int64_t n, const int32_t *ti, const int32_t *tj, const double *tval,
+                            int64_t *row_ptr, int32_t *col, double *val) {
+  uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (n + 1));
+  int64_t *idx = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+  for (int64_t t = 0; t < n; ++t) {
+    if (ti[t] < 0 || tj[t] < 0 || ti[t] >= n_rows) {
+      free(key);
+      free(idx);
+      return -ORC_EINVAL;
+    }
+    key[t] = ((uint64_t)(uint32_t)ti[t] << 32) | (uint32_t)tj[t]; /* hash key */
+    idx[t] = t;
+  }
+  g_trip_key = key;
+  qsort(idx, (size_t)n, sizeof(int64_t), trip_cmp);
+  for (int64_t r = 0; r <= n_rows; ++r) row_ptr[r] = 0;
+  int64_t u = -1;
+  for (int64_t s = 0; s < n; ++s) {
+    const int64_t t = idx[s];
+    if (s == 0 || key[t] != key[idx[s - 1]]) {
+      ++u;
+      col[u] = tj[t];
+      row_ptr[ti[t] + 1] += 1;
+      for (int e = 0; e < 9; ++e) val[9 * u + e] = tval[9 * t + e];
+    } else {
+      for (int e = 0; e < 9; ++e) val[9 * u + e] = val[9 * u + e] + tval[9 * t + e];
+    }
+  }
+  for (int64_t r = 0; r < n_rows; ++r) row_ptr[r + 1] += row_ptr[r];
+  free(key);
+  free(idx);
+  return u + 1;
+}

@@ -63,6 +63,11 @@ class _HaloMatrix(C.Structure):
                 ("col", C.c_void_p), ("val", C.c_void_p)]
 
 
+class _TripletPlan(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_trip", C.c_int64), ("nnzb", C.c_int64), ("cap_nnzb", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("seg_ptr", C.c_void_p), ("seg_idx", C.c_void_p)]
+
+
 class _ProfEntry(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("count", C.c_int64), ("total_ms", C.c_double)]
 
@@ -77,7 +82,7 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate",
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
            "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
-           "agipc_tag_rods"]
+           "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce"]
 
 
 def lib():
@@ -111,6 +116,8 @@ def lib():
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
+        L.agipc_triplet_plan.argtypes = [P, i64, i64, P, P, C.POINTER(_TripletPlan)]
+        L.agipc_triplet_reduce.argtypes = [P, C.POINTER(_TripletPlan), P, P]
         for nm in ("agipc_tag_shells", "agipc_tag_rods"):
             getattr(L, nm).argtypes = [P, i64, P, P, P, P, P, f64, i64, i32, P, P, C.POINTER(i64)]
         L.agipc_coarse_halo.argtypes = [P, P, i64, i64, P, i64, P, P, i64, C.POINTER(i64)]
@@ -466,3 +473,34 @@ def tag_rods(h: Handle, segs, seg_slots, x_rest, x_prev, x_cur, threshold: float
     """NEXT#4: step 1 for rods (edges); flags accumulate into slot_tags unless reset."""
     return _tag_elems("agipc_tag_rods", h, segs, seg_slots, x_rest, x_prev, x_cur, threshold, slot_tags, reset,
                       seg_norm, count)
+
+
+class TripletPlan:
+    """NEXT#3 (supp Sec 2): the once-per-mesh key sort of the fine Hessian triplets;
+    reduce(tval) -> the unique BSR values of one Newton step."""
+
+    def __init__(self, h: Handle, n_rows: int, ti, tj, cap_nnzb: int | None = None):
+        self.h = h
+        dev = ti.device
+        n = ti.shape[0]
+        self.row_ptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+        self.seg_idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        cap = n if cap_nnzb is None else int(cap_nnzb)
+        for attempt in range(2):
+            self.col = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            self.seg_ptr = torch.empty(cap + 1, dtype=torch.int64, device=dev)
+            self._p = _TripletPlan(0, 0, 0, cap, _p(self.row_ptr), _p(self.col), _p(self.seg_ptr), _p(self.seg_idx))
+            st = lib().agipc_triplet_plan(h._h, int(n_rows), int(n), _p(ti), _p(tj), C.byref(self._p))
+            if st == ENOSPACE and attempt == 0:
+                cap = int(self._p.nnzb)
+                continue
+            h._check(st)
+            break
+        self.nnzb = int(self._p.nnzb)
+        self.col = self.col[:self.nnzb]
+
+    def reduce(self, tval, out=None):
+        if out is None:
+            out = torch.empty((self.nnzb, 3, 3), dtype=torch.float64, device=tval.device)
+        self.h._check(lib().agipc_triplet_reduce(self.h._h, C.byref(self._p), _p(tval), _p(out)))
+        return out

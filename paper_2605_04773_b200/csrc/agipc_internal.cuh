@@ -40,6 +40,7 @@ enum ProfPhase {
   PROF_ASM_NUMERIC,
   PROF_PROLONG,
   PROF_DIST,
+  PROF_TRIPLETS,
   PROF_N
 };
 

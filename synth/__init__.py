@@ -613,3 +613,13 @@ def boundary_triangles(mesh: Mesh) -> np.ndarray:
     key = (fs[:, 0] * N + fs[:, 1]) * N + fs[:, 2]
     u, idx, cnt = np.unique(key, return_index=True, return_counts=True)
     return faces[idx[cnt == 1]].astype(np.int32)
+
+
+def tet_triplets(mesh: Mesh, E: float = 1e5, nu: float = 0.3, dt: float = 0.01):
+    """NEXT#3 input: the unreduced element Hessian triplets of dt^2 K_lin -- 16 (i, j, B) per tet
+    in tet order (a, b row-major) -- as (ti int32, tj int32, val float64 [16T,3,3])."""
+    K, _ = stiffness_blocks(mesh.X, mesh.tets, E, nu)
+    t = mesh.tets.astype(np.int64)
+    ti = np.repeat(t, 4, axis=1).reshape(-1).astype(np.int32)
+    tj = np.tile(t, (1, 4)).reshape(-1).astype(np.int32)
+    return ti, tj, (dt * dt) * K.reshape(-1, 3, 3)

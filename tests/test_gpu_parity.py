@@ -447,3 +447,44 @@ def test_mixed_tets_shells_rods_then_map(P, h):
     P.tag_rods(h, dev(segs, torch.int32), dev(ss, torch.int32), dm.x_rest, xpd, xcd, th, tags)
     assert np.array_equal(tags.cpu().numpy(), t2)
     check_map(P, h, m, dm, t2, 32)
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT#3: fine-level hash reduction (bit-exact: same in-order sums as the oracle)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["c1_tets", "random", "hub"])
+def test_triplet_reduction_bit_exact(P, h, case):
+    rng = np.random.default_rng(11)
+    if case == "c1_tets":
+        m = synth.kuhn_grid(10)
+        ti, tj, v = synth.tet_triplets(m)
+        n_rows = m.n_nodes
+    elif case == "random":
+        n_rows, n = 500, 200000
+        ti, tj = rng.integers(0, n_rows, n).astype(np.int32), rng.integers(0, 800, n).astype(np.int32)
+        v = rng.standard_normal((n, 3, 3))
+    else:  # one row with thousands of triplets (the CTA-wide sort path) plus short rows
+        n_rows = 50
+        ti = np.concatenate([np.full(5000, 7), rng.integers(0, n_rows, 3000)]).astype(np.int32)
+        tj = rng.integers(0, 3000, ti.shape[0]).astype(np.int32)
+        v = rng.standard_normal((ti.shape[0], 3, 3)) * 10.0 ** rng.integers(-8, 8, (ti.shape[0], 1, 1))
+    rp, col, val = oracle.reduce_triplets(n_rows, ti, tj, v)
+    plan = P.TripletPlan(h, n_rows, dev(ti, torch.int32), dev(tj, torch.int32), cap_nnzb=16)  # exercises retry
+    assert plan.nnzb == col.shape[0]
+    assert np.array_equal(plan.row_ptr.cpu().numpy(), rp) and np.array_equal(plan.col.cpu().numpy(), col)
+    got = plan.reduce(dev(v, torch.float64)).cpu().numpy()
+    assert np.array_equal(got, val)
+
+
+def test_triplet_reduction_full_c2_equals_fine_pattern(P, h):
+    c = synth.config_c2()
+    m = c["mesh"]
+    ti, tj, v = synth.tet_triplets(m)
+    plan = P.TripletPlan(h, m.n_nodes, dev(ti, torch.int32), dev(tj, torch.int32))
+    assert np.array_equal(plan.row_ptr.cpu().numpy(), m.bsr_ptr) and np.array_equal(plan.col.cpu().numpy(), m.bsr_col)
+    got = plan.reduce(dev(v, torch.float64)).cpu().numpy()
+    rows = np.random.default_rng(0).integers(0, m.n_nodes, 2000)   # sampled rows against the oracle
+    sel = np.isin(ti, rows)
+    rp, col, val = oracle.reduce_triplets(m.n_nodes, ti[sel], tj[sel], v[sel])
+    for r in np.unique(rows):
+        assert np.array_equal(got[m.bsr_ptr[r]:m.bsr_ptr[r + 1]], val[rp[r]:rp[r + 1]])
