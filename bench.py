@@ -404,6 +404,32 @@ def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=
     byt = Nn * 72 + T * (12 + 24) + S * (8 + 8) + E2
     out["tag_shells_rods"] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
                               "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 3), "nodes": Nn, "tris": T, "segs": S}
+    # NEXT#3: fine hash reduction of C2's element triplets (16 per tet): plan once, reduce per step
+    c2 = synth.kuhn_grid(47)
+    ti, tj, tv = synth.tet_triplets(c2)
+    tid, tjd, tvd = t(ti, torch.int32), t(tj, torch.int32), t(tv.reshape(-1, 9), torch.float64)
+    a, b = ev(), ev()
+    a.record()
+    plan = P.TripletPlan(h, c2.n_nodes, tid, tjd, cap_nnzb=c2.bsr_col.shape[0])
+    b.record()
+    torch.cuda.synchronize()
+    ms_plan = a.elapsed_time(b)
+    val = torch.empty((plan.nnzb, 3, 3), dtype=torch.float64, device=y_c.device)
+    tr = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = ev(), ev()
+        a.record()
+        plan.reduce(tvd, val)
+        b.record()
+        torch.cuda.synchronize()
+        tr.append(a.elapsed_time(b))
+    ms = statistics.median(tr)
+    n3 = ti.shape[0]
+    byt = 72 * n3 + 4 * n3 + 8 * (plan.nnzb + 1) + 72 * plan.nnzb
+    out["triplet_reduction"] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
+                                "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 3), "plan_ms": round(ms_plan, 3),
+                                "triplets": int(n3), "blocks": int(plan.nnzb), "workload": "C2 tets, 16 per tet"}
     return out
 
 
