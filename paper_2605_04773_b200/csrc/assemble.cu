@@ -647,6 +647,7 @@ template <bool NUMERIC>
 __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[MID_WARPS];
   __shared__ long long s_key[MID_WARPS][MID_CAP];
+  __shared__ double s_carry[MID_WARPS][4][9];  // partial sums of a run continuing into the next window
   const int w = threadIdx.x >> 5, l = lane_id();
   ChildTab &tab = s_tab[w];
   long long *key = s_key[w];
@@ -716,11 +717,9 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       // passes its partial sums on in `carry` (added by the lanes of the next window's first run).
       const int ncb_a = ncb_of(a, n3);
       for (int p = 0; p < ncb_a; ++p) {
-      double carry[4][9];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int x = 0; x < 9; ++x) carry[q][x] = 0.0;
+      double(*carry)[9] = s_carry[w];
+      if (l < 36) carry[l / 9][l % 9] = 0.0;
+      __syncwarp();
       int rb = 0, carry_cp = 0;
       const long long rs = A.crp[slot_of(a, p, n3)];
       for (int e0 = 0; e0 < T; e0 += 32) {
@@ -794,8 +793,12 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
             }
           }
           const bool any_cont = __shfl_sync(FULL_MASK, cont ? 1 : 0, 31);
+          __syncwarp();  // every lane has read carry[q] above
+          if (l == 31) {
 #pragma unroll
-          for (int x = 0; x < 9; ++x) carry[q][x] = any_cont ? __shfl_sync(FULL_MASK, v[x], 31) : 0.0;
+            for (int x = 0; x < 9; ++x) carry[q][x] = any_cont ? v[x] : 0.0;
+          }
+          __syncwarp();
         }
         carry_cp = last_cp;
         rb += __shfl_sync(FULL_MASK, incl, 31);
