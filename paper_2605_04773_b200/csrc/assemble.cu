@@ -247,6 +247,12 @@ __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t 
 // ------------------------------------------------------------------------------------
 // Large nodes: 32-children chunks emit (a, b) for every large column b != a (warp de-dup with
 // __match_any_sync; duplicates across chunks are removed by the per-node sort), and (a, a).
+__global__ void k_task_node(int64_t n_c, const int64_t *__restrict__ task_ptr, int32_t *__restrict__ task_node) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_c)
+    for (int64_t t = task_ptr[c]; t < task_ptr[c + 1]; ++t) task_node[t] = (int32_t)c;
+}
+
 struct LargeArgs {
   int64_t n_c;
   const int32_t *child_list;
@@ -260,6 +266,7 @@ struct LargeArgs {
   const double *X;
   const double *g_f;
   const int64_t *task_ptr;
+  const int32_t *task_node;  // owner node of every large-row task (chunk)
   const AsmScal *sc;
   int2 *pairs;
   long long pair_cap;
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
   for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
-    const int a = lower_bound_dev<int64_t>(A.task_ptr, (int)A.n_c + 1, t + 1) - 1;
+    const int a = A.task_node[t];
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
     const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
@@ -919,7 +926,7 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
   for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
-    const int a = lower_bound_dev<int64_t>(A.task_ptr, (int)A.n_c + 1, t + 1) - 1;
+    const int a = A.task_node[t];
     if (ncb_of(a, n3) != NCB) continue;
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
@@ -1177,6 +1184,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_children, gN, 256, 0, N, out->new_map, H->row_ptr, cursor, child_list, rowsum);
   LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks, sc);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
+  WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
+  LAUNCH(h, k_task_node, gC, 256, 0, n_c, (const int64_t *)task_ptr, task_node);
   // small nodes: the warp list (<= 32 candidate entries) and the tile list (> 32, with the
   // prefix of their entries)
   WS(h, f16, int32_t, "asm_f16", n_c);
@@ -1234,7 +1243,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
-  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
+  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.task_node = task_node; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
   LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
