@@ -909,15 +909,16 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 // by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
 // two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
-#define LSTAGE 512
+#define LSTAGE 256
 
 template <int NCB>
 __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE];
-  __shared__ int s_i[4][LSTAGE];
-  __shared__ int s_j[4][LSTAGE];
-  __shared__ int s_b[4][LSTAGE];  // interface entries (staged from the top): column aggregate
+  __shared__ int s_i[4][LSTAGE];     // child slot c of the entry's row (weights in s_wc)
+  __shared__ int s_b[4][LSTAGE];     // interface entries (staged from the top): column aggregate
+  __shared__ double s_xj[4][LSTAGE][3];  // X_bar of the entry's column node (w_j)
+  __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
   const int w = threadIdx.x >> 5, l = lane_id();
   // lane = (block group, p, q half): NCB = 4 -> 8 lanes per block, 2 q per lane
   constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
@@ -931,6 +932,13 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
     const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+    if (l < s) {
+      const int64_t ci = tab.ci[l];
+      s_wc[w][l][0] = __ldg(A.X + 3 * ci);
+      s_wc[w][l][1] = __ldg(A.X + 3 * ci + 1);
+      s_wc[w][l][2] = __ldg(A.X + 3 * ci + 2);
+    }
+    __syncwarp();
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
     const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
@@ -946,21 +954,23 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
         const int e = base + e0 + l;
         bool diag = false;
         long long k = 0;
-        int i = 0, j = 0, b = -1;
+        int c = 0, j = 0, b = -1;
+        double xj0 = 0.0, xj1 = 0.0, xj2 = 0.0;
         if (e0 + l < n) {
-          int c;
           entry_of(tab, s, e, c, k);
-          i = tab.ci[c];
           j = A.col[k];
           b = A.nm[j];
+          xj0 = __ldg(A.X + 3 * (int64_t)j);  // independent of nm[j]: in flight together
+          xj1 = __ldg(A.X + 3 * (int64_t)j + 1);
+          xj2 = __ldg(A.X + 3 * (int64_t)j + 2);
           diag = b == a;
         }
         const unsigned m = __ballot_sync(FULL_MASK, diag);
         if (diag) {
           const int pos = cnt + __popc(m & ((1u << l) - 1u));
           s_k[w][pos] = k;
-          s_i[w][pos] = i;
-          s_j[w][pos] = j;
+          s_i[w][pos] = c;
+          s_xj[w][pos][0] = xj0; s_xj[w][pos][1] = xj1; s_xj[w][pos][2] = xj2;
         }
         cnt += __popc(m);
         // large-large interface block: staged from the top, reduced per column aggregate below
@@ -969,45 +979,32 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
         if (itf) {
           const int pos = LSTAGE - 1 - (icnt + __popc(mi & ((1u << l) - 1u)));
           s_k[w][pos] = k;
-          s_i[w][pos] = i;
-          s_j[w][pos] = j;
+          s_i[w][pos] = c;
           s_b[w][pos] = b;
+          s_xj[w][pos][0] = xj0; s_xj[w][pos][1] = xj1; s_xj[w][pos][2] = xj2;
         }
         icnt += __popc(mi);
       }
       __syncwarp();
-      for (int d = gq; d < cnt; d += 4 * G) {  // four diagonal blocks per group in flight
-        long long kk[4];
-        int ii[4], jj[4];
-        bool ok[4];
+      for (int d = gq; d < cnt; d += 2 * G) {  // two diagonal blocks per group in flight
+        const bool two = d + G < cnt;
+        const int d1 = two ? d + G : d;
+        const long long k0 = s_k[w][d], k1 = s_k[w][d1];
+        double B0[9], B1[9];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          ok[u] = d + u * G < cnt;
-          const int dd = ok[u] ? d + u * G : d;
-          kk[u] = s_k[w][dd];
-          ii[u] = s_i[w][dd];
-          jj[u] = s_j[w][dd];
+        for (int x = 0; x < 9; ++x) {
+          B0[x] = __ldg(A.val + 9 * k0 + x);
+          B1[x] = __ldg(A.val + 9 * k1 + x);
         }
-        double Bv[4][9];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int x = 0; x < 9; ++x) Bv[u][x] = __ldg(A.val + 9 * kk[u] + x);
-        double wi[4], wj[4][QN];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          wi[u] = ok[u] ? wgt(A.X, ii[u], NCB, p) : 0.0;
-#pragma unroll
-          for (int qq = 0; qq < QN; ++qq) wj[u][qq] = wgt(A.X, jj[u], NCB, q0 + qq);
-        }
+        const double wi0 = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d]][p];
+        const double wi1 = !two ? 0.0 : (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d1]][p];
 #pragma unroll
         for (int qq = 0; qq < QN; ++qq) {
+          const int q = q0 + qq;
+          const double c0 = wi0 * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][d][q]);
+          const double c1 = wi1 * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][d1][q]);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double c = wi[u] * wj[u][qq];
-#pragma unroll
-            for (int x = 0; x < 9; ++x) acc[qq][x] += c * Bv[u][x];
-          }
+          for (int x = 0; x < 9; ++x) acc[qq][x] += c0 * B0[x] + c1 * B1[x];
         }
       }
       __syncwarp();
@@ -1032,14 +1029,14 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
         for (int d = f + gq; d < icnt; d += G) {
           if (s_b[w][i0 + d] != b0) continue;
           const long long kk = s_k[w][i0 + d];
-          const double wi = wgt(A.X, s_i[w][i0 + d], NCB, p);
-          const int jj = s_j[w][i0 + d];
+          const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][i0 + d]][p];
           double Bv[9];
 #pragma unroll
           for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * kk + x);
 #pragma unroll
           for (int qq = 0; qq < QI; ++qq) {
-            const double c = q0 + qq < ncb_b ? wi * wgt(A.X, jj, ncb_b, q0 + qq) : 0.0;
+            const int q = q0 + qq;
+            const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : s_xj[w][i0 + d][q]) : 0.0;
 #pragma unroll
             for (int x = 0; x < 9; ++x) ac[qq][x] += c * Bv[x];
           }
