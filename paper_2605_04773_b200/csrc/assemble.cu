@@ -247,6 +247,12 @@ __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t 
 // ------------------------------------------------------------------------------------
 // Large nodes: 32-children chunks emit (a, b) for every large column b != a (warp de-dup with
 // __match_any_sync; duplicates across chunks are removed by the per-node sort), and (a, a).
+__global__ void k_fine_class(int64_t N, const int32_t *__restrict__ nm, const uint8_t *__restrict__ is_small,
+                             uint8_t *__restrict__ fcls) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < N) fcls[f] = is_small[nm[f]];
+}
+
 __global__ void k_task_node(int64_t n_c, const int64_t *__restrict__ task_ptr, int32_t *__restrict__ task_node) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n_c)
@@ -267,6 +273,7 @@ struct LargeArgs {
   const double *g_f;
   const int64_t *task_ptr;
   const int32_t *task_node;  // owner node of every large-row task (chunk)
+  const uint8_t *fcls;       // [N] is_small[new_map[f]]: the class of fine node f's aggregate
   const AsmScal *sc;
   int2 *pairs;
   long long pair_cap;
@@ -950,21 +957,34 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
     for (int base = 0; base < T; base += LSTAGE) {
       const int n = min(LSTAGE, T - base);
       int cnt = 0, icnt = 0;
+      // software pipeline: the column of the next batch is loaded while this batch's column
+      // aggregate, class and X_bar (all independent of each other) are in flight
+      int c_nx = 0, j_nx = 0;
+      long long k_nx = 0;
+      if (l < n) {
+        entry_of(tab, s, base + l, c_nx, k_nx);
+        j_nx = A.col[k_nx];
+      }
       for (int e0 = 0; e0 < n; e0 += 32) {
-        const int e = base + e0 + l;
+        const bool valid = e0 + l < n;
         bool diag = false;
-        long long k = 0;
-        int c = 0, j = 0, b = -1;
+        const long long k = k_nx;
+        const int c = c_nx, j = j_nx;
+        int b = -1;
+        bool small_col = true;
         double xj0 = 0.0, xj1 = 0.0, xj2 = 0.0;
-        if (e0 + l < n) {
-          entry_of(tab, s, e, c, k);
-          j = A.col[k];
+        if (valid) {
           b = A.nm[j];
-          xj0 = __ldg(A.X + 3 * (int64_t)j);  // independent of nm[j]: in flight together
+          small_col = A.fcls[j];
+          xj0 = __ldg(A.X + 3 * (int64_t)j);
           xj1 = __ldg(A.X + 3 * (int64_t)j + 1);
           xj2 = __ldg(A.X + 3 * (int64_t)j + 2);
-          diag = b == a;
         }
+        if (e0 + 32 + l < n) {
+          entry_of(tab, s, base + e0 + 32 + l, c_nx, k_nx);
+          j_nx = A.col[k_nx];
+        }
+        diag = valid && b == a;
         const unsigned m = __ballot_sync(FULL_MASK, diag);
         if (diag) {
           const int pos = cnt + __popc(m & ((1u << l) - 1u));
@@ -974,7 +994,7 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
         }
         cnt += __popc(m);
         // large-large interface block: staged from the top, reduced per column aggregate below
-        const bool itf = b >= 0 && b != a && !A.is_small[b];
+        const bool itf = valid && b != a && !small_col;
         const unsigned mi = __ballot_sync(FULL_MASK, itf);
         if (itf) {
           const int pos = LSTAGE - 1 - (icnt + __popc(mi & ((1u << l) - 1u)));
@@ -1183,6 +1203,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
   WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
   LAUNCH(h, k_task_node, gC, 256, 0, n_c, (const int64_t *)task_ptr, task_node);
+  WS(h, fcls, uint8_t, "asm_fcls", N);
+  LAUNCH(h, k_fine_class, gN, 256, 0, N, (const int32_t *)out->new_map, (const uint8_t *)is_small, fcls);
   // small nodes: the warp list (<= 32 candidate entries) and the tile list (> 32, with the
   // prefix of their entries)
   WS(h, f16, int32_t, "asm_f16", n_c);
@@ -1240,7 +1262,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
-  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.task_node = task_node; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
+  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.task_node = task_node; LA.fcls = fcls; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
   LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
