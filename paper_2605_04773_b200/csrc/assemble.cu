@@ -512,6 +512,7 @@ template <int SEG, bool NUMERIC>
 __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   constexpr int NSEG = 32 / SEG;
   __shared__ ChildTab s_tab[8 * NSEG];
+  __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][9];  // numeric: per-lane parked block
   const int w = threadIdx.x >> 5, l = lane_id();
   const int sg = l / SEG, sl = l % SEG;
   const unsigned smask = SEG == 32 ? FULL_MASK : (((1u << SEG) - 1u) << (sg * SEG));
@@ -598,16 +599,21 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
       for (int q = 0; q < Q; ++q) {
         const double coef = (valid && pv && q < ncb_b) ? wi * wgt(A.X, sj, ncb_b, q) : 0.0;
+        // run sums: every lane parks coef * B in shared memory, the tail lane of each run adds
+        // its run (head .. tail, short) in lane order
+#pragma unroll
+        for (int x = 0; x < 9; ++x) s_v[w][l][x] = coef * B[x];
+        __syncwarp();
         double v[9];
+        if (tail) {
+          const int h0 = sg * SEG + hl;
 #pragma unroll
-        for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+          for (int x = 0; x < 9; ++x) v[x] = s_v[w][h0][x];
+          for (int t = h0 + 1; t <= l; ++t)
 #pragma unroll
-        for (int o = 1; o < SEG; o <<= 1)  // segmented inclusive scan inside runs
-#pragma unroll
-          for (int x = 0; x < 9; ++x) {
-            const double t = __shfl_up_sync(FULL_MASK, v[x], o, SEG);
-            if (sl - o >= hl) v[x] += t;
-          }
+            for (int x = 0; x < 9; ++x) v[x] += s_v[w][t][x];
+        }
+        __syncwarp();
         if (tail && pv && q < ncb_b) {
           const long long pos = rs + cp + q;
           A.ccol[pos] = slot_of(bs, q, n3);
