@@ -286,8 +286,10 @@ struct LargeArgs {
   double *g_c;
 };
 
+#define SEEN_CAP 128
 __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
+  __shared__ int s_seen[4][SEEN_CAP];  // large columns already emitted by this chunk
   const int w = threadIdx.x >> 5, l = lane_id();
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
@@ -296,6 +298,7 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
     const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+    int nseen = 0;
     for (int e0 = 0; e0 < T; e0 += 32) {
       const int e = e0 + l;
       int key = -1;
@@ -303,11 +306,27 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
         int c;
         long long k;
         entry_of(tab, s, e, c, k);
-        const int b = A.nm[A.col[k]];
-        if (b != a && !A.is_small[b]) key = b;
+        const int j = A.col[k];
+        if (!A.fcls[j]) {
+          const int b = A.nm[j];
+          if (b != a) key = b;
+        }
       }
       const unsigned peers = __match_any_sync(FULL_MASK, key);
-      const bool emit = key >= 0 && (__ffs(peers) - 1) == l;
+      bool emit = key >= 0 && (__ffs(peers) - 1) == l;
+      if (emit)  // one pair per (chunk, column): skip columns this chunk already emitted
+        for (int q = 0; q < min(nseen, SEEN_CAP); ++q)
+          if (s_seen[w][q] == key) {
+            emit = false;
+            break;
+          }
+      const unsigned me = __ballot_sync(FULL_MASK, emit);
+      if (emit) {
+        const int pos = nseen + __popc(me & ((1u << l) - 1u));
+        if (pos < SEEN_CAP) s_seen[w][pos] = key;
+      }
+      nseen += __popc(me);
+      __syncwarp();
       const unsigned m = __ballot_sync(FULL_MASK, emit);
       if (!m) continue;
       long long pb = 0;
