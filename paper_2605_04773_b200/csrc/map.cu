@@ -127,6 +127,7 @@ __device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles
 // compacted warp-wide (one global atomic per 32 entries).  Then the register closure /
 // election of group_tile per chunk, and one decoupled look-back per CTA tile.
 #define L0_CHUNKS 4
+#define L0_XCAP 256
 
 __global__ void __launch_bounds__(MAP_THREADS)
     k_level0(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
@@ -136,6 +137,8 @@ __global__ void __launch_bounds__(MAP_THREADS)
   __shared__ TileSmem S;
   __shared__ long long s_ptr[MAP_WARPS][33];
   __shared__ uint32_t s_h[MAP_WARPS][32];
+  __shared__ int s_gb[MAP_WARPS][32];             // first node of the group of each chunk row
+  __shared__ int2 s_cross[MAP_WARPS][L0_XCAP];    // per-warp buffer of tagged cross edges
   if (threadIdx.x == 0) S.tile = atomicAdd(tile_counter, 1);
   __syncthreads();
   const int tile = S.tile;
@@ -143,7 +146,17 @@ __global__ void __launch_bounds__(MAP_THREADS)
   const int gs = geo.gs, cn = geo.gpw * gs;  // nodes per chunk
   const int gin = lane / gs, lig = lane - gin * gs, base_lane = gin * gs;
   int local[L0_CHUNKS], off[L0_CHUNKS];
-  int wcount = 0;
+  int wcount = 0, nx = 0;  // nx: cross edges buffered by this warp
+  // flush the warp's buffered cross edges with ONE global atomic (a single counter shared by
+  // the whole grid is the contended resource)
+  auto flush = [&]() {
+    unsigned long long cb = 0;
+    if (lane == 0) cb = atomicAdd(cross_count, (unsigned long long)nx);
+    cb = __shfl_sync(FULL_MASK, cb, 0);
+    for (int t = lane; t < nx; t += 32) cross[cb + t] = s_cross[w][t];
+    __syncwarp();
+    nx = 0;
+  };
 #pragma unroll
   for (int c = 0; c < L0_CHUNKS; ++c) {
     const int64_t q = ((int64_t)tile * MAP_WARPS + w) * L0_CHUNKS + c;
@@ -154,6 +167,7 @@ __global__ void __launch_bounds__(MAP_THREADS)
     if (lane <= nn) s_ptr[w][lane] = adj_ptr[v0 + lane];
     if (lane == 0 && nn == 32) s_ptr[w][32] = adj_ptr[v0 + 32];
     s_h[w][lane] = 0u;
+    s_gb[w][lane] = (int)(v0 + (lane / gs) * gs);  // v0 is a multiple of gs
     __syncwarp();
     if (nn > 0) {
       const long long E0 = s_ptr[w][0], E1 = s_ptr[w][nn];
@@ -170,18 +184,17 @@ __global__ void __launch_bounds__(MAP_THREADS)
           const int mid = (lo + hi) >> 1;
           if (s_ptr[w][mid] <= e) lo = mid; else hi = mid;
         }
-        const int64_t vv = v0 + lo;
-        const int64_t gv = vv / gs;
+        const int vv = (int)(v0 + lo);
+        const int gb = s_gb[w][lo];
         const bool tg = valid && t;
-        const bool intra = tg && (int64_t)u / gs == gv;
-        const bool cr = tg && !intra && (int64_t)u > vv;
-        if (intra) atomicOr(&s_h[w][lo], 1u << (int)(u - gv * gs));
+        const bool intra = tg && u >= gb && u < gb + gs;
+        const bool cr = tg && !intra && u > vv;
+        if (intra) atomicOr(&s_h[w][lo], 1u << (u - gb));
         const unsigned b = __ballot_sync(FULL_MASK, cr);
         if (b) {
-          unsigned long long cb = 0;
-          if (lane == 0) cb = atomicAdd(cross_count, (unsigned long long)__popc(b));
-          cb = __shfl_sync(FULL_MASK, cb, 0);
-          if (cr) cross[cb + __popc(b & ((1u << lane) - 1u))] = make_int2((int)vv, u);
+          if (nx + __popc(b) > L0_XCAP) flush();
+          if (cr) s_cross[w][nx + __popc(b & ((1u << lane) - 1u))] = make_int2(vv, u);
+          nx += __popc(b);
         }
       }
     }
@@ -200,6 +213,8 @@ __global__ void __launch_bounds__(MAP_THREADS)
     wcount += __popc(bal);
     __syncwarp();
   }
+  __syncwarp();
+  if (nx) flush();
   if (lane == 0) S.warp[w] = wcount;
   __syncthreads();
   if (w == 0) {
