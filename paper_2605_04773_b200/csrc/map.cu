@@ -238,6 +238,28 @@ __global__ void __launch_bounds__(MAP_THREADS)
   }
 }
 
+// CTA-wide stream compaction: returns this thread's output position for keep == true, with ONE
+// global atomic per CTA (a single grid-wide counter is the contended resource).  All threads of
+// the CTA must call it; s_w holds blockDim/32 ints, s_base one 64-bit word.
+__device__ __forceinline__ unsigned long long cta_compact(bool keep, unsigned long long *counter, int *s_w,
+                                                          unsigned long long *s_base) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const unsigned b = __ballot_sync(FULL_MASK, keep);
+  if (l == 0) s_w[w] = __popc(b);
+  __syncthreads();
+  if (w == 0) {
+    const int c = l < nw ? s_w[l] : 0;
+    const int ci = warp_incl_scan(c);
+    if (l < nw) s_w[l] = ci - c;
+    const int tot = __shfl_sync(FULL_MASK, ci, 31);
+    if (l == 0) *s_base = tot ? atomicAdd(counter, (unsigned long long)tot) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long pos = *s_base + s_w[w] + __popc(b & ((1u << l) - 1u));
+  __syncthreads();  // s_w / s_base are reused by the next call
+  return pos;
+}
+
 // Map the tagged fine cross edges through the level-0 map and de-duplicate them with an
 // open-addressing hash set (key (a << 32 | b) + 1; a < b because the level-0 map is monotone
 // across groups).  The slots a call fills are recorded and cleared again at the end.
@@ -245,6 +267,8 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
                                   const int32_t *__restrict__ m0, unsigned long long *__restrict__ table,
                                   unsigned long long tmask, int2 *__restrict__ E_out,
                                   unsigned long long *__restrict__ ne_out, unsigned long long *__restrict__ used) {
+  __shared__ int s_w[32];
+  __shared__ unsigned long long s_base;
   const int64_t ne = (int64_t)*ne_ptr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne; base += stride) {
@@ -270,12 +294,8 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
         slot = (slot + 1) & tmask;
       }
     }
-    const unsigned b = __ballot_sync(FULL_MASK, keep);
-    unsigned long long wbase = 0;
-    if ((threadIdx.x & 31) == 0 && b) wbase = atomicAdd(ne_out, (unsigned long long)__popc(b));
-    wbase = __shfl_sync(FULL_MASK, wbase, 0);
+    const unsigned long long pos = cta_compact(keep, ne_out, s_w, &s_base);
     if (keep) {
-      const unsigned long long pos = wbase + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));
       E_out[pos] = o;
       used[pos] = slot;
     }
@@ -320,6 +340,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
   __shared__ int s_w[TAIL_WARPS];
   __shared__ int s_red[TAIL_WARPS];
   __shared__ int s_total;
+  __shared__ int s_cw[TAIL_WARPS];
+  __shared__ unsigned long long s_cbase;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -437,11 +459,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
           hit = true;
         }
       }
-      const unsigned b = __ballot_sync(FULL_MASK, keep);
-      unsigned long long wbase = 0;
-      if (lane == 0 && b) wbase = atomicAdd(A.ne + (1 - cur), (unsigned long long)__popc(b));
-      wbase = __shfl_sync(FULL_MASK, wbase, 0);
-      if (keep) Eo[wbase + __popc(b & ((1u << lane) - 1u))] = o;
+      const unsigned long long pos = cta_compact(keep, A.ne + (1 - cur), s_cw, &s_cbase);
+      if (keep) Eo[pos] = o;
     }
     if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
     for (int64_t c = gtid; c < n1; c += gstride) {
