@@ -156,6 +156,32 @@ __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
 // ------------------------------------------------------------------------------------
 // Warp helpers: children table, entry lookup, bitonic sort + unique in shared memory
 // ------------------------------------------------------------------------------------
+// Warp-buffered emission of (large row, column) pairs: one global atomic on the grid-wide pair
+// counter per PAIR_BUF pairs instead of one per 32 entries (the counter is contended).
+#define PAIR_BUF 128
+__device__ __forceinline__ void pairs_flush(int2 *buf, int &nb, int2 *pairs, long long cap, AsmScal *scw) {
+  const int l = lane_id();
+  unsigned long long pb = 0;
+  if (l == 0 && nb) pb = atomicAdd((unsigned long long *)&scw->pair_count, (unsigned long long)nb);
+  pb = __shfl_sync(FULL_MASK, pb, 0);
+  for (int t = l; t < nb; t += 32) {
+    const long long pos = (long long)pb + t;
+    if (pos < cap) pairs[pos] = buf[t];
+    else scw->err_overflow = 1;
+  }
+  __syncwarp();
+  nb = 0;
+}
+__device__ __forceinline__ void pairs_push(bool emit, int2 val, int2 *buf, int &nb, int2 *pairs, long long cap,
+                                           AsmScal *scw) {
+  const unsigned m = __ballot_sync(FULL_MASK, emit);
+  if (!m) return;
+  if (nb + __popc(m) > PAIR_BUF) pairs_flush(buf, nb, pairs, cap, scw);
+  if (emit) buf[nb + __popc(m & ((1u << lane_id()) - 1u))] = val;
+  nb += __popc(m);
+  __syncwarp();
+}
+
 struct ChildTab {
   int ci[32];
   long long rb[32];
@@ -290,7 +316,9 @@ struct LargeArgs {
 __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ int s_seen[4][SEEN_CAP];  // large columns already emitted by this chunk
+  __shared__ int2 s_pb[4][PAIR_BUF];
   const int w = threadIdx.x >> 5, l = lane_id();
+  int npb = 0;
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
   for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
@@ -327,24 +355,13 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
       }
       nseen += __popc(me);
       __syncwarp();
-      const unsigned m = __ballot_sync(FULL_MASK, emit);
-      if (!m) continue;
-      long long pb = 0;
-      if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
-      pb = __shfl_sync(FULL_MASK, pb, 0);
-      if (emit) {
-        const long long pos = pb + __popc(m & ((1u << l) - 1u));
-        if (pos < A.pair_cap) A.pairs[pos] = make_int2(a, key);
-        else A.scw->err_overflow = 1;
-      }
+      pairs_push(emit, make_int2(a, key), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
     }
-    if (chunk == 0 && l == 0) {  // the diagonal block (a, a) always exists
-      const long long pos = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, 1ull);
-      if (pos < A.pair_cap) A.pairs[pos] = make_int2(a, a);
-      else A.scw->err_overflow = 1;
-    }
+    // the diagonal block (a, a) always exists
+    pairs_push(chunk == 0 && l == 0, make_int2(a, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
     __syncwarp();
   }
+  pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
 }
 
 __global__ void k_pair_count(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
@@ -532,6 +549,8 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   constexpr int NSEG = 32 / SEG;
   __shared__ ChildTab s_tab[8 * NSEG];
   __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][9];  // numeric: per-lane parked block
+  __shared__ int2 s_pb[NUMERIC ? 1 : 8][NUMERIC ? 1 : PAIR_BUF];  // symbolic: buffered pairs
+  int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
   const int sg = l / SEG, sl = l % SEG;
   const unsigned smask = SEG == 32 ? FULL_MASK : (((1u << SEG) - 1u) << (sg * SEG));
@@ -577,18 +596,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const int U12 = __popc((__ballot_sync(FULL_MASK, head && bs >= n3) & smask) >> (sg * SEG));
       if (segv && sl == 0) A.rowlen[a] = U + 3 * U12;
       const bool emit = head && !A.is_small[bs];  // transposed pair (large column, small node)
-      const unsigned m = __ballot_sync(FULL_MASK, emit);
-      if (m) {
-        long long pb = 0;
-        if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
-        pb = __shfl_sync(FULL_MASK, pb, 0);
-        if (emit) {
-          const long long pos = pb + __popc(m & ((1u << l) - 1u));
-          if (pos < A.pair_cap) A.pairs[pos] = make_int2(bs, a);
-          else A.scw->err_overflow = 1;
-        }
-      }
-      __syncwarp();
+      pairs_push(emit, make_int2(bs, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
       continue;
     }
     // numeric: column position of every run, run membership, run tails
@@ -672,6 +680,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
     }
     __syncwarp();
   }
+  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
 }
 
 // ------------------------------------------------------------------------------------
@@ -687,6 +696,8 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[MID_WARPS];
   __shared__ long long s_key[MID_WARPS][MID_CAP];
   __shared__ double s_carry[MID_WARPS][4][9];  // partial sums of a run continuing into the next window
+  __shared__ int2 s_pb[NUMERIC ? 1 : MID_WARPS][NUMERIC ? 1 : PAIR_BUF];  // symbolic: buffered pairs
+  int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
   ChildTab &tab = s_tab[w];
   long long *key = s_key[w];
@@ -734,17 +745,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       run_base += __shfl_sync(FULL_MASK, incl, 31);
       if (!NUMERIC) {
         const bool emit = head && !A.is_small[b];  // transposed pair (large column, small node)
-        const unsigned m = __ballot_sync(FULL_MASK, emit);
-        if (m) {
-          long long pb = 0;
-          if (l == 0) pb = (long long)atomicAdd((unsigned long long *)&A.scw->pair_count, (unsigned long long)__popc(m));
-          pb = __shfl_sync(FULL_MASK, pb, 0);
-          if (emit) {
-            const long long pos = pb + __popc(m & ((1u << l) - 1u));
-            if (pos < A.pair_cap) A.pairs[pos] = make_int2(b, a);
-            else A.scw->err_overflow = 1;
-          }
-        }
+        pairs_push(emit, make_int2(b, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
         continue;
       }
     }
@@ -869,6 +870,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
     if (!NUMERIC && l == 0) A.rowlen[a] = run_base;
     __syncwarp();
   }
+  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
 }
 
 // split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
