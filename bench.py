@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--partitioned", action="store_true", help="use the partitioned path even at N=1")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
+    ap.add_argument("--pcg-storage", default="full", choices=["full", "sym"],
+                    help="coarse PCG SpMV: full storage (k_spmv_sell) or the upper half (k_spmv_sym, NEXT#2)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: several ranks may share one GPU (correctness runs only)")
     return ap.parse_args()
@@ -194,7 +196,9 @@ def run_agipc(args, world, rank, local_rank):
     gd = t(g, torch.float64)
     xp = t(m.X, torch.float64)
     xcd = [t(x, torch.float64) for x in xcs]
-    step = CoarseningStep(h, dm, Hrp, Hcol, Hval, check_every=args.check_every)
+    sym = args.pcg_storage == "sym"
+    step = CoarseningStep(h, dm, Hrp, Hcol, Hval, check_every=args.check_every,
+                          pcg_storage=P.STORAGE_SYM if sym else P.STORAGE_FULL)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -248,7 +252,8 @@ def run_agipc(args, world, rank, local_rank):
     n_spmv, ms_spmv = prof.get("pcg_spmv", (0, 0.0))
     # algorithmic bytes per SpMV launch: 72 B values + 4 B col per block, 8 B row_ptr per row,
     # p read once (24 B/row), q written once (24 B/row)
-    bytes_spmv = sum(z[2] * (76 * z[1] + 8 * (z[0] + 1) + 48 * z[0]) for z in sizes)
+    # (symmetric SpMV: the diagonal + upper blocks only, (nnzb + n) / 2 of them)
+    bytes_spmv = sum(z[2] * (76 * ((z[1] + z[0]) // 2 if sym else z[1]) + 8 * (z[0] + 1) + 48 * z[0]) for z in sizes)
     bytes_per_launch = bytes_spmv / max(1, iters)
     # the library times the kernels of every 8th PCG iteration (sampled, live in the timed region)
     avg_spmv_s = (ms_spmv * 1e-3 / n_spmv) if n_spmv else None
@@ -257,7 +262,7 @@ def run_agipc(args, world, rank, local_rank):
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("k_spmv_sell")
+            traffic = json.load(open(tf)).get("k_spmv_sym" if sym else "k_spmv_sell")
         except Exception:  # noqa: BLE001
             traffic = None
     # coarsen+assemble algorithmic bytes (SURVEY §8(d) model) for context
@@ -323,7 +328,8 @@ def run_agipc(args, world, rank, local_rank):
         "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,
         "pcg_iters_per_step": round(iters / args.steps, 1),
         "coarsen_assemble_gbs": round(b_coarsen / (coarsen_ms * 1e-3) / 1e9, 1),
-        "roofline": {"kernel": "k_spmv_sell (PCG SpMV + fused p update + p.q)", "bound": "hbm",
+        "roofline": {"kernel": ("k_spmv_sym (PCG symmetric SpMV over the upper half + fused p update + p.q)" if sym
+                                else "k_spmv_sell (PCG SpMV + fused p update + p.q)"), "bound": "hbm",
                      "achieved": None if achieved is None else round(achieved, 1), "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": None if achieved is None else round(achieved / hbm, 4),

@@ -211,6 +211,35 @@ AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const
                                        int zero_x0, double rel_tol, int max_iters, int check_every,
                                        agipc_pcg_stats *stats);
 
+/* ---- NEXT#2: symmetric (diagonal + upper-triangular) storage -----------------------------
+ * "both FEM elasticity and IPC contact/friction Hessians are symmetric, so we store and
+ * accumulate only the diagonal and upper-triangular entries ... This reduces memory traffic ...
+ * for both the fine-mesh Hessian and the subsequent coarse system" (main Sec 6).
+ *
+ * agipc_bsr_upper: U = the blocks of a full-storage BSR A (columns ascending per row) with
+ *   col >= row, same order.  row_ptr : out [n_rows+1]; col : out [cap_nnzb]; val : out
+ *   [cap_nnzb][3][3].  *nnzb_upper [host] = the block count; ENOSPACE (row_ptr written) if it
+ *   exceeds cap_nnzb -- call again with a larger capacity.  Synchronises the stream.
+ *
+ * agipc_pcg_solve_sym: agipc_pcg_solve (same stopping rule, preconditioner, stats and errors)
+ *   whose SpMV streams only the diagonal + upper blocks once per iteration and applies each
+ *   block twice: q_i += A_ij p_j and, for j > i, q_j += A_ij^T p_i.  A must be symmetric
+ *   (A_ji = A_ij^T; not checked).  storage:
+ *     AGIPC_STORAGE_FULL  : A in full storage, every block streamed (= agipc_pcg_solve);
+ *     AGIPC_STORAGE_SYM   : A in full storage; the per-solve re-layout keeps col >= row only;
+ *     AGIPC_STORAGE_UPPER : A holds only col >= row (e.g. from agipc_bsr_upper); a block
+ *                           below the diagonal returns EINVAL.
+ *   The scatter sums in shared memory and L2 in no fixed order, so q (and the iterate) is
+ *   reproducible only up to rounding; the SPD/tolerance contract is that of agipc_pcg_solve. */
+#define AGIPC_STORAGE_FULL 0
+#define AGIPC_STORAGE_SYM 1
+#define AGIPC_STORAGE_UPPER 2
+AGIPC_API agipc_status agipc_bsr_upper(agipc_handle h, const agipc_bsr *A, int64_t cap_nnzb, int64_t *row_ptr,
+                                       int32_t *col, double *val, int64_t *nnzb_upper /*[host]*/);
+AGIPC_API agipc_status agipc_pcg_solve_sym(agipc_handle h, const agipc_bsr *A, int storage, const double *b,
+                                           double *x, int zero_x0, double rel_tol, int max_iters,
+                                           int check_every, agipc_pcg_stats *stats);
+
 /* ---- NEXT#4: step 1 for shells and rods ------------------------------------------------
  * "applicable to various element types (shells, volumes, rods)" (main Sec 4.2).
  *   shells (triangles a,b,c): rest tangent basis t1 = e1/|e1|, n = e1 x e2 / |e1 x e2|,

@@ -50,6 +50,10 @@ def lib():
         L.orc_rel_residual.argtypes = [i64, P, P, P, P, P]
         L.orc_rel_residual.restype = f64
         L.orc_spmv.argtypes = [i64, P, P, P, P, P]
+        L.orc_bsr_upper.argtypes = [i64, P, P, P, P, P, P]
+        L.orc_bsr_upper.restype = i64
+        L.orc_spmv_upper.argtypes = [i64, P, P, P, P, P]
+        L.orc_spmv_upper.restype = None
         L.orc_block_jacobi.argtypes = [i64, P, P, P, P, P]
         L.orc_block_jacobi.restype = i32
         L.orc_prolongate.argtypes = [i64, P, i64, P, P, P]
@@ -186,6 +190,27 @@ def spmv(row_ptr, col, val, x):
     n = rp.shape[0] - 1
     y = np.empty(3 * n)
     lib().orc_spmv(n, _p(rp), _p(cl), _p(vl), _p(_c(x, np.float64)), _p(y))
+    return y.reshape(n, 3)
+
+
+def bsr_upper(row_ptr, col, val):
+    """NEXT#2: diagonal + upper blocks of a full-storage BSR -> (row_ptr, col, val)."""
+    rp = _c(row_ptr, np.int64); cl = _c(col, np.int32); vl = _c(val, np.float64)
+    n = rp.shape[0] - 1
+    nb = int(lib().orc_bsr_upper(n, _p(rp), _p(cl), _p(vl), None, None, None))
+    urp = np.zeros(n + 1, np.int64)
+    ucol = np.zeros(max(nb, 1), np.int32)
+    uval = np.zeros((max(nb, 1), 3, 3))
+    lib().orc_bsr_upper(n, _p(rp), _p(cl), _p(vl), _p(urp), _p(ucol), _p(uval))
+    return urp, ucol[:nb], uval[:nb]
+
+
+def spmv_upper(urp, ucol, uval, x):
+    """NEXT#2: y = A x for the symmetric A given by its diagonal + upper blocks."""
+    rp = _c(urp, np.int64); cl = _c(ucol, np.int32); vl = _c(uval, np.float64)
+    n = rp.shape[0] - 1
+    y = np.empty(3 * n)
+    lib().orc_spmv_upper(n, _p(rp), _p(cl), _p(vl), _p(_c(x, np.float64)), _p(y))
     return y.reshape(n, 3)
 
 

@@ -523,6 +523,45 @@ void orc_spmv(int64_t n, const int64_t *rp, const int32_t *col, const double *va
 }
 
 /* ========================================================================== */
+/* NEXT#2 -- symmetric storage (main Sec 6: "we store and accumulate   */
+/* only the diagonal and upper-triangular entries").  Upper storage U of a    */
+/* full BSR A keeps the blocks with col >= row in order; the product of the   */
+/* symmetric operator from U is y_i = sum_{j>=i} U_ij x_j + sum_{j<i} U_ji^T x_j */
+/* written out literally.  orc_bsr_upper returns the block count (urp/ucol/   */
+/* uval may be NULL to count only).                                           */
+/* ========================================================================== */
+int64_t orc_bsr_upper(int64_t n, const int64_t *rp, const int32_t *col, const double *val, int64_t *urp,
+                      int32_t *ucol, double *uval) {
+  int64_t k = 0;
+  if (urp) urp[0] = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      if (col[e] < i) continue;
+      if (ucol) ucol[k] = col[e];
+      if (uval) memcpy(uval + 9 * k, val + 9 * e, 9 * sizeof(double));
+      ++k;
+    }
+    if (urp) urp[i + 1] = k;
+  }
+  return k;
+}
+
+void orc_spmv_upper(int64_t n, const int64_t *urp, const int32_t *ucol, const double *uval, const double *x,
+                    double *y) {
+  for (int64_t t = 0; t < 3 * n; ++t) y[t] = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = urp[i]; e < urp[i + 1]; ++e) {
+      const int64_t j = ucol[e];
+      const double *B = uval + 9 * e;
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) {
+          y[3 * i + a] += B[3 * a + c] * x[3 * j + c];   /* U_ij x_j            */
+          if (j != i) y[3 * j + c] += B[3 * a + c] * x[3 * i + a]; /* (U_ij^T x_i)_c */
+        }
+    }
+}
+
+/* ========================================================================== */
 /* NEXT#1 -- prolongation d_f = U^T d_c (main Sec 4.3: "we mathematically */
 /* prolongate the displacement to the fine mesh using the transpose of the     */
 /* restriction operator").  For a 3-DoF parent d_f = d_c[c]; for a 12-DoF parent */

@@ -82,7 +82,7 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate",
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
            "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
-           "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce"]
+           "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym"]
 
 
 def lib():
@@ -114,6 +114,8 @@ def lib():
         L.agipc_assemble_coarse.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, C.POINTER(_Bsr), P,
                                             C.POINTER(_Coarse)]
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
+        L.agipc_pcg_solve_sym.argtypes = [P, C.POINTER(_Bsr), i32, P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
+        L.agipc_bsr_upper.argtypes = [P, C.POINTER(_Bsr), i64, P, P, P, C.POINTER(i64)]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
         L.agipc_triplet_plan.argtypes = [P, i64, i64, P, P, C.POINTER(_TripletPlan)]
@@ -319,21 +321,51 @@ def assemble_coarse(h: Handle, mesh: DeviceMesh, map, n_coarse: int, affine_thre
                         bufs.val[:nb], bufs.g_c[:ns] if g_fine is not None else None)
 
 
+STORAGE_FULL, STORAGE_SYM, STORAGE_UPPER = 0, 1, 2  # include/agipc.h AGIPC_STORAGE_* (NEXT#2)
+
+
 def pcg_solve(h: Handle, row_ptr, col, val, b, x=None, rel_tol: float = 1e-3, max_iters: int = 10000,
-              check_every: int = 16, zero_x0: bool = False):
+              check_every: int = 16, zero_x0: bool = False, storage: int = STORAGE_FULL):
     """Step 4 (block-Jacobi PCG).  x is the initial guess; if None (or zero_x0) the solve starts
     from x0 = 0 in the kernels.  x is overwritten.  Returns (x, stats dict).  NOT_CONVERGED is
-    reported in stats, not raised."""
+    reported in stats, not raised.  storage != STORAGE_FULL calls agipc_pcg_solve_sym (NEXT#2,
+    P:1126): STORAGE_SYM streams the upper half of a full-storage matrix, STORAGE_UPPER takes a
+    matrix that holds only its diagonal + upper blocks (see bsr_upper)."""
     n = row_ptr.shape[0] - 1
     zero_x0 = x is None or zero_x0
     if x is None:
         x = torch.empty((n, 3), dtype=torch.float64, device=b.device)
     bsr = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), _p(val))
     stats = _PcgStats()
-    h._check(lib().agipc_pcg_solve(h._h, C.byref(bsr), _p(b), _p(x), int(bool(zero_x0)), float(rel_tol),
-                                   int(max_iters), int(check_every), C.byref(stats)), allow=(NOT_CONVERGED,))
+    if storage == STORAGE_FULL:
+        st = lib().agipc_pcg_solve(h._h, C.byref(bsr), _p(b), _p(x), int(bool(zero_x0)), float(rel_tol),
+                                   int(max_iters), int(check_every), C.byref(stats))
+    else:
+        st = lib().agipc_pcg_solve_sym(h._h, C.byref(bsr), int(storage), _p(b), _p(x), int(bool(zero_x0)),
+                                       float(rel_tol), int(max_iters), int(check_every), C.byref(stats))
+    h._check(st, allow=(NOT_CONVERGED,))
     return x, dict(iters=int(stats.iters), status=int(stats.status), rel_residual=float(stats.rel_residual),
                    b_norm=float(stats.b_norm))
+
+
+def bsr_upper(h: Handle, row_ptr, col, val, cap_nnzb: int | None = None):
+    """NEXT#2: the diagonal + upper blocks (col >= row) of a full-storage BSR.
+    Returns (row_ptr, col, val) of the upper storage."""
+    n = row_ptr.shape[0] - 1
+    dev = row_ptr.device
+    bsr = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), _p(val))
+    urp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    cap = (col.shape[0] + n) // 2 + 1 if cap_nnzb is None else int(cap_nnzb)
+    while True:
+        ucol = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        uval = torch.empty((max(cap, 1), 3, 3), dtype=torch.float64, device=dev)
+        nb = C.c_int64(0)
+        st = lib().agipc_bsr_upper(h._h, C.byref(bsr), int(cap), _p(urp), _p(ucol), _p(uval), C.byref(nb))
+        if st == ENOSPACE:
+            cap = int(nb.value)
+            continue
+        h._check(st)
+        return urp, ucol[:nb.value], uval[:nb.value]
 
 
 def prolongate(h: Handle, mesh: DeviceMesh, new_map, n3: int, n_slots: int, x_c, alpha: float = 1.0, out=None):

@@ -48,6 +48,9 @@ struct PcgGraph {
   int chunk = 0;
   int grid1 = 0, grid2 = 0;
   bool prof = false;
+  bool sym = false;
+  int win = 0, all_red = 0, upd_u = 0;
+  const void *yext = nullptr;
   std::vector<cudaEvent_t> ev;  // profiling: 3 events per iteration of the chunk
 };
 
@@ -109,14 +112,23 @@ __device__ __forceinline__ void dinv_apply(const double *__restrict__ D, const d
 // setup: block-Jacobi and the SELL layout
 // ------------------------------------------------------------------------------------
 // D^-1 of every row's 3x3 diagonal block (adjugate / determinant).
+// ub != nullptr (symmetric solve): ub[r] = first position of row r with col >= r, i.e. where the
+// diagonal + upper half of the row starts (NEXT#2).
 __global__ void k_dinv(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
-                       const double *__restrict__ val, double *__restrict__ Dinv, PcgState *st) {
+                       const double *__restrict__ val, double *__restrict__ Dinv, PcgState *st,
+                       int64_t *__restrict__ ub, int upper_only) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int64_t lo = rp[r], hi = rp[r + 1];
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
     if (col[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  if (ub) ub[r] = lo;
+  if (upper_only && lo != rp[r]) {  // AGIPC_STORAGE_UPPER input with a block below the diagonal
+    st->status = AGIPC_EINVAL;
+    st->done = 1;
+    return;
   }
   bool ok = lo < rp[r + 1] && col[lo] == r;
   double M[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -146,11 +158,13 @@ __global__ void k_dinv(int64_t n, const int64_t *__restrict__ rp, const int32_t 
 // (distributed solve: the rank's rows x ghost columns); hrp == nullptr: none
 __device__ __forceinline__ int64_t nseg_local(int64_t len) { return len <= SEG_MAX ? 1 : (len + SEG_MAX - 1) / SEG_MAX; }
 
-__global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ hrp,
-                            int32_t *__restrict__ nseg) {
+// rows are [rb[r], re[r]) of the matrix: rb = row_ptr, re = row_ptr + 1 for the full matrix;
+// rb = ub (k_dinv) for the diagonal + upper half streamed by the symmetric solve (NEXT#2)
+__global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rb, const int64_t *__restrict__ re,
+                            const int64_t *__restrict__ hrp, int32_t *__restrict__ nseg) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) {
-    int64_t ns = nseg_local(rp[r + 1] - rp[r]);
+    int64_t ns = nseg_local(re[r] - rb[r]);
     if (hrp) ns += (hrp[r + 1] - hrp[r] + SEG_MAX - 1) / SEG_MAX;
     nseg[r] = (int32_t)ns;
   }
@@ -158,13 +172,13 @@ __global__ void k_seg_count(int64_t n, const int64_t *__restrict__ rp, const int
 
 // virtual row v = segment k of row r: blocks [rp[r] + 64k, ...) of length <= 64 (halo segments
 // carry HALO_BIT and index hrp)
-__global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ hrp,
-                           const int64_t *__restrict__ vr_ptr, int32_t *__restrict__ v_row,
-                           int32_t *__restrict__ v_len, PcgState *st) {
+__global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rb, const int64_t *__restrict__ re,
+                           const int64_t *__restrict__ hrp, const int64_t *__restrict__ vr_ptr,
+                           int32_t *__restrict__ v_row, int32_t *__restrict__ v_len, PcgState *st) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r == 0) st->nv = vr_ptr[n];
   if (r < n) {
-    const int64_t len = rp[r + 1] - rp[r];
+    const int64_t len = re[r] - rb[r];
     const int64_t nl = nseg_local(len);
     const int64_t v0 = vr_ptr[r], nv = vr_ptr[r + 1] - v0;
     for (int64_t k = 0; k < nv; ++k) {
@@ -175,21 +189,22 @@ __global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rp, const int6
   }
 }
 
-// sort the virtual rows of each window by decreasing length (ties: ascending id)
+// sort the virtual rows of each window of `win` (power of two <= SORT_WIN) by decreasing length
+// (ties: ascending id)
 __global__ void __launch_bounds__(1024) k_window_sort(const PcgState *st, const int32_t *__restrict__ v_len,
-                                                      int32_t *__restrict__ perm) {
+                                                      int32_t *__restrict__ perm, int win) {
   __shared__ unsigned long long s_key[SORT_WIN];
   const long long nv = st->nv;
-  const long long w0 = (long long)blockIdx.x * SORT_WIN;
+  const long long w0 = (long long)blockIdx.x * win;
   if (w0 >= nv) return;
-  for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+  for (int i = threadIdx.x; i < win; i += blockDim.x) {
     long long v = w0 + i;
     s_key[i] = v < nv ? ((unsigned long long)(SEG_MAX - VLEN(v_len[v])) << 32) | (unsigned long long)i : ~0ull;
   }
   __syncthreads();
-  for (int k = 2; k <= SORT_WIN; k <<= 1)
+  for (int k = 2; k <= win; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+      for (int i = threadIdx.x; i < win; i += blockDim.x) {
         int ixj = i ^ j;
         if (ixj > i) {
           unsigned long long a = s_key[i], b = s_key[ixj];
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(1024) k_window_sort(const PcgState *st, const 
       }
       __syncthreads();
     }
-  for (int i = threadIdx.x; i < SORT_WIN; i += blockDim.x) {
+  for (int i = threadIdx.x; i < win; i += blockDim.x) {
     long long v = w0 + i;
     if (v < nv) perm[v] = (int32_t)(w0 + (long long)(s_key[i] & 0xffffffffull));
   }
@@ -247,7 +262,8 @@ __global__ void k_sell_scalars(int64_t ns_bound, const int64_t *__restrict__ spt
 }
 
 // warp per slice: component-major tiles; padding = zero blocks pointing at the row itself
-__global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+__global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, const int64_t *__restrict__ re,
+                            const int32_t *__restrict__ col,
                             const double *__restrict__ val, const int64_t *__restrict__ hrp,
                             const int32_t *__restrict__ hcol, const double *__restrict__ hval,
                             const int64_t *__restrict__ vr_ptr,
@@ -270,8 +286,8 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, 
       len = VLEN(vl);
       halo = (vl & HALO_BIT) != 0;
       const long long k = v - vr_ptr[row];
-      if (!halo) k0 = rp[row] + (long long)SEG_MAX * k;
-      else k0 = hrp[row] + (long long)SEG_MAX * (k - nseg_local(rp[row + 1] - rp[row]));
+      if (!halo) k0 = rb[row] + (long long)SEG_MAX * k;
+      else k0 = hrp[row] + (long long)SEG_MAX * (k - nseg_local(re[row] - rb[row]));
     }
     const int32_t *cs = halo ? hcol : col;
     const double *vs = halo ? hval : val;
@@ -289,6 +305,39 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rp, 
   }
 }
 
+// y = A x for A given as its diagonal + upper blocks (NEXT#2, x0 != 0 only): warp per row,
+// y_i += A_ij x_j and y_j += A_ij^T x_i (j > i) by fp64 reductions into y (zeroed by the caller).
+__global__ void k_ax_upper(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                           const double *__restrict__ val, const double *__restrict__ x, double *y) {
+  const int l = lane_id();
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double xi0 = x[3 * row], xi1 = x[3 * row + 1], xi2 = x[3 * row + 2];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int64_t k = rp[row] + l; k < rp[row + 1]; k += 32) {
+      const int64_t c = col[k];
+      const double *m = val + 9 * k;
+      const double x0 = x[3 * c], x1 = x[3 * c + 1], x2 = x[3 * c + 2];
+      a0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      a1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      a2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
+      if (c != row) {
+        atomicAdd(y + 3 * c, m[0] * xi0 + m[3] * xi1 + m[6] * xi2);
+        atomicAdd(y + 3 * c + 1, m[1] * xi0 + m[4] * xi1 + m[7] * xi2);
+        atomicAdd(y + 3 * c + 2, m[2] * xi0 + m[5] * xi1 + m[8] * xi2);
+      }
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (l == 0) {
+      atomicAdd(y + 3 * row, a0);
+      atomicAdd(y + 3 * row + 1, a1);
+      atomicAdd(y + 3 * row + 2, a2);
+    }
+  }
+}
+
 // r = b - A x (or b); z = D^-1 r; rz = r.z, rr = r.r, bb = b.b; p_old = 0 and beta = 0, so the
 // first K1 forms p = z exactly
 __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *__restrict__ rp,
@@ -296,13 +345,16 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
                                                       const double *__restrict__ b, double *__restrict__ x,
                                                       const double *__restrict__ Dinv, double *__restrict__ r,
                                                       double *__restrict__ z, double *__restrict__ p, double *parts,
-                                                      PcgState *st, int zero_x0, double *red) {
+                                                      PcgState *st, int zero_x0, double *red,
+                                                      const double *__restrict__ ax) {
   __shared__ double s_red[PCG_WARPS];
   const int w = threadIdx.x >> 5, l = lane_id();
   double rz = 0.0, rr = 0.0, bb = 0.0;
   for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + w; row < n; row += (int64_t)gridDim.x * PCG_WARPS) {
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    if (!zero_x0) {  // (A x)_row, one warp, flat over the row's values
+    if (!zero_x0 && ax) {  // (A x)_row precomputed from upper storage (k_ax_upper)
+      y0 = ax[3 * row]; y1 = ax[3 * row + 1]; y2 = ax[3 * row + 2];
+    } else if (!zero_x0) {  // (A x)_row, one warp, flat over the row's values
       const int64_t k0 = rp[row], ne = 9 * (rp[row + 1] - k0);
       for (int64_t e = l; e < ne; e += 32) {
         const int blk = (int)(e / 9), rem = (int)(e - 9 * (int64_t)blk), ii = rem / 3, jj = rem - 3 * ii;
@@ -463,38 +515,231 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
   }
 }
 
+// ------------------------------------------------------------------------------------
+// K1 of the symmetric solve (NEXT#2, "store ... only the diagonal and upper-triangular
+// entries ... reduces memory traffic ... for the subsequent coarse system").  The SELL layout
+// holds only the blocks with col >= row, so every stored block is streamed once per iteration
+// and used twice: q_i += A_ij p_j (gather, as in k_spmv_sell) and q_j += A_ij^T p_i (scatter,
+// j > i).  Persistent CTAs claim whole windows of `win` virtual rows; a window covers the
+// contiguous row range [lo, hi] (virtual rows are numbered by row), so a scatter target inside
+// it is summed in shared memory and written once by this CTA (y_tin); a target outside, or a
+// row whose segments straddle two windows, goes to y_ext by fp64 reductions in L2 (zeroed by
+// K2 after use).  p.q = sum_i p_i.(A_ii p_i) + 2 sum_{i<j} p_i.(A_ij p_j) from the gather part.
+// Reduction order in shared memory / L2 is not fixed: q is deterministic only up to rounding.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void red_f64(double *p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void sym_blk(const BlkLoad &b, int64_t c3, int64_t i3, double beta, double pi0, double pi1,
+                                        double pi2, int64_t lo3, int64_t nr3, double *s_acc, double *yext,
+                                        double &d0, double &d1, double &d2, double &o0, double &o1, double &o2) {
+  const double x0 = b.z[0] + beta * b.p[0], x1 = b.z[1] + beta * b.p[1], x2 = b.z[2] + beta * b.p[2];
+  const double g0 = b.m[0] * x0 + b.m[1] * x1 + b.m[2] * x2;
+  const double g1 = b.m[3] * x0 + b.m[4] * x1 + b.m[5] * x2;
+  const double g2 = b.m[6] * x0 + b.m[7] * x1 + b.m[8] * x2;
+  if (c3 == i3) {  // diagonal block (or SELL padding: zero block pointing at the row)
+    d0 += g0; d1 += g1; d2 += g2;
+  } else {
+    o0 += g0; o1 += g1; o2 += g2;
+    const double t0 = b.m[0] * pi0 + b.m[3] * pi1 + b.m[6] * pi2;
+    const double t1 = b.m[1] * pi0 + b.m[4] * pi1 + b.m[7] * pi2;
+    const double t2 = b.m[2] * pi0 + b.m[5] * pi1 + b.m[8] * pi2;
+    const int64_t off = c3 - lo3;
+    if ((uint64_t)off < (uint64_t)nr3) {
+      atomicAdd(s_acc + off, t0);
+      atomicAdd(s_acc + off + 1, t1);
+      atomicAdd(s_acc + off + 2, t2);
+    } else {
+      red_f64(yext + c3, t0);
+      red_f64(yext + c3 + 1, t1);
+      red_f64(yext + c3 + 2, t2);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PCG_THREADS, 2) k_spmv_sym(const int64_t *__restrict__ sptr,
+                                                          const int32_t *__restrict__ scol,
+                                                          const double *__restrict__ sval,
+                                                          const int32_t *__restrict__ s_vrow,
+                                                          const int32_t *__restrict__ v_row,
+                                                          const int64_t *__restrict__ vr_ptr,
+                                                          const double *__restrict__ z, const double *__restrict__ pold,
+                                                          double *__restrict__ pnew, double *__restrict__ qseg,
+                                                          double *__restrict__ ytin, double *yext, int win,
+                                                          int *counter, double *parts, PcgState *st, int all_red) {
+  if (*(volatile int *)&st->done) return;
+  extern __shared__ double s_acc[];  // [3 * win]
+  __shared__ double s_red[PCG_WARPS];
+  __shared__ int s_w;
+  const double beta = st->beta;
+  const long long ns = st->ns, nv = st->nv;
+  const long long nwin = (nv + win - 1) / win;
+  const int l = lane_id(), w = threadIdx.x >> 5;
+  const int spw = win >> 5;  // slices per window
+  double pq = 0.0;
+  while (true) {
+    if (threadIdx.x == 0) s_w = atomicAdd(counter, 1);
+    __syncthreads();
+    const long long W = s_w;
+    if (W >= nwin) break;
+    const long long v0 = W * win, v1 = min(v0 + win, nv);
+    const int64_t lo = v_row[v0], hi = v_row[v1 - 1];
+    const int nr = (int)(hi - lo + 1);
+    const int64_t nr3 = all_red ? 0 : 3 * (int64_t)nr;  // all_red: every scatter target through L2
+    for (int t = threadIdx.x; t < 3 * nr; t += PCG_THREADS) s_acc[t] = 0.0;
+    __syncthreads();
+    const long long s_end = min((W + 1) * spw, ns);
+    for (long long s = W * spw + w; s < s_end; s += PCG_WARPS) {
+      const long long base = sptr[s];
+      const int L = (int)((sptr[s + 1] - base) >> 5);
+      const int32_t *cp = scol + base + l;
+      const double *vp = sval + 9 * base + l;
+      const int v = s_vrow[32 * s + l];
+      const int64_t row = v >= 0 ? v_row[v] : -1;
+      const int64_t i3 = 3 * row;
+      double pi0 = 0.0, pi1 = 0.0, pi2 = 0.0;
+      if (v >= 0) {
+        pi0 = z[i3] + beta * pold[i3];
+        pi1 = z[i3 + 1] + beta * pold[i3 + 1];
+        pi2 = z[i3 + 2] + beta * pold[i3 + 2];
+      }
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, o0 = 0.0, o1 = 0.0, o2 = 0.0;
+      // padding lanes (v < 0) hold zero blocks pointing at row 0: treat them as diagonal
+      const int64_t ii3 = v >= 0 ? i3 : -1;
+      int64_t n0 = L > 0 ? 3 * (int64_t)__ldcs(cp) : 0, n1 = L > 1 ? 3 * (int64_t)__ldcs(cp + 32) : 0;
+      int j = 0;
+      for (; j + 1 < L; j += 2) {
+        BlkLoad b0, b1;
+        const int64_t c0 = n0, c1 = n1;
+        blk_load(b0, vp + 288 * (int64_t)j, c0, z, pold);
+        blk_load(b1, vp + 288 * (int64_t)(j + 1), c1, z, pold);
+        if (j + 2 < L) n0 = 3 * (int64_t)__ldcs(cp + 32 * (j + 2));
+        if (j + 3 < L) n1 = 3 * (int64_t)__ldcs(cp + 32 * (j + 3));
+        sym_blk(b0, v >= 0 ? c0 : -1, ii3, beta, pi0, pi1, pi2, 3 * lo, nr3, s_acc, yext, d0, d1, d2, o0, o1, o2);
+        sym_blk(b1, v >= 0 ? c1 : -1, ii3, beta, pi0, pi1, pi2, 3 * lo, nr3, s_acc, yext, d0, d1, d2, o0, o1, o2);
+      }
+      if (j < L) {
+        BlkLoad b0;
+        const int64_t c0 = n0;
+        blk_load(b0, vp + 288 * (int64_t)j, c0, z, pold);
+        sym_blk(b0, v >= 0 ? c0 : -1, ii3, beta, pi0, pi1, pi2, 3 * lo, nr3, s_acc, yext, d0, d1, d2, o0, o1, o2);
+      }
+      if (v >= 0) {
+        if (vr_ptr[row] == v) {  // the first segment stores the row's new direction
+          pnew[i3] = pi0; pnew[i3 + 1] = pi1; pnew[i3 + 2] = pi2;
+        }
+        qseg[3 * (int64_t)v] = d0 + o0;
+        qseg[3 * (int64_t)v + 1] = d1 + o1;
+        qseg[3 * (int64_t)v + 2] = d2 + o2;
+        pq += pi0 * d0 + pi1 * d1 + pi2 * d2 + 2.0 * (pi0 * o0 + pi1 * o1 + pi2 * o2);
+      }
+    }
+    __syncthreads();
+    // flush: rows whose virtual rows all lie in this window are owned here (plain stores);
+    // a straddling row receives scatter from two windows and goes through L2 reductions
+    for (int t = threadIdx.x; t < nr; t += PCG_THREADS) {
+      const int64_t row = lo + t;
+      const double a0 = s_acc[3 * t], a1 = s_acc[3 * t + 1], a2 = s_acc[3 * t + 2];
+      if (vr_ptr[row] >= v0 && vr_ptr[row + 1] <= v1) {
+        ytin[3 * row] = a0; ytin[3 * row + 1] = a1; ytin[3 * row + 2] = a2;
+      } else {
+        red_f64(yext + 3 * row, a0);
+        red_f64(yext + 3 * row + 1, a1);
+        red_f64(yext + 3 * row + 2, a2);
+      }
+    }
+    __syncthreads();
+  }
+  pq = block_sum(pq, s_red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = pq;
+  if (last_block(st)) {
+    double PQ = reduce_parts(parts, gridDim.x, s_red);
+    if (threadIdx.x == 0) {
+      st->pq = PQ;
+      if (!isfinite(PQ) || !isfinite(st->rz)) {
+        st->status = AGIPC_EBREAKDOWN;
+        st->done = 1;
+        st->it += 1;
+      } else if (PQ <= 0.0) {
+        st->status = AGIPC_EINDEFINITE;
+        st->done = 1;
+        st->it += 1;
+      } else {
+        st->alpha = st->rz / PQ;
+      }
+    }
+  }
+}
+
 // K2: thread per slot; q = sum of the row's segments (fixed order); x += alpha p; r -= alpha q;
-// z = D^-1 r; last CTA: ||r|| <= tol ||b||, iteration count, beta.
+// z = D^-1 r; last CTA: ||r|| <= tol ||b||, iteration count, beta.  Each thread takes U
+// slots per pass and issues all their independent loads before the arithmetic (the kernel is
+// latency-bound at 2 CTAs per SM, the grid size that keeps the last-block reduction cheap).
+template <int U>
 __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t *__restrict__ vr_ptr,
                                                         double *__restrict__ x, double *__restrict__ r,
                                                         double *__restrict__ z, const double *__restrict__ p,
                                                         const double *__restrict__ qseg,
                                                         const double *__restrict__ Dinv, int *next_counter,
-                                                        double *parts, PcgState *st, double *red) {
+                                                        double *parts, PcgState *st, double *red,
+                                                        const double *__restrict__ ytin, double *__restrict__ yext) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double alpha = st->alpha;
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_counter = 0;
   double rz = 0.0, rr = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * PCG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * PCG_THREADS) {
-    const int64_t v0 = vr_ptr[i], v1 = vr_ptr[i + 1];
-    double q0 = qseg[3 * v0], q1 = qseg[3 * v0 + 1], q2 = qseg[3 * v0 + 2];
-    for (int64_t v = v0 + 1; v < v1; ++v) {
-      q0 += qseg[3 * v];
-      q1 += qseg[3 * v + 1];
-      q2 += qseg[3 * v + 2];
+  const int64_t stride = (int64_t)gridDim.x * PCG_THREADS;
+  for (int64_t i0 = (int64_t)blockIdx.x * PCG_THREADS + threadIdx.x; i0 < n; i0 += U * stride) {
+    int64_t v0[U], v1[U];
+    double q[U][3], xv[U][3], rv[U][3], pv[U][3], D[U][9];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        v0[u] = vr_ptr[i]; v1[u] = vr_ptr[i + 1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xv[u][c] = x[3 * i + c]; rv[u][c] = r[3 * i + c]; pv[u][c] = p[3 * i + c];
+        }
+#pragma unroll
+        for (int e = 0; e < 9; ++e) D[u][e] = Dinv[9 * i + e];
+      }
     }
-    const int64_t k = 3 * i;
-    x[k] += alpha * p[k];
-    x[k + 1] += alpha * p[k + 1];
-    x[k + 2] += alpha * p[k + 2];
-    const double r0 = r[k] - alpha * q0, r1 = r[k + 1] - alpha * q1, r2 = r[k + 2] - alpha * q2;
-    r[k] = r0; r[k + 1] = r1; r[k + 2] = r2;
-    double z0, z1, z2;
-    dinv_apply(Dinv + 9 * i, r0, r1, r2, z0, z1, z2);
-    z[k] = z0; z[k + 1] = z1; z[k + 2] = z2;
-    rz += r0 * z0 + r1 * z1 + r2 * z2;
-    rr += r0 * r0 + r1 * r1 + r2 * r2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        q[u][0] = qseg[3 * v0[u]]; q[u][1] = qseg[3 * v0[u] + 1]; q[u][2] = qseg[3 * v0[u] + 2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) continue;
+      for (int64_t v = v0[u] + 1; v < v1[u]; ++v) {
+        q[u][0] += qseg[3 * v];
+        q[u][1] += qseg[3 * v + 1];
+        q[u][2] += qseg[3 * v + 2];
+      }
+      const int64_t k = 3 * i;
+      if (yext) {  // symmetric solve: the scattered A_ji^T p_j parts (NEXT#2); y_ext is re-zeroed
+        q[u][0] += ytin[k] + yext[k];
+        q[u][1] += ytin[k + 1] + yext[k + 1];
+        q[u][2] += ytin[k + 2] + yext[k + 2];
+        yext[k] = 0.0; yext[k + 1] = 0.0; yext[k + 2] = 0.0;
+      }
+      x[k] = xv[u][0] + alpha * pv[u][0];
+      x[k + 1] = xv[u][1] + alpha * pv[u][1];
+      x[k + 2] = xv[u][2] + alpha * pv[u][2];
+      const double r0 = rv[u][0] - alpha * q[u][0], r1 = rv[u][1] - alpha * q[u][1], r2 = rv[u][2] - alpha * q[u][2];
+      r[k] = r0; r[k + 1] = r1; r[k + 2] = r2;
+      double z0, z1, z2;
+      dinv_apply(D[u], r0, r1, r2, z0, z1, z2);
+      z[k] = z0; z[k + 1] = z1; z[k + 2] = z2;
+      rz += r0 * z0 + r1 * z1 + r2 * z2;
+      rr += r0 * r0 + r1 * r1 + r2 * r2;
+    }
   }
   const int G = gridDim.x;
   rz = block_sum(rz, s_red);
@@ -538,6 +783,12 @@ struct PcgBufs {
   PcgState *st;
   int64_t ns_bound;
   int G1, G2;
+  // symmetric solve (NEXT#2): windows of `win` virtual rows, scatter targets y_tin / y_ext
+  bool sym = false;
+  int win = SORT_WIN;
+  double *ytin = nullptr, *yext = nullptr;
+  int all_red = 0;
+  int upd_u = 1;  // slots per K2 thread pass
 };
 
 // iteration j reads p_old = P[j&1] and writes p_new = P[(j+1)&1] (the chunk length is even)
@@ -547,11 +798,17 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
     double *pold = B.P[k & 1], *pnew = B.P[(k + 1) & 1];
     const bool sample = ev && (k % PROF_EVERY) == 0;  // sampled kernel timing (low overhead)
     if (sample) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
-    k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z, pold,
-                                             pnew, B.qseg, B.counters + (k & 1), B.parts, B.st, nullptr);
+    if (B.sym)
+      k_spmv_sym<<<B.G1, PCG_THREADS, 3 * sizeof(double) * B.win, s>>>(
+          B.sptr, B.scol, B.sval, B.s_vrow, B.v_row, B.vr_ptr, B.z, pold, pnew, B.qseg, B.ytin, B.yext, B.win,
+          B.counters + (k & 1), B.parts, B.st, B.all_red);
+    else
+      k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z,
+                                               pold, pnew, B.qseg, B.counters + (k & 1), B.parts, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
-    k_update<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
-                                          B.parts, B.st, nullptr);
+    auto k2 = B.upd_u == 2 ? k_update<2> : k_update<1>;
+    k2<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
+                                          B.parts, B.st, nullptr, B.ytin, B.yext);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
   }
   cudaError_t e = cudaGetLastError();
@@ -562,10 +819,23 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
 // Block-Jacobi + SELL layout + k_init, shared by the 1-GPU solve and the distributed solve.
 // Ah (nullable): halo matrix of the rank's rows x ghost columns (columns >= n index the ghost
 // region of the vectors, n_gs slots).  red != nullptr: k_init leaves rank partials in red.
+// storage (1-GPU solve only): AGIPC_STORAGE_FULL streams every block (k_spmv_sell);
+// AGIPC_STORAGE_SYM keeps only the diagonal + upper blocks of a full-storage A in the SELL copy
+// and AGIPC_STORAGE_UPPER takes A already stored that way; both run k_spmv_sym (NEXT#2).
 static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *Ah, int64_t n_gs, const double *b,
                               const double *x, int zero_x0, double rel_tol, int max_iters, PcgBufs &B,
-                              PcgState *hst, double *red) {
+                              PcgState *hst, double *red, int storage = AGIPC_STORAGE_FULL) {
   const int64_t n = A->n_rows;
+  B.sym = storage != AGIPC_STORAGE_FULL;
+  B.win = SORT_WIN;
+  if (B.sym) {
+    B.win = 1024;
+    if (const char *e = getenv("AGIPC_SYM_WIN")) {  // experiments: 128 .. 4096, power of two
+      int w = atoi(e);
+      if (w >= 128 && w <= SORT_WIN && (w & (w - 1)) == 0) B.win = w;
+    }
+    B.all_red = getenv("AGIPC_SYM_RED") ? 1 : 0;
+  }
   const int64_t nh = Ah ? Ah->nnzb : 0;
   cudaStream_t s0 = h->stream;
   const int64_t nv_bound = n + (A->nnzb + nh) / SEG_MAX + (Ah ? n : 0) + 1;  // virtual rows
@@ -590,8 +860,21 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   WS(h, order, int32_t, "pcg_order", B.ns_bound); B.order = order;
   WS(h, ctr, int, "pcg_counters", 2); B.counters = ctr;
   int occ = 0;
-  CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
-  B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
+  if (B.sym) {
+    const size_t smem = 3 * sizeof(double) * B.win;
+    CU_TRY(h, cudaFuncSetAttribute(k_spmv_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sym, PCG_THREADS, smem));
+    B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nv_bound, B.win), (int64_t)std::max(1, occ) * h->sm_count));
+    WS(h, yt, double, "pcg_ytin", 3 * n + 2); B.ytin = yt;
+    WS(h, ye, double, "pcg_yext", 3 * n + 2); B.yext = ye;
+  } else {
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
+    B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
+    B.ytin = B.yext = nullptr;
+  }
+  // K2: 2 CTAs per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl: 3-8 CTAs per SM
+  // or 2 slots per pass are not faster)
+  B.upd_u = 1;
   B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 2 * (int64_t)h->sm_count));
   const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
   const int Gp = std::max(std::max(B.G1, B.G2), Gi);
@@ -609,14 +892,20 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaMemsetAsync(B.P[0] + 3 * n, 0, sizeof(double) * 3 * n_gs, s0));
     CU_TRY(h, cudaMemsetAsync(B.P[1] + 3 * n, 0, sizeof(double) * 3 * n_gs, s0));
   }
-  LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp);
+  const int64_t *rb = A->row_ptr, *re = A->row_ptr + 1;
+  int64_t *ub = nullptr;
+  if (storage == AGIPC_STORAGE_SYM) {
+    WS(h, ubw, int64_t, "pcg_ub", n + 1); ub = ubw; rb = ubw;
+  }
+  LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp, ub,
+         storage == AGIPC_STORAGE_UPPER ? 1 : 0);
   // SELL layout (once per solve)
   const int64_t *hrp = Ah ? Ah->row_ptr : nullptr;
-  LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, hrp, nseg);
+  LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, nseg);
   agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
   if (sst != AGIPC_OK) return sst;
-  LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
-  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, SORT_WIN), 1024, 0, stp, B.v_len, B.perm);
+  LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
+  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, B.win), 1024, 0, stp, B.v_len, B.perm, B.win);
   LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
   sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
   if (sst != AGIPC_OK) return sst;
@@ -629,16 +918,28 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   WS(h, scol, int32_t, "pcg_scol", sell_blocks + 32); B.scol = scol;
   WS(h, sval, double, "pcg_sval", 9 * sell_blocks + 288); B.sval = sval;
   LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
-         0, stp, A->row_ptr, A->col, A->val, hrp, Ah ? Ah->col : nullptr, Ah ? Ah->val : nullptr, B.vr_ptr, B.perm,
+         0, stp, rb, re, A->col, A->val, hrp, Ah ? Ah->col : nullptr, Ah ? Ah->val : nullptr, B.vr_ptr, B.perm,
          B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
+  const double *ax = nullptr;
+  if (B.sym) {
+    CU_TRY(h, cudaMemsetAsync(B.ytin, 0, sizeof(double) * 3 * n, s0));  // straddling rows keep 0
+    CU_TRY(h, cudaMemsetAsync(B.yext, 0, sizeof(double) * 3 * n, s0));
+    if (storage == AGIPC_STORAGE_UPPER && !zero_x0) {  // r = b - A x0 from the upper half
+      WS(h, axw, double, "pcg_ax", 3 * n + 2);
+      CU_TRY(h, cudaMemsetAsync(axw, 0, sizeof(double) * 3 * n, s0));
+      LAUNCH(h, k_ax_upper, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 16 * h->sm_count)), 256, 0, n,
+             A->row_ptr, A->col, A->val, B.x, axw);
+      ax = axw;
+    }
+  }
   LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
-         parts, stp, zero_x0, red);
+         parts, stp, zero_x0, red, ax);
   return AGIPC_OK;
 }
 
-extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const double *b, double *x,
-                                        int zero_x0, double rel_tol, int max_iters, int check_every,
-                                        agipc_pcg_stats *stats) {
+static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int storage, const double *b, double *x,
+                                   int zero_x0, double rel_tol, int max_iters, int check_every,
+                                   agipc_pcg_stats *stats) {
   if (!h) return AGIPC_EINVAL;
   if (!A || !stats || max_iters < 0 || A->n_rows < 0 || !(rel_tol >= 0.0))
     return set_err(h, AGIPC_EINVAL, "pcg_solve: bad arguments");
@@ -654,7 +955,7 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
   if (ast != AGIPC_OK) return ast;
   PcgBufs B;
-  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr);
+  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr, storage);
   if (ast != AGIPC_OK) return ast;
   if (max_iters == 0) {
     CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
@@ -671,7 +972,8 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
     chunk += chunk & 1;  // even: the p ping-pong parity is the same at every graph launch
     const void *key[8] = {B.sval, B.scol, B.x, B.qseg, B.Dinv, B.sptr, B.P[0], B.parts};
     bool same = g->exec && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
-                g->grid2 == B.G2 && g->prof == h->prof;
+                g->grid2 == B.G2 && g->prof == h->prof && g->sym == B.sym && g->win == B.win && g->yext == B.yext &&
+                g->all_red == B.all_red && g->upd_u == B.upd_u;
     for (int i = 0; i < 8 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
@@ -697,6 +999,11 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
       g->grid1 = B.G1;
       g->grid2 = B.G2;
       g->prof = h->prof;
+      g->sym = B.sym;
+      g->win = B.win;
+      g->yext = B.yext;
+      g->all_red = B.all_red;
+      g->upd_u = B.upd_u;
       for (int i = 0; i < 8; ++i) g->key[i] = key[i];
     }
     CU_TRY(h, cudaEventRecord(g->ev_in, s0));
@@ -732,11 +1039,27 @@ extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, cons
   stats->status = hst->done ? hst->status : AGIPC_NOT_CONVERGED;
   stats->b_norm = sqrt(hst->bn2);
   stats->rel_residual = hst->bn2 > 0 ? sqrt(hst->rr) / sqrt(hst->bn2) : sqrt(hst->rr);
+  if (stats->status == AGIPC_EINVAL) return set_err(h, AGIPC_EINVAL, "pcg_solve: upper storage has a block below the diagonal");
   if (stats->status == AGIPC_ESINGULAR) return set_err(h, AGIPC_ESINGULAR, "pcg_solve: singular diagonal block");
   if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "pcg_solve: p^T A p <= 0");
   if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "pcg_solve: NaN/Inf");
   if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
   return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const double *b, double *x,
+                                        int zero_x0, double rel_tol, int max_iters, int check_every,
+                                        agipc_pcg_stats *stats) {
+  return pcg_solve_impl(h, A, AGIPC_STORAGE_FULL, b, x, zero_x0, rel_tol, max_iters, check_every, stats);
+}
+
+extern "C" agipc_status agipc_pcg_solve_sym(agipc_handle h, const agipc_bsr *A, int storage, const double *b,
+                                            double *x, int zero_x0, double rel_tol, int max_iters, int check_every,
+                                            agipc_pcg_stats *stats) {
+  if (!h) return AGIPC_EINVAL;
+  if (storage != AGIPC_STORAGE_FULL && storage != AGIPC_STORAGE_SYM && storage != AGIPC_STORAGE_UPPER)
+    return set_err(h, AGIPC_EINVAL, "pcg_solve_sym: bad storage %d", storage);
+  return pcg_solve_impl(h, A, storage, b, x, zero_x0, rel_tol, max_iters, check_every, stats);
 }
 
 // ------------------------------------------------------------------------------------
@@ -896,8 +1219,8 @@ extern "C" agipc_status agipc_dpcg_update(agipc_handle h, double *red) {
   double *pnew = B.P[(d->k + 1) & 1];
   ProfScope prof(h, PROF_PCG_UPDATE, h->stream);
   LAUNCH(h, k_dscalars, 1, 1, 0, B.st, (const double *)red, (int)DP_ALPHA);
-  LAUNCH(h, k_update, (unsigned)B.G2, PCG_THREADS, 0, d->n, B.vr_ptr, B.x, B.r, B.z, (const double *)pnew, B.qseg,
-         B.Dinv, B.counters + ((d->k + 1) & 1), B.parts, B.st, red);
+  LAUNCH(h, k_update<1>, (unsigned)B.G2, PCG_THREADS, 0, d->n, B.vr_ptr, B.x, B.r, B.z, (const double *)pnew, B.qseg,
+         B.Dinv, B.counters + ((d->k + 1) & 1), B.parts, B.st, red, (const double *)nullptr, (double *)nullptr);
   d->k += 1;
   d->pending = DP_UPDATE;
   return AGIPC_OK;
@@ -945,5 +1268,66 @@ extern "C" agipc_status agipc_dpcg_finish(agipc_handle h, const double *red, dou
   if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "dpcg: p^T A p <= 0");
   if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "dpcg: NaN/Inf");
   if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
+  return AGIPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT#2: diagonal + upper storage of a full-storage BSR.  Row r keeps the blocks
+// with col >= r in their order; row pointers by a scan of the per-row counts.
+// ------------------------------------------------------------------------------------
+__global__ void k_upper_count(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                              int64_t *__restrict__ ub, int32_t *__restrict__ cnt) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t lo = rp[r], hi = rp[r + 1];
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (col[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  ub[r] = lo;
+  cnt[r] = (int32_t)(rp[r + 1] - lo);
+}
+
+// warp per row: columns, then the 9 values of each block as a flat coalesced copy
+__global__ void k_upper_copy(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ ub,
+                             const int32_t *__restrict__ col, const double *__restrict__ val,
+                             const int64_t *__restrict__ urp, int32_t *__restrict__ ucol, double *__restrict__ uval) {
+  const int l = lane_id();
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t s0 = ub[r], d0 = urp[r], len = urp[r + 1] - d0;
+    for (int64_t k = l; k < len; k += 32) ucol[d0 + k] = col[s0 + k];
+    for (int64_t k = l; k < 9 * len; k += 32) uval[9 * d0 + k] = val[9 * s0 + k];
+  }
+}
+
+extern "C" agipc_status agipc_bsr_upper(agipc_handle h, const agipc_bsr *A, int64_t cap_nnzb, int64_t *row_ptr,
+                                        int32_t *col, double *val, int64_t *nnzb_upper) {
+  if (!h) return AGIPC_EINVAL;
+  if (!A || !nnzb_upper || A->n_rows < 0 || cap_nnzb < 0) return set_err(h, AGIPC_EINVAL, "bsr_upper: bad arguments");
+  const int64_t n = A->n_rows;
+  *nnzb_upper = 0;
+  if (!row_ptr || (n > 0 && (!A->row_ptr || (A->nnzb > 0 && (!A->col || !A->val)))))
+    return set_err(h, AGIPC_EINVAL, "bsr_upper: null pointer");
+  CU_TRY(h, cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  if (n == 0) {
+    CU_TRY(h, cudaMemsetAsync(row_ptr, 0, sizeof(int64_t), s));
+    return AGIPC_OK;
+  }
+  WS(h, ub, int64_t, "upper_ub", n + 1);
+  WS(h, cnt, int32_t, "upper_cnt", n + 1);
+  LAUNCH(h, k_upper_count, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, ub, cnt);
+  agipc_status st = scan_exclusive_i64(h, SCAN_SRC_I32, cnt, n, row_ptr);
+  if (st != AGIPC_OK) return st;
+  int64_t *hn = (int64_t *)pinned_get(h, sizeof(int64_t), &st);
+  if (st != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemcpyAsync(hn, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CU_TRY(h, cudaStreamSynchronize(s));
+  *nnzb_upper = *hn;
+  if (*hn > cap_nnzb || (*hn > 0 && (!col || !val)))
+    return set_err(h, AGIPC_ENOSPACE, "bsr_upper: %lld blocks > capacity %lld", (long long)*hn, (long long)cap_nnzb);
+  LAUNCH(h, k_upper_copy, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 16 * h->sm_count)), 256, 0, n,
+         A->row_ptr, (const int64_t *)ub, A->col, A->val, (const int64_t *)row_ptr, col, val);
   return AGIPC_OK;
 }

@@ -8,7 +8,8 @@ import dataclasses
 
 import torch
 
-from . import (CoarseBuffers, DeviceMesh, Handle, assemble_coarse, build_map, pcg_solve, prolongate, tag_edges)
+from . import (STORAGE_FULL, CoarseBuffers, DeviceMesh, Handle, assemble_coarse, build_map, pcg_solve, prolongate,
+               tag_edges)
 
 
 @dataclasses.dataclass
@@ -27,8 +28,9 @@ class CoarseningStep:
 
     def __init__(self, h: Handle, mesh: DeviceMesh, H_row_ptr, H_col, H_val, group_size=32,
                  affine_threshold=32, theta=5e-5, rel_tol=1e-3, max_iters=10000, check_every=16,
-                 refine_iters=0):
+                 refine_iters=0, pcg_storage=STORAGE_FULL):
         self.h, self.mesh = h, mesh
+        self.pcg_storage = pcg_storage  # STORAGE_SYM: the coarse SpMV streams the upper half (NEXT#2)
         self.H = (H_row_ptr, H_col, H_val)
         self.group_size, self.affine_threshold, self.theta = group_size, affine_threshold, theta
         self.rel_tol, self.max_iters, self.check_every = rel_tol, max_iters, check_every
@@ -55,7 +57,7 @@ class CoarseningStep:
             self.x = torch.empty((int(n * 1.25) + 16, 3), dtype=torch.float64, device=cs.val.device)
         x = self.x[:n]
         _, st = pcg_solve(self.h, cs.row_ptr, cs.col, cs.val, cs.g_c, x, self.rel_tol, self.max_iters,
-                          self.check_every, zero_x0=True)
+                          self.check_every, zero_x0=True, storage=self.pcg_storage)
         return x, st
 
     def refine(self, cs, y_c, g_fine):
