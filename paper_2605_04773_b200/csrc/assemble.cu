@@ -945,8 +945,8 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
 #define LSTAGE 256
 
-template <int NCB>
-__global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
+template <int NCB, int NB>
+__global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE];
   __shared__ int s_i[4][LSTAGE];     // child slot c of the entry's row (weights in s_wc)
@@ -1033,25 +1033,27 @@ __global__ void __launch_bounds__(128, 4) k_num_large(LargeArgs A) {
         icnt += __popc(mi);
       }
       __syncwarp();
-      for (int d = gq; d < cnt; d += 2 * G) {  // two diagonal blocks per group in flight
-        const bool two = d + G < cnt;
-        const int d1 = two ? d + G : d;
-        const long long k0 = s_k[w][d], k1 = s_k[w][d1];
-        double B0[9], B1[9];
+      for (int d = gq; d < cnt; d += NB * G) {  // NB diagonal blocks per group in flight
+        double Bv[NB][9], wi[NB];
+        int dd[NB];
 #pragma unroll
-        for (int x = 0; x < 9; ++x) {
-          B0[x] = __ldg(A.val + 9 * k0 + x);
-          B1[x] = __ldg(A.val + 9 * k1 + x);
+        for (int u = 0; u < NB; ++u) {
+          const bool ok = d + u * G < cnt;
+          dd[u] = ok ? d + u * G : d;
+          const long long kk = s_k[w][dd[u]];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) Bv[u][x] = __ldg(A.val + 9 * kk + x);
+          wi[u] = !ok ? 0.0 : (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][dd[u]]][p];
         }
-        const double wi0 = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d]][p];
-        const double wi1 = !two ? 0.0 : (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d1]][p];
 #pragma unroll
         for (int qq = 0; qq < QN; ++qq) {
           const int q = q0 + qq;
-          const double c0 = wi0 * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][d][q]);
-          const double c1 = wi1 * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][d1][q]);
 #pragma unroll
-          for (int x = 0; x < 9; ++x) acc[qq][x] += c0 * B0[x] + c1 * B1[x];
+          for (int u = 0; u < NB; ++u) {
+            const double c = wi[u] * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][dd[u]][q]);
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[qq][x] += c * Bv[u][x];
+          }
         }
       }
       __syncwarp();
@@ -1341,7 +1343,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
-  LAUNCH(h, k_num_large<4>, glarge, 128, 0, LA);
-  if (hsc->n_large3 > 0) LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
+  // 2 diagonal blocks per group in flight: 3 or 4 (at 3 CTAs/SM) measured slower, 1.63 / 1.61 vs
+  // 1.51 ms numeric at C3 (profiles/r01h/bench_nb*.jsonl)
+  LAUNCH(h, (k_num_large<4, 2>), glarge, 128, 0, LA);
+  if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large<1, 2>), glarge, 128, 0, LA);
   return AGIPC_OK;
 }

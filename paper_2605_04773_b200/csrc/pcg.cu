@@ -789,7 +789,42 @@ struct PcgBufs {
   double *ytin = nullptr, *yext = nullptr;
   int all_red = 0;
   int upd_u = 1;  // slots per K2 thread pass
+  double *arena = nullptr;  // x, r, z, p0, p1, qseg, Dinv (+ ytin, yext): one L2 window
+  size_t arena_bytes = 0;
 };
+
+
+// L2 residency of the PCG vectors (B200: 126 MB L2).  The matrix is streamed with evict-first
+// loads; the vector arena gets a persisting access-policy window on the solve stream (the
+// captured kernel nodes inherit it).  AGIPC_L2_WINDOW=0 disables it (A/B runs).  Sets the
+// device's persisting-L2 limit (cudaLimitPersistingL2CacheSize) to the window size.
+static void pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size_t bytes) {
+  const char *e = getenv("AGIPC_L2_WINDOW");
+  const bool on = !(e && atoi(e) == 0) && base && bytes > 0;
+  cudaStreamAttrValue v;
+  memset(&v, 0, sizeof(v));
+  if (on) {
+    int max_win = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+    if (max_win <= 0 || max_persist <= 0) {
+      cudaGetLastError();
+      return;
+    }
+    const size_t win = std::min(bytes, (size_t)max_win);
+    const size_t persist = std::min(win, (size_t)max_persist);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)win);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+}
 
 // iteration j reads p_old = P[j&1] and writes p_new = P[(j+1)&1] (the chunk length is even)
 static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int64_t n, const PcgBufs &B,
@@ -841,13 +876,23 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   const int64_t nv_bound = n + (A->nnzb + nh) / SEG_MAX + (Ah ? n : 0) + 1;  // virtual rows
   const int64_t nx = n + n_gs;  // owned + ghost slots (z and p carry the ghost region)
   B.ns_bound = cdiv(nv_bound, 32);
-  WS(h, xw, double, "pcg_x", 3 * n + 2); B.x = xw;
-  WS(h, r, double, "pcg_r", 3 * n + 2); B.r = r;
-  WS(h, z, double, "pcg_z", 3 * nx + 2); B.z = z;
-  WS(h, p0, double, "pcg_p0", 3 * nx + 2); B.P[0] = p0;
-  WS(h, p1, double, "pcg_p1", 3 * nx + 2); B.P[1] = p1;
-  WS(h, qs, double, "pcg_qseg", 3 * nv_bound + 2); B.qseg = qs;
-  WS(h, Dinv, double, "pcg_dinv", 9 * n + 2); B.Dinv = Dinv;
+  // the per-iteration vectors live in one arena so that one L2 access-policy window (persisting)
+  // covers them: the SpMV streams the matrix with evict-first loads, K2 and the gathers then hit
+  // L2 instead of HBM (pcg_l2_window)
+  {
+    const int64_t len[9] = {3 * n + 2, 3 * n + 2, 3 * nx + 2, 3 * nx + 2, 3 * nx + 2, 3 * nv_bound + 2, 9 * n + 2,
+                            storage != AGIPC_STORAGE_FULL ? 3 * n + 2 : 0, storage != AGIPC_STORAGE_FULL ? 3 * n + 2 : 0};
+    int64_t off[10];
+    off[0] = 0;
+    for (int i = 0; i < 9; ++i) off[i + 1] = off[i] + ((len[i] + 31) & ~(int64_t)31);  // 256-B aligned
+    WS(h, arena, double, "pcg_vec_arena", off[9]);
+    B.x = arena + off[0]; B.r = arena + off[1]; B.z = arena + off[2];
+    B.P[0] = arena + off[3]; B.P[1] = arena + off[4]; B.qseg = arena + off[5]; B.Dinv = arena + off[6];
+    B.ytin = len[7] ? arena + off[7] : nullptr;
+    B.yext = len[8] ? arena + off[8] : nullptr;
+    B.arena = arena;
+    B.arena_bytes = sizeof(double) * (size_t)off[9];
+  }
   WS(h, vr, int64_t, "pcg_vr_ptr", n + 1); B.vr_ptr = vr;
   WS(h, nseg, int32_t, "pcg_nseg", n);
   WS(h, vrow, int32_t, "pcg_v_row", nv_bound); B.v_row = vrow;
@@ -865,12 +910,9 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaFuncSetAttribute(k_spmv_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sym, PCG_THREADS, smem));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nv_bound, B.win), (int64_t)std::max(1, occ) * h->sm_count));
-    WS(h, yt, double, "pcg_ytin", 3 * n + 2); B.ytin = yt;
-    WS(h, ye, double, "pcg_yext", 3 * n + 2); B.yext = ye;
   } else {
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
-    B.ytin = B.yext = nullptr;
   }
   // K2: 2 CTAs per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl: 3-8 CTAs per SM
   // or 2 slots per pass are not faster)
@@ -970,6 +1012,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     }
     int chunk = std::max(2, std::min(check_every, max_iters));
     chunk += chunk & 1;  // even: the p ping-pong parity is the same at every graph launch
+    pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);
     const void *key[8] = {B.sval, B.scol, B.x, B.qseg, B.Dinv, B.sptr, B.P[0], B.parts};
     bool same = g->exec && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
                 g->grid2 == B.G2 && g->prof == h->prof && g->sym == B.sym && g->win == B.win && g->yext == B.yext &&

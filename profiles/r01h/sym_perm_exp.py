@@ -50,6 +50,20 @@ def main():
     st = CoarseningStep(h, dm, t(m.bsr_ptr, torch.int64), t(m.bsr_col, torch.int32), t(H, torch.float64))
     _, info, cs = st.coarsen(t(c["x_prev"], torch.float64), t(c["x_cur"], torch.float64), t(g, torch.float64))
     systems = {"slot_order": (cs.row_ptr, cs.col, cs.val, cs.g_c), "locality_order": permuted(cs, m.n_nodes)}
+    if "--full" in sys.argv:  # full storage, slot order (A/B of environment settings per process)
+        rp, col, val, b = systems["slot_order"]
+        x = torch.empty_like(b)
+        P.pcg_solve(h, rp, col, val, b, x, 0.0, 64, 32, zero_x0=True)
+        h.profile(True)
+        for _ in range(3):
+            _, s = P.pcg_solve(h, rp, col, val, b, x, 0.0, 256, 32, zero_x0=True)
+        pr = h.profile_read()
+        h.profile(False)
+        sp, up, so = pr["pcg_spmv"], pr["pcg_update"], pr["pcg_solve"]
+        print(json.dumps({"l2_window": os.environ.get("AGIPC_L2_WINDOW", "1"),
+                          "spmv_us": round(1e3 * sp[1] / sp[0], 2), "update_us": round(1e3 * up[1] / up[0], 2),
+                          "us_per_iter": round(1e3 * so[1] / (3 * 256), 2)}), flush=True)
+        return
     if "--update" in sys.argv:  # K2 launch shape sweep (full storage, slot order)
         rp, col, val, b = systems["slot_order"]
         for ctas in ("2", "3", "4", "8"):
