@@ -65,6 +65,8 @@ void pcg_graph_free(PcgGraph *g) {
 }
 
 // Block-wide sum of one double (fixed order: warp shuffles then warp 0), result in thread 0.
+// NT = threads per CTA (s_red holds NT / 32 entries).
+template <int NT = PCG_THREADS>
 __device__ __forceinline__ double block_sum(double v, double *s_red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -72,7 +74,7 @@ __device__ __forceinline__ double block_sum(double v, double *s_red) {
   __syncthreads();
   double r = 0.0;
   if (w == 0) {
-    r = l < PCG_WARPS ? s_red[l] : 0.0;
+    r = l < NT / 32 ? s_red[l] : 0.0;
     r = warp_sum(r);
   }
   __syncthreads();
@@ -95,10 +97,11 @@ __device__ __forceinline__ bool last_block(PcgState *st) {
 }
 
 // fixed-order reduction of nparts partials by one CTA
+template <int NT = PCG_THREADS>
 __device__ __forceinline__ double reduce_parts(const double *parts, int nparts, double *s_red) {
   double v = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += PCG_THREADS) v += __ldcg(parts + i);
-  return block_sum(v, s_red);
+  for (int i = threadIdx.x; i < nparts; i += NT) v += __ldcg(parts + i);
+  return block_sum<NT>(v, s_red);
 }
 
 __device__ __forceinline__ void dinv_apply(const double *__restrict__ D, const double r0, const double r1,
@@ -676,8 +679,8 @@ __global__ void __launch_bounds__(PCG_THREADS, 2) k_spmv_sym(const int64_t *__re
 // z = D^-1 r; last CTA: ||r|| <= tol ||b||, iteration count, beta.  Each thread takes U
 // slots per pass and issues all their independent loads before the arithmetic (the kernel is
 // latency-bound at 2 CTAs per SM, the grid size that keeps the last-block reduction cheap).
-template <int U>
-__global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t *__restrict__ vr_ptr,
+template <int U, int NT = PCG_THREADS>
+__global__ void __launch_bounds__(NT) k_update(int64_t n, const int64_t *__restrict__ vr_ptr,
                                                         double *__restrict__ x, double *__restrict__ r,
                                                         double *__restrict__ z, const double *__restrict__ p,
                                                         const double *__restrict__ qseg,
@@ -685,12 +688,12 @@ __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t
                                                         double *parts, PcgState *st, double *red,
                                                         const double *__restrict__ ytin, double *__restrict__ yext) {
   if (*(volatile int *)&st->done) return;
-  __shared__ double s_red[PCG_WARPS];
+  __shared__ double s_red[NT / 32];
   const double alpha = st->alpha;
   if (blockIdx.x == 0 && threadIdx.x == 0) *next_counter = 0;
   double rz = 0.0, rr = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * PCG_THREADS;
-  for (int64_t i0 = (int64_t)blockIdx.x * PCG_THREADS + threadIdx.x; i0 < n; i0 += U * stride) {
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  for (int64_t i0 = (int64_t)blockIdx.x * NT + threadIdx.x; i0 < n; i0 += U * stride) {
     int64_t v0[U], v1[U];
     double q[U][3], xv[U][3], rv[U][3], pv[U][3], D[U][9];
 #pragma unroll
@@ -742,15 +745,15 @@ __global__ void __launch_bounds__(PCG_THREADS) k_update(int64_t n, const int64_t
     }
   }
   const int G = gridDim.x;
-  rz = block_sum(rz, s_red);
-  rr = block_sum(rr, s_red);
+  rz = block_sum<NT>(rz, s_red);
+  rr = block_sum<NT>(rr, s_red);
   if (threadIdx.x == 0) {
     parts[G + blockIdx.x] = rz;
     parts[2 * G + blockIdx.x] = rr;
   }
   if (last_block(st)) {
-    double RZ = reduce_parts(parts + G, G, s_red);
-    double RR = reduce_parts(parts + 2 * G, G, s_red);
+    double RZ = reduce_parts<NT>(parts + G, G, s_red);
+    double RR = reduce_parts<NT>(parts + 2 * G, G, s_red);
     if (threadIdx.x == 0 && red) {
       red[0] = RZ; red[1] = RR;
     } else if (threadIdx.x == 0) {
@@ -841,8 +844,7 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
       k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z,
                                                pold, pnew, B.qseg, B.counters + (k & 1), B.parts, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
-    auto k2 = B.upd_u == 2 ? k_update<2> : k_update<1>;
-    k2<<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
+    k_update<1, PCG_THREADS><<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
                                           B.parts, B.st, nullptr, B.ytin, B.yext);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 2], s, cudaEventRecordExternal);
   }
@@ -914,8 +916,8 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
   }
-  // K2: 2 CTAs per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl: 3-8 CTAs per SM
-  // or 2 slots per pass are not faster)
+  // K2: 2 CTAs of 256 threads per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl,
+  // upd_nt.jsonl: 3-8 CTAs per SM, 2 slots per pass or 512-thread CTAs are not faster)
   B.upd_u = 1;
   B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 2 * (int64_t)h->sm_count));
   const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
@@ -1262,7 +1264,7 @@ extern "C" agipc_status agipc_dpcg_update(agipc_handle h, double *red) {
   double *pnew = B.P[(d->k + 1) & 1];
   ProfScope prof(h, PROF_PCG_UPDATE, h->stream);
   LAUNCH(h, k_dscalars, 1, 1, 0, B.st, (const double *)red, (int)DP_ALPHA);
-  LAUNCH(h, k_update<1>, (unsigned)B.G2, PCG_THREADS, 0, d->n, B.vr_ptr, B.x, B.r, B.z, (const double *)pnew, B.qseg,
+  LAUNCH(h, (k_update<1, PCG_THREADS>), (unsigned)B.G2, PCG_THREADS, 0, d->n, B.vr_ptr, B.x, B.r, B.z, (const double *)pnew, B.qseg,
          B.Dinv, B.counters + ((d->k + 1) & 1), B.parts, B.st, red, (const double *)nullptr, (double *)nullptr);
   d->k += 1;
   d->pending = DP_UPDATE;
