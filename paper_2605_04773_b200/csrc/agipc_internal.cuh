@@ -41,6 +41,8 @@ enum ProfPhase {
   PROF_PROLONG,
   PROF_DIST,
   PROF_TRIPLETS,
+  PROF_MAP_LEVEL0,
+  PROF_MAP_TAIL,
   PROF_N
 };
 
@@ -59,6 +61,7 @@ struct agipc_handle_s {
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
+  size_t tail_smem = 0;  // build_map: dynamic smem the tail kernel attribute allows (set once)
   struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;

@@ -97,7 +97,7 @@ static void prof_flush(agipc_handle h) {
 static const char *kPhaseNames[PROF_N] = {"tag_edges", "build_map", "assemble_coarse", "pcg_setup",
                                           "pcg_spmv", "pcg_update", "pcg_solve",
                                           "asm_classify", "asm_symbolic", "asm_numeric",
-                                          "prolongate", "dist_halo", "triplets"};
+                                          "prolongate", "dist_halo", "triplets", "map_level0", "map_tail"};
 
 extern "C" {
 

@@ -19,6 +19,8 @@
 //    trip per level; the recursion stops at the first level without an intra-group edge.
 #include <cooperative_groups.h>
 
+#include <memory>
+
 #include "agipc_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -544,10 +546,13 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   int *tile_counter = (int *)(status + tiles0 + 1);
 
   // ---- level 0: warp-per-group hashing over the fine mesh (fused look-back scan) ----
+  std::unique_ptr<ProfScope> ps_l0(new ProfScope(h, PROF_MAP_LEVEL0, s0));
   LAUNCH(h, k_level0, (unsigned)tiles0, MAP_THREADS, 0, N, geo, mesh->adj_ptr, mesh->adj_nbr, slot_tags, map, cross,
          &sc->cross, status, tile_counter, &sc->nvals[0]);
 
+  ps_l0.reset();
   // ---- levels >= 1: one cooperative persistent kernel ----
+  std::unique_ptr<ProfScope> ps_tail;
   if (max_levels != 1) {
     WS(h, EA, int2, "map_EA", ecap);
     WS(h, EB, int2, "map_EB", ecap);
@@ -590,16 +595,23 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     A.level_n = sc->level_n;
     const size_t smem = sizeof(int32_t) * (size_t)tiles_max;
     if (smem > 200 * 1024) return set_err(h, AGIPC_ERANGE, "build_map: %lld nodes exceed the tail kernel", (long long)N);
-    CU_TRY(h, cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tail, TAIL_THREADS, smem));
-    if (occ < 1) return set_err(h, AGIPC_ECUDA, "build_map: tail kernel cannot be resident");
+    if (smem > h->tail_smem) {  // host-side attribute + residency check once per size (they cost
+      // tens of microseconds of host time while the GPU waits for the cooperative launch)
+      const size_t want = std::max(smem, (size_t)16 * 1024);
+      CU_TRY(h, cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+      int occ = 0;
+      CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tail, TAIL_THREADS, want));
+      if (occ < 1) return set_err(h, AGIPC_ECUDA, "build_map: tail kernel cannot be resident");
+      h->tail_smem = want;
+    }
     const int grid = h->sm_count;  // one CTA per SM: cheap grid barriers
     void *args[] = {&A};
     cudaError_t pre = cudaGetLastError();
     if (pre != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pending CUDA error before k_tail: %s", cudaGetErrorString(pre));
+    ps_tail.reset(new ProfScope(h, PROF_MAP_TAIL, s0));
     CU_TRY(h, cudaLaunchCooperativeKernel((const void *)k_tail, grid, TAIL_THREADS, args, smem, s0));
     h->launches += 1;
+    ps_tail.reset();
     LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl);
   }
   if (agg_size) {
