@@ -548,7 +548,8 @@ template <int SEG, bool NUMERIC>
 __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   constexpr int NSEG = 32 / SEG;
   __shared__ ChildTab s_tab[8 * NSEG];
-  __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][9];  // numeric: per-lane parked block
+  // numeric: per-lane parked block B_ij (9), X_bar of its row child (3) and of its column node (3)
+  __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][15];
   __shared__ int2 s_pb[NUMERIC ? 1 : 8][NUMERIC ? 1 : PAIR_BUF];  // symbolic: buffered pairs
   int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
@@ -620,43 +621,60 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const int Ub = A.nb_cnt[bs];
       mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
     }
+    // park B and the affine coordinates once; a run of one entry (the common case) never reads
+    // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
+    const int h0 = sg * SEG + hl;
+    const bool multi = __ballot_sync(FULL_MASK, tail && h0 != l) != 0u;  // warp-uniform
+    if (multi) {
+#pragma unroll
+      for (int x = 0; x < 9; ++x) s_v[w][l][x] = B[x];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s_v[w][l][9 + c] = (valid && ncb_a == 4) ? __ldg(A.X + 3 * (int64_t)si + c) : 0.0;
+        s_v[w][l][12 + c] = (valid && ncb_b == 4) ? __ldg(A.X + 3 * (int64_t)sj + c) : 0.0;
+      }
+    }
+    __syncwarp();
     for (int p = 0; p < PA; ++p) {
       const bool pv = p < ncb_a;
-      const double wi = (valid && pv) ? wgt(A.X, si, ncb_a, p) : 0.0;
       const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
       for (int q = 0; q < Q; ++q) {
-        const double coef = (valid && pv && q < ncb_b) ? wi * wgt(A.X, sj, ncb_b, q) : 0.0;
-        // run sums: every lane parks coef * B in shared memory, the tail lane of each run adds
-        // its run (head .. tail, short) in lane order
-#pragma unroll
-        for (int x = 0; x < 9; ++x) s_v[w][l][x] = coef * B[x];
-        __syncwarp();
+        if (!(tail && pv && q < ncb_b)) continue;
+        // coef = w_i[p] w_j[q] (Eq 4), the same product order as the oracle's weights
+        const double coef = wgt(A.X, si, ncb_a, p) * wgt(A.X, sj, ncb_b, q);
         double v[9];
-        if (tail) {
-          const int h0 = sg * SEG + hl;
+        if (h0 == l) {
 #pragma unroll
-          for (int x = 0; x < 9; ++x) v[x] = s_v[w][h0][x];
-          for (int t = h0 + 1; t <= l; ++t)
+          for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+        } else {
+          for (int t = h0; t <= l; ++t) {
+            const double wit = (ncb_a == 4 && p < 3) ? s_v[w][t][9 + p] : 1.0;
+            const double wjt = (ncb_b == 4 && q < 3) ? s_v[w][t][12 + q] : 1.0;
+            const double ct = wit * wjt;
+            if (t == h0) {
 #pragma unroll
-            for (int x = 0; x < 9; ++x) v[x] += s_v[w][t][x];
-        }
-        __syncwarp();
-        if (tail && pv && q < ncb_b) {
-          const long long pos = rs + cp + q;
-          A.ccol[pos] = slot_of(bs, q, n3);
-          double *dst = A.cval + 9 * pos;
+              for (int x = 0; x < 9; ++x) v[x] = ct * s_v[w][t][x];
+            } else {
 #pragma unroll
-          for (int x = 0; x < 9; ++x) dst[x] = v[x];
-          if (mbase >= 0) {
-            double *mt = A.cval + 9 * (A.crp[slot_of(bs, q, n3)] + mbase + p);
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
+              for (int x = 0; x < 9; ++x) v[x] += ct * s_v[w][t][x];
+            }
           }
+        }
+        const long long pos = rs + cp + q;
+        A.ccol[pos] = slot_of(bs, q, n3);
+        double *dst = A.cval + 9 * pos;
+#pragma unroll
+        for (int x = 0; x < 9; ++x) dst[x] = v[x];
+        if (mbase >= 0) {
+          double *mt = A.cval + 9 * (A.crp[slot_of(bs, q, n3)] + mbase + p);
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
         }
       }
     }
+    __syncwarp();
     if (A.g_f) {  // g_c[slot(a,p)] = sum over the children of w_i[p] g_f[i]
       for (int p = 0; p < PA; ++p) {
         double g0 = 0, g1 = 0, g2 = 0;
