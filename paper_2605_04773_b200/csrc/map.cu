@@ -313,12 +313,13 @@ __global__ void k_clear_slots(const unsigned long long *__restrict__ ne_ptr, con
 
 #define TAIL_THREADS 1024
 #define TAIL_WARPS (TAIL_THREADS / 32)
+#define TAIL_SUB 2  // group blocks per warp per tile (a tile = TAIL_WARPS * TAIL_SUB * gpw * gs nodes)
 
 struct TailArgs {
   GroupGeom geo;
   int max_levels;
   int64_t N;
-  int tile_nodes;          // nodes per tile = TAIL_WARPS * gpw * gs
+  int tile_nodes;          // nodes per tile = TAIL_WARPS * TAIL_SUB * gpw * gs
   int2 *E[2];
   unsigned long long *ne;  // [2] edge counts of E[0], E[1]; ne[0] = level-1 edges on entry
   uint32_t *h;             // [>= n1], zero on entry
@@ -391,23 +392,33 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
     // ---- P2: Alg S1/S2 per tile (closure, election, tile-local rank); clears the hashes ----
     const int64_t ntiles = (n + TN - 1) / TN;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int64_t v = ((t * TAIL_WARPS + w) * geo.gpw + gin) * gs + lig;
-      const bool active = (gin < geo.gpw) && (v < n);
-      uint32_t hv = 0;
-      if (active) {
-        hv = (1u << lig) | A.h[v];
-        A.h[v] = 0u;
+      // a warp takes TAIL_SUB consecutive blocks of gpw groups (all hashes loaded up front)
+      int64_t v[TAIL_SUB];
+      bool active[TAIL_SUB];
+      uint32_t hv[TAIL_SUB];
+#pragma unroll
+      for (int r = 0; r < TAIL_SUB; ++r) {
+        v[r] = (((t * TAIL_WARPS + w) * TAIL_SUB + r) * geo.gpw + gin) * gs + lig;
+        active[r] = (gin < geo.gpw) && (v[r] < n);
+        hv[r] = active[r] ? (1u << lig) | A.h[v[r]] : 0u;
       }
-      for (int k = 0; k < gs; ++k) {
-        const uint32_t tt = __shfl_sync(FULL_MASK, hv, (base_lane + k) & 31);
-        if ((hv >> k) & 1u) hv |= tt;
+      int local[TAIL_SUB], wcount = 0;
+#pragma unroll
+      for (int r = 0; r < TAIL_SUB; ++r) {
+        if (active[r]) A.h[v[r]] = 0u;
+        uint32_t x = hv[r];
+        for (int k = 0; k < gs; ++k) {
+          const uint32_t tt = __shfl_sync(FULL_MASK, x, (base_lane + k) & 31);
+          if ((x >> k) & 1u) x |= tt;
+        }
+        const bool elected = active[r] && ((x & ((1u << lig) - 1u)) == 0u);
+        const unsigned bal = __ballot_sync(FULL_MASK, elected);
+        const unsigned gelect = (bal >> base_lane) & geo.gmask;
+        const int first = active[r] ? __ffs(x) - 1 : 0;
+        local[r] = wcount + __popc(gelect & ((1u << first) - 1u)) + __popc(bal & ((1u << base_lane) - 1u));
+        wcount += __popc(bal);
       }
-      const bool elected = active && ((hv & ((1u << lig) - 1u)) == 0u);
-      const unsigned bal = __ballot_sync(FULL_MASK, elected);
-      const unsigned gelect = (bal >> base_lane) & geo.gmask;
-      const int first = active ? __ffs(hv) - 1 : 0;
-      const int local = __popc(gelect & ((1u << first) - 1u)) + __popc(bal & ((1u << base_lane) - 1u));
-      if (lane == 0) s_w[w] = __popc(bal);
+      if (lane == 0) s_w[w] = wcount;
       __syncthreads();
       if (w == 0) {
         const int c = s_w[lane];
@@ -416,7 +427,9 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         if (lane == 31) A.tcount[t] = ci;
       }
       __syncthreads();
-      if (active) A.mk[v] = s_w[w] + local;
+#pragma unroll
+      for (int r = 0; r < TAIL_SUB; ++r)
+        if (active[r]) A.mk[v[r]] = s_w[w] + local[r];
       __syncthreads();
     }
     if (gtid == 0) A.ne[1 - cur] = 0;
@@ -465,9 +478,15 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       if (keep) Eo[pos] = o;
     }
     if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
-    for (int64_t c = gtid; c < n1; c += gstride) {
-      const int32_t u = level == 2 ? (int32_t)c : A.comp[c];
-      A.comp[c] = s_pref[u / TN] + A.mk[u];
+    for (int64_t c = gtid; c < n1; c += 2 * gstride) {  // two independent gathers in flight
+      const int64_t c1 = c + gstride;
+      const bool two = c1 < n1;
+      const int32_t u0 = level == 2 ? (int32_t)c : A.comp[c];
+      const int32_t u1 = !two ? 0 : level == 2 ? (int32_t)c1 : A.comp[c1];
+      const int32_t m0 = A.mk[u0];
+      const int32_t m1 = two ? A.mk[u1] : 0;
+      A.comp[c] = s_pref[u0 / TN] + m0;
+      if (two) A.comp[c1] = s_pref[u1 / TN] + m1;
     }
     if (gtid == 0) {
       A.ctrl[fl] = 0;
@@ -560,7 +579,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     WS(h, hh, uint32_t, "map_h", N);
     WS(h, mk, int32_t, "map_mk", N);
     WS(h, comp, int32_t, "map_comp", N);
-    const int tile_nodes = TAIL_WARPS * geo.gpw * geo.gs;
+    const int tile_nodes = TAIL_WARPS * TAIL_SUB * geo.gpw * geo.gs;
     const int64_t tiles_max = cdiv(N, tile_nodes) + 1;
     WS(h, tcount, int32_t, "map_tcount", tiles_max);
     // hash set for the level-1 edge de-duplication (zeroed once; used slots are cleared after use)
