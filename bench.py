@@ -287,38 +287,64 @@ def run_agipc(args, world, rank, local_rank):
         step2 = CoarseningStep(h, dm, Hrp, Hcol, dH, check_every=args.check_every)
         copy_s = torch.cuda.Stream()
         h_ready = torch.cuda.Event()
+        # the paper's symmetric storage: the host holds the diagonal + upper blocks of
+        # H_f (a selection of the synthetic input); the static upper pattern is uploaded once,
+        # the values every step, and agipc_bsr_expand_upper rebuilds the full rows on the device
+        brow = np.repeat(np.arange(m.n_nodes), np.diff(m.bsr_ptr))
+        upper = m.bsr_col >= brow
+        hHu = pin(H[upper])
+        Urp = t(np.concatenate([[0], np.cumsum(np.bincount(brow[upper], minlength=m.n_nodes))]), torch.int64)
+        Ucol = t(m.bsr_col[upper], torch.int32)
+        dHu = torch.empty(tuple(hHu.shape), dtype=torch.float64, device=dev)
+        dHu.copy_(hHu)
+        P.bsr_expand_upper(h, Hrp, Hcol, Urp, Ucol, dHu, out=dH, check=True)  # pattern validated once
         ne = args.e2e_steps or args.steps
-        e2e_t = []
-        bi = bo = 0
-        for s in range(ne + 1):
-            flush.zero_()
-            k = s % 10
-            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            # H_f and g_f upload on a copy stream, overlapped with steps 1-2 (which do not read
-            # them); the assembly waits for it.  Inside the timed region either way.
-            copy_s.wait_event(e0)
-            with torch.cuda.stream(copy_s):
-                dH.copy_(hH, non_blocking=True); dg.copy_(hg, non_blocking=True)
-                h_ready.record(copy_s)
-            dxp.copy_(hx, non_blocking=True); dxc.copy_(hxc[k], non_blocking=True)
-            _, _, cs = step2.coarsen(dxp, dxc, dg, hessian_ready=h_ready)
-            if hgc.shape[0] < cs.n_slots:
-                hgc = torch.empty((cs.n_slots, 3), dtype=torch.float64).pin_memory()
-            hgc[:cs.n_slots].copy_(cs.g_c, non_blocking=True)
-            e1.record()
-            torch.cuda.synchronize()
-            if s > 0:  # the first e2e step re-sizes step2's buffers
-                e2e_t.append(e0.elapsed_time(e1))
-                bi = (hx.numel() + hxc[k].numel() + hH.numel() + hg.numel()) * 8
-                bo = cs.n_slots * 24
-        ev2 = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ev2, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(float(ev2.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
+
+        def e2e_run(sym_upload):
+            nonlocal hgc
+            times, bi, bo = [], 0, 0
+            for s in range(ne + 1):
+                flush.zero_()
+                k = s % 10
+                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                # H_f and g_f upload on a copy stream, overlapped with steps 1-2 (which do not
+                # read them); the assembly waits for it.  Inside the timed region either way.
+                copy_s.wait_event(e0)
+                with torch.cuda.stream(copy_s):
+                    h.sync_stream(copy_s)
+                    if sym_upload:
+                        dHu.copy_(hHu, non_blocking=True)
+                        P.bsr_expand_upper(h, Hrp, Hcol, Urp, Ucol, dHu, out=dH, check=False)
+                    else:
+                        dH.copy_(hH, non_blocking=True)
+                    dg.copy_(hg, non_blocking=True)
+                    h_ready.record(copy_s)
+                h.sync_stream()
+                dxp.copy_(hx, non_blocking=True); dxc.copy_(hxc[k], non_blocking=True)
+                _, _, cs = step2.coarsen(dxp, dxc, dg, hessian_ready=h_ready)
+                if hgc.shape[0] < cs.n_slots:
+                    hgc = torch.empty((cs.n_slots, 3), dtype=torch.float64).pin_memory()
+                hgc[:cs.n_slots].copy_(cs.g_c, non_blocking=True)
+                e1.record()
+                torch.cuda.synchronize()
+                if s > 0:  # the first e2e step re-sizes step2's buffers
+                    times.append(e0.elapsed_time(e1))
+                    bi = (hx.numel() + hxc[k].numel() + (hHu.numel() if sym_upload else hH.numel()) + hg.numel()) * 8
+                    bo = cs.n_slots * 24
+            ev2 = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(ev2, op=dist.ReduceOp.MAX)
+            return float(ev2.item()), bi, bo
+
+        v_full, bi_full, _ = e2e_run(False)
+        v_sym, bi, bo = e2e_run(True)
+        e2e = {"value": round(v_sym, 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
                "d2h_bytes_per_step": int(bo),
-               "scope": "H2D(x_prev, x_cur, H_f, g_f) + tag + map + assemble + D2H(g_c), pinned host memory; "
-                        "the H_f/g_f upload runs on a copy stream overlapped with tag + map"}
+               "scope": "H2D(x_prev, x_cur, H_f in symmetric (diagonal + upper) storage P:1126, g_f) + "
+                        "agipc_bsr_expand_upper + tag + map + assemble + D2H(g_c), pinned host memory; the "
+                        "H_f/g_f upload and expansion run on a copy stream overlapped with tag + map",
+               "full_storage_upload": {"value": round(v_full, 3), "h2d_bytes_per_step": int(bi_full)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -236,6 +236,16 @@ AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const
 #define AGIPC_STORAGE_UPPER 2
 AGIPC_API agipc_status agipc_bsr_upper(agipc_handle h, const agipc_bsr *A, int64_t cap_nnzb, int64_t *row_ptr,
                                        int32_t *col, double *val, int64_t *nnzb_upper /*[host]*/);
+/* agipc_bsr_expand_upper: the fine Hessian arrives in symmetric storage and the
+ *   assembly reads full rows: val (out, [full->nnzb][3][3]) on the full pattern (full->row_ptr,
+ *   full->col; full->val unused) gets U_ij for col >= row and U_ji^T below the diagonal.  The
+ *   full pattern must be the symmetric closure of U's (same column order, every diagonal
+ *   block stored first in its U row).  check != 0: the kernel counts pattern mismatches and
+ *   the call synchronises the stream and returns EINVAL if any (val is then unreliable);
+ *   check == 0: no host round trip (for a pattern pair validated once -- the topology is
+ *   static), mismatching blocks are skipped silently. */
+AGIPC_API agipc_status agipc_bsr_expand_upper(agipc_handle h, const agipc_bsr *full, const agipc_bsr *U, double *val,
+                                              int check);
 AGIPC_API agipc_status agipc_pcg_solve_sym(agipc_handle h, const agipc_bsr *A, int storage, const double *b,
                                            double *x, int zero_x0, double rel_tol, int max_iters,
                                            int check_every, agipc_pcg_stats *stats);

@@ -54,6 +54,8 @@ def lib():
         L.orc_bsr_upper.restype = i64
         L.orc_spmv_upper.argtypes = [i64, P, P, P, P, P]
         L.orc_spmv_upper.restype = None
+        L.orc_bsr_expand_upper.argtypes = [i64, P, P, P, P, P, P]
+        L.orc_bsr_expand_upper.restype = i64
         L.orc_block_jacobi.argtypes = [i64, P, P, P, P, P]
         L.orc_block_jacobi.restype = i32
         L.orc_prolongate.argtypes = [i64, P, i64, P, P, P]
@@ -212,6 +214,17 @@ def spmv_upper(urp, ucol, uval, x):
     y = np.empty(3 * n)
     lib().orc_spmv_upper(n, _p(rp), _p(cl), _p(vl), _p(_c(x, np.float64)), _p(y))
     return y.reshape(n, 3)
+
+
+def bsr_expand_upper(row_ptr, col, urp, ucol, uval):
+    """NEXT#2: full-storage values on the pattern (row_ptr, col) from upper storage.
+    Returns (val, number of full blocks without a source block)."""
+    rp = _c(row_ptr, np.int64); cl = _c(col, np.int32)
+    n = rp.shape[0] - 1
+    val = np.zeros((cl.shape[0], 3, 3))
+    miss = int(lib().orc_bsr_expand_upper(n, _p(rp), _p(cl), _p(_c(urp, np.int64)), _p(_c(ucol, np.int32)),
+                                          _p(_c(uval, np.float64)), _p(val)))
+    return val, miss
 
 
 def block_jacobi(row_ptr, col, val):

@@ -561,6 +561,28 @@ void orc_spmv_upper(int64_t n, const int64_t *urp, const int32_t *ucol, const do
     }
 }
 
+/* Full storage from upper storage (the inverse of orc_bsr_upper on a symmetric */
+/* pattern): full(i,j) = U(i,j) for j >= i and U(j,i)^T for j < i.  The full    */
+/* pattern (rp, col) is given; returns the number of full blocks with no source */
+/* in U (0 for a consistent pair of patterns).                                  */
+int64_t orc_bsr_expand_upper(int64_t n, const int64_t *rp, const int32_t *col, const int64_t *urp,
+                             const int32_t *ucol, const double *uval, double *val) {
+  int64_t missing = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int64_t j = col[e];
+      const int64_t r = j >= i ? i : j, c = j >= i ? j : i; /* stored as U(r, c) */
+      int64_t f = -1;
+      for (int64_t k = urp[r]; k < urp[r + 1]; ++k)
+        if (ucol[k] == c) { f = k; break; }
+      if (f < 0) { ++missing; memset(val + 9 * e, 0, 9 * sizeof(double)); continue; }
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          val[9 * e + 3 * a + b] = j >= i ? uval[9 * f + 3 * a + b] : uval[9 * f + 3 * b + a];
+    }
+  return missing;
+}
+
 /* ========================================================================== */
 /* NEXT#1 -- prolongation d_f = U^T d_c (main Sec 4.3: "we mathematically */
 /* prolongate the displacement to the fine mesh using the transpose of the     */

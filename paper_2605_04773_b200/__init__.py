@@ -82,7 +82,8 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_build_map", "agipc_assemble_coarse", "agipc_pcg_solve", "agipc_prolongate",
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
            "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
-           "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym"]
+           "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym",
+           "agipc_bsr_expand_upper"]
 
 
 def lib():
@@ -116,6 +117,7 @@ def lib():
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_pcg_solve_sym.argtypes = [P, C.POINTER(_Bsr), i32, P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_bsr_upper.argtypes = [P, C.POINTER(_Bsr), i64, P, P, P, C.POINTER(i64)]
+        L.agipc_bsr_expand_upper.argtypes = [P, C.POINTER(_Bsr), C.POINTER(_Bsr), P, i32]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
         L.agipc_triplet_plan.argtypes = [P, i64, i64, P, P, C.POINTER(_TripletPlan)]
@@ -366,6 +368,19 @@ def bsr_upper(h: Handle, row_ptr, col, val, cap_nnzb: int | None = None):
             continue
         h._check(st)
         return urp, ucol[:nb.value], uval[:nb.value]
+
+
+def bsr_expand_upper(h: Handle, row_ptr, col, u_row_ptr, u_col, u_val, out=None, check: bool = True):
+    """NEXT#2: full-storage values on the pattern (row_ptr, col) from the diagonal + upper
+    blocks (u_row_ptr, u_col, u_val) -- the symmetric storage of P:1126.  check=False skips the
+    pattern check and its host synchronisation (for a validated, static pattern).  Returns out."""
+    n = row_ptr.shape[0] - 1
+    if out is None:
+        out = torch.empty((col.shape[0], 3, 3), dtype=torch.float64, device=u_val.device)
+    full = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), None)
+    U = _Bsr(n, u_col.shape[0], _p(u_row_ptr), _p(u_col), _p(u_val))
+    h._check(lib().agipc_bsr_expand_upper(h._h, C.byref(full), C.byref(U), _p(out), int(bool(check))))
+    return out
 
 
 def prolongate(h: Handle, mesh: DeviceMesh, new_map, n3: int, n_slots: int, x_c, alpha: float = 1.0, out=None):

@@ -1376,3 +1376,89 @@ extern "C" agipc_status agipc_bsr_upper(agipc_handle h, const agipc_bsr *A, int6
          A->row_ptr, (const int64_t *)ub, A->col, A->val, (const int64_t *)row_ptr, col, val);
   return AGIPC_OK;
 }
+
+// ------------------------------------------------------------------------------------
+// NEXT#2 for the fine input: full-storage values from the diagonal + upper blocks (P:1126 --
+// the Hessian is produced and shipped in symmetric storage; the assembly reads full rows).
+// Warp per row i: the row's col >= i part is one contiguous run in both storages (flat,
+// coalesced copy); each strict-upper block U_ij is mirrored as U_ij^T into row j, found by a
+// binary search over row j's col < j part.  flags[0] counts pattern mismatches, flags[1] the
+// blocks written.
+// ------------------------------------------------------------------------------------
+__global__ void k_expand_upper(int64_t n, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                               const int64_t *__restrict__ urp, const int32_t *__restrict__ ucol,
+                               const double *__restrict__ uval, double *__restrict__ val,
+                               unsigned long long *flags) {
+  const int l = lane_id();
+  unsigned long long bad = 0, wrote = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t u0 = urp[i], ulen = urp[i + 1] - u0;
+    const int64_t flen = rp[i + 1] - rp[i];
+    const int64_t f0 = rp[i] + flen - ulen;  // where the row's col >= i part starts in full storage
+    if (ulen > flen) {
+      bad += l == 0;
+      continue;
+    }
+    for (int64_t k = l; k < 9 * ulen; k += 32) val[9 * f0 + k] = uval[9 * u0 + k];
+    for (int64_t e = l; e < ulen; e += 32) {
+      const int32_t j = ucol[u0 + e];
+      if (col[f0 + e] != j || j < i || (e == 0) != (j == i)) {
+        ++bad;
+        continue;
+      }
+      ++wrote;
+      if (j == i) continue;
+      // mirror: row j, column i, in the col < j part of row j
+      int64_t lo = rp[j], hi = rp[j] + (rp[j + 1] - rp[j]) - (urp[j + 1] - urp[j]);
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < i) lo = mid + 1; else hi = mid;
+      }
+      if (lo >= rp[j + 1] || col[lo] != i) {
+        ++bad;
+        continue;
+      }
+      ++wrote;
+      const double *s = uval + 9 * (u0 + e);
+      double *d = val + 9 * lo;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) d[3 * r + c] = s[3 * c + r];
+    }
+  }
+  bad = warp_sum(bad);
+  wrote = warp_sum(wrote);
+  if (l == 0) {
+    if (bad) atomicAdd(flags, bad);
+    if (wrote) atomicAdd(flags + 1, wrote);
+  }
+}
+
+extern "C" agipc_status agipc_bsr_expand_upper(agipc_handle h, const agipc_bsr *full, const agipc_bsr *U,
+                                               double *val, int check) {
+  if (!h) return AGIPC_EINVAL;
+  if (!full || !U || full->n_rows != U->n_rows || full->n_rows < 0)
+    return set_err(h, AGIPC_EINVAL, "bsr_expand_upper: bad arguments");
+  const int64_t n = full->n_rows;
+  if (n == 0) return AGIPC_OK;
+  if (!full->row_ptr || !U->row_ptr || (full->nnzb > 0 && (!full->col || !val)) || (U->nnzb > 0 && (!U->col || !U->val)))
+    return set_err(h, AGIPC_EINVAL, "bsr_expand_upper: null pointer");
+  CU_TRY(h, cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  WS(h, flags, unsigned long long, "expand_flags", 2);
+  CU_TRY(h, cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), s));
+  LAUNCH(h, k_expand_upper, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 16 * h->sm_count)), 256, 0,
+         n, full->row_ptr, full->col, U->row_ptr, U->col, U->val, val, flags);
+  if (!check) return AGIPC_OK;  // stream-ordered, no host round trip (pattern validated before)
+  agipc_status st;
+  unsigned long long *hf = (unsigned long long *)pinned_get(h, 2 * sizeof(unsigned long long), &st);
+  if (st != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemcpyAsync(hf, flags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CU_TRY(h, cudaStreamSynchronize(s));
+  if (hf[0] || (int64_t)hf[1] != full->nnzb)
+    return set_err(h, AGIPC_EINVAL, "bsr_expand_upper: patterns disagree (%llu mismatches, %llu of %lld blocks written)",
+                   hf[0], hf[1], (long long)full->nnzb);
+  return AGIPC_OK;
+}

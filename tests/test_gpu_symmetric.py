@@ -196,3 +196,39 @@ def test_pcg_sym_full_size(P, h, cfg):
     if cfg == "c2":
         check_solve(P, h, oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], P.STORAGE_SYM, 1e-3, band=True)
         check_solve(P, h, oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], P.STORAGE_UPPER, 1e-3, band=True)
+
+
+def test_bsr_expand_upper_bit_exact(P, h):
+    """Fine Hessians arrive in symmetric storage; the device expansion equals the
+    oracle's definition bit for bit and inverts agipc_bsr_upper."""
+    cases = []
+    for n in (10, 47):
+        m = synth.kuhn_grid(n)
+        cases.append((m.bsr_ptr, m.bsr_col, synth.fine_hessian(m)))
+    oa = coarse_c1(thr=5)
+    cases.append((oa["row_ptr"], oa["col"], oa["val"]))
+    cases.append(arrow_spd())
+    for rp, col, val in cases:
+        urp, ucol, uval = oracle.bsr_upper(rp, col, val)
+        ref, miss = oracle.bsr_expand_upper(rp, col, urp, ucol, uval)
+        assert miss == 0
+        drp, dcol = dev(rp, torch.int64), dev(col, torch.int32)
+        out = P.bsr_expand_upper(h, drp, dcol, dev(urp, torch.int64), dev(ucol, torch.int32), dev(uval, torch.float64))
+        assert np.array_equal(out.cpu().numpy(), ref)
+        sym = all(np.array_equal(val[e], val[np.searchsorted(col[rp[j]:rp[j + 1]], i) + rp[j]].T)
+                  for i in range(len(rp) - 1) for e in range(rp[i], rp[i + 1]) for j in [col[e]])
+        if sym:  # the synthetic fine Hessians are bitwise symmetric: expansion restores them
+            assert np.array_equal(out.cpu().numpy(), val)
+        # round trip through the device selection; unchecked (stream-ordered) variant
+        u2 = P.bsr_upper(h, drp, dcol, dev(val, torch.float64))
+        out2 = P.bsr_expand_upper(h, drp, dcol, *u2, check=False)
+        assert np.array_equal(out2.cpu().numpy(), ref)
+    # a pattern that is not the symmetric closure of U's is rejected
+    rp, col, val = cases[0]
+    urp, ucol, uval = oracle.bsr_upper(rp, col, val)
+    bad = ucol.copy()
+    bad[urp[1] - 1] += 1                                          # last upper column of row 0 shifted
+    with pytest.raises(P.AgipcError) as e:
+        P.bsr_expand_upper(h, dev(rp, torch.int64), dev(col, torch.int32), dev(urp, torch.int64),
+                           dev(bad, torch.int32), dev(uval, torch.float64))
+    assert e.value.status == P.EINVAL

@@ -106,3 +106,25 @@ def test_quadratic_form_from_the_upper_half():
         D = dense(rp, col, val, n)
         ref = x.reshape(-1) @ D @ x.reshape(-1)
         assert abs(q - ref) <= 1e-12 * (np.abs(x.reshape(-1)) @ np.abs(D) @ np.abs(x.reshape(-1)))
+
+
+def test_expand_upper_inverts_the_selection_bitwise():
+    for rp, col, val, n in cases():
+        urp, ucol, uval = oracle.bsr_upper(rp, col, val)
+        full, miss = oracle.bsr_expand_upper(rp, col, urp, ucol, uval)
+        assert miss == 0 and np.array_equal(full, val)
+        # the dense picture: upper half and mirrored strict part
+        assert np.array_equal(dense(rp, col, full, n), dense_from_upper(urp, ucol, uval, n))
+
+
+def test_expand_upper_reports_missing_sources():
+    m = synth.kuhn_grid(3)
+    H = synth.fine_hessian(m)
+    urp, ucol, uval = oracle.bsr_upper(m.bsr_ptr, m.bsr_col, H)
+    # drop the last upper block of row 0: its block and its mirror have no source
+    keep = np.ones(len(ucol), bool)
+    keep[urp[1] - 1] = False
+    urp2 = urp.copy()
+    urp2[1:] -= 1
+    full, miss = oracle.bsr_expand_upper(m.bsr_ptr, m.bsr_col, urp2, ucol[keep], uval[keep])
+    assert miss == 2
