@@ -67,6 +67,11 @@ AGIPC_API agipc_status agipc_create(agipc_handle *h, int cuda_device);
 AGIPC_API agipc_status agipc_destroy(agipc_handle h);
 /* stream: a cudaStream_t passed as void* (e.g. torch.cuda.current_stream().cuda_stream). */
 AGIPC_API agipc_status agipc_set_stream(agipc_handle h, void *stream);
+/* One-shot: the next agipc_assemble_coarse makes its numeric phase (the only part that reads
+ * H_fine values and g_fine) wait for this CUDA event (cudaEvent_t as void*; NULL clears), so an
+ * upload of the values on another stream overlaps steps 1-2 AND the classification + symbolic
+ * phases of step 3. */
+AGIPC_API agipc_status agipc_set_values_event(agipc_handle h, void *event);
 AGIPC_API const char *agipc_last_error(agipc_handle h);
 AGIPC_API const char *agipc_status_string(agipc_status s);
 AGIPC_API void agipc_version(int *major /*[host]*/, int *minor /*[host]*/);

@@ -83,7 +83,7 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
            "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
            "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym",
-           "agipc_bsr_expand_upper"]
+           "agipc_bsr_expand_upper", "agipc_set_values_event"]
 
 
 def lib():
@@ -117,6 +117,7 @@ def lib():
         L.agipc_pcg_solve.argtypes = [P, C.POINTER(_Bsr), P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_pcg_solve_sym.argtypes = [P, C.POINTER(_Bsr), i32, P, P, i32, f64, i32, i32, C.POINTER(_PcgStats)]
         L.agipc_bsr_upper.argtypes = [P, C.POINTER(_Bsr), i64, P, P, P, C.POINTER(i64)]
+        L.agipc_set_values_event.argtypes = [P, P]
         L.agipc_bsr_expand_upper.argtypes = [P, C.POINTER(_Bsr), C.POINTER(_Bsr), P, i32]
         L.agipc_prolongate.argtypes = [P, C.POINTER(_Mesh), P, i64, i64, P, f64, P]
         L.agipc_gather_rows.argtypes = [P, P, P, i64, i32, P]
@@ -185,6 +186,11 @@ class Handle:
         return st
 
     @property
+    def set_values_event(self, event: torch.cuda.Event | None):
+        """One-shot: the next assemble_coarse's numeric phase waits for `event` (see
+        agipc_set_values_event)."""
+        self._check(lib().agipc_set_values_event(self._h, C.c_void_p(event.cuda_event if event is not None else 0)))
+
     def kernel_launches(self) -> int:
         return int(lib().agipc_kernel_launches(self._h))
 

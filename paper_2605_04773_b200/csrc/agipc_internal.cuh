@@ -61,7 +61,8 @@ struct agipc_handle_s {
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
-  size_t tail_smem = 0;  // build_map: dynamic smem the tail kernel attribute allows (set once)
+  size_t tail_smem = 0;
+  cudaEvent_t values_event = nullptr;  // agipc_set_values_event (one-shot, consumed by assemble)  // build_map: dynamic smem the tail kernel attribute allows (set once)
   struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;

@@ -142,6 +142,12 @@ agipc_status agipc_set_stream(agipc_handle h, void *stream) {
   return AGIPC_OK;
 }
 
+agipc_status agipc_set_values_event(agipc_handle h, void *event) {
+  if (!h) return AGIPC_EINVAL;
+  h->values_event = (cudaEvent_t)event;
+  return AGIPC_OK;
+}
+
 const char *agipc_last_error(agipc_handle h) { return h ? h->err.c_str() : "null handle"; }
 
 const char *agipc_status_string(agipc_status s) {

@@ -1349,6 +1349,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemcpyAsync(out->row_ptr, crp_ws, sizeof(int64_t) * (out->n_slots + 1), cudaMemcpyDeviceToDevice, st_));
 
   ps_sym.reset();
+  if (h->values_event) {  // H_fine / g_fine values uploaded on another stream (one-shot)
+    cudaEvent_t ev = h->values_event;
+    h->values_event = nullptr;
+    CU_TRY(h, cudaStreamWaitEvent(st_, ev, 0));
+  }
   ProfScope ps_num(h, PROF_ASM_NUMERIC, st_);
   // ---- D. numeric ----
   if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));

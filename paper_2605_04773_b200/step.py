@@ -44,12 +44,12 @@ class CoarseningStep:
 
     def coarsen(self, x_prev, x_cur, g_fine, count=False, hessian_ready=None):
         """Steps 1-3.  Returns (n_flagged, map_info, CoarseSystem).  hessian_ready: optional CUDA
-        event the assembly waits for (steps 1-2 do not read H_f or g_f, so their upload can
-        overlap them on another stream)."""
+        event the numeric assembly waits for (steps 1-2 and the classification / symbolic parts of
+        step 3 do not read H_f or g_f values, so their upload can overlap them on another stream)."""
         _, nf = tag_edges(self.h, self.mesh, x_prev, x_cur, self.theta, self.slot_tags, count=count)
         _, info = build_map(self.h, self.mesh, self.slot_tags, self.group_size, 0, self.map)
         if hessian_ready is not None:
-            torch.cuda.current_stream().wait_event(hessian_ready)
+            self.h.set_values_event(hessian_ready)
         cs = assemble_coarse(self.h, self.mesh, self.map, info["n_coarse"], self.affine_threshold, *self.H,
                              g_fine, self.bufs)
         return nf, info, cs

@@ -232,3 +232,35 @@ def test_bsr_expand_upper_bit_exact(P, h):
         P.bsr_expand_upper(h, dev(rp, torch.int64), dev(col, torch.int32), dev(urp, torch.int64),
                            dev(bad, torch.int32), dev(uval, torch.float64))
     assert e.value.status == P.EINVAL
+
+
+def test_values_event_orders_a_late_upload(P, h):
+    """agipc_set_values_event: the numeric assembly waits for values uploaded on another stream
+    (delayed here by a spin kernel), so the result equals the synchronous one bit for bit."""
+    from paper_2605_04773_b200.step import CoarseningStep
+    c = synth.config_c1()
+    m = c["mesh"]
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    dm = P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device="cuda:0")
+    rp, cl = dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32)
+    xp, xc = dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64)
+    ref_step = CoarseningStep(h, dm, rp, cl, dev(H, torch.float64))
+    _, _, ref = ref_step.coarsen(xp, xc, dev(g, torch.float64))
+    ref_val, ref_g = ref.val.clone(), ref.g_c.clone()
+    dH = torch.zeros((m.bsr_col.shape[0], 3, 3), dtype=torch.float64, device="cuda:0")
+    dg = torch.zeros((m.n_nodes, 3), dtype=torch.float64, device="cuda:0")
+    hH = torch.as_tensor(H).pin_memory()
+    hg = torch.as_tensor(g).pin_memory()
+    side = torch.cuda.Stream()
+    ready = torch.cuda.Event()
+    step = CoarseningStep(h, dm, rp, cl, dH)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)            # ~10 ms: the upload lands long after steps 1-2
+        dH.copy_(hH, non_blocking=True)
+        dg.copy_(hg, non_blocking=True)
+        ready.record(side)
+    _, _, cs = step.coarsen(xp, xc, dg, hessian_ready=ready)
+    torch.cuda.synchronize()
+    assert torch.equal(cs.val, ref_val) and torch.equal(cs.g_c, ref_g)
