@@ -185,12 +185,12 @@ class Handle:
             raise AgipcError(st, lib().agipc_last_error(self._h).decode())
         return st
 
-    @property
     def set_values_event(self, event: torch.cuda.Event | None):
         """One-shot: the next assemble_coarse's numeric phase waits for `event` (see
         agipc_set_values_event)."""
         self._check(lib().agipc_set_values_event(self._h, C.c_void_p(event.cuda_event if event is not None else 0)))
 
+    @property
     def kernel_launches(self) -> int:
         return int(lib().agipc_kernel_launches(self._h))
 
