@@ -264,7 +264,12 @@ __global__ void k_sell_scalars(int64_t ns_bound, const int64_t *__restrict__ spt
   st->sell_blocks = sptr[ns_bound];
 }
 
-// warp per slice: component-major tiles; padding = zero blocks pointing at the row itself
+// Position of component e of lane l's block inside a 288-double block-column tile: components
+// are paired, (0,1) (2,3) (4,5) (6,7) as [pair][lane][2], component 8 as [lane] -- so the SpMV
+// reads a block with four 16-B loads and one 8-B load, every warp access fully coalesced.
+__host__ __device__ __forceinline__ int tile_off(int e, int l) { return e < 8 ? 64 * (e >> 1) + 2 * l + (e & 1) : 256 + l; }
+
+// warp per slice: block-column tiles (tile_off); padding = zero blocks pointing at the row itself
 __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, const int64_t *__restrict__ re,
                             const int32_t *__restrict__ col,
                             const double *__restrict__ val, const int64_t *__restrict__ hrp,
@@ -300,10 +305,10 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
       const long long t = base + 32LL * j;
       const bool real = j < len;
       scol[t + l] = real ? cs[k0 + j] : row;
-      double *dst = sval + 9 * t + l;
+      double *dst = sval + 9 * t;  // tile of the block column (see blk_load for the layout)
       const double *src = vs + 9 * (k0 + j);
 #pragma unroll
-      for (int e = 0; e < 9; ++e) dst[32 * e] = real ? src[e] : 0.0;
+      for (int e = 0; e < 9; ++e) dst[tile_off(e, l)] = real ? src[e] : 0.0;
     }
   }
 }
@@ -419,10 +424,17 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
 struct BlkLoad {
   double m[9], z[3], p[3];
 };
-__device__ __forceinline__ void blk_load(BlkLoad &b, const double *__restrict__ v0, int64_t c0,
+__device__ __forceinline__ void blk_load(BlkLoad &b, const double *__restrict__ tile, int l, int64_t c0,
                                          const double *__restrict__ z, const double *__restrict__ pold) {
+  // components (0,1) (2,3) (4,5) (6,7): one 16-B load per lane (512 contiguous bytes per warp);
+  // component 8: one 8-B load (256 bytes per warp)
 #pragma unroll
-  for (int e = 0; e < 9; ++e) b.m[e] = __ldcs(v0 + 32 * e);
+  for (int p = 0; p < 4; ++p) {
+    const double2 v = __ldcs(reinterpret_cast<const double2 *>(tile + 64 * p + 2 * l));
+    b.m[2 * p] = v.x;
+    b.m[2 * p + 1] = v.y;
+  }
+  b.m[8] = __ldcs(tile + 256 + l);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     b.z[k] = __ldg(z + c0 + k);
@@ -464,14 +476,14 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
     const long long base = sptr[s];
     const int L = (int)((sptr[s + 1] - base) >> 5);
     const int32_t *cp = scol + base + l;
-    const double *vp = sval + 9 * base + l;
+    const double *vp = sval + 9 * base;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     int64_t n0 = L > 0 ? 3 * (int64_t)__ldcs(cp) : 0, n1 = L > 1 ? 3 * (int64_t)__ldcs(cp + 32) : 0;
     int j = 0;
     for (; j + 1 < L; j += 2) {
       BlkLoad b0, b1;  // all 30 loads of the pair are issued before any FMA
-      blk_load(b0, vp + 288 * (int64_t)j, n0, z, pold);
-      blk_load(b1, vp + 288 * (int64_t)(j + 1), n1, z, pold);
+      blk_load(b0, vp + 288 * (int64_t)j, l, n0, z, pold);
+      blk_load(b1, vp + 288 * (int64_t)(j + 1), l, n1, z, pold);
       if (j + 2 < L) n0 = 3 * (int64_t)__ldcs(cp + 32 * (j + 2));  // prefetch the next pair's columns
       if (j + 3 < L) n1 = 3 * (int64_t)__ldcs(cp + 32 * (j + 3));
       blk_fma(b0, beta, a0, a1, a2);
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
     }
     if (j < L) {
       BlkLoad b0;
-      blk_load(b0, vp + 288 * (int64_t)j, n0, z, pold);
+      blk_load(b0, vp + 288 * (int64_t)j, l, n0, z, pold);
       blk_fma(b0, beta, a0, a1, a2);
     }
     const int v = s_vrow[32 * s + l];
@@ -597,7 +609,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 2) k_spmv_sym(const int64_t *__re
       const long long base = sptr[s];
       const int L = (int)((sptr[s + 1] - base) >> 5);
       const int32_t *cp = scol + base + l;
-      const double *vp = sval + 9 * base + l;
+      const double *vp = sval + 9 * base;
       const int v = s_vrow[32 * s + l];
       const int64_t row = v >= 0 ? v_row[v] : -1;
       const int64_t i3 = 3 * row;
@@ -615,8 +627,8 @@ __global__ void __launch_bounds__(PCG_THREADS, 2) k_spmv_sym(const int64_t *__re
       for (; j + 1 < L; j += 2) {
         BlkLoad b0, b1;
         const int64_t c0 = n0, c1 = n1;
-        blk_load(b0, vp + 288 * (int64_t)j, c0, z, pold);
-        blk_load(b1, vp + 288 * (int64_t)(j + 1), c1, z, pold);
+        blk_load(b0, vp + 288 * (int64_t)j, l, c0, z, pold);
+        blk_load(b1, vp + 288 * (int64_t)(j + 1), l, c1, z, pold);
         if (j + 2 < L) n0 = 3 * (int64_t)__ldcs(cp + 32 * (j + 2));
         if (j + 3 < L) n1 = 3 * (int64_t)__ldcs(cp + 32 * (j + 3));
         sym_blk(b0, v >= 0 ? c0 : -1, ii3, beta, pi0, pi1, pi2, 3 * lo, nr3, s_acc, yext, d0, d1, d2, o0, o1, o2);
@@ -625,7 +637,7 @@ __global__ void __launch_bounds__(PCG_THREADS, 2) k_spmv_sym(const int64_t *__re
       if (j < L) {
         BlkLoad b0;
         const int64_t c0 = n0;
-        blk_load(b0, vp + 288 * (int64_t)j, c0, z, pold);
+        blk_load(b0, vp + 288 * (int64_t)j, l, c0, z, pold);
         sym_blk(b0, v >= 0 ? c0 : -1, ii3, beta, pi0, pi1, pi2, 3 * lo, nr3, s_acc, yext, d0, d1, d2, o0, o1, o2);
       }
       if (v >= 0) {

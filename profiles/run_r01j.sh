@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-1 final-state capture: GPU tests, smoke, bench line, launch list, --set full of the PCG kernels
-OUT=gpurun_out/r01j
+OUT=gpurun_out/${TAG:-r01j}
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1; echo smoke=$? >> $OUT/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo rc=$? >> $OUT/pytest_gpu.log
