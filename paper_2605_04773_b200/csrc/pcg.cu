@@ -49,7 +49,7 @@ struct PcgGraph {
   int grid1 = 0, grid2 = 0;
   bool prof = false;
   bool sym = false;
-  int win = 0, all_red = 0, upd_u = 0;
+  int win = 0, all_red = 0, upd_u = 0, spmv_un = 0;
   const void *yext = nullptr;
   std::vector<cudaEvent_t> ev;  // profiling: 3 events per iteration of the chunk
 };
@@ -450,7 +450,8 @@ __device__ __forceinline__ void blk_fma(const BlkLoad &b, double beta, double &a
 
 // Persistent grid (resident CTAs only); every warp repeatedly claims the next slice of the
 // longest-first order from counter[parity] (reset by K2 for the next iteration).
-__global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__restrict__ sptr,
+template <int UN, int MINB>
+__global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *__restrict__ sptr,
                                                            const int32_t *__restrict__ scol,
                                                            const double *__restrict__ sval,
                                                            const int32_t *__restrict__ s_vrow,
@@ -478,22 +479,27 @@ __global__ void __launch_bounds__(PCG_THREADS, 3) k_spmv_sell(const int64_t *__r
     const int32_t *cp = scol + base + l;
     const double *vp = sval + 9 * base;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    int64_t n0 = L > 0 ? 3 * (int64_t)__ldcs(cp) : 0, n1 = L > 1 ? 3 * (int64_t)__ldcs(cp + 32) : 0;
+    int64_t nc[UN];  // column offsets of the next UN blocks (prefetched one group ahead)
+#pragma unroll
+    for (int u = 0; u < UN; ++u) nc[u] = u < L ? 3 * (int64_t)__ldcs(cp + 32 * u) : 0;
     int j = 0;
-    for (; j + 1 < L; j += 2) {
-      BlkLoad b0, b1;  // all 30 loads of the pair are issued before any FMA
-      blk_load(b0, vp + 288 * (int64_t)j, l, n0, z, pold);
-      blk_load(b1, vp + 288 * (int64_t)(j + 1), l, n1, z, pold);
-      if (j + 2 < L) n0 = 3 * (int64_t)__ldcs(cp + 32 * (j + 2));  // prefetch the next pair's columns
-      if (j + 3 < L) n1 = 3 * (int64_t)__ldcs(cp + 32 * (j + 3));
-      blk_fma(b0, beta, a0, a1, a2);
-      blk_fma(b1, beta, a0, a1, a2);
+    for (; j + UN - 1 < L; j += UN) {
+      BlkLoad b[UN];  // all 15 UN loads of the group are issued before any FMA
+#pragma unroll
+      for (int u = 0; u < UN; ++u) blk_load(b[u], vp + 288 * (int64_t)(j + u), l, nc[u], z, pold);
+#pragma unroll
+      for (int u = 0; u < UN; ++u)
+        if (j + UN + u < L) nc[u] = 3 * (int64_t)__ldcs(cp + 32 * (j + UN + u));
+#pragma unroll
+      for (int u = 0; u < UN; ++u) blk_fma(b[u], beta, a0, a1, a2);  // blocks in column order
     }
-    if (j < L) {
-      BlkLoad b0;
-      blk_load(b0, vp + 288 * (int64_t)j, l, n0, z, pold);
-      blk_fma(b0, beta, a0, a1, a2);
-    }
+#pragma unroll
+    for (int u = 0; u < UN - 1; ++u)
+      if (j + u < L) {
+        BlkLoad b0;
+        blk_load(b0, vp + 288 * (int64_t)(j + u), l, nc[u], z, pold);
+        blk_fma(b0, beta, a0, a1, a2);
+      }
     const int v = s_vrow[32 * s + l];
     if (v >= 0) {
       const int64_t row = v_row[v];
@@ -790,6 +796,14 @@ __global__ void k_copy_out(int64_t n3, const double *__restrict__ src, double *_
   if (i < n3) dst[i] = src[i];
 }
 
+typedef void (*SpmvKernel)(const int64_t *, const int32_t *, const double *, const int32_t *, const int32_t *,
+                           const int32_t *, const int64_t *, const double *, const double *, double *, double *,
+                           int *, double *, PcgState *, double *);
+// k_spmv_sell variants: UN blocks per thread in flight at MINB CTAs per SM (register budget)
+static SpmvKernel spmv_kernel(int un) {
+  return un == 4 ? k_spmv_sell<4, 2> : un == 3 ? k_spmv_sell<3, 2> : k_spmv_sell<2, 3>;
+}
+
 struct PcgBufs {
   double *x, *r, *z, *P[2], *qseg, *Dinv, *parts, *sval;
   int64_t *vr_ptr, *sptr;
@@ -805,6 +819,7 @@ struct PcgBufs {
   int all_red = 0;
   int upd_u = 1;  // slots per K2 thread pass
   double *arena = nullptr;  // x, r, z, p0, p1, qseg, Dinv (+ ytin, yext): one L2 window
+  int spmv_un = 3;          // blocks per thread in flight in k_spmv_sell
   size_t arena_bytes = 0;
 };
 
@@ -853,8 +868,9 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
           B.sptr, B.scol, B.sval, B.s_vrow, B.v_row, B.vr_ptr, B.z, pold, pnew, B.qseg, B.ytin, B.yext, B.win,
           B.counters + (k & 1), B.parts, B.st, B.all_red);
     else
-      k_spmv_sell<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z,
-                                               pold, pnew, B.qseg, B.counters + (k & 1), B.parts, B.st, nullptr);
+      spmv_kernel(B.spmv_un)<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
+                                                          B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (k & 1),
+                                                          B.parts, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
     k_update<1, PCG_THREADS><<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
                                           B.parts, B.st, nullptr, B.ytin, B.yext);
@@ -925,7 +941,11 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sym, PCG_THREADS, smem));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(nv_bound, B.win), (int64_t)std::max(1, occ) * h->sm_count));
   } else {
-    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell, PCG_THREADS, 0));
+    // 3 blocks per thread in flight at 2 CTAs/SM: 82.0 -> 76.7 us per SpMV at C3 vs 2 at 3 CTAs/SM
+    // (4 at 2 CTAs/SM: 77.9 us; profiles/r01o/un*.txt).  AGIPC_SPMV_UN selects another variant.
+    B.spmv_un = 3;
+    if (const char *e = getenv("AGIPC_SPMV_UN")) B.spmv_un = atoi(e) == 4 ? 4 : atoi(e) == 2 ? 2 : 3;
+    CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_kernel(B.spmv_un), PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
   }
   // K2: 2 CTAs of 256 threads per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl,
@@ -1030,7 +1050,8 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     const void *key[8] = {B.sval, B.scol, B.x, B.qseg, B.Dinv, B.sptr, B.P[0], B.parts};
     bool same = g->exec && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
                 g->grid2 == B.G2 && g->prof == h->prof && g->sym == B.sym && g->win == B.win && g->yext == B.yext &&
-                g->all_red == B.all_red && g->upd_u == B.upd_u;
+                g->all_red == B.all_red && g->upd_u == B.upd_u &&
+                g->spmv_un == B.spmv_un;
     for (int i = 0; i < 8 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
@@ -1061,6 +1082,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
       g->yext = B.yext;
       g->all_red = B.all_red;
       g->upd_u = B.upd_u;
+      g->spmv_un = B.spmv_un;
       for (int i = 0; i < 8; ++i) g->key[i] = key[i];
     }
     CU_TRY(h, cudaEventRecord(g->ev_in, s0));
@@ -1260,7 +1282,7 @@ extern "C" agipc_status agipc_dpcg_spmv(agipc_handle h, const double *recvbuf, d
   if (d->n_gs > 0)
     LAUNCH(h, k_ghost_in, (unsigned)std::min<int64_t>(cdiv(3 * d->n_gs, 256), 4 * h->sm_count), 256, 0, d->n, d->n_gs,
            recvbuf, B.z, (const double *)pold, pnew, (const PcgState *)B.st);
-  LAUNCH(h, k_spmv_sell, (unsigned)B.G1, PCG_THREADS, 0, B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
+  LAUNCH(h, spmv_kernel(B.spmv_un), (unsigned)B.G1, PCG_THREADS, 0, B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
          B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (d->k & 1), B.parts, B.st, red);
   d->pending = DP_ALPHA;
   return AGIPC_OK;
