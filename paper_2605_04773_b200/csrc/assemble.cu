@@ -961,7 +961,7 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 // by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
 // two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
-#define LSTAGE 256
+#define LSTAGE 192
 
 template <int NCB, int NB>
 __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) {
@@ -971,6 +971,7 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
   __shared__ int s_b[4][LSTAGE];     // interface entries (staged from the top): column aggregate
   __shared__ double s_xj[4][LSTAGE][3];  // X_bar of the entry's column node (w_j)
   __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
+  __shared__ double s_B[4][32][9];       // phase 2: 32 diagonal blocks staged per warp (one per lane)
   const int w = threadIdx.x >> 5, l = lane_id();
   // lane = (block group, p, q half): NCB = 4 -> 8 lanes per block, 2 q per lane
   constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
@@ -1051,28 +1052,28 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
         icnt += __popc(mi);
       }
       __syncwarp();
-      for (int d = gq; d < cnt; d += NB * G) {  // NB diagonal blocks per group in flight
-        double Bv[NB][9], wi[NB];
-        int dd[NB];
+      // phase 2: every lane stages one diagonal block (32 independent 72-B loads in flight per
+      // warp), then lane (group, p, q half) accumulates the staged blocks d = gq, gq + G, ...
+      for (int d0 = 0; d0 < cnt; d0 += 32) {
+        if (d0 + l < cnt) {
+          const long long kk = s_k[w][d0 + l];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-          const bool ok = d + u * G < cnt;
-          dd[u] = ok ? d + u * G : d;
-          const long long kk = s_k[w][dd[u]];
-#pragma unroll
-          for (int x = 0; x < 9; ++x) Bv[u][x] = __ldg(A.val + 9 * kk + x);
-          wi[u] = !ok ? 0.0 : (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][dd[u]]][p];
+          for (int x = 0; x < 9; ++x) s_B[w][l][x] = __ldg(A.val + 9 * kk + x);
         }
+        __syncwarp();
+        const int dn = min(32, cnt - d0);
+        for (int dd = gq; dd < dn; dd += G) {
+          const int d = d0 + dd;
+          const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d]][p];
 #pragma unroll
-        for (int qq = 0; qq < QN; ++qq) {
-          const int q = q0 + qq;
+          for (int qq = 0; qq < QN; ++qq) {
+            const int q = q0 + qq;
+            const double c = wi * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][d][q]);
 #pragma unroll
-          for (int u = 0; u < NB; ++u) {
-            const double c = wi[u] * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][dd[u]][q]);
-#pragma unroll
-            for (int x = 0; x < 9; ++x) acc[qq][x] += c * Bv[u][x];
+            for (int x = 0; x < 9; ++x) acc[qq][x] += c * s_B[w][dd][x];
           }
         }
+        __syncwarp();
       }
       __syncwarp();
       // interface entries [LSTAGE - icnt, LSTAGE): one pass per distinct column aggregate b0,
