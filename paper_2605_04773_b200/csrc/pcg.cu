@@ -307,8 +307,13 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
       scol[t + l] = real ? cs[k0 + j] : row;
       double *dst = sval + 9 * t;  // tile of the block column (see blk_load for the layout)
       const double *src = vs + 9 * (k0 + j);
+      double v[9];
 #pragma unroll
-      for (int e = 0; e < 9; ++e) dst[tile_off(e, l)] = real ? src[e] : 0.0;
+      for (int e = 0; e < 9; ++e) v[e] = real ? src[e] : 0.0;
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp)  // one 16-B store per component pair: 512 B per warp
+        *reinterpret_cast<double2 *>(dst + tile_off(2 * pp, l)) = make_double2(v[2 * pp], v[2 * pp + 1]);
+      dst[tile_off(8, l)] = v[8];
     }
   }
 }
@@ -1109,6 +1114,14 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
         it_before = hst->it;
         if (hst->done || launched >= max_iters) break;
       }
+    }
+    // the solve's vectors were persisting L2 lines; release them so the next Newton step's
+    // coarsen/assemble kernels get the whole L2 (the loop above has synchronised the solve)
+    if (B.arena) {
+      cudaStreamAttrValue v;
+      memset(&v, 0, sizeof(v));
+      if (cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+      if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
     }
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
     CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
