@@ -176,7 +176,7 @@ def run_reference(args, world, rank):
                                       "single-threaded C oracle"},
            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "input_generation_s": round(gen_s, 1)}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # --------------------------------------------------------------------------------------
@@ -380,7 +380,7 @@ def run_agipc(args, world, rank, local_rank):
         "next_rows": next_rows,
         "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=5):
@@ -633,10 +633,29 @@ def run_partitioned(args, world, rank, local_rank):
         "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": None,
         "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+# The result is ONE JSON line on stdout.  Library banners (e.g. NCCL's version line, printed from
+# C code at communicator creation) would interleave with it, so the process's fd 1 is pointed at
+# stderr for the whole run and the JSON line goes to the saved original stdout.
+_STDOUT_FD = None
+
+
+def emit(out):
+    line = (json.dumps(out) + "\n").encode()
+    if _STDOUT_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_STDOUT_FD, line)
 
 
 def main():
+    global _STDOUT_FD
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

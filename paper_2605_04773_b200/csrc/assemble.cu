@@ -519,6 +519,8 @@ __device__ __forceinline__ double seg_sum(double v) {
 
 struct WarpArgs {
   int64_t n_w;
+  long long *mkeys;            // mid nodes: sorted (column, entry) keys, written by the symbolic
+  const int64_t *e_off;        //   pass at e_off[wi], reused by the numeric pass (no second sort)
   const int32_t *wlist;        // small nodes handled by this kernel
   const int32_t *child_list;
   const int64_t *child_ptr;
@@ -724,6 +726,11 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
     const int a = A.wlist[wi];
     const int s = A.size_new[a];
     const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);  // T <= MID_CAP
+    long long *gkeys = A.mkeys + A.e_off[wi];
+    if (NUMERIC) {  // the symbolic pass left the sorted keys of this node in global memory
+      for (int e = l; e < T; e += 32) key[e] = gkeys[e];
+      __syncwarp();
+    } else {
     const int P = next_pow2(T);
     for (int e = l; e < P; e += 32) {
       long long kk = LLONG_MAX;
@@ -750,6 +757,8 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
         }
         __syncwarp();
       }
+    for (int e = l; e < T; e += 32) gkeys[e] = key[e];
+    }
     // runs of equal column; colpos = prefix of the run weights (12-DoF columns count 4)
     int run_base = 0;
     for (int e0 = 0; !NUMERIC && e0 < T; e0 += 32) {
@@ -1297,6 +1306,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WA.X = mesh->x_rest; WA.g_f = gfp; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
+  WA.mkeys = nullptr; WA.e_off = nullptr;
   WarpArgs WB = WA, WM;
   WB.n_w = n_w32; WB.wlist = w32;
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
@@ -1305,6 +1315,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
   WM = WA;
   WM.n_w = n_small; WM.wlist = small_list;
+  {  // mid-node entries: sum of their candidate entries <= the fine blocks
+    WS(h, mkeys, long long, "asm_mid_keys", nnzb_f + 1);
+    WM.mkeys = mkeys;
+    WM.e_off = e_off;
+  }
   const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_small, MID_WARPS), 32 * h->sm_count));
   if (n_small > 0) LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   LargeArgs LA;
