@@ -586,9 +586,17 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       entry_of(tab, s, sl, c, k);
       i = tab.ci[c];
       j = A.col[k];
-      b = A.nm[j];
+      if (!NUMERIC) b = A.nm[j];
     }
-    const long long key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
+    // sorted (column, entry) keys: computed by the symbolic pass and kept at wi * SEG + sl for
+    // the numeric pass (no second new_map gather and sort)
+    long long key;
+    if (!NUMERIC) {
+      key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
+      if (segv) A.mkeys[wi * SEG + sl] = key;
+    } else {
+      key = segv ? A.mkeys[wi * SEG + sl] : (((long long)INT_MAX << 5) | sl);
+    }
     const int bs = (int)(key >> 5), src = (int)(key & 31);
     const long long prevk = __shfl_up_sync(FULL_MASK, key, 1, SEG);
     const bool valid = sl < T;
@@ -1309,6 +1317,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WA.mkeys = nullptr; WA.e_off = nullptr;
   WarpArgs WB = WA, WM;
   WB.n_w = n_w32; WB.wlist = w32;
+  {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
+    WS(h, skeys, long long, "asm_small_keys", 16 * n_w16 + 32 * n_w32 + 1);
+    WA.mkeys = skeys;
+    WB.mkeys = skeys + 16 * n_w16;
+  }
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
   const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
