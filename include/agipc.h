@@ -11,6 +11,15 @@
  *                             main Eq 4)
  *   4. agipc_pcg_solve        block-Jacobi PCG on the coarse system
  *   5. agipc_prolongate       d_f = U^T d_c back to the fine nodes (NEXT#1)
+ * and the rows SURVEY 8(f) ranks next:
+ *   agipc_bsr_upper / agipc_bsr_expand_upper / agipc_pcg_solve_sym
+ *                             symmetric (diagonal + upper) storage (NEXT#2)
+ *   agipc_triplet_plan / agipc_triplet_reduce
+ *                             fine-level hash reduction of element triplets (NEXT#3)
+ *   agipc_tag_shells / agipc_tag_rods
+ *                             step 1 for triangles and edges (NEXT#4)
+ * plus the partitioned multi-GPU pieces (agipc_gather_rows, agipc_coarse_halo,
+ * agipc_assemble_halo, agipc_dpcg_*) and agipc_set_values_event (upload overlap).
  *
  * Conventions (all entry points):
  *  - Array arguments are DEVICE pointers owned by the caller (e.g. PyTorch CUDA tensors,
