@@ -25,7 +25,7 @@
 #define PCG_THREADS 256
 #define PCG_WARPS (PCG_THREADS / 32)
 #define SEG_MAX 64          // blocks per virtual row
-#define SORT_WIN 4096       // virtual rows per sorting window (sigma = 128 slices)
+#define SORT_WIN 8192       // virtual rows per sorting window (sigma = 256 slices)
 #define PROF_EVERY 8        // profiling: time the kernels of every 8th iteration
 #define HALO_BIT (1 << 30)  // v_len flag: the virtual row is a segment of the halo matrix (8(e))
 #define VLEN(x) ((x) & (HALO_BIT - 1))
@@ -196,7 +196,7 @@ __global__ void k_seg_fill(int64_t n, const int64_t *__restrict__ rb, const int6
 // (ties: ascending id)
 __global__ void __launch_bounds__(1024) k_window_sort(const PcgState *st, const int32_t *__restrict__ v_len,
                                                       int32_t *__restrict__ perm, int win) {
-  __shared__ unsigned long long s_key[SORT_WIN];
+  extern __shared__ unsigned long long s_key[];  // [win] (dynamic: up to 64 KB)
   const long long nv = st->nv;
   const long long w0 = (long long)blockIdx.x * win;
   if (w0 >= nv) return;
@@ -986,7 +986,10 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
   if (sst != AGIPC_OK) return sst;
   LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
-  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, B.win), 1024, 0, stp, B.v_len, B.perm, B.win);
+  CU_TRY(h, cudaFuncSetAttribute(k_window_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(unsigned long long) * SORT_WIN)));
+  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, B.win), 1024, sizeof(unsigned long long) * B.win, stp, B.v_len,
+         B.perm, B.win);
   LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
   sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
   if (sst != AGIPC_OK) return sst;
