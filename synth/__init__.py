@@ -20,8 +20,49 @@ nu = 0.3, dt = 0.01, E per config, g_f ~ N(0,1).
 """
 from __future__ import annotations
 
+import ctypes as _C
 import dataclasses
+import os
+import subprocess
+
 import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_GEN_SRC = os.path.join(_HERE, "_gen.c")
+_GEN_LIB = os.path.join(_HERE, "libsynthgen.so")
+_gen = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the fast input generator (_gen.c, gcc + OpenMP).  Input generation only."""
+    if force or not os.path.exists(_GEN_LIB) or os.path.getmtime(_GEN_LIB) < os.path.getmtime(_GEN_SRC):
+        tmp = _GEN_LIB + ".%d.tmp" % os.getpid()
+        subprocess.check_call(["gcc", "-O3", "-std=gnu99", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", tmp, _GEN_SRC, "-lm"])
+        os.replace(tmp, _GEN_LIB)
+    return _GEN_LIB
+
+
+def _lib():
+    global _gen
+    if _gen is None:
+        build()
+        L = _C.CDLL(_GEN_LIB)
+        P, i64, f64 = _C.c_void_p, _C.c_int64, _C.c_double
+        L.syn_kuhn_grid.argtypes = [i64, f64, f64, f64, f64, i64, i64, i64] + [P] * 11
+        L.syn_kuhn_grid.restype = _C.c_int
+        L.syn_fine_hessian.argtypes = [i64, i64, P, P, P, f64, f64, f64, f64, _C.c_int, _C.c_int, P, P, P, P]
+        L.syn_fine_hessian.restype = i64
+        L.syn_merge_pattern.argtypes = [i64, P, P, i64, P, P, P, P]
+        L.syn_merge_pattern.restype = i64
+        L.syn_bsr_slots.argtypes = [i64, P, P, P, P, P]
+        L.syn_bsr_slots.restype = None
+        _gen = L
+    return _gen
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_C.c_void_p)
 
 __all__ = [
     "Mesh", "kuhn_grid", "mesh_from_tets", "stiffness_blocks", "fine_hessian",
@@ -137,6 +178,15 @@ def mesh_from_tets(X: np.ndarray, tets: np.ndarray, ijk=None, n_side=0, extra_pa
 
 def bsr_slot(mesh: Mesh, u, v) -> np.ndarray:
     """BSR slot of blocks (u, v) (general lookup; -1 if absent)."""
+    u = np.ascontiguousarray(np.asarray(u, np.int64).reshape(-1))
+    v = np.ascontiguousarray(np.asarray(v, np.int64).reshape(-1))
+    out = np.empty(u.shape[0], np.int64)
+    _lib().syn_bsr_slots(u.shape[0], _ptr(mesh.bsr_ptr), _ptr(mesh.bsr_col), _ptr(u), _ptr(v), _ptr(out))
+    return out
+
+
+def bsr_slot_py(mesh: Mesh, u, v) -> np.ndarray:
+    """numpy version of bsr_slot (pins the fast one in tests/test_synth_fast.py)."""
     N = mesh.n_nodes
     brow = np.repeat(np.arange(N, dtype=np.int64), np.diff(mesh.bsr_ptr))
     key = brow * N + mesh.bsr_col
@@ -151,7 +201,35 @@ def kuhn_grid(n: int, order: str = "morton", side: float = 1.0, origin=(0.0, 0.0
     given side centred on ``origin``.  Each cube is split along its
     (0,0,0)-(1,1,1) diagonal into the 6 path tets.  Nodes are renumbered in
     Morton order (``order='morton'``) or kept lexicographic (``'lex'``); tets
-    are sorted by their smallest node id (stable)."""
+    are sorted by their smallest node id (stable).  The Morton grid is built by the
+    C generator (_gen.c, O(N), OpenMP); kuhn_grid_py is the numpy definition it is pinned to."""
+    if order != "morton":
+        return kuhn_grid_py(n, order, side, origin)
+    assert n >= 2
+    N, T = n ** 3, 6 * (n - 1) ** 3
+    E = 3 * n * n * (n - 1) + 3 * n * (n - 1) ** 2 + (n - 1) ** 3
+    X = np.empty((N, 3), np.float64)
+    ijk = np.empty((N, 3), np.int32)
+    tets = np.empty((T, 4), np.int32)
+    adj_ptr = np.empty(N + 1, np.int64)
+    adj_nbr = np.empty(2 * E, np.int32)
+    ts = np.empty((T, 12), np.int32)
+    edges = np.empty((E, 2), np.int32)
+    eos = np.empty(2 * E, np.int64)
+    bsr_ptr = np.empty(N + 1, np.int64)
+    bsr_col = np.empty(N + 2 * E, np.int32)
+    diag = np.empty(N, np.int64)
+    o = [float(v) for v in origin]
+    rc = _lib().syn_kuhn_grid(n, float(side), o[0], o[1], o[2], N, T, E, *[_ptr(a) for a in (
+        X, ijk, tets, adj_ptr, adj_nbr, ts, edges, eos, bsr_ptr, bsr_col, diag)])
+    if rc != 0:
+        raise RuntimeError(f"syn_kuhn_grid({n}) failed: {rc}")
+    return Mesh(X=X, tets=tets, adj_ptr=adj_ptr, adj_nbr=adj_nbr, tet_slots=ts, edges=edges, edge_of_slot=eos,
+                bsr_ptr=bsr_ptr, bsr_col=bsr_col, diag_slot=diag, ijk=ijk, n_side=n)
+
+
+def kuhn_grid_py(n: int, order: str = "morton", side: float = 1.0, origin=(0.0, 0.0, 0.0)) -> Mesh:
+    """numpy definition of kuhn_grid (any order)."""
     assert n >= 2
     g = np.arange(n)
     I, J, K = np.meshgrid(g, g, g, indexing="ij")
@@ -242,10 +320,29 @@ def _slot_index(mesh: Mesh, t0: int, t1: int) -> np.ndarray:
 
 
 def fine_hessian(mesh: Mesh, E: float = 1e5, nu: float = 0.3, rho: float = 1000.0,
-                 dt: float = 0.01, mass: bool = True, stiffness: bool = True,
-                 chunk: int = 1 << 18) -> np.ndarray:
-    """Values of H_f in the mesh's BSR pattern: float64 [N+2E, 3, 3] row-major
-    blocks.  ``E`` may be a per-tet array (multi-material scenes)."""
+                 dt: float = 0.01, mass: bool = True, stiffness: bool = True) -> np.ndarray:
+    """Values of H_f in the mesh's BSR pattern: float64 [nnzb, 3, 3] row-major
+    blocks.  ``E`` may be a per-tet array (multi-material scenes).  C generator (_gen.c):
+    row-centric sums over each node's tets in ascending tet order, so H is bitwise symmetric;
+    fine_hessian_py is the numpy definition it is pinned to (equal within rounding)."""
+    N, T = mesh.n_nodes, mesh.n_tets
+    nnzb = mesh.bsr_col.shape[0]
+    H = np.empty((nnzb, 3, 3), np.float64)
+    Earr = None
+    if np.ndim(E) > 0:
+        Earr = np.ascontiguousarray(np.broadcast_to(np.asarray(E, np.float64), (T,)))
+    miss = _lib().syn_fine_hessian(N, T, _ptr(mesh.tets), _ptr(mesh.X), _ptr(Earr), float(E) if Earr is None else 0.0,
+                                   float(nu), float(rho), float(dt), int(bool(mass)), int(bool(stiffness)),
+                                   _ptr(mesh.bsr_ptr), _ptr(mesh.bsr_col), _ptr(mesh.diag_slot), _ptr(H))
+    if miss != 0:
+        raise RuntimeError(f"fine_hessian: {miss} tet blocks missing from the BSR pattern")
+    return H
+
+
+def fine_hessian_py(mesh: Mesh, E: float = 1e5, nu: float = 0.3, rho: float = 1000.0,
+                    dt: float = 0.01, mass: bool = True, stiffness: bool = True,
+                    chunk: int = 1 << 18) -> np.ndarray:
+    """numpy/torch-CPU definition of fine_hessian (scatter in tet order)."""
     import torch  # index_add_ is only used as a fast scatter for input generation
     N = mesh.n_nodes
     nnzb = mesh.bsr_col.shape[0]
@@ -461,7 +558,35 @@ def slab_gradient(gid: np.ndarray, seed: int = 0) -> np.ndarray:
 # objects (Hessian entries, never tagged: coarsening stays inside objects)
 # ----------------------------------------------------------------------------
 
-def c4_scene(n: int = 57, k: int = 3, gap: float = 1e-3, side: float = 1.0, seed: int = 0):
+def _replicate_with_extras(base: Mesh, nobj: int, X, tets, ijk, pairs) -> Mesh:
+    """The mesh of nobj disjoint copies of `base` (object-major node ids) plus symmetric
+    Hessian-only pattern entries `pairs` -- equal to mesh_from_tets(X, tets, extra_pairs=pairs)
+    (pinned in tests/test_synth_fast.py), without its global sorts."""
+    N0, E0, S0 = base.n_nodes, base.n_edges, base.adj_nbr.shape[0]
+    N = N0 * nobj
+    oN = np.arange(nobj, dtype=np.int64)
+    adj_ptr = np.concatenate([[0], (base.adj_ptr[1:][None, :] + (oN * S0)[:, None]).reshape(-1)])
+    adj_nbr = (base.adj_nbr[None, :].astype(np.int64) + (oN * N0)[:, None]).reshape(-1).astype(np.int32)
+    ts = (base.tet_slots[None].astype(np.int64) + (oN * S0)[:, None, None]).reshape(-1, 12).astype(np.int32)
+    edges = (base.edges[None].astype(np.int64) + (oN * N0)[:, None, None]).reshape(-1, 2).astype(np.int32)
+    eos = (base.edge_of_slot[None, :] + (oN * E0)[:, None]).reshape(-1)
+    nb0 = base.bsr_col.shape[0]
+    bptr = np.concatenate([[0], (base.bsr_ptr[1:][None, :] + (oN * nb0)[:, None]).reshape(-1)])
+    bcol = (base.bsr_col[None, :].astype(np.int64) + (oN * N0)[:, None]).reshape(-1).astype(np.int32)
+    ex = np.ascontiguousarray(np.asarray(pairs, np.int32))
+    L = _lib()
+    optr = np.empty(N + 1, np.int64)
+    L.syn_merge_pattern(N, _ptr(bptr), _ptr(bcol), ex.shape[0], _ptr(ex), _ptr(optr), None, None)
+    ocol = np.empty(int(optr[N]), np.int32)
+    diag = np.empty(N, np.int64)
+    L.syn_merge_pattern(N, _ptr(bptr), _ptr(bcol), ex.shape[0], _ptr(ex), _ptr(optr), _ptr(ocol), _ptr(diag))
+    return Mesh(X=np.ascontiguousarray(X), tets=np.ascontiguousarray(tets, np.int32), adj_ptr=adj_ptr,
+                adj_nbr=adj_nbr, tet_slots=ts, edges=edges, edge_of_slot=eos, bsr_ptr=optr, bsr_col=ocol,
+                diag_slot=diag, ijk=np.ascontiguousarray(ijk, np.int32), n_side=base.n_side,
+                n_extra=int(ocol.shape[0] - bcol.shape[0]))
+
+
+def c4_scene(n: int = 57, k: int = 3, gap: float = 1e-3, side: float = 1.0, seed: int = 0, fast: bool = True):
     base = kuhn_grid(n, side=side)
     N0 = base.n_nodes
     nobj = k ** 3
@@ -492,7 +617,8 @@ def c4_scene(n: int = 57, k: int = 3, gap: float = 1e-3, side: float = 1.0, seed
             normals.append(np.broadcast_to(nrm, (hi.shape[0], 3)))
     pairs = np.concatenate(pairs)
     normals = np.concatenate(normals)
-    m = mesh_from_tets(X, tets, ijk=ijk, n_side=n, extra_pairs=pairs)
+    m = _replicate_with_extras(base, nobj, X, tets, ijk, pairs) if fast else \
+        mesh_from_tets(X, tets, ijk=ijk, n_side=n, extra_pairs=pairs)
     E_tet = np.repeat(np.asarray([(1e5, 1e6, 1e7)[o % 3] for o in range(nobj)]), base.n_tets)
     rng = np.random.default_rng([seed, 41])
     axes = rng.standard_normal((nobj, 3))
