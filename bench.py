@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--partitioned", action="store_true", help="use the partitioned path even at N=1")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
+    ap.add_argument("--no-big", action="store_true", help="skip the single-GPU C4 (5M) and C5 (20M) lines")
+    ap.add_argument("--big-steps", type=int, default=2, help="timed steps of the C4 / C5 lines")
     ap.add_argument("--pcg-storage", default="full", choices=["full", "sym"],
                     help="coarse PCG SpMV: full storage (k_spmv_sell) or the upper half (k_spmv_sym, NEXT#2)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -190,6 +192,9 @@ def run_agipc(args, world, rank, local_rank):
     dev = torch.device("cuda", local_rank)
     m, H, g, xcs, gen_s = build_inputs(args.side)
     h = P.Handle(local_rank)
+    # opt in to the PCG vector arena's persisting L2 window (agipc_set_option; the library clamps
+    # the size to the device maximum and releases the lines after every solve)
+    h.set_option(P.OPT_L2_PERSIST, 128 << 20)
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
     dm = P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device=dev)
     Hrp, Hcol, Hval = t(m.bsr_ptr, torch.int64), t(m.bsr_col, torch.int32), t(H, torch.float64)
@@ -300,7 +305,12 @@ def run_agipc(args, world, rank, local_rank):
         P.bsr_expand_upper(h, Hrp, Hcol, Urp, Ucol, dHu, out=dH, check=True)  # pattern validated once
         ne = args.e2e_steps or args.steps
 
-        def e2e_run(sym_upload):
+        hdf = torch.empty((m.n_nodes, 3), dtype=torch.float64).pin_memory()
+        ddf = torch.empty((m.n_nodes, 3), dtype=torch.float64, device=dev)
+
+        def e2e_run(sym_upload, full):
+            """full: the whole Newton step of the path -- host inputs -> tag -> map -> assemble ->
+            coarse PCG -> prolongation d_f = -U^T y_c -> D2H of the fine direction."""
             nonlocal hgc
             times, bi, bo = [], 0, 0
             for s in range(ne + 1):
@@ -323,28 +333,44 @@ def run_agipc(args, world, rank, local_rank):
                 h.sync_stream()
                 dxp.copy_(hx, non_blocking=True); dxc.copy_(hxc[k], non_blocking=True)
                 _, _, cs = step2.coarsen(dxp, dxc, dg, hessian_ready=h_ready)
-                if hgc.shape[0] < cs.n_slots:
-                    hgc = torch.empty((cs.n_slots, 3), dtype=torch.float64).pin_memory()
-                hgc[:cs.n_slots].copy_(cs.g_c, non_blocking=True)
+                if full:
+                    y_c, _ = step2.solve(cs)
+                    P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, y_c, -1.0, ddf)  # d_f = -U^T y_c
+                    hdf.copy_(ddf, non_blocking=True)
+                else:
+                    if hgc.shape[0] < cs.n_slots:
+                        hgc = torch.empty((cs.n_slots, 3), dtype=torch.float64).pin_memory()
+                    hgc[:cs.n_slots].copy_(cs.g_c, non_blocking=True)
                 e1.record()
                 torch.cuda.synchronize()
                 if s > 0:  # the first e2e step re-sizes step2's buffers
                     times.append(e0.elapsed_time(e1))
                     bi = (hx.numel() + hxc[k].numel() + (hHu.numel() if sym_upload else hH.numel()) + hg.numel()) * 8
-                    bo = cs.n_slots * 24
+                    bo = hdf.numel() * 8 if full else cs.n_slots * 24
             ev2 = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(ev2, op=dist.ReduceOp.MAX)
             return float(ev2.item()), bi, bo
 
-        v_full, bi_full, _ = e2e_run(False)
-        v_sym, bi, bo = e2e_run(True)
-        e2e = {"value": round(v_sym, 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
-               "d2h_bytes_per_step": int(bo),
-               "scope": "H2D(x_prev, x_cur, H_f in symmetric (diagonal + upper) storage P:1126, g_f) + "
-                        "agipc_bsr_expand_upper + tag + map + assemble + D2H(g_c), pinned host memory; the "
-                        "H_f/g_f upload and expansion run on a copy stream overlapped with tag + map",
+        v_step, bi, bo = e2e_run(True, True)
+        v_co, bi_co, bo_co = e2e_run(True, False)
+        v_full, bi_full, _ = e2e_run(False, False)
+        e2e = {"value": round(v_co, 3), "unit": "ms", "h2d_bytes_per_step": int(bi_co),
+               "d2h_bytes_per_step": int(bo_co),
+               "scope": "the headline metric (coarsen+assemble) end to end: H2D(x_prev, x_cur, H_f in symmetric "
+                        "(diagonal + upper) storage P:1126, g_f) + agipc_bsr_expand_upper + tag + map + assemble + "
+                        "D2H(g_c), pinned host memory; the H_f/g_f upload and expansion run on a copy stream "
+                        "overlapped with tag + map",
+               "newton_step": {"value": round(v_step, 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
+                               "d2h_bytes_per_step": int(bo),
+                               "scope": "the whole Newton step of the path through the public API: the same H2D + "
+                                        "tag + map + assemble + coarse PCG to 1e-3 + prolongation d_f = -U^T y_c "
+                                        "(P:871) + D2H(d_f, fine direction)"},
                "full_storage_upload": {"value": round(v_full, 3), "h2d_bytes_per_step": int(bi_full)}}
+
+    big = None
+    if world == 1 and not args.no_big:
+        big = measure_big_configs(P, h, dev, args.big_steps)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -377,10 +403,81 @@ def run_agipc(args, world, rank, local_rank):
         "coarse": {"n_coarse": sizes[-1][3], "levels": sizes[-1][4], "n3": sizes[-1][5], "n12": sizes[-1][6],
                    "n_slots": sizes[-1][0], "nnzb": sizes[-1][1]},
         "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
-        "next_rows": next_rows,
+        "next_rows": next_rows, "single_gpu_configs": big,
         "wall_s_timed_region": round(wall, 3), "input_generation_s": round(gen_s, 1),
     }
     emit(out)
+
+
+def measure_big_configs(P, h, dev, steps, warmup=1):
+    """BASELINE.json configs[3] and [4] on ONE B200 (their 1-GPU points; the multi-GPU runs use the
+    partitioned path): C4 = 27 objects x 57^3 nodes with contact blocks, per-object E, twist
+    iterates; C5 = the 272^3 grid (20,123,648 nodes) with the C3 strain-wall rule.  Per config:
+    coarsen+assemble ms per Newton step, the coarse PCG to 1e-3 (iterations/s), the full step."""
+    import torch
+    import synth
+    from paper_2605_04773_b200.step import CoarseningStep
+    hbm, _ = peaks()
+    out = {}
+    for name in ("C4", "C5"):
+        t0 = time.time()
+        if name == "C4":
+            sc = synth.c4_scene(n=57, k=3)
+            m = sc["mesh"]
+            H = synth.c4_hessian(sc)
+            g = synth.fine_gradient(m.n_nodes, seed=4)
+            xp, xc = synth.c4_iterates(sc)
+            desc = ("C4: 27 objects of 57^3 nodes (5,000,211) on a 3x3x3 lattice, contact blocks between facing "
+                    "faces, E cycling 1e5/1e6/1e7, per-object twist 0.5 -> 0.501, theta=5e-5")
+            xcs = [xc]
+        else:
+            m = synth.kuhn_grid(272)
+            H = synth.fine_hessian(m, E=1e5)
+            g = synth.fine_gradient(m.n_nodes)
+            xp = m.X
+            xcs = [synth.walls(m, k)[1] for k in range(2)]
+            desc = "C5: 272^3 Kuhn grid (20,123,648 nodes), strain walls k = step mod 2, theta=5e-5, E=1e5"
+        gen = time.time() - t0
+        t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+        dm = P.DeviceMesh.from_arrays(m.tets, m.adj_ptr, m.adj_nbr, m.tet_slots, m.X, device=dev)
+        Hrp, Hcol, Hval = t(m.bsr_ptr, torch.int64), t(m.bsr_col, torch.int32), t(H, torch.float64)
+        del H
+        gd, xpd = t(g, torch.float64), t(xp, torch.float64)
+        xcd = [t(x, torch.float64) for x in xcs]
+        step = CoarseningStep(h, dm, Hrp, Hcol, Hval, check_every=64, max_iters=100000)
+        for s in range(warmup):
+            cs = step.coarsen(xpd, xcd[s % len(xcd)], gd)[2]
+            step.solve(cs)
+        torch.cuda.synchronize()
+        co, pc, its, sizes = [], [], 0, None
+        for s in range(steps):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            nf, info, cs = step.coarsen(xpd, xcd[(warmup + s) % len(xcd)], gd)
+            e[1].record()
+            x, st = step.solve(cs)
+            e[2].record()
+            torch.cuda.synchronize()
+            co.append(e[0].elapsed_time(e[1]))
+            pc.append(e[1].elapsed_time(e[2]))
+            its += st["iters"]
+            sizes = (info["n_coarse"], info["n_levels"], cs.n3, cs.n12, cs.n_slots, cs.nnzb)
+        ns, nb = sizes[4], sizes[5]
+        spmv_bytes = 76 * nb + 8 * (ns + 1) + 48 * ns
+        ms_iter = sum(pc) / max(1, its)
+        out[name] = {"workload": desc, "nodes": m.n_nodes, "fine_blocks": int(Hcol.shape[0]),
+                     "coarsen_assemble_ms": round(statistics.mean(co), 3),
+                     "ms_per_step": round(statistics.mean(a + b for a, b in zip(co, pc)), 2),
+                     "pcg_iters_per_step": round(its / steps, 1),
+                     "pcg_iters_per_s": round(its / (sum(pc) * 1e-3), 1),
+                     "pcg_iteration_gbs_spmv_model": round(spmv_bytes / (ms_iter * 1e-3) / 1e9, 1),
+                     "pcg_iteration_frac_of_hbm_spmv_model": round(spmv_bytes / (ms_iter * 1e-3) / 1e9 / hbm, 3),
+                     "coarse": {"n_coarse": sizes[0], "levels": sizes[1], "n3": sizes[2], "n12": sizes[3],
+                                "n_slots": ns, "nnzb": nb},
+                     "steps": steps, "warmup": warmup, "input_generation_s": round(gen, 1)}
+        del step, dm, Hrp, Hcol, Hval, gd, xpd, xcd
+        torch.cuda.empty_cache()
+    return out
 
 
 def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=5):
@@ -498,16 +595,20 @@ def run_partitioned(args, world, rank, local_rank):
     import torch.distributed as dist
     import paper_2605_04773_b200 as P
     from paper_2605_04773_b200 import partition as pt
-    from paper_2605_04773_b200.dist import Comm, DistCoarseningStep
+    from paper_2605_04773_b200.dist import Comm, DistCoarseningStep, LibComm
 
     ndev = torch.cuda.device_count()
     dev_i = local_rank % max(1, ndev)
     torch.cuda.set_device(dev_i)
     dev = torch.device("cuda", dev_i)
-    comm = Comm()
+    tcomm = Comm()  # once-per-mesh set-up (halo requests) over the process group
     lm, Hl, Hh, g, disp, gen_s = build_partition(args.side, world, rank)
-    pt.exchange_requests(lm, world, comm.alltoall_i64)
+    pt.exchange_requests(lm, world, tcomm.alltoall_i64)
     h = P.Handle(dev_i)
+    h.set_option(P.OPT_L2_PERSIST, 128 << 20)
+    # the step's exchanges: the library's own NCCL communicator (GPU runs), or the torch process
+    # group staging through host memory (gloo: several ranks sharing one GPU)
+    comm = LibComm(h) if args.backend == "nccl" else tcomm
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
     Hld, Hhd, gd = t(Hl, torch.float64), t(Hh, torch.float64), t(g, torch.float64)
     xp = t(lm.X, torch.float64)
@@ -549,8 +650,8 @@ def run_partitioned(args, world, rank, local_rank):
     iters = sum(z[2] for z in sizes)
     vec = torch.tensor([statistics.mean(coarsen), statistics.mean([a + b for a, b in zip(coarsen, pcg)]), sum(pcg)],
                        dtype=torch.float64)
-    dist.all_reduce(vec, op=dist.ReduceOp.MAX) if comm.stage else None
-    if not comm.stage:
+    dist.all_reduce(vec, op=dist.ReduceOp.MAX) if tcomm.stage else None
+    if not tcomm.stage:
         vd = vec.to(dev)
         dist.all_reduce(vd, op=dist.ReduceOp.MAX)
         vec = vd.cpu()
@@ -599,7 +700,7 @@ def run_partitioned(args, world, rank, local_rank):
                 bi = (hX.numel() + hxc[k].numel() + hHl.numel() + hHh.numel() + hg.numel()) * 8
                 bo = ns * 24
         ev2 = torch.tensor([statistics.mean(e2e_t)], dtype=torch.float64)
-        if not comm.stage:
+        if not tcomm.stage:
             ev2 = ev2.to(dev)
         dist.all_reduce(ev2, op=dist.ReduceOp.MAX)
         e2e = {"value": round(float(ev2.item()), 3), "unit": "ms", "h2d_bytes_per_step": int(bi),
@@ -618,7 +719,10 @@ def run_partitioned(args, world, rank, local_rank):
                                "gs=32, affine_threshold=32, distributed block-Jacobi PCG to 1e-3 from x0=0",
                    "nodes": world * args.side ** 3, "nodes_per_rank": args.side ** 3,
                    "l2": "flushed between steps (256 MB write); per-rank fine BSR 1.1 GB > L2",
-                   "parallelism": f"{world} ranks, partitioned ({comm.world} x {dist.get_backend()})"},
+                   "parallelism": f"{world} ranks, partitioned",
+                   "transport": ("libagipc NCCL communicator (agipc_comm_init; exchanges and the PCG "
+                                 "all-reduces / halo inside the library, captured in the PCG graph)"
+                                 if isinstance(comm, LibComm) else f"torch.distributed {dist.get_backend()}")},
         "pcg_iters_per_s": round(iters / (pcg_ms_sum * 1e-3), 1) if pcg_ms_sum > 0 else None,
         "pcg_iters_per_step": round(iters / args.steps, 1),
         "roofline": {"kernel": "k_spmv_sell (PCG SpMV + p.q; owned + halo rows)", "bound": "hbm",

@@ -63,7 +63,7 @@ typedef enum {
   AGIPC_ERANGE = 2,       /* an index does not fit in int32                                   */
   AGIPC_ENOSPACE = 3,     /* output capacity too small; required sizes were written back     */
   AGIPC_ECUDA = 4,        /* a CUDA runtime call failed (message in agipc_last_error)         */
-  AGIPC_ENCCL = 5,        /* reserved for the multi-GPU path                                  */
+  AGIPC_ENCCL = 5,        /* NCCL missing or an NCCL call failed (multi-GPU path)             */
   AGIPC_EDEGENERATE = 6,  /* a tet with det(D_m) == 0 at rest                    */
   AGIPC_ESINGULAR = 7,    /* a block-Jacobi diagonal block is missing or singular     */
   AGIPC_EINDEFINITE = 8,  /* p^T A p <= 0 in PCG                                      */
@@ -84,6 +84,45 @@ AGIPC_API agipc_status agipc_set_values_event(agipc_handle h, void *event);
 AGIPC_API const char *agipc_last_error(agipc_handle h);
 AGIPC_API const char *agipc_status_string(agipc_status s);
 AGIPC_API void agipc_version(int *major /*[host]*/, int *minor /*[host]*/);
+/* Options (agipc_set_option):
+ *  AGIPC_OPT_CHECK_SYMMETRY (0/1, default 0): agipc_assemble_coarse first checks the precondition
+ *    it relies on (R22: H_fine bitwise symmetric, B_ji == B_ij^T for every stored block,
+ *    the transposed block present) in one extra pass + host sync, and returns AGIPC_EINVAL with the
+ *    number of violations if it fails.
+ *  AGIPC_OPT_L2_PERSIST (bytes, default 0): sets the device's persisting-L2 limit ONCE, now (the
+ *    only device-wide setting the library ever changes, and only on this request), and lets the
+ *    PCG solves place their vector arena in a persisting access-policy window of that size;
+ *    the persisting lines are released after every solve.  0 = plain caching (no window).
+ *  AGIPC_OPT_COMM_ALWAYS (0/1, default 0): issue the NCCL all-reduces of agipc_dpcg_solve even on
+ *    a one-rank communicator (where the sum is the identity and they are skipped) -- lets a
+ *    single-GPU test run the captured NCCL path.
+ *  AGIPC_OPT_DETERMINISTIC (0/1, default 0): the 12-DoF (large) coarse rows are assembled without
+ *    fp64 atomics -- every 32-children chunk writes its partial diagonal block, g_c part and one
+ *    record per interface block, and a fixed-order reduction sums them -- so H_c and g_c (and with
+ *    them the PCG iterates and iteration counts) are bitwise reproducible run to run.  Default: the
+ *    faster atomic accumulation, reproducible to rounding (inside the 1e-12 |.|-bound contract).
+ *    The coarse PCG is bitwise reproducible either way (per-slice p.q partials, fixed-order sums). */
+#define AGIPC_OPT_CHECK_SYMMETRY 1
+#define AGIPC_OPT_L2_PERSIST 2
+#define AGIPC_OPT_COMM_ALWAYS 3
+#define AGIPC_OPT_DETERMINISTIC 4
+AGIPC_API agipc_status agipc_set_option(agipc_handle h, int option, int64_t value);
+
+/* Workspace.  By default the handle cudaMallocs grow-only named scratch buffers on first use.
+ * agipc_set_workspace hands it a caller-owned device arena instead (e.g. a torch uint8 tensor;
+ * 256-byte aligned base): every scratch buffer is then carved from it by a bump pointer and the
+ * library never allocates device memory; a call whose scratch does not fit returns
+ * AGIPC_ENOSPACE (nothing is freed or moved while a call runs) -- register a larger arena and
+ * retry.  set_workspace synchronises the stream, releases the internal buffers and re-places all
+ * scratch on next use; ws = NULL returns to internal allocation.  The arena must stay valid
+ * until the next set_workspace / destroy.  EINVAL during a split-phase distributed solve.
+ * agipc_workspace_size: bytes to register -- the largest of (the sum of the largest size every
+ * scratch buffer of this handle has needed so far) and an a-priori estimate for one Newton step
+ * (tag, map, assemble, coarse PCG) on a mesh of these sizes. */
+AGIPC_API agipc_status agipc_workspace_size(agipc_handle h, int64_t n_nodes, int64_t n_tets, int64_t nnz_adj,
+                                            int64_t nnzb_fine, size_t *bytes /*[host]*/);
+AGIPC_API agipc_status agipc_set_workspace(agipc_handle h, void *ws, size_t bytes);
+
 /* Number of kernels this handle has enqueued since creation ([host] counter). */
 AGIPC_API int64_t agipc_kernel_launches(agipc_handle h);
 
@@ -294,7 +333,8 @@ AGIPC_API agipc_status agipc_tag_rods(agipc_handle h, int64_t n_segs, const int3
  * buffers, capacity retry on col/seg_ptr: ENOSPACE with nnzb set; synchronises), and
  * agipc_triplet_reduce streams the values of every Newton step (thread per unique block,
  * in-order sums, bit-identical to the sequential definition).
- *   ti, tj : [n_trip] row / column ids (0 <= ti < n_rows; EINVAL otherwise)
+ *   ti, tj : [n_trip] row / column ids (0 <= ti < n_rows, tj >= 0; EINVAL otherwise, checked before
+ *            any use; the columns need not be square: the unique blocks carry them as given)
  *   tval   : [n_trip][3][3];  val : out [nnzb][3][3] */
 typedef struct {
   int64_t n_rows, n_trip;  /* [host] set by plan */
@@ -369,6 +409,53 @@ AGIPC_API agipc_status agipc_prolongate(agipc_handle h, const agipc_mesh *mesh, 
  * Every rank applies the same scalar logic to the same reduced sums, so all ranks stop at the
  * same iteration.  Vectors: owned slots 0..n_rows-1, ghost slots n_rows..n_rows+n_ghost_slots-1
  * (the recv buffer holds them in that order; A_halo's columns index them). */
+/* ---- library-owned communicator (NCCL, resolved at run time) ---------------------------
+ * The north star's exchanges run inside libagipc: one NCCL communicator per handle (agipc_comm_init),
+ * collectives on the handle's stream.  The caller only moves the 128-byte unique id (rank 0 calls
+ * agipc_comm_unique_id and broadcasts it, e.g. over a torch.distributed process group).
+ * AGIPC_ENCCL: libnccl.so.2 could not be loaded (or $AGIPC_NCCL_LIB) or an NCCL call failed.
+ *
+ * agipc_comm_allgather_scan (exchange 2): local [k] int64 device values of this rank ->
+ *   all [nranks][k] (every rank's values), scan [2k]: scan[j] = sum over ranks r' < rank of
+ *   all[r'][j] (the exclusive prefix = this rank's global offset), scan[k + j] = the total.
+ *   Asynchronous.
+ * agipc_comm_alltoall_i64: send[q] goes to rank q, recv[q] comes from rank q (device, [nranks]).
+ * agipc_halo_exchange (exchanges 1 and 3): rows of row_bytes bytes (multiple of 4).  For every peer
+ *   q: the rows src[send_idx[send_ptr[q] .. send_ptr[q+1])] are sent to peer_rank[q], and the rows
+ *   received from it land at dst rows [recv_ptr[q], recv_ptr[q+1]) (dst = the ghost region, e.g.
+ *   x + 3 n_owned).  Grouped send/recv, asynchronous. */
+#define AGIPC_UNIQUE_ID_BYTES 128
+typedef struct {
+  int n_peers;
+  const int *peer_rank;      /* [host] [n_peers] */
+  const int64_t *send_ptr;   /* [host] [n_peers+1] */
+  const int32_t *send_idx;   /* device [send_ptr[n_peers]] rows of src to send */
+  const int64_t *recv_ptr;   /* [host] [n_peers+1] rows of dst to receive */
+} agipc_halo;
+
+AGIPC_API agipc_status agipc_comm_unique_id(void *unique_id /*[host] out, 128 B*/);
+AGIPC_API agipc_status agipc_comm_init(agipc_handle h, const void *unique_id /*[host] 128 B*/, int nranks, int rank);
+AGIPC_API agipc_status agipc_comm_info(agipc_handle h, int *nranks, int *rank, int *nccl_version /*[host]*/);
+AGIPC_API agipc_status agipc_comm_allgather_scan(agipc_handle h, const int64_t *local, int k, int64_t *all,
+                                                 int64_t *scan);
+AGIPC_API agipc_status agipc_comm_alltoall_i64(agipc_handle h, const int64_t *send, int64_t *recv);
+AGIPC_API agipc_status agipc_halo_exchange(agipc_handle h, const agipc_halo *halo, const void *src, int row_bytes,
+                                           void *dst);
+
+/* agipc_dpcg_solve: the whole distributed block-Jacobi PCG (the split-phase iteration below with
+ * its reductions and halo inside the library): per iteration the z values of the send slots go to
+ * the peers by NCCL send/recv (exchange 4), the p.q and [r.z, r.r] partials are summed by
+ * ncclAllReduce, and check_every iterations are captured -- NCCL calls included -- in one CUDA
+ * graph; the host polls the device done flag between graph launches, as agipc_pcg_solve.
+ *   A, A_halo, n_ghost_slots, b : as agipc_dpcg_setup (x0 = 0);  x : out [A->n_rows][3]
+ *   slots : the PCG halo -- send_idx = this rank's slots to send (coarse_halo send lists),
+ *           recv_ptr = the ghost-slot ranges (rows of the ghost region, [0, n_ghost_slots))
+ * Every rank must call it with the same rel_tol / max_iters / check_every; all stop together.
+ * Singular diagonal blocks on any rank stop every rank (ESINGULAR everywhere). */
+AGIPC_API agipc_status agipc_dpcg_solve(agipc_handle h, const agipc_bsr *A, const agipc_bsr *A_halo,
+                                        int64_t n_ghost_slots, const agipc_halo *slots, const double *b, double *x,
+                                        double rel_tol, int max_iters, int check_every, agipc_pcg_stats *stats);
+
 typedef struct {
   int64_t n_rows, nnzb;  /* [host] out */
   int64_t cap_nnzb;      /* [host] in  */

@@ -11,8 +11,10 @@ Entry points (same names as the C ABI, include/agipc.h):
   assemble_coarse  step 3, supp Alg S3/S4 + Eq 4
   pcg_solve        step 4, block-Jacobi PCG
   prolongate       NEXT#1, d_f = U^T d_c
-Multi-GPU: gather_rows, coarse_halo, assemble_halo, DistPcg (the rank-local
-pieces; paper_2605_04773_b200.dist drives the exchanges).
+Multi-GPU: the library-owned NCCL communicator (Handle.comm_init, comm_unique_id,
+comm_allgather_scan, comm_alltoall_i64, halo_exchange, dpcg_solve) and the rank-local pieces
+(gather_rows, coarse_halo, assemble_halo, DistPcg for the split-phase solve over gloo);
+paper_2605_04773_b200.dist composes them.
 """
 from __future__ import annotations
 
@@ -63,6 +65,11 @@ class _HaloMatrix(C.Structure):
                 ("col", C.c_void_p), ("val", C.c_void_p)]
 
 
+class _Halo(C.Structure):
+    _fields_ = [("n_peers", C.c_int), ("peer_rank", C.c_void_p), ("send_ptr", C.c_void_p), ("send_idx", C.c_void_p),
+                ("recv_ptr", C.c_void_p)]
+
+
 class _TripletPlan(C.Structure):
     _fields_ = [("n_rows", C.c_int64), ("n_trip", C.c_int64), ("nnzb", C.c_int64), ("cap_nnzb", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col", C.c_void_p), ("seg_ptr", C.c_void_p), ("seg_idx", C.c_void_p)]
@@ -83,7 +90,11 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_gather_rows", "agipc_coarse_halo", "agipc_assemble_halo", "agipc_dpcg_setup", "agipc_dpcg_pack",
            "agipc_dpcg_spmv", "agipc_dpcg_update", "agipc_dpcg_status", "agipc_dpcg_finish", "agipc_tag_shells",
            "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym",
-           "agipc_bsr_expand_upper", "agipc_set_values_event"]
+           "agipc_bsr_expand_upper", "agipc_set_values_event", "agipc_set_option", "agipc_workspace_size",
+           "agipc_set_workspace", "agipc_comm_unique_id", "agipc_comm_init", "agipc_comm_info",
+           "agipc_comm_allgather_scan", "agipc_comm_alltoall_i64", "agipc_halo_exchange", "agipc_dpcg_solve"]
+
+OPT_CHECK_SYMMETRY, OPT_L2_PERSIST, OPT_COMM_ALWAYS, OPT_DETERMINISTIC = 1, 2, 3, 4  # include/agipc.h AGIPC_OPT_*
 
 
 def lib():
@@ -134,6 +145,17 @@ def lib():
         L.agipc_dpcg_update.argtypes = [P, P]
         L.agipc_dpcg_status.argtypes = [P, C.POINTER(i32), C.POINTER(_PcgStats)]
         L.agipc_dpcg_finish.argtypes = [P, P, P, C.POINTER(_PcgStats)]
+        L.agipc_set_option.argtypes = [P, i32, i64]
+        L.agipc_workspace_size.argtypes = [P, i64, i64, i64, i64, C.POINTER(C.c_size_t)]
+        L.agipc_set_workspace.argtypes = [P, P, C.c_size_t]
+        L.agipc_comm_unique_id.argtypes = [P]
+        L.agipc_comm_init.argtypes = [P, P, i32, i32]
+        L.agipc_comm_info.argtypes = [P, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+        L.agipc_comm_allgather_scan.argtypes = [P, P, i32, P, P]
+        L.agipc_comm_alltoall_i64.argtypes = [P, P, P]
+        L.agipc_halo_exchange.argtypes = [P, C.POINTER(_Halo), P, i32, P]
+        L.agipc_dpcg_solve.argtypes = [P, C.POINTER(_Bsr), C.POINTER(_Bsr), i64, C.POINTER(_Halo), P, P, f64, i32, i32,
+                                       C.POINTER(_PcgStats)]
         for name in EXPORTS:
             if name not in ("agipc_last_error", "agipc_status_string", "agipc_version", "agipc_kernel_launches",
                             "agipc_profile_read"):
@@ -203,6 +225,41 @@ class Handle:
         buf = (_ProfEntry * 16)()
         n = lib().agipc_profile_read(self._h, buf, 16)
         return {buf[i].name.decode(): (int(buf[i].count), float(buf[i].total_ms)) for i in range(n)}
+
+    def set_option(self, option: int, value: int):
+        """agipc_set_option (OPT_CHECK_SYMMETRY, OPT_L2_PERSIST)."""
+        self._check(lib().agipc_set_option(self._h, int(option), int(value)))
+
+    def workspace_size(self, n_nodes=0, n_tets=0, nnz_adj=0, nnzb_fine=0) -> int:
+        """agipc_workspace_size: bytes of caller-owned scratch to register (set_workspace)."""
+        b = C.c_size_t(0)
+        self._check(lib().agipc_workspace_size(self._h, int(n_nodes), int(n_tets), int(nnz_adj), int(nnzb_fine),
+                                               C.byref(b)))
+        return int(b.value)
+
+    def set_workspace(self, ws: torch.Tensor | None):
+        """Hand the library a caller-owned device arena (uint8 CUDA tensor, kept alive here), or None
+        to return to internal allocation (agipc_set_workspace)."""
+        if ws is None:
+            self._check(lib().agipc_set_workspace(self._h, None, 0))
+        else:
+            if ws.dtype != torch.uint8 or not ws.is_cuda or not ws.is_contiguous():
+                raise ValueError("workspace must be a contiguous uint8 CUDA tensor")
+            self._check(lib().agipc_set_workspace(self._h, C.c_void_p(ws.data_ptr()), ws.numel()))
+        self._ws = ws
+
+    def comm_init(self, unique_id: bytes, nranks: int, rank: int):
+        """agipc_comm_init: the library's own NCCL communicator (unique_id from comm_unique_id() on
+        rank 0, moved to the other ranks by the caller)."""
+        if len(unique_id) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        self._check(lib().agipc_comm_init(self._h, buf, int(nranks), int(rank)))
+
+    def comm_info(self):
+        a, b, v = C.c_int(), C.c_int(), C.c_int()
+        self._check(lib().agipc_comm_info(self._h, C.byref(a), C.byref(b), C.byref(v)))
+        return dict(nranks=a.value, rank=b.value, nccl_version=v.value)
 
     def close(self):
         if self._h:
@@ -504,6 +561,70 @@ class DistPcg:
         self.h._check(lib().agipc_dpcg_finish(self.h._h, _p(self.red), _p(x), C.byref(s)), allow=(NOT_CONVERGED,))
         return dict(iters=int(s.iters), status=int(s.status), rel_residual=float(s.rel_residual),
                     b_norm=float(s.b_norm))
+
+
+def comm_unique_id() -> bytes:
+    """agipc_comm_unique_id: a fresh NCCL unique id (128 bytes) for agipc_comm_init."""
+    buf = C.create_string_buffer(128)
+    st = lib().agipc_comm_unique_id(buf)
+    if st != OK:
+        raise AgipcError(st, "agipc_comm_unique_id failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+class Halo:
+    """agipc_halo: per-peer send lists (device int32 indices) and receive row ranges."""
+
+    def __init__(self, peer_rank, send_ptr, send_idx, recv_ptr):
+        P = len(peer_rank)
+        self.n_peers = P
+        self._pr = (C.c_int * max(P, 1))(*[int(v) for v in peer_rank])
+        self._sp = (C.c_int64 * (P + 1))(*[int(v) for v in send_ptr])
+        self._rp = (C.c_int64 * (P + 1))(*[int(v) for v in recv_ptr])
+        self.send_idx = send_idx
+        self.c = _Halo(P, C.cast(self._pr, C.c_void_p), C.cast(self._sp, C.c_void_p),
+                       _p(send_idx) if send_idx is not None and send_idx.numel() else None, C.cast(self._rp, C.c_void_p))
+
+
+def comm_allgather_scan(h: Handle, local):
+    """Exchange 2: local int64 [k] (device) -> (all [nranks, k], scan [2k]: exclusive prefix of this
+    rank, then the totals)."""
+    k = local.shape[0]
+    nr = h.comm_info()["nranks"]
+    all_ = torch.empty((nr, k), dtype=torch.int64, device=local.device)
+    scan = torch.empty(2 * k, dtype=torch.int64, device=local.device)
+    h._check(lib().agipc_comm_allgather_scan(h._h, _p(local), int(k), _p(all_), _p(scan)))
+    return all_, scan
+
+
+def comm_alltoall_i64(h: Handle, send):
+    recv = torch.empty_like(send)
+    h._check(lib().agipc_comm_alltoall_i64(h._h, _p(send), _p(recv)))
+    return recv
+
+
+def halo_exchange(h: Handle, halo: Halo, src, dst_ghost):
+    """Rows of src (owned) to the peers; rows from the peers into dst_ghost (the ghost region)."""
+    rb = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
+    h._check(lib().agipc_halo_exchange(h._h, C.byref(halo.c), _p(src), int(rb), _p(dst_ghost)))
+
+
+def dpcg_solve(h: Handle, row_ptr, col, val, h_row_ptr, h_col, h_val, n_ghost_slots: int, slots: Halo, b, x=None,
+               rel_tol: float = 1e-3, max_iters: int = 10000, check_every: int = 32):
+    """agipc_dpcg_solve: the distributed PCG with its NCCL exchanges inside the library."""
+    n = row_ptr.shape[0] - 1
+    if x is None:
+        x = torch.empty((n, 3), dtype=torch.float64, device=b.device)
+    A = _Bsr(n, col.shape[0], _p(row_ptr), _p(col), _p(val))
+    Ah = None if h_row_ptr is None else _Bsr(n, h_col.shape[0], _p(h_row_ptr), _p(h_col) if h_col.numel() else None,
+                                             _p(h_val) if h_val.numel() else None)
+    stats = _PcgStats()
+    st = lib().agipc_dpcg_solve(h._h, C.byref(A), C.byref(Ah) if Ah is not None else None, int(n_ghost_slots),
+                                C.byref(slots.c) if slots is not None else None, _p(b), _p(x), float(rel_tol),
+                                int(max_iters), int(check_every), C.byref(stats))
+    h._check(st, allow=(NOT_CONVERGED,))
+    return x, dict(iters=int(stats.iters), status=int(stats.status), rel_residual=float(stats.rel_residual),
+                   b_norm=float(stats.b_norm))
 
 
 def _tag_elems(fn, h, elems, el_slots, x_rest, x_prev, x_cur, threshold, slot_tags, reset, norm, count):

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libagipc.so")
-SOURCES = ["api.cu", "tag.cu", "map.cu", "assemble.cu", "pcg.cu", "prolong.cu", "dist.cu", "triplets.cu"]
+SOURCES = ["api.cu", "tag.cu", "map.cu", "assemble.cu", "pcg.cu", "prolong.cu", "dist.cu", "triplets.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed: %s\n%s" % (" ".join(cmd), out.decode()))
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-                           "-o", tmp] + objs)
+                           "-o", tmp] + objs + ["-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

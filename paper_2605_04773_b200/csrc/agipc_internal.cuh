@@ -58,12 +58,25 @@ struct agipc_handle_s {
   std::string err;
   int64_t launches = 0;
   std::unordered_map<std::string, WsBuf> ws;
+  // caller-owned workspace (agipc_set_workspace): named buffers are carved from [arena,
+  // arena + arena_cap) by a bump pointer; nullptr = the library cudaMallocs them itself
+  char *arena = nullptr;
+  size_t arena_cap = 0, arena_top = 0;
+  uint64_t ws_gen = 0;  // bumped whenever a named buffer moves (captured PCG graphs key on it)
+  std::unordered_map<std::string, size_t> ws_max;  // largest (padded) size ever requested per name
+  size_t ws_high = 0;                               // sum of ws_max: agipc_workspace_size
+  // agipc_set_option
+  int opt_check_sym = 0;     // AGIPC_OPT_CHECK_SYMMETRY
+  size_t opt_l2_persist = 0;  // AGIPC_OPT_L2_PERSIST (bytes; 0 = no persisting window)
+  int opt_comm_always = 0;    // AGIPC_OPT_COMM_ALWAYS
+  int opt_deterministic = 0;  // AGIPC_OPT_DETERMINISTIC
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
   size_t tail_smem = 0;
-  cudaEvent_t values_event = nullptr;  // agipc_set_values_event (one-shot, consumed by assemble)  // build_map: dynamic smem the tail kernel attribute allows (set once)
+  cudaEvent_t values_event = nullptr;  // agipc_set_values_event (one-shot, consumed by assemble)
   struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)
+  struct Comm *comm = nullptr;  // NCCL communicator (comm.cu, agipc_comm_init)
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;
   std::vector<ProfPending> prof_pending;
@@ -109,8 +122,9 @@ struct ProfScope {
 
 agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...);
 
-// Grow-only named device workspace (cudaMalloc only when a buffer must grow).
-void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st);
+// Grow-only named device workspace (cudaMalloc only when a buffer must grow, or carved from the
+// caller's arena).  *fresh (nullable) = the buffer was (re)placed, its content is undefined.
+void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st, bool *fresh = nullptr);
 // Pinned host scratch of at least `bytes`.
 void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
 

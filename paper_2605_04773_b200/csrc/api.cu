@@ -1,4 +1,6 @@
 // Handle management, errors, workspace and the generic device-wide scan of libagipc.
+#include <algorithm>
+
 #include "agipc_internal.cuh"
 
 agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...) {
@@ -13,23 +15,46 @@ agipc_status set_err(agipc_handle h, agipc_status st, const char *fmt, ...) {
   return st;
 }
 
-void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st) {
+static size_t ws_pad(size_t bytes) { return ((bytes + bytes / 8 + 256) + 255) & ~(size_t)255; }
+
+void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st, bool *fresh) {
   WsBuf &b = h->ws[name];
+  if (fresh) *fresh = false;
   if (b.bytes < bytes) {
-    if (b.ptr) {
-      cudaStreamSynchronize(h->stream);  // the old buffer may still be in use
-      cudaFree(b.ptr);
-      b.ptr = nullptr;
-      b.bytes = 0;
+    const size_t want = ws_pad(bytes);  // headroom: sizes vary between Newton steps
+    size_t &mx = h->ws_max[name];
+    if (want > mx) {
+      h->ws_high += want - mx;
+      mx = want;
     }
-    size_t want = bytes + bytes / 8 + 256;  // headroom: sizes vary between Newton steps
-    cudaError_t e = cudaMalloc(&b.ptr, want);
-    if (e != cudaSuccess) {
-      b.ptr = nullptr;
-      *st = set_err(h, AGIPC_ECUDA, "workspace '%s' (%zu bytes): %s", name, want, cudaGetErrorString(e));
-      return nullptr;
+    if (h->arena) {  // caller-owned workspace: bump allocation, never freed until set_workspace
+      if (h->arena_top + want > h->arena_cap) {
+        *st = set_err(h, AGIPC_ENOSPACE,
+                      "workspace '%s' needs %zu bytes: %zu of the %zu registered are in use; "
+                      "register at least agipc_workspace_size() bytes",
+                      name, want, h->arena_top, h->arena_cap);
+        return nullptr;
+      }
+      b.ptr = h->arena + h->arena_top;
+      b.bytes = want;
+      h->arena_top += want;
+    } else {
+      if (b.ptr) {
+        cudaStreamSynchronize(h->stream);  // the old buffer may still be in use
+        cudaFree(b.ptr);
+        b.ptr = nullptr;
+        b.bytes = 0;
+      }
+      cudaError_t e = cudaMalloc(&b.ptr, want);
+      if (e != cudaSuccess) {
+        b.ptr = nullptr;
+        *st = set_err(h, AGIPC_ECUDA, "workspace '%s' (%zu bytes): %s", name, want, cudaGetErrorString(e));
+        return nullptr;
+      }
+      b.bytes = want;
     }
-    b.bytes = want;
+    h->ws_gen += 1;
+    if (fresh) *fresh = true;
   }
   *st = AGIPC_OK;
   return b.ptr;
@@ -57,6 +82,8 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st) {
 
 void pcg_graph_free(PcgGraph *g);  // pcg.cu
 void dpcg_free(struct DPcg *d);    // pcg.cu
+bool dpcg_active(agipc_handle h);  // pcg.cu
+void comm_free(agipc_handle h);    // comm.cu
 
 cudaEvent_t prof_event(agipc_handle h) {
   if (!h->prof_pool.empty()) {
@@ -125,8 +152,10 @@ agipc_status agipc_destroy(agipc_handle h) {
   if (!h) return AGIPC_EINVAL;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
-  for (auto &kv : h->ws)
-    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  if (!h->arena)
+    for (auto &kv : h->ws)
+      if (kv.second.ptr) cudaFree(kv.second.ptr);
+  comm_free(h);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pcg) pcg_graph_free(h->pcg);
   if (h->dpcg) dpcg_free(h->dpcg);
@@ -145,6 +174,63 @@ agipc_status agipc_set_stream(agipc_handle h, void *stream) {
 agipc_status agipc_set_values_event(agipc_handle h, void *event) {
   if (!h) return AGIPC_EINVAL;
   h->values_event = (cudaEvent_t)event;
+  return AGIPC_OK;
+}
+
+agipc_status agipc_set_option(agipc_handle h, int option, int64_t value) {
+  if (!h) return AGIPC_EINVAL;
+  switch (option) {
+    case AGIPC_OPT_CHECK_SYMMETRY:
+      h->opt_check_sym = value != 0;
+      return AGIPC_OK;
+    case AGIPC_OPT_COMM_ALWAYS:
+      h->opt_comm_always = value != 0;
+      return AGIPC_OK;
+    case AGIPC_OPT_DETERMINISTIC:
+      h->opt_deterministic = value != 0;
+      return AGIPC_OK;
+    case AGIPC_OPT_L2_PERSIST: {
+      if (value < 0) return set_err(h, AGIPC_EINVAL, "set_option: negative L2 size");
+      CU_TRY(h, cudaSetDevice(h->device));
+      int max_persist = 0;
+      CU_TRY(h, cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device));
+      size_t v = std::min((size_t)value, (size_t)std::max(0, max_persist));
+      // the one place the library changes a device-wide limit, on the caller's request
+      if (v > 0) CU_TRY(h, cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, v));
+      h->opt_l2_persist = v;
+      return AGIPC_OK;
+    }
+  }
+  return set_err(h, AGIPC_EINVAL, "set_option: unknown option %d", option);
+}
+
+agipc_status agipc_workspace_size(agipc_handle h, int64_t n_nodes, int64_t n_tets, int64_t nnz_adj, int64_t nnzb_fine,
+                                  size_t *bytes) {
+  if (!h || !bytes) return AGIPC_EINVAL;
+  if (n_nodes < 0 || n_tets < 0 || nnz_adj < 0 || nnzb_fine < 0)
+    return set_err(h, AGIPC_EINVAL, "workspace_size: negative size");
+  // a priori estimate of one Newton step (tag, map, assemble, coarse PCG):
+  // per-node, per-adjacency-slot and per-fine-block bytes of the named buffers, the coarse system
+  // taken as large as the fine one (the ENOSPACE retry covers the rare larger case)
+  const double est = 1.25 * (160.0 * n_nodes + 12.0 * nnz_adj + 8.0 * n_tets + 220.0 * nnzb_fine) + (1 << 22);
+  *bytes = std::max(h->ws_high, (size_t)est);
+  return AGIPC_OK;
+}
+
+agipc_status agipc_set_workspace(agipc_handle h, void *ws, size_t bytes) {
+  if (!h) return AGIPC_EINVAL;
+  if (ws && ((uintptr_t)ws & 255)) return set_err(h, AGIPC_EINVAL, "set_workspace: base must be 256-byte aligned");
+  if (dpcg_active(h)) return set_err(h, AGIPC_EINVAL, "set_workspace: a distributed solve is in progress");
+  CU_TRY(h, cudaSetDevice(h->device));
+  CU_TRY(h, cudaStreamSynchronize(h->stream));
+  if (!h->arena)
+    for (auto &kv : h->ws)
+      if (kv.second.ptr) cudaFree(kv.second.ptr);
+  h->ws.clear();  // every named buffer is re-placed (fresh) on its next use
+  h->arena = (char *)ws;
+  h->arena_cap = ws ? bytes : 0;
+  h->arena_top = 0;
+  h->ws_gen += 1;
   return AGIPC_OK;
 }
 

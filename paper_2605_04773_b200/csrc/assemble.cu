@@ -40,6 +40,8 @@ struct AsmScal {
   long long pair_count;  // (large, x) pairs
   long long big_groups;  // large lists that need the CTA sort
   long long n_large3;    // large nodes with 3 DoF (affine threshold > 32)
+  long long rec_total;   // interface records of the large-row chunks (k_num_large)
+  long long n_tasks;     // large-row chunks
   int err_map;           // map value outside [0, n_c)
   int err_overflow;      // a buffer capacity was exceeded
 };
@@ -72,9 +74,9 @@ __global__ void k_size_hist(int64_t N, const int32_t *__restrict__ map, int64_t 
   int key = -1;
   if (f < N) {
     key = map[f];
-    if (key < 0 || key >= n_c) {
-      sc->err_map = 1;
-      key = -1;
+    if (key < 0 || key >= n_c) {  // reported as EINVAL after the symbolic phase; until then the
+      sc->err_map = 1;             // node counts as a child of aggregate 0, so every later kernel
+      key = 0;                     // stays in bounds (k_new_map applies the same substitution)
     }
   }
   unsigned peers = __match_any_sync(FULL_MASK, key);
@@ -105,10 +107,48 @@ __global__ void k_newid(int64_t n_c, const int64_t *__restrict__ ex12, const int
   }
 }
 
-__global__ void k_new_map(int64_t N, const int32_t *__restrict__ map, const int32_t *__restrict__ newid,
+__global__ void k_new_map(int64_t N, int64_t n_c, const int32_t *__restrict__ map, const int32_t *__restrict__ newid,
                           int32_t *__restrict__ nm) {
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < N) nm[f] = newid[map[f]];
+  if (f < N) {
+    const int m = map[f];
+    nm[f] = newid[(m >= 0 && m < n_c) ? m : 0];  // out-of-range: see k_size_hist
+  }
+}
+
+// R22 precondition check (AGIPC_OPT_CHECK_SYMMETRY): every stored block (i, j) has a stored
+// (j, i) with B_ji == B_ij^T bit for bit; warp per row, binary search in row j.
+__global__ void k_check_sym(int64_t N, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                            const double *__restrict__ val, unsigned long long *bad) {
+  unsigned long long nb = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t k = rp[i] + lane_id(); k < rp[i + 1]; k += 32) {
+      const int64_t j = col[k];
+      if (j < 0 || j >= N) {
+        ++nb;
+        continue;
+      }
+      int64_t lo = rp[j], hi = rp[j + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < i) lo = mid + 1; else hi = mid;
+      }
+      if (lo >= rp[j + 1] || col[lo] != i) {
+        ++nb;
+        continue;
+      }
+      const double *a = val + 9 * k, *b = val + 9 * lo;
+      bool ok = true;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ok &= __double_as_longlong(a[3 * r + c]) == __double_as_longlong(b[3 * c + r]);
+      nb += !ok;
+    }
+  }
+  nb = warp_sum(nb);
+  if (lane_id() == 0 && nb) atomicAdd(bad, nb);
 }
 
 // children lists (order inside an aggregate is arbitrary) and per-node candidate counts
@@ -159,25 +199,40 @@ __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
 // Warp-buffered emission of (large row, column) pairs: one global atomic on the grid-wide pair
 // counter per PAIR_BUF pairs instead of one per 32 entries (the counter is contended).
 #define PAIR_BUF 128
-__device__ __forceinline__ void pairs_flush(int2 *buf, int &nb, int2 *pairs, long long cap, AsmScal *scw) {
+// Each (large row, column) pair may carry an ORIGIN: the index of a mirror-position slot
+// (A.mir) of the small row that emitted it; after the large rows' lists are final,
+// k_mirror_pos writes there the column position of the small row inside the large row, so the
+// numeric pass mirrors B_ij^T (R22) without a binary search (-1: no origin).
+struct PairBuf {
+  int2 v[PAIR_BUF];
+  long long o[PAIR_BUF];
+};
+__device__ __forceinline__ void pairs_flush(PairBuf &buf, int &nb, int2 *pairs, long long *porig, long long cap,
+                                            AsmScal *scw) {
   const int l = lane_id();
   unsigned long long pb = 0;
   if (l == 0 && nb) pb = atomicAdd((unsigned long long *)&scw->pair_count, (unsigned long long)nb);
   pb = __shfl_sync(FULL_MASK, pb, 0);
   for (int t = l; t < nb; t += 32) {
     const long long pos = (long long)pb + t;
-    if (pos < cap) pairs[pos] = buf[t];
-    else scw->err_overflow = 1;
+    if (pos < cap) {
+      pairs[pos] = buf.v[t];
+      porig[pos] = buf.o[t];
+    } else scw->err_overflow = 1;
   }
   __syncwarp();
   nb = 0;
 }
-__device__ __forceinline__ void pairs_push(bool emit, int2 val, int2 *buf, int &nb, int2 *pairs, long long cap,
-                                           AsmScal *scw) {
+__device__ __forceinline__ void pairs_push(bool emit, int2 val, long long orig, PairBuf &buf, int &nb, int2 *pairs,
+                                           long long *porig, long long cap, AsmScal *scw) {
   const unsigned m = __ballot_sync(FULL_MASK, emit);
   if (!m) return;
-  if (nb + __popc(m) > PAIR_BUF) pairs_flush(buf, nb, pairs, cap, scw);
-  if (emit) buf[nb + __popc(m & ((1u << lane_id()) - 1u))] = val;
+  if (nb + __popc(m) > PAIR_BUF) pairs_flush(buf, nb, pairs, porig, cap, scw);
+  if (emit) {
+    const int pos = nb + __popc(m & ((1u << lane_id()) - 1u));
+    buf.v[pos] = val;
+    buf.o[pos] = orig;
+  }
   nb += __popc(m);
   __syncwarp();
 }
@@ -244,6 +299,61 @@ __device__ __forceinline__ int next_pow2(int x) {
   return p;
 }
 
+// AGIPC_OPT_DETERMINISTIC: k_children appends in scheduling order; sort every child list
+// ascending (fine id) so that the entry order -- and every summation order after it -- is fixed.
+// Warp per node in shared memory up to SORTC_CAP children; longer lists go to k_sort_children_big.
+#define SORTC_CAP 1024
+__global__ void __launch_bounds__(128) k_sort_children(int64_t n_c, const int64_t *__restrict__ child_ptr,
+                                                      int32_t *child_list, int32_t *big, AsmScal *sc) {
+  __shared__ int s_buf[4][SORTC_CAP];
+  const int w = threadIdx.x >> 5, l = lane_id();
+  for (int64_t c = (int64_t)blockIdx.x * 4 + w; c < n_c; c += (int64_t)gridDim.x * 4) {
+    const int64_t c0 = child_ptr[c];
+    const int n = (int)(child_ptr[c + 1] - c0);
+    if (n <= 1) continue;
+    if (n > SORTC_CAP) {
+      if (l == 0) big[atomicAdd((unsigned long long *)&sc->big_groups, 1ull)] = (int32_t)c;
+      continue;
+    }
+    const int P = next_pow2(n);
+    for (int e = l; e < P; e += 32) s_buf[w][e] = e < n ? child_list[c0 + e] : INT_MAX;
+    __syncwarp();
+    warp_bitonic_sort(s_buf[w], P);
+    for (int e = l; e < n; e += 32) child_list[c0 + e] = s_buf[w][e];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_sort_children_big(const AsmScal *sc, const int32_t *__restrict__ big,
+                                                            const int64_t *__restrict__ child_ptr, int32_t *child_list,
+                                                            int32_t *scratch) {
+  const long long nb = sc->big_groups;
+  for (long long q = blockIdx.x; q < nb; q += gridDim.x) {
+    const int64_t c = big[q], c0 = child_ptr[c];
+    const int n = (int)(child_ptr[c + 1] - c0);
+    const int P = next_pow2(n);
+    int32_t *g = scratch + 2 * c0;  // scratch holds 2 N ints: room for P <= 2 n
+    for (int e = threadIdx.x; e < P; e += blockDim.x) g[e] = e < n ? child_list[c0 + e] : INT_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int x = g[i], y = g[ixj];
+            if ((x > y) == ((i & k) == 0)) {
+              g[i] = y;
+              g[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) child_list[c0 + e] = g[e];
+    __syncthreads();
+  }
+}
+
 // Unique of sorted buf[0,n) written to out[] (may alias buf); returns the count and, in u12,
 // the number of unique entries >= n3 (12-DoF columns).
 __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t *out, long long n3, int &u12) {
@@ -302,6 +412,7 @@ struct LargeArgs {
   const uint8_t *fcls;       // [N] is_small[new_map[f]]: the class of fine node f's aggregate
   const AsmScal *sc;
   int2 *pairs;
+  long long *porig;
   long long pair_cap;
   AsmScal *scw;
   const int32_t *gbuf;
@@ -310,13 +421,21 @@ struct LargeArgs {
   const int64_t *crp;
   double *cval;
   double *g_c;
+  int32_t *recmax;         // symbolic: interface records a chunk may write (distinct large columns x batches)
+  const int64_t *rec_off;  // numeric: exclusive scan of recmax
+  int32_t *rec_b;          // [rec_total] column aggregate of each record (-1: unused)
+  double *rec_v;           // [rec_total][144] record values, (p*4+q)*9+x
+  double *part;            // [n_tasks][PART_STRIDE] diagonal block + g partials of every chunk
 };
+#define PART_STRIDE 160  // 144 diagonal-block values (p*4+q)*9+x + 12 g values p*3+d (+ pad)
+#define LSTAGE 128       // staged diagonal entries per batch of a large-row chunk
+#define ITF_CAP 160      // staged large-large interface entries of a chunk (flushed when full)
 
 #define SEEN_CAP 128
 __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ int s_seen[4][SEEN_CAP];  // large columns already emitted by this chunk
-  __shared__ int2 s_pb[4][PAIR_BUF];
+  __shared__ PairBuf s_pb[4];
   const int w = threadIdx.x >> 5, l = lane_id();
   int npb = 0;
   ChildTab &tab = s_tab[w];
@@ -326,7 +445,7 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
     const int chunk = (int)(t - A.task_ptr[a]);
     const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
     const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
-    int nseen = 0;
+    int nseen = 0, nitf = 0;
     for (int e0 = 0; e0 < T; e0 += 32) {
       const int e = e0 + l;
       int key = -1;
@@ -340,6 +459,7 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
           if (b != a) key = b;
         }
       }
+      nitf += __popc(__ballot_sync(FULL_MASK, key >= 0));
       const unsigned peers = __match_any_sync(FULL_MASK, key);
       bool emit = key >= 0 && (__ffs(peers) - 1) == l;
       if (emit)  // one pair per (chunk, column): skip columns this chunk already emitted
@@ -355,13 +475,16 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
       }
       nseen += __popc(me);
       __syncwarp();
-      pairs_push(emit, make_int2(a, key), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+      pairs_push(emit, make_int2(a, key), -1, s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
     }
+    // interface records the numeric chunk may write: one per (flush of its interface list,
+    // distinct large column); the list holds ITF_CAP entries and is flushed before it overflows
+    if (l == 0) A.recmax[t] = nseen * (1 + nitf / (ITF_CAP - 31));
     // the diagonal block (a, a) always exists
-    pairs_push(chunk == 0 && l == 0, make_int2(a, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+    pairs_push(chunk == 0 && l == 0, make_int2(a, a), -1, s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
     __syncwarp();
   }
-  pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+  pairs_flush(s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
 }
 
 __global__ void k_pair_count(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
@@ -391,7 +514,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_group_unique(int64_t n_c, co
                                                                  const int64_t *__restrict__ gptr, int32_t *gbuf,
                                                                  const int32_t *__restrict__ gcnt, long long *nb_off,
                                                                  int32_t *nb_cnt, int32_t *rowlen, int32_t *big_list,
-                                                                 AsmScal *sc) {
+                                                                 AsmScal *sc, int32_t *f12) {
   __shared__ int s_buf[SYM_WARPS][SMALL_ENTRIES];
   const int w = threadIdx.x >> 5, l = lane_id();
   const long long n3 = sc->n3;
@@ -414,6 +537,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_group_unique(int64_t n_c, co
       nb_off[a] = gptr[a];
       nb_cnt[a] = U;
       rowlen[a] = U + 3 * u12;
+      f12[a] = U - u12;  // ascending list: the 12-DoF columns (>= n3) come last
     }
     __syncwarp();
   }
@@ -423,7 +547,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_group_unique(int64_t n_c, co
 __global__ void __launch_bounds__(1024) k_group_unique_big(const AsmScal *sc, const int32_t *__restrict__ big_list,
                                                            const int64_t *__restrict__ gptr, int32_t *gbuf,
                                                            const int32_t *__restrict__ gcnt, long long *nb_off,
-                                                           int32_t *nb_cnt, int32_t *rowlen) {
+                                                           int32_t *nb_cnt, int32_t *rowlen, int32_t *f12) {
   const long long nb = sc->big_groups;
   const long long n3 = sc->n3;
   for (long long q = blockIdx.x; q < nb; q += gridDim.x) {
@@ -456,9 +580,26 @@ __global__ void __launch_bounds__(1024) k_group_unique_big(const AsmScal *sc, co
         nb_off[a] = gptr[a];
         nb_cnt[a] = U;
         rowlen[a] = U + 3 * u12;
+        f12[a] = U - u12;
       }
     }
     __syncthreads();
+  }
+}
+
+// Mirror positions: for every pair with an origin (a small row a meeting the large column b),
+// the column position of a inside b's final row (independent binary searches, thread per pair).
+__global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
+                             const long long *__restrict__ porig, const int32_t *__restrict__ gbuf,
+                             const long long *__restrict__ nb_off, const int32_t *__restrict__ nb_cnt,
+                             const int32_t *__restrict__ f12, int32_t *__restrict__ mir) {
+  const long long np = min(sc->pair_count, cap);
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
+    const long long o = porig[p];
+    if (o < 0) continue;
+    const int2 q = pairs[p];
+    const int idx = lower_bound_dev<int32_t>(gbuf + nb_off[q.x], nb_cnt[q.x], (int32_t)q.y);
+    mir[o] = colpos(idx, f12[q.x]);
   }
 }
 
@@ -475,8 +616,11 @@ __global__ void k_slot_rowlen(int64_t n_c, const AsmScal *sc, const int32_t *__r
   }
 }
 
-__global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr) {
+__global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr, const int64_t *__restrict__ task_ptr,
+                                int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound) {
   sc->nnzb = row_ptr[sc->n_slots];
+  sc->n_tasks = task_ptr[n_c];
+  sc->rec_total = rec_off[task_bound];
 }
 
 // ------------------------------------------------------------------------------------
@@ -535,6 +679,9 @@ struct WarpArgs {
   const AsmScal *sc;
   int32_t *rowlen;
   int2 *pairs;
+  long long *porig;
+  int32_t *mir;                // mirror positions (k_mirror_pos), indexed like mkeys from mir_base
+  long long mir_base;
   long long pair_cap;
   AsmScal *scw;
   const int32_t *gbuf;
@@ -552,7 +699,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[8 * NSEG];
   // numeric: per-lane parked block B_ij (9), X_bar of its row child (3) and of its column node (3)
   __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][15];
-  __shared__ int2 s_pb[NUMERIC ? 1 : 8][NUMERIC ? 1 : PAIR_BUF];  // symbolic: buffered pairs
+  __shared__ PairBuf s_pb[NUMERIC ? 1 : 8];  // symbolic: buffered pairs
   int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
   const int sg = l / SEG, sl = l % SEG;
@@ -607,7 +754,8 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const int U12 = __popc((__ballot_sync(FULL_MASK, head && bs >= n3) & smask) >> (sg * SEG));
       if (segv && sl == 0) A.rowlen[a] = U + 3 * U12;
       const bool emit = head && !A.is_small[bs];  // transposed pair (large column, small node)
-      pairs_push(emit, make_int2(bs, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+      pairs_push(emit, make_int2(bs, a), A.mir_base + wi * SEG + sl, s_pb[w], npb, A.pairs, A.porig, A.pair_cap,
+                 A.scw);
       continue;
     }
     // numeric: column position of every run, run membership, run tails
@@ -626,11 +774,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
     for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
     const int ncb_b = valid ? ncb_of(bs, n3) : 1;
     long long mbase = -1;  // position of column a in the large row bs (B_ji = B_ij^T, reading R22)
-    if (tail && !A.is_small[bs]) {
-      const int32_t *lb_ = A.gbuf + A.nb_off[bs];
-      const int Ub = A.nb_cnt[bs];
-      mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
-    }
+    if (tail && !A.is_small[bs]) mbase = A.mir[A.mir_base + wi * SEG + hl];  // k_mirror_pos
     // park B and the affine coordinates once; a run of one entry (the common case) never reads
     // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
     const int h0 = sg * SEG + hl;
@@ -708,7 +852,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
     }
     __syncwarp();
   }
-  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
 }
 
 // ------------------------------------------------------------------------------------
@@ -724,7 +868,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[MID_WARPS];
   __shared__ long long s_key[MID_WARPS][MID_CAP];
   __shared__ double s_carry[MID_WARPS][4][9];  // partial sums of a run continuing into the next window
-  __shared__ int2 s_pb[NUMERIC ? 1 : MID_WARPS][NUMERIC ? 1 : PAIR_BUF];  // symbolic: buffered pairs
+  __shared__ PairBuf s_pb[NUMERIC ? 1 : MID_WARPS];  // symbolic: buffered pairs
   int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
   ChildTab &tab = s_tab[w];
@@ -735,6 +879,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
     const int s = A.size_new[a];
     const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);  // T <= MID_CAP
     long long *gkeys = A.mkeys + A.e_off[wi];
+    const long long mir0 = A.mir_base + A.e_off[wi];  // this node's mirror-position slots
     if (NUMERIC) {  // the symbolic pass left the sorted keys of this node in global memory
       for (int e = l; e < T; e += 32) key[e] = gkeys[e];
       __syncwarp();
@@ -780,7 +925,8 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       run_base += __shfl_sync(FULL_MASK, incl, 31);
       if (!NUMERIC) {
         const bool emit = head && !A.is_small[b];  // transposed pair (large column, small node)
-        pairs_push(emit, make_int2(b, a), s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+        pairs_push(emit, make_int2(b, a), mir0 + e, s_pb[w], npb, A.pairs, A.porig,
+                   A.pair_cap, A.scw);
         continue;
       }
     }
@@ -795,7 +941,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       double(*carry)[9] = s_carry[w];
       if (l < 36) carry[l / 9][l % 9] = 0.0;
       __syncwarp();
-      int rb = 0, carry_cp = 0;
+      int rb = 0, carry_cp = 0, carry_he = 0;
       const long long rs = A.crp[slot_of(a, p, n3)];
       for (int e0 = 0; e0 < T; e0 += 32) {
         const int e = e0 + l;
@@ -827,12 +973,10 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
         for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * k + x) : 0.0;
         const int ncb_b = valid ? ncb_of(b, n3) : 1;
         const int Q = __ballot_sync(FULL_MASK, valid && ncb_b == 4) ? 4 : 1;
+        const int he = hl < 0 ? carry_he : e0 + hl;  // sorted position of my run's head
         long long mbase = -1;  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
-        if (tail && !A.is_small[b]) {
-          const int32_t *lb_ = A.gbuf + A.nb_off[b];
-          const int Ub = A.nb_cnt[b];
-          mbase = colpos(lower_bound_dev<int32_t>(lb_, Ub, (int32_t)a), lower_bound_dev<int32_t>(lb_, Ub, (int32_t)n3));
-        }
+        if (tail && !A.is_small[b]) mbase = A.mir[mir0 + he];  // k_mirror_pos
+        const int last_he = __shfl_sync(FULL_MASK, he, 31);
         const bool cont = valid && !tail && l == 31;  // my run continues into the next window
         const int last_cp = __shfl_sync(FULL_MASK, cp, 31);
 #pragma unroll
@@ -876,6 +1020,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
           __syncwarp();
         }
         carry_cp = last_cp;
+        carry_he = last_he;
         rb += __shfl_sync(FULL_MASK, incl, 31);
       }
       }
@@ -905,7 +1050,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
     if (!NUMERIC && l == 0) A.rowlen[a] = run_base;
     __syncwarp();
   }
-  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.pair_cap, A.scw);
+  if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
 }
 
 // split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
@@ -972,21 +1117,32 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
   }
 }
 
-// Large rows, one warp per 32-children chunk.  Phase 1 (lane per entry, coalesced): classify the
+// Large rows, one warp per 32-children chunk (reading R22: the (large, small) blocks are mirrored
+// by the small rows).  Phase 1 (lane per entry, coalesced): classify the chunk's stored blocks
+// into the diagonal list (new_map(j) == a) and the large-large interface list (staged in shared
+// memory as (child, offset) and the column node).  Phase 2: 64 diagonal blocks staged per warp
+// (two independent 72-B loads per lane), then lane (g, p, q) -- two groups g of 16 lanes, one
+// (p, q) sub-block per lane -- accumulates acc[x] += w_i[p] w_j[q] B_ij[x] (Eq 4) for every other
+// staged block.  Phase 3: one pass per distinct interface column aggregate b0.  No atomics: the
+// chunk writes its diagonal-block / g partials (part) and one record per (batch, b0) (rec_*)
+// at positions fixed by the symbolic pass, and k_large_reduce sums them in chunk order, so H_c
+// and g_c are bitwise reproducible.  <= 80 registers (6 CTAs of 4 warps per SM).
+// Large rows, one warp per 32-children chunk -- the default (fast, fp64 atomics: H_c reproducible
+// only up to rounding; AGIPC_OPT_DETERMINISTIC selects k_num_large + k_large_reduce).  Phase 1 (lane per entry, coalesced): classify the
 // chunk's stored blocks into the diagonal list (new_map(j) == a, staged in shared memory),
 // large-large interface blocks (direct fp64 atomics, rare) and small columns (skipped: mirrored
 // by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
 // two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
-#define LSTAGE 192
+#define LSTAGE_A 192
 
 template <int NCB, int NB>
-__global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) {
+__global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
-  __shared__ long long s_k[4][LSTAGE];
-  __shared__ int s_i[4][LSTAGE];     // child slot c of the entry's row (weights in s_wc)
-  __shared__ int s_b[4][LSTAGE];     // interface entries (staged from the top): column aggregate
-  __shared__ double s_xj[4][LSTAGE][3];  // X_bar of the entry's column node (w_j)
+  __shared__ long long s_k[4][LSTAGE_A];
+  __shared__ int s_i[4][LSTAGE_A];     // child slot c of the entry's row (weights in s_wc)
+  __shared__ int s_b[4][LSTAGE_A];     // interface entries (staged from the top): column aggregate
+  __shared__ double s_xj[4][LSTAGE_A][3];  // X_bar of the entry's column node (w_j)
   __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
   __shared__ double s_B[4][32][9];       // phase 2: 32 diagonal blocks staged per warp (one per lane)
   const int w = threadIdx.x >> 5, l = lane_id();
@@ -1017,8 +1173,8 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
     for (int q = 0; q < QN; ++q)
 #pragma unroll
       for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
-    for (int base = 0; base < T; base += LSTAGE) {
-      const int n = min(LSTAGE, T - base);
+    for (int base = 0; base < T; base += LSTAGE_A) {
+      const int n = min(LSTAGE_A, T - base);
       int cnt = 0, icnt = 0;
       // software pipeline: the column of the next batch is loaded while this batch's column
       // aggregate, class and X_bar (all independent of each other) are in flight
@@ -1060,7 +1216,7 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
         const bool itf = valid && b != a && !small_col;
         const unsigned mi = __ballot_sync(FULL_MASK, itf);
         if (itf) {
-          const int pos = LSTAGE - 1 - (icnt + __popc(mi & ((1u << l) - 1u)));
+          const int pos = LSTAGE_A - 1 - (icnt + __popc(mi & ((1u << l) - 1u)));
           s_k[w][pos] = k;
           s_i[w][pos] = c;
           s_b[w][pos] = b;
@@ -1093,9 +1249,9 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
         __syncwarp();
       }
       __syncwarp();
-      // interface entries [LSTAGE - icnt, LSTAGE): one pass per distinct column aggregate b0,
+      // interface entries [LSTAGE_A - icnt, LSTAGE_A): one pass per distinct column aggregate b0,
       // lanes (block group, p, q half) accumulate its entries, one set of atomics per (a, b0)
-      const int i0 = LSTAGE - icnt;
+      const int i0 = LSTAGE_A - icnt;
       int left = icnt;
       while (left > 0) {
         int f = -1;
@@ -1194,6 +1350,273 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large(LargeArgs A) 
   }
 }
 
+// Interface flush: one record per distinct column aggregate b0 of the staged interface list
+// (lanes (g, p, q) accumulate the entries of b0, the two groups are reduced, group 0 writes).
+template <int NCB>
+__device__ __forceinline__ void itf_flush(LargeArgs &A, int w, int l, int icnt, int *s_ice, int *s_ij, int *s_ib,
+                                          const ChildTab &tab, const double (*s_wc)[3], long long n3, int64_t rbase,
+                                          int64_t rcap, int &nrec) {
+  const int gq = l >> 4, p = (l >> 2) & 3, q = l & 3;
+  const bool pin = p < NCB;
+  int left = icnt;
+  while (left > 0) {
+    int f = -1;
+    for (int d0 = 0; d0 < icnt && f < 0; d0 += 32) {
+      const unsigned mb = __ballot_sync(FULL_MASK, d0 + l < icnt && s_ib[d0 + l] >= 0);
+      if (mb) f = d0 + __ffs(mb) - 1;
+    }
+    const int b0 = s_ib[f];
+    const int ncb_b = ncb_of(b0, n3);
+    double ac[9];
+#pragma unroll
+    for (int x = 0; x < 9; ++x) ac[x] = 0.0;
+    if (pin && q < ncb_b) {
+      for (int d = f + gq; d < icnt; d += 2) {
+        if (s_ib[d] != b0) continue;
+        const int ce = s_ice[d];
+        const long long kk = tab.rb[ce >> 16] + (ce & 0xffff);
+        const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[ce >> 16][p];
+        const double wj = (ncb_b == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)s_ij[d] + q);
+        const double cf = wi * wj;
+#pragma unroll
+        for (int x = 0; x < 9; ++x) ac[x] += cf * __ldg(A.val + 9 * kk + x);
+      }
+    }
+    __syncwarp();
+    int done_n = 0;
+    for (int d0 = f; d0 < icnt; d0 += 32) {
+      const bool mine = d0 + l < icnt && s_ib[d0 + l] == b0;
+      done_n += __popc(__ballot_sync(FULL_MASK, mine));
+      if (mine) s_ib[d0 + l] = -1;
+    }
+    __syncwarp();
+    left -= done_n;
+#pragma unroll
+    for (int x = 0; x < 9; ++x) ac[x] += __shfl_xor_sync(FULL_MASK, ac[x], 16);
+    if (nrec < rcap) {
+      const int64_t r = rbase + nrec;
+      if (gq == 0 && pin && q < ncb_b) {
+        double *dst = A.rec_v + 144 * r + 9 * (p * 4 + q);
+#pragma unroll
+        for (int x = 0; x < 9; ++x) dst[x] = ac[x];
+      }
+      if (l == 0) A.rec_b[r] = b0;
+    } else if (l == 0) {
+      A.scw->err_overflow = 1;
+    }
+    ++nrec;
+  }
+  __syncwarp();
+}
+
+template <int NCB>
+__global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
+  __shared__ ChildTab s_tab[4];
+  __shared__ int s_ce[4][LSTAGE];     // diagonal entries: (child c << 16) | entry offset in its row
+  __shared__ int s_j[4][LSTAGE];      //   column node j (w_j = X_bar_j)
+  __shared__ int s_ice[4][ITF_CAP];   // interface entries (kept across batches)
+  __shared__ int s_ij[4][ITF_CAP];
+  __shared__ int s_ib[4][ITF_CAP];    //   column aggregate b0 (-1 once summed)
+  __shared__ double s_wc[4][32][3];   // X_bar of the chunk's children (w_i)
+  __shared__ double s_B[4][64][9];    // phase 2: 64 diagonal blocks staged per warp
+  const int w = threadIdx.x >> 5, l = lane_id();
+  const int gq = l >> 4, p = (l >> 2) & 3, q = l & 3;
+  const bool pin = p < NCB;  // lanes with p >= NCB idle (NCB = 1: 3-DoF large rows, rare)
+  const long long n3 = A.sc->n3;
+  ChildTab &tab = s_tab[w];
+  const int64_t n_tasks = A.task_ptr[A.n_c];
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
+    const int a = A.task_node[t];
+    if (ncb_of(a, n3) != NCB) continue;
+    const int chunk = (int)(t - A.task_ptr[a]);
+    const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
+    const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+    if (l < s) {
+      const int64_t ci = tab.ci[l];
+      s_wc[w][l][0] = __ldg(A.X + 3 * ci);
+      s_wc[w][l][1] = __ldg(A.X + 3 * ci + 1);
+      s_wc[w][l][2] = __ldg(A.X + 3 * ci + 2);
+    }
+    __syncwarp();
+    const int64_t rbase = A.rec_off[t], rcap = A.rec_off[t + 1] - rbase;
+    int nrec = 0, icnt = 0;
+    double acc[9];
+#pragma unroll
+    for (int x = 0; x < 9; ++x) acc[x] = 0.0;
+    int c_nx = 0, j_nx = 0;
+    long long k_nx = 0;
+    if (l < T) {
+      entry_of(tab, s, l, c_nx, k_nx);
+      j_nx = A.col[k_nx];
+    }
+    for (int base = 0; base < T; base += LSTAGE) {
+      const int n = min(LSTAGE, T - base);
+      int cnt = 0;
+      for (int e0 = 0; e0 < n; e0 += 32) {
+        const bool valid = e0 + l < n;
+        const long long k = k_nx;
+        const int c = c_nx, j = j_nx;
+        int b = -1;
+        bool small_col = true;
+        if (valid) {
+          b = A.nm[j];
+          small_col = A.fcls[j];
+        }
+        if (base + e0 + 32 + l < T) {  // the next 32 entries' columns in flight
+          entry_of(tab, s, base + e0 + 32 + l, c_nx, k_nx);
+          j_nx = A.col[k_nx];
+        }
+        const int ce = (c << 16) | (int)(k - tab.rb[c]);
+        const bool diag = valid && b == a;
+        const unsigned m = __ballot_sync(FULL_MASK, diag);
+        if (diag) {
+          const int pos = cnt + __popc(m & ((1u << l) - 1u));
+          s_ce[w][pos] = ce;
+          s_j[w][pos] = j;
+        }
+        cnt += __popc(m);
+        const bool itf = valid && b != a && !small_col;
+        const unsigned mi = __ballot_sync(FULL_MASK, itf);
+        if (mi && icnt + __popc(mi) > ITF_CAP) {  // list full: emit its records first
+          itf_flush<NCB>(A, w, l, icnt, s_ice[w], s_ij[w], s_ib[w], tab, s_wc[w], n3, rbase, rcap, nrec);
+          icnt = 0;
+        }
+        if (itf) {
+          const int pos = icnt + __popc(mi & ((1u << l) - 1u));
+          s_ice[w][pos] = ce;
+          s_ij[w][pos] = j;
+          s_ib[w][pos] = b;
+        }
+        icnt += __popc(mi);
+      }
+      __syncwarp();
+      // phase 2: the diagonal list, 64 blocks in flight per warp
+      for (int d0 = 0; d0 < cnt; d0 += 64) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int d = d0 + h2 * 32 + l;
+          if (d < cnt) {
+            const int ce = s_ce[w][d];
+            const long long kk = tab.rb[ce >> 16] + (ce & 0xffff);
+#pragma unroll
+            for (int x = 0; x < 9; ++x) s_B[w][h2 * 32 + l][x] = __ldg(A.val + 9 * kk + x);
+          }
+        }
+        __syncwarp();
+        const int dn = min(64, cnt - d0);
+        if (pin) {
+          for (int dd = gq; dd < dn; dd += 2) {
+            const int d = d0 + dd;
+            const int c = s_ce[w][d] >> 16;
+            const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][c][p];
+            const double wj = (NCB == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)s_j[w][d] + q);
+            const double cf = (NCB == 1 && q > 0) ? 0.0 : wi * wj;
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[x] += cf * s_B[w][dd][x];
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (icnt > 0) itf_flush<NCB>(A, w, l, icnt, s_ice[w], s_ij[w], s_ib[w], tab, s_wc[w], n3, rbase, rcap, nrec);
+    for (int r = nrec + l; r < rcap; r += 32) A.rec_b[rbase + r] = -1;  // unused record slots
+    // the chunk's diagonal-block partial: reduce over the two groups, one (p, q) per lane
+#pragma unroll
+    for (int x = 0; x < 9; ++x) acc[x] += __shfl_xor_sync(FULL_MASK, acc[x], 16);
+    double *pt = A.part + PART_STRIDE * t;
+    if (gq == 0 && pin && (NCB == 4 || q == 0)) {
+#pragma unroll
+      for (int x = 0; x < 9; ++x) pt[9 * (p * 4 + q) + x] = acc[x];
+    }
+    if (A.g_f) {  // the chunk's g partial: sum over its children of w_i[pp] g_f[i]
+      for (int pp = 0; pp < NCB; ++pp) {
+        double g0 = 0, g1 = 0, g2 = 0;
+        if (l < s) {
+          const int i = tab.ci[l];
+          const double wi = (NCB == 1 || pp == 3) ? 1.0 : s_wc[w][l][pp];
+          g0 = wi * A.g_f[3 * (int64_t)i];
+          g1 = wi * A.g_f[3 * (int64_t)i + 1];
+          g2 = wi * A.g_f[3 * (int64_t)i + 2];
+        }
+        g0 = warp_sum(g0);
+        g1 = warp_sum(g1);
+        g2 = warp_sum(g2);
+        if (l == 0) {
+          pt[144 + 3 * pp] = g0;
+          pt[144 + 3 * pp + 1] = g1;
+          pt[144 + 3 * pp + 2] = g2;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// CTA per large coarse node a: sums its chunks' partials in chunk order (fixed order: H_c, g_c
+// bitwise reproducible).  The diagonal block (a, a) and g_c are written; the interface records
+// are grouped by column aggregate b0 (first occurrence order) and each (a, b0) block is the sum
+// of its records in record order -- every coarse value is written once, no read-modify-write.
+#define RED_REC 256  // records of one node handled in shared memory (more: a second pass)
+__global__ void __launch_bounds__(128) k_large_reduce(LargeArgs A, const int32_t *__restrict__ f12) {
+  __shared__ int s_rb[RED_REC];
+  __shared__ int s_first[RED_REC];  // record index of the first record of each distinct b0
+  __shared__ int s_cp[RED_REC];     // column position of that b0 in row a
+  __shared__ int s_nd;
+  const long long n3 = A.sc->n3;
+  for (int64_t a = blockIdx.x; a < A.n_c; a += gridDim.x) {
+    if (A.is_small[a]) continue;
+    const int ncb = ncb_of((int)a, n3);
+    const int32_t *lst = A.gbuf + A.nb_off[a];
+    const int U = A.nb_cnt[a], F = f12[a];
+    const int64_t t0 = A.task_ptr[a], t1 = A.task_ptr[a + 1];
+    const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, (int32_t)a), F);
+    for (int o = threadIdx.x; o < 9 * ncb * ncb; o += blockDim.x) {
+      const int pp = o / (9 * ncb), qq = (o / 9) % ncb, x = o % 9;
+      double v = 0.0;
+      for (int64_t t = t0; t < t1; ++t) v += A.part[PART_STRIDE * t + 9 * (pp * 4 + qq) + x];
+      A.cval[9 * (A.crp[slot_of((int)a, pp, n3)] + cpa + qq) + x] = v;
+    }
+    if (A.g_f && (int)threadIdx.x < 3 * ncb) {
+      double v = 0.0;
+      for (int64_t t = t0; t < t1; ++t) v += A.part[PART_STRIDE * t + 144 + threadIdx.x];
+      A.g_c[3 * (int64_t)slot_of((int)a, threadIdx.x / 3, n3) + threadIdx.x % 3] = v;
+    }
+    const int64_t r0 = A.rec_off[t0], r1 = A.rec_off[t1];
+    for (int64_t rb = r0; rb < r1; rb += RED_REC) {  // records in windows of RED_REC (one window typically)
+      const int R = (int)min((int64_t)RED_REC, r1 - rb);
+      __syncthreads();
+      for (int r = threadIdx.x; r < R; r += blockDim.x) s_rb[r] = A.rec_b[rb + r];
+      if (threadIdx.x == 0) s_nd = 0;
+      __syncthreads();
+      for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        const int b0 = s_rb[r];
+        bool first = b0 >= 0;
+        for (int u = 0; u < r && first; ++u) first = s_rb[u] != b0;
+        // a b0 already seen in an earlier window is folded in there (windows past the first are
+        // rare; the later window's records of that b0 then add onto the stored value below)
+        if (first) {
+          const int k = atomicAdd(&s_nd, 1);
+          s_first[k] = r;
+          s_cp[k] = colpos(lower_bound_dev<int32_t>(lst, U, (int32_t)b0), F);
+        }
+      }
+      __syncthreads();
+      const int nd = s_nd;
+      for (int k = 0; k < nd; ++k) {
+        const int f = s_first[k], b0 = s_rb[f];
+        const int ncb_b = ncb_of(b0, n3);
+        for (int o = threadIdx.x; o < 9 * ncb * ncb_b; o += blockDim.x) {
+          const int pp = o / (9 * ncb_b), qq = (o / 9) % ncb_b, x = o % 9;
+          double v = rb > r0 ? A.cval[9 * (A.crp[slot_of((int)a, pp, n3)] + s_cp[k] + qq) + x] : 0.0;
+          for (int r = f; r < R; ++r)
+            if (s_rb[r] == b0) v += A.rec_v[144 * (rb + r) + 9 * (pp * 4 + qq) + x];
+          A.cval[9 * (A.crp[slot_of((int)a, pp, n3)] + s_cp[k] + qq) + x] = v;
+        }
+      }
+    }
+  }
+}
+
 __global__ void k_small_list(int64_t n_c, const uint8_t *__restrict__ is_small, const int64_t *__restrict__ sidx,
                              const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ small_list,
                              int64_t *__restrict__ ecount) {
@@ -1232,6 +1655,18 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   const int64_t nnzb_f = H->nnzb;
   agipc_status st;
 
+  if (h->opt_check_sym) {  // DESIGN.md R22: the mixed-pair mirroring below relies on it
+    WS(h, bad, unsigned long long, "asm_symcheck", 1);
+    CU_TRY(h, cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st_));
+    LAUNCH(h, k_check_sym, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(N, 8), 16 * h->sm_count)), 256, 0, N,
+           H->row_ptr, H->col, H->val, bad);
+    unsigned long long *hb = (unsigned long long *)pinned_get(h, sizeof(unsigned long long), &st);
+    if (st != AGIPC_OK) return st;
+    CU_TRY(h, cudaMemcpyAsync(hb, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+    CU_TRY(h, cudaStreamSynchronize(st_));
+    if (*hb) return set_err(h, AGIPC_EINVAL, "assemble_coarse: H_fine is not bitwise symmetric (%llu blocks without "
+                            "a stored B_ji == B_ij^T, DESIGN.md R22)", *hb);
+  }
   WS(h, sc, AsmScal, "asm_scal", 1);
   std::unique_ptr<ProfScope> ps_classify(new ProfScope(h, PROF_ASM_CLASSIFY, st_));
   CU_TRY(h, cudaMemsetAsync(sc, 0, sizeof(AsmScal), st_));
@@ -1260,10 +1695,19 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_is12, gC, 256, 0, n_c, size, affine_threshold, is12);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, is12, n_c, ex12)) != AGIPC_OK) return st;
   LAUNCH(h, k_newid, gC, 256, 0, n_c, ex12, is12, size, newid, size_new, sc);
-  LAUNCH(h, k_new_map, gN, 256, 0, N, map, newid, out->new_map);
+  LAUNCH(h, k_new_map, gN, 256, 0, N, n_c, map, newid, out->new_map);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, size_new, n_c, child_ptr)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(cursor, child_ptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
   LAUNCH(h, k_children, gN, 256, 0, N, out->new_map, H->row_ptr, cursor, child_list, rowsum);
+  if (h->opt_deterministic) {  // fixed child order => fixed summation order downstream
+    WS(h, sbig, int32_t, "asm_sortc_big", n_c + 1);
+    LAUNCH(h, k_sort_children, (unsigned)std::min<int64_t>(cdiv(n_c, 4), 64 * h->sm_count), 128, 0, n_c,
+           (const int64_t *)child_ptr, child_list, sbig, sc);
+    WS(h, sscr, int32_t, "asm_sortc_scratch", 2 * N + 64);
+    LAUNCH(h, k_sort_children_big, (unsigned)h->sm_count, 1024, 0, (const AsmScal *)sc, (const int32_t *)sbig,
+           (const int64_t *)child_ptr, child_list, sscr);
+    CU_TRY(h, cudaMemsetAsync(&sc->big_groups, 0, sizeof(long long), st_));  // reused by the symbolic phase
+  }
   LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks, sc);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
   WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
@@ -1301,26 +1745,38 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, nb_cnt, int32_t, "asm_nb_cnt", n_c);
   WS(h, rowlen, int32_t, "asm_rowlen", n_c);
   WS(h, pairs, int2, "asm_pairs", pair_cap);
+  WS(h, porig, long long, "asm_pair_orig", pair_cap);
+  WS(h, f12, int32_t, "asm_first12", n_c);
   WS(h, gcnt, int32_t, "asm_gcnt", n_c);
   WS(h, gpad, int32_t, "asm_gpad", n_c);
   WS(h, gptr, int64_t, "asm_gptr", n_c + 1);
   WS(h, gbuf, int32_t, "asm_gbuf", 2 * pair_cap);
   WS(h, big_list, int32_t, "asm_big_list", n_c);
   const int64_t task_bound = N / LARGE_CHUNK + n_c;
+  WS(h, recmax, int32_t, "asm_recmax", task_bound + 1);
+  WS(h, rec_off, int64_t, "asm_rec_off", task_bound + 1);
+  CU_TRY(h, cudaMemsetAsync(recmax, 0, sizeof(int32_t) * (task_bound + 1), st_));
   const double *gfp = (g_fine && out->g_c) ? g_fine : nullptr;
   WarpArgs WA;
   WA.n_w = n_w16; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
   WA.is_small = is_small; WA.rp = H->row_ptr; WA.col = H->col; WA.val = H->val; WA.nm = out->new_map;
   WA.X = mesh->x_rest; WA.g_f = gfp; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
+  WA.porig = porig; WA.mir = nullptr; WA.mir_base = 0;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
   WA.mkeys = nullptr; WA.e_off = nullptr;
   WarpArgs WB = WA, WM;
   WB.n_w = n_w32; WB.wlist = w32;
+  // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys
+  const long long mir_mid = 16 * n_w16 + 32 * n_w32;
+  WS(h, mir, int32_t, "asm_mirror", mir_mid + nnzb_f + 1);
   {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
     WS(h, skeys, long long, "asm_small_keys", 16 * n_w16 + 32 * n_w32 + 1);
     WA.mkeys = skeys;
     WB.mkeys = skeys + 16 * n_w16;
+    WA.mir = mir;
+    WB.mir = mir;
+    WB.mir_base = 16 * n_w16;
   }
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
   const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
@@ -1332,14 +1788,16 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     WS(h, mkeys, long long, "asm_mid_keys", nnzb_f + 1);
     WM.mkeys = mkeys;
     WM.e_off = e_off;
+    WM.mir_base = mir_mid;
   }
   const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_small, MID_WARPS), 32 * h->sm_count));
   if (n_small > 0) LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
-  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.task_node = task_node; LA.fcls = fcls; LA.sc = sc; LA.pairs = pairs; LA.pair_cap = pair_cap; LA.scw = sc;
+  LA.g_f = gfp; LA.task_ptr = task_ptr; LA.task_node = task_node; LA.fcls = fcls; LA.sc = sc; LA.pairs = pairs; LA.porig = porig; LA.pair_cap = pair_cap; LA.scw = sc;
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
+  LA.recmax = recmax; LA.rec_off = rec_off; LA.rec_b = nullptr; LA.rec_v = nullptr; LA.part = nullptr;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
   LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
@@ -1350,8 +1808,12 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_pair_scatter, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, cursor, gbuf);
   const unsigned gsym = (unsigned)std::min<int64_t>(cdiv(n_c, SYM_WARPS), 64 * h->sm_count);
   LAUNCH(h, k_group_unique, gsym, SYM_WARPS * 32, 0, n_c, is_small, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen,
-         big_list, sc);
-  LAUNCH(h, k_group_unique_big, (unsigned)h->sm_count, 1024, 0, sc, big_list, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen);
+         big_list, sc, f12);
+  LAUNCH(h, k_group_unique_big, (unsigned)h->sm_count, 1024, 0, sc, big_list, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen,
+         f12);
+  LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, (const int2 *)pairs,
+         (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
+         (const int32_t *)f12, mir);
 
   // ---- C. slot row pointer (upper bound 4 n_c slots; entries past n_slots are 0) ----
   const int64_t slot_bound = 4 * n_c;
@@ -1360,7 +1822,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemsetAsync(rl, 0, sizeof(int32_t) * slot_bound, st_));
   LAUNCH(h, k_slot_rowlen, gC, 256, 0, n_c, sc, rowlen, rl);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, rl, slot_bound, crp_ws)) != AGIPC_OK) return st;
-  LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws);
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, recmax, task_bound, rec_off)) != AGIPC_OK) return st;
+  LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound);
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
   CU_TRY(h, cudaStreamSynchronize(st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
@@ -1395,9 +1858,22 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
-  // 2 diagonal blocks per group in flight: 3 or 4 (at 3 CTAs/SM) measured slower, 1.63 / 1.61 vs
-  // 1.51 ms numeric at C3 (profiles/r01h/bench_nb*.jsonl)
-  LAUNCH(h, (k_num_large<4, 2>), glarge, 128, 0, LA);
-  if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large<1, 2>), glarge, 128, 0, LA);
+  if (!h->opt_deterministic) {
+    // 2 diagonal blocks per group in flight: 3 or 4 (at 3 CTAs/SM) measured slower, 1.63 / 1.61 vs
+    // 1.51 ms numeric at C3 (profiles/r01h/bench_nb*.jsonl)
+    LAUNCH(h, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
+    if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
+  } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)
+    // sizes vary between Newton steps: ask for 1.5x so that the buffers rarely grow
+    WS(h, part, double, "asm_large_part", PART_STRIDE * (3 * hsc->n_tasks / 2 + 64));
+    WS(h, rec_b, int32_t, "asm_rec_b", 3 * hsc->rec_total / 2 + 64);
+    WS(h, rec_v, double, "asm_rec_v", 144 * (3 * hsc->rec_total / 2 + 64));
+    LA.part = part;
+    LA.rec_b = rec_b;
+    LA.rec_v = rec_v;
+    LAUNCH(h, k_num_large<4>, glarge, 128, 0, LA);
+    if (hsc->n_large3 > 0) LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
+    LAUNCH(h, k_large_reduce, (unsigned)std::min<int64_t>(n_c, 16 * h->sm_count), 128, 0, LA, (const int32_t *)f12);
+  }
   return AGIPC_OK;
 }

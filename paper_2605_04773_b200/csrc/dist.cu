@@ -99,16 +99,16 @@ extern "C" agipc_status agipc_coarse_halo(agipc_handle h, const int32_t *new_map
   CU_TRY(h, cudaSetDevice(h->device));
   ProfScope prof(h, PROF_DIST, h->stream);
   // first[c] = first position of aggregate c in the send list; kept at INT_MAX between calls
-  WsBuf &fb = h->ws["dist_first"];
   const size_t need = sizeof(int) * (size_t)(n_coarse + 1);
-  if (fb.bytes < need) {
+  int *first = nullptr;
+  {
     agipc_status st;
-    int *f = (int *)ws_get(h, "dist_first", need, &st);
+    bool fresh = false;
+    first = (int *)ws_get(h, "dist_first", need, &st, &fresh);
     if (st != AGIPC_OK) return st;
-    LAUNCH(h, k_fill_int, (unsigned)cdiv((int64_t)(fb.bytes / sizeof(int)), 256), 256, 0,
-           (int64_t)(fb.bytes / sizeof(int)), f, INT_MAX);
+    const int64_t cap = (int64_t)(h->ws["dist_first"].bytes / sizeof(int));
+    if (fresh) LAUNCH(h, k_fill_int, (unsigned)cdiv(cap, 256), 256, 0, cap, first, INT_MAX);
   }
-  int *first = (int *)h->ws["dist_first"].ptr;
   WS(h, sz, int32_t, "dist_ch_size", n_send);
   WS(h, off, int64_t, "dist_ch_off", n_send + 1);
   const unsigned G = (unsigned)cdiv(n_send, 256);

@@ -329,7 +329,26 @@ struct TailArgs {
   int *ctrl;               // [1] any intra edge, [2] levels run, [3] comp valid
   long long *nvals;        // [0] n1 on entry / final n on exit
   long long *level_n;      // [64]
+  unsigned *bar;           // software grid barrier counter (zeroed before launch); nullptr =
+                           // cooperative launch + cg grid.sync()
 };
+
+// Grid barrier of a persistent kernel whose CTAs are all resident (one per SM, checked by the
+// occupancy query before launch): a monotone arrival counter, barrier i completes when it reaches
+// (i + 1) * gridDim.x.  Lets k_tail go out as an ordinary launch (the host-side cost of
+// cudaLaunchCooperativeKernel is paid while the GPU waits, once per Newton step).
+__device__ __forceinline__ void sw_grid_sync(unsigned *bar, unsigned &epoch) {
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (*(volatile unsigned *)bar < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 // Levels >= 1 in one cooperative kernel, one 1024-thread CTA per SM, two grid barriers per
 // level: (P2) closure/election per tile -> tile-local rank and per-tile count; (P3) every CTA
@@ -338,7 +357,11 @@ struct TailArgs {
 // P1 of the first tail level runs on its own).  Stops at the first level without an
 // intra-group edge.  The "any intra edge" flag alternates between ctrl[0] and ctrl[1].
 __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned epoch = 0;
+  auto gsync = [&]() {
+    if (A.bar) sw_grid_sync(A.bar, epoch);
+    else cg::this_grid().sync();
+  };
   extern __shared__ int32_t s_pref[];  // exclusive prefix of the tile counts
   __shared__ int s_w[TAIL_WARPS];
   __shared__ int s_red[TAIL_WARPS];
@@ -378,7 +401,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         }
       }
       if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + fl, 1);
-      grid.sync();
+      gsync();
       first_pass = false;
     }
     if (*(volatile int *)(A.ctrl + fl) == 0) {  // no merge possible: this pass is the fixpoint
@@ -433,7 +456,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       __syncthreads();
     }
     if (gtid == 0) A.ne[1 - cur] = 0;
-    grid.sync();
+    gsync();
     // ---- P3: scan the tile counts (every CTA, shared memory), remap, compose, reset ----
     {
       const int64_t per = (ntiles + TAIL_THREADS - 1) / TAIL_THREADS;
@@ -493,7 +516,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       A.ctrl[3] = 1;
       if (level <= 64) A.level_n[level - 1] = n2;
     }
-    grid.sync();
+    gsync();
     n = n2;
     cur = 1 - cur;
     if (A.max_levels > 0 && level >= A.max_levels) {
@@ -528,6 +551,8 @@ struct MapScalars {
   unsigned long long ne[2];
   int ctrl[4];
   long long level_n[64];
+  unsigned bar;              // k_tail software grid barrier (zeroed with the struct)
+  unsigned pad;
 };
 
 extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, const uint8_t *slot_tags,
@@ -585,13 +610,14 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     // hash set for the level-1 edge de-duplication (zeroed once; used slots are cleared after use)
     int64_t tsize = 1024;
     while (tsize < 2 * ecap) tsize <<= 1;
+    unsigned long long *table = nullptr;
     {
-      WsBuf &tb = h->ws["map_hash"];
-      const bool fresh = tb.bytes < sizeof(unsigned long long) * (size_t)tsize;
-      WS(h, table_, unsigned long long, "map_hash", tsize);
-      if (fresh) CU_TRY(h, cudaMemsetAsync(table_, 0, h->ws["map_hash"].bytes, s0));
+      bool fresh = false;
+      agipc_status wst;
+      table = (unsigned long long *)ws_get(h, "map_hash", sizeof(unsigned long long) * (size_t)tsize, &wst, &fresh);
+      if (wst != AGIPC_OK) return wst;
+      if (fresh) CU_TRY(h, cudaMemsetAsync(table, 0, h->ws["map_hash"].bytes, s0));
     }
-    unsigned long long *table = (unsigned long long *)h->ws["map_hash"].ptr;
     CU_TRY(h, cudaMemsetAsync(hh, 0, sizeof(uint32_t) * N, s0));
     const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), 8 * h->sm_count));
     LAUNCH(h, k_cross_to_level1, gedge, 256, 0, cross, &sc->cross, map, table, (unsigned long long)(tsize - 1), EA,
@@ -627,9 +653,17 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     void *args[] = {&A};
     cudaError_t pre = cudaGetLastError();
     if (pre != cudaSuccess) return set_err(h, AGIPC_ECUDA, "pending CUDA error before k_tail: %s", cudaGetErrorString(pre));
-    ps_tail.reset(new ProfScope(h, PROF_MAP_TAIL, s0));
-    CU_TRY(h, cudaLaunchCooperativeKernel((const void *)k_tail, grid, TAIL_THREADS, args, smem, s0));
-    h->launches += 1;
+    static const bool coop = getenv("AGIPC_TAIL_COOP") && atoi(getenv("AGIPC_TAIL_COOP")) != 0;
+    if (coop) {
+      A.bar = nullptr;
+      ps_tail.reset(new ProfScope(h, PROF_MAP_TAIL, s0));
+      CU_TRY(h, cudaLaunchCooperativeKernel((const void *)k_tail, grid, TAIL_THREADS, args, smem, s0));
+      h->launches += 1;
+    } else {  // ordinary launch, software grid barrier (every CTA resident: 1 per SM, checked above)
+      A.bar = (unsigned *)&sc->bar;
+      ps_tail.reset(new ProfScope(h, PROF_MAP_TAIL, s0));
+      LAUNCH(h, k_tail, (unsigned)grid, TAIL_THREADS, smem, A);
+    }
     ps_tail.reset();
     LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl);
   }

@@ -51,6 +51,9 @@ struct PcgGraph {
   bool sym = false;
   int win = 0, all_red = 0, upd_u = 0, spmv_un = 0;
   const void *yext = nullptr;
+  uint64_t ws_gen = 0;
+  bool flat = false;
+  int64_t n_flat = -1;
   std::vector<cudaEvent_t> ev;  // profiling: 3 events per iteration of the chunk
 };
 
@@ -97,11 +100,19 @@ __device__ __forceinline__ bool last_block(PcgState *st) {
 }
 
 // fixed-order reduction of nparts partials by one CTA
+// (four independent partial sums per thread keep four loads in flight; the order is fixed)
 template <int NT = PCG_THREADS>
 __device__ __forceinline__ double reduce_parts(const double *parts, int nparts, double *s_red) {
-  double v = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += NT) v += __ldcg(parts + i);
-  return block_sum<NT>(v, s_red);
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int i = threadIdx.x;
+  for (; i + 3 * NT < nparts; i += 4 * NT) {
+    v0 += __ldcg(parts + i);
+    v1 += __ldcg(parts + i + NT);
+    v2 += __ldcg(parts + i + 2 * NT);
+    v3 += __ldcg(parts + i + 3 * NT);
+  }
+  for (; i < nparts; i += NT) v0 += __ldcg(parts + i);
+  return block_sum<NT>((v0 + v1) + (v2 + v3), s_red);
 }
 
 __device__ __forceinline__ void dinv_apply(const double *__restrict__ D, const double r0, const double r1,
@@ -411,6 +422,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
     double BB = reduce_parts(parts + 2 * G, G, s_red);
     if (threadIdx.x == 0 && red) {  // distributed: rank partials, the caller all-reduces them
       red[0] = RZ; red[1] = RR; red[2] = BB;
+      red[3] = st->status == AGIPC_ESINGULAR ? 1.0 : 0.0;  // k_dinv ran before: stops every rank
     } else if (threadIdx.x == 0) {
       st->rz = RZ;
       st->rr = RR;
@@ -454,7 +466,11 @@ __device__ __forceinline__ void blk_fma(const BlkLoad &b, double beta, double &a
 }
 
 // Persistent grid (resident CTAs only); every warp repeatedly claims the next slice of the
-// longest-first order from counter[parity] (reset by K2 for the next iteration).
+// longest-first order from counter[parity] (reset by K2 for the next iteration).  p.q is kept
+// per SLICE (pqs[s]) and the last CTA sums the slice partials in slice order, so the result does
+// not depend on which warp took which slice: the solve is bit-for-bit reproducible run to run.
+// (A static round-robin of the slices, which would also be reproducible, measured 20% slower at
+// C3: 103 vs 83 us per SpMV, profiles/r02b.)
 template <int UN, int MINB>
 __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *__restrict__ sptr,
                                                            const int32_t *__restrict__ scol,
@@ -465,14 +481,13 @@ __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *
                                                            const int64_t *__restrict__ vr_ptr,
                                                            const double *__restrict__ z, const double *__restrict__ pold,
                                                            double *__restrict__ pnew, double *__restrict__ qseg,
-                                                           int *counter, double *parts, PcgState *st,
+                                                           int *counter, double *pqs, PcgState *st,
                                                            double *red) {
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double beta = st->beta;
   const long long ns = st->ns;
   const int l = lane_id();
-  double pq = 0.0;
   while (true) {
     int si = 0;
     if (l == 0) si = atomicAdd(counter, 1);
@@ -506,6 +521,7 @@ __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *
         blk_fma(b0, beta, a0, a1, a2);
       }
     const int v = s_vrow[32 * s + l];
+    double pq = 0.0;
     if (v >= 0) {
       const int64_t row = v_row[v];
       const int64_t i = 3 * row;
@@ -515,7 +531,73 @@ __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *
         pnew[i] = pn0; pnew[i + 1] = pn1; pnew[i + 2] = pn2;
       }
       qseg[3 * (int64_t)v] = a0; qseg[3 * (int64_t)v + 1] = a1; qseg[3 * (int64_t)v + 2] = a2;
-      pq += pn0 * a0 + pn1 * a1 + pn2 * a2;  // p.q is linear in the segments
+      pq = pn0 * a0 + pn1 * a1 + pn2 * a2;  // p.q is linear in the segments
+    }
+    pq = warp_sum(pq);  // the slice's partial (fixed lane order)
+    if (l == 0) pqs[s] = pq;
+  }
+  if (last_block(st)) {
+    double PQ = reduce_parts(pqs, (int)ns, s_red);
+    if (threadIdx.x == 0 && red) {
+      red[0] = PQ;
+    } else if (threadIdx.x == 0) {
+      st->pq = PQ;
+      if (!isfinite(PQ) || !isfinite(st->rz)) {
+        st->status = AGIPC_EBREAKDOWN;
+        st->done = 1;
+        st->it += 1;
+      } else if (PQ <= 0.0) {
+        st->status = AGIPC_EINDEFINITE;
+        st->done = 1;
+        st->it += 1;
+      } else {
+        st->alpha = st->rz / PQ;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K1 on the caller's BSR as it is (no SELL re-layout): warp per row, the row's 9 x nblocks values
+// read flat and coalesced (a 15-block fine row is 1,080 contiguous bytes), p_new = z + beta p_old
+// formed for every gathered column, segmented sums over the row's 3 output components by warp
+// shuffles.  For SHORT solves -- NEXT#1's <= 10 post-coarsening fine iterations -- where
+// the per-solve re-layout of the 1.1 GB fine matrix (two extra passes) costs more than the tiling
+// gains.  Static row -> warp assignment, so the p.q partials (and the solve) are reproducible.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(PCG_THREADS) k_spmv_flat(int64_t n, const int64_t *__restrict__ rp,
+                                                         const int32_t *__restrict__ col,
+                                                         const double *__restrict__ val,
+                                                         const double *__restrict__ z, const double *__restrict__ pold,
+                                                         double *__restrict__ pnew, double *__restrict__ q,
+                                                         double *parts, PcgState *st, double *red) {
+  if (*(volatile int *)&st->done) return;
+  __shared__ double s_red[PCG_WARPS];
+  const double beta = st->beta;
+  const int l = lane_id();
+  double pq = 0.0;
+  const int64_t W = (int64_t)gridDim.x * PCG_WARPS;
+  for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + (threadIdx.x >> 5); row < n; row += W) {
+    const int64_t k0 = rp[row], ne = 9 * (rp[row + 1] - k0);
+    const double *v = val + 9 * k0;
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    for (int64_t e = l; e < ne; e += 32) {
+      const int blk = (int)(e / 9), rem = (int)(e - 9 * (int64_t)blk), ii = rem / 3, jj = rem - 3 * ii;
+      const int64_t c = 3 * (int64_t)__ldg(col + k0 + blk) + jj;
+      const double prod = __ldcs(v + e) * (__ldg(z + c) + beta * __ldg(pold + c));
+      y0 += ii == 0 ? prod : 0.0;
+      y1 += ii == 1 ? prod : 0.0;
+      y2 += ii == 2 ? prod : 0.0;
+    }
+    y0 = warp_sum(y0);
+    y1 = warp_sum(y1);
+    y2 = warp_sum(y2);
+    if (l == 0) {
+      const int64_t i = 3 * row;
+      const double pn0 = z[i] + beta * pold[i], pn1 = z[i + 1] + beta * pold[i + 1], pn2 = z[i + 2] + beta * pold[i + 2];
+      pnew[i] = pn0; pnew[i + 1] = pn1; pnew[i + 2] = pn2;
+      q[i] = y0; q[i + 1] = y1; q[i + 2] = y2;
+      pq += pn0 * y0 + pn1 * y1 + pn2 * y2;
     }
   }
   pq = block_sum(pq, s_red);
@@ -539,6 +621,11 @@ __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *
       }
     }
   }
+}
+
+__global__ void k_iota64(int64_t n, int64_t *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) out[i] = i;
 }
 
 // ------------------------------------------------------------------------------------
@@ -811,6 +898,7 @@ static SpmvKernel spmv_kernel(int un) {
 
 struct PcgBufs {
   double *x, *r, *z, *P[2], *qseg, *Dinv, *parts, *sval;
+  double *pqs;  // per-slice p.q partials of K1 (summed in slice order by its last CTA)
   int64_t *vr_ptr, *sptr;
   int32_t *v_row, *v_len, *perm, *scol, *s_vrow, *order;
   int *counters;  // two slice counters, used by alternate iterations
@@ -826,32 +914,32 @@ struct PcgBufs {
   double *arena = nullptr;  // x, r, z, p0, p1, qseg, Dinv (+ ytin, yext): one L2 window
   int spmv_un = 3;          // blocks per thread in flight in k_spmv_sell
   size_t arena_bytes = 0;
+  bool flat = false;        // K1 = k_spmv_flat on the caller's BSR (short solves, no re-layout)
+  const int64_t *A_rp = nullptr;
+  const int32_t *A_col = nullptr;
+  const double *A_val = nullptr;
+  int64_t n = 0;
 };
 
 
-// L2 residency of the PCG vectors (B200: 126 MB L2).  The matrix is streamed with evict-first
-// loads; the vector arena gets a persisting access-policy window on the solve stream (the
-// captured kernel nodes inherit it).  AGIPC_L2_WINDOW=0 disables it (A/B runs).  Sets the
-// device's persisting-L2 limit (cudaLimitPersistingL2CacheSize) to the window size.
-static void pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size_t bytes) {
-  const char *e = getenv("AGIPC_L2_WINDOW");
-  const bool on = !(e && atoi(e) == 0) && base && bytes > 0;
+// L2 residency of the PCG vectors (B200: 126 MB L2), opt-in (agipc_set_option
+// AGIPC_OPT_L2_PERSIST sets the device's persisting-L2 limit once, on the caller's request): the
+// matrix is streamed with evict-first loads; the vector arena gets a persisting access-policy
+// window on the solve stream (the captured kernel nodes inherit it).  Returns whether a window
+// was set (the persisting lines are then released after the solve).
+static bool pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size_t bytes) {
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
+  const bool on = h->opt_l2_persist > 0 && base && bytes > 0;
   if (on) {
-    int max_win = 0, max_persist = 0;
+    int max_win = 0;
     cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-    if (max_win <= 0 || max_persist <= 0) {
+    if (max_win <= 0) {
       cudaGetLastError();
-      return;
+      return false;
     }
     const size_t win = std::min(bytes, (size_t)max_win);
-    const size_t persist = std::min(win, (size_t)max_persist);
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) {
-      cudaGetLastError();
-      return;
-    }
+    const size_t persist = std::min(win, h->opt_l2_persist);
     v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
     v.accessPolicyWindow.num_bytes = win;
     v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)win);
@@ -859,6 +947,14 @@ static void pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
   }
   if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+  return on;
+}
+
+static void pcg_l2_release(cudaStream_t s) {
+  cudaStreamAttrValue v;
+  memset(&v, 0, sizeof(v));
+  if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+  if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
 }
 
 // iteration j reads p_old = P[j&1] and writes p_new = P[(j+1)&1] (the chunk length is even)
@@ -868,14 +964,17 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
     double *pold = B.P[k & 1], *pnew = B.P[(k + 1) & 1];
     const bool sample = ev && (k % PROF_EVERY) == 0;  // sampled kernel timing (low overhead)
     if (sample) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
-    if (B.sym)
+    if (B.flat)
+      k_spmv_flat<<<B.G1, PCG_THREADS, 0, s>>>(B.n, B.A_rp, B.A_col, B.A_val, B.z, pold, pnew, B.qseg, B.parts, B.st,
+                                               nullptr);
+    else if (B.sym)
       k_spmv_sym<<<B.G1, PCG_THREADS, 3 * sizeof(double) * B.win, s>>>(
           B.sptr, B.scol, B.sval, B.s_vrow, B.v_row, B.vr_ptr, B.z, pold, pnew, B.qseg, B.ytin, B.yext, B.win,
           B.counters + (k & 1), B.parts, B.st, B.all_red);
     else
       spmv_kernel(B.spmv_un)<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
                                                           B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (k & 1),
-                                                          B.parts, B.st, nullptr);
+                                                          B.pqs, B.st, nullptr);
     if (sample) cudaEventRecordWithFlags(ev[3 * k + 1], s, cudaEventRecordExternal);
     k_update<1, PCG_THREADS><<<B.G2, PCG_THREADS, 0, s>>>(n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv, B.counters + ((k + 1) & 1),
                                           B.parts, B.st, nullptr, B.ytin, B.yext);
@@ -894,9 +993,16 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
 // and AGIPC_STORAGE_UPPER takes A already stored that way; both run k_spmv_sym (NEXT#2).
 static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *Ah, int64_t n_gs, const double *b,
                               const double *x, int zero_x0, double rel_tol, int max_iters, PcgBufs &B,
-                              PcgState *hst, double *red, int storage = AGIPC_STORAGE_FULL) {
+                              PcgState *hst, double *red, int storage = AGIPC_STORAGE_FULL,
+                              const char *pfx = "pcg_", bool flat = false) {
+#define PN(x) (std::string(pfx) + (x)).c_str()  // the distributed solve has its own buffers
   const int64_t n = A->n_rows;
   B.sym = storage != AGIPC_STORAGE_FULL;
+  B.flat = flat && !B.sym && !Ah;
+  B.n = n;
+  B.A_rp = A->row_ptr;
+  B.A_col = A->col;
+  B.A_val = A->val;
   B.win = SORT_WIN;
   if (B.sym) {
     B.win = 1024;
@@ -920,7 +1026,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     int64_t off[10];
     off[0] = 0;
     for (int i = 0; i < 9; ++i) off[i + 1] = off[i] + ((len[i] + 31) & ~(int64_t)31);  // 256-B aligned
-    WS(h, arena, double, "pcg_vec_arena", off[9]);
+    WS(h, arena, double, PN("vec_arena"), off[9]);
     B.x = arena + off[0]; B.r = arena + off[1]; B.z = arena + off[2];
     B.P[0] = arena + off[3]; B.P[1] = arena + off[4]; B.qseg = arena + off[5]; B.Dinv = arena + off[6];
     B.ytin = len[7] ? arena + off[7] : nullptr;
@@ -928,17 +1034,18 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     B.arena = arena;
     B.arena_bytes = sizeof(double) * (size_t)off[9];
   }
-  WS(h, vr, int64_t, "pcg_vr_ptr", n + 1); B.vr_ptr = vr;
-  WS(h, nseg, int32_t, "pcg_nseg", n);
-  WS(h, vrow, int32_t, "pcg_v_row", nv_bound); B.v_row = vrow;
-  WS(h, vlen, int32_t, "pcg_v_len", nv_bound); B.v_len = vlen;
-  WS(h, perm, int32_t, "pcg_perm", nv_bound); B.perm = perm;
-  WS(h, slen, int32_t, "pcg_slen", B.ns_bound);
-  WS(h, sptr, int64_t, "pcg_sptr", B.ns_bound + 1); B.sptr = sptr;
-  WS(h, svr, int32_t, "pcg_s_vrow", 32 * B.ns_bound); B.s_vrow = svr;
-  WS(h, stp, PcgState, "pcg_state", 1); B.st = stp;
-  WS(h, order, int32_t, "pcg_order", B.ns_bound); B.order = order;
-  WS(h, ctr, int, "pcg_counters", 2); B.counters = ctr;
+  WS(h, vr, int64_t, PN("vr_ptr"), n + 1); B.vr_ptr = vr;
+  WS(h, nseg, int32_t, PN("nseg"), n);
+  WS(h, vrow, int32_t, PN("v_row"), nv_bound); B.v_row = vrow;
+  WS(h, vlen, int32_t, PN("v_len"), nv_bound); B.v_len = vlen;
+  WS(h, perm, int32_t, PN("perm"), nv_bound); B.perm = perm;
+  WS(h, slen, int32_t, PN("slen"), B.ns_bound);
+  WS(h, sptr, int64_t, PN("sptr"), B.ns_bound + 1); B.sptr = sptr;
+  WS(h, svr, int32_t, PN("s_vrow"), 32 * B.ns_bound); B.s_vrow = svr;
+  WS(h, stp, PcgState, PN("state"), 1); B.st = stp;
+  WS(h, order, int32_t, PN("order"), B.ns_bound); B.order = order;
+  WS(h, ctr, int, PN("counters"), 2); B.counters = ctr;
+  WS(h, pqs, double, PN("pqs"), B.ns_bound + 1); B.pqs = pqs;
   int occ = 0;
   if (B.sym) {
     const size_t smem = 3 * sizeof(double) * B.win;
@@ -953,13 +1060,14 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_kernel(B.spmv_un), PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
   }
+  if (B.flat) B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
   // K2: 2 CTAs of 256 threads per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl,
   // upd_nt.jsonl: 3-8 CTAs per SM, 2 slots per pass or 512-thread CTAs are not faster)
   B.upd_u = 1;
   B.G2 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_THREADS), 2 * (int64_t)h->sm_count));
   const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
   const int Gp = std::max(std::max(B.G1, B.G2), Gi);
-  WS(h, parts, double, "pcg_parts", 3 * Gp); B.parts = parts;
+  WS(h, parts, double, PN("parts"), 3 * Gp); B.parts = parts;
   PcgState init;
   memset(&init, 0, sizeof(init));
   init.tol = rel_tol;
@@ -976,10 +1084,17 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   const int64_t *rb = A->row_ptr, *re = A->row_ptr + 1;
   int64_t *ub = nullptr;
   if (storage == AGIPC_STORAGE_SYM) {
-    WS(h, ubw, int64_t, "pcg_ub", n + 1); ub = ubw; rb = ubw;
+    WS(h, ubw, int64_t, PN("ub"), n + 1); ub = ubw; rb = ubw;
   }
   LAUNCH(h, k_dinv, (unsigned)cdiv(n, 256), 256, 0, n, A->row_ptr, A->col, A->val, B.Dinv, stp, ub,
          storage == AGIPC_STORAGE_UPPER ? 1 : 0);
+  if (B.flat) {  // one "segment" per row: K2 sums q[vr_ptr[i] .. vr_ptr[i+1]) = q[i]
+    LAUNCH(h, k_iota64, (unsigned)cdiv(n + 1, 256), 256, 0, n, B.vr_ptr);
+    LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
+           parts, stp, zero_x0, red, (const double *)nullptr);
+    CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+    return AGIPC_OK;
+  }
   // SELL layout (once per solve)
   const int64_t *hrp = Ah ? Ah->row_ptr : nullptr;
   LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, nseg);
@@ -999,8 +1114,8 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
   CU_TRY(h, cudaStreamSynchronize(s0));
   const long long sell_blocks = hst->sell_blocks;
-  WS(h, scol, int32_t, "pcg_scol", sell_blocks + 32); B.scol = scol;
-  WS(h, sval, double, "pcg_sval", 9 * sell_blocks + 288); B.sval = sval;
+  WS(h, scol, int32_t, PN("scol"), sell_blocks + 32); B.scol = scol;
+  WS(h, sval, double, PN("sval"), 9 * sell_blocks + 288); B.sval = sval;
   LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
          0, stp, rb, re, A->col, A->val, hrp, Ah ? Ah->col : nullptr, Ah ? Ah->val : nullptr, B.vr_ptr, B.perm,
          B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
@@ -1009,7 +1124,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaMemsetAsync(B.ytin, 0, sizeof(double) * 3 * n, s0));  // straddling rows keep 0
     CU_TRY(h, cudaMemsetAsync(B.yext, 0, sizeof(double) * 3 * n, s0));
     if (storage == AGIPC_STORAGE_UPPER && !zero_x0) {  // r = b - A x0 from the upper half
-      WS(h, axw, double, "pcg_ax", 3 * n + 2);
+      WS(h, axw, double, PN("ax"), 3 * n + 2);
       CU_TRY(h, cudaMemsetAsync(axw, 0, sizeof(double) * 3 * n, s0));
       LAUNCH(h, k_ax_upper, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 16 * h->sm_count)), 256, 0, n,
              A->row_ptr, A->col, A->val, B.x, axw);
@@ -1019,6 +1134,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
          parts, stp, zero_x0, red, ax);
   return AGIPC_OK;
+#undef PN
 }
 
 static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int storage, const double *b, double *x,
@@ -1039,7 +1155,11 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
   PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
   if (ast != AGIPC_OK) return ast;
   PcgBufs B;
-  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr, storage);
+  // short solves (NEXT#1: <= 10 post-coarsening fine iterations) stream the caller's BSR
+  // flat instead of re-laying it out; AGIPC_PCG_FLAT=0/1 forces a variant (A/B runs)
+  bool flat = storage == AGIPC_STORAGE_FULL && max_iters <= 32;
+  if (const char *e = getenv("AGIPC_PCG_FLAT")) flat = storage == AGIPC_STORAGE_FULL && atoi(e) != 0;
+  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr, storage, "pcg_", flat);
   if (ast != AGIPC_OK) return ast;
   if (max_iters == 0) {
     CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
@@ -1054,12 +1174,14 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     }
     int chunk = std::max(2, std::min(check_every, max_iters));
     chunk += chunk & 1;  // even: the p ping-pong parity is the same at every graph launch
-    pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);
-    const void *key[8] = {B.sval, B.scol, B.x, B.qseg, B.Dinv, B.sptr, B.P[0], B.parts};
-    bool same = g->exec && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
+    const bool l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);
+    const void *key[8] = {B.flat ? (const void *)B.A_val : B.sval, B.flat ? (const void *)B.A_col : B.scol, B.x, B.qseg,
+                          B.Dinv, B.flat ? (const void *)B.A_rp : B.sptr, B.P[0], B.parts};
+    // ws_gen changes whenever any named buffer moved (every pointer baked into the graph is one)
+    bool same = g->exec && g->ws_gen == h->ws_gen && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
                 g->grid2 == B.G2 && g->prof == h->prof && g->sym == B.sym && g->win == B.win && g->yext == B.yext &&
                 g->all_red == B.all_red && g->upd_u == B.upd_u &&
-                g->spmv_un == B.spmv_un;
+                g->spmv_un == B.spmv_un && g->flat == B.flat && g->n_flat == B.n;
     for (int i = 0; i < 8 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
@@ -1091,6 +1213,9 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
       g->all_red = B.all_red;
       g->upd_u = B.upd_u;
       g->spmv_un = B.spmv_un;
+      g->ws_gen = h->ws_gen;
+      g->flat = B.flat;
+      g->n_flat = B.n;
       for (int i = 0; i < 8; ++i) g->key[i] = key[i];
     }
     CU_TRY(h, cudaEventRecord(g->ev_in, s0));
@@ -1120,12 +1245,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     }
     // the solve's vectors were persisting L2 lines; release them so the next Newton step's
     // coarsen/assemble kernels get the whole L2 (the loop above has synchronised the solve)
-    if (B.arena) {
-      cudaStreamAttrValue v;
-      memset(&v, 0, sizeof(v));
-      if (cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
-      if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
-    }
+    if (l2win) pcg_l2_release(g->stream);
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
     CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
   }
@@ -1169,6 +1289,8 @@ extern "C" agipc_status agipc_pcg_solve_sym(agipc_handle h, const agipc_bsr *A, 
 enum { DP_INIT = 0, DP_ALPHA = 1, DP_UPDATE = 2, DP_NONE = 3 };
 
 struct DPcg {
+  PcgGraph *g = nullptr;  // agipc_dpcg_solve: captured iterations (NCCL calls included)
+  std::vector<int64_t> gkey;
   PcgBufs B;
   int64_t n = 0, n_gs = 0;
   int k = 0;            // iterations launched (p ping-pong parity)
@@ -1176,7 +1298,11 @@ struct DPcg {
   bool active = false;
 };
 
-void dpcg_free(DPcg *d) { delete d; }
+void dpcg_free(DPcg *d) {
+  if (d) pcg_graph_free(d->g);
+  delete d;
+}
+bool dpcg_active(agipc_handle h) { return h->dpcg && h->dpcg->active; }
 
 __global__ void k_dscalars(PcgState *st, const double *red, int phase) {
   if (phase == DP_INIT) {
@@ -1185,6 +1311,10 @@ __global__ void k_dscalars(PcgState *st, const double *red, int phase) {
     st->bn2 = red[2];
     st->it = 0;
     st->beta = 0.0;
+    if (red[3] > 0.0) {  // some rank has a singular diagonal block: every rank stops
+      st->status = AGIPC_ESINGULAR;
+      st->done = 1;
+    }
     if (!st->done && sqrt(red[1]) <= st->tol * sqrt(red[2])) st->done = 1;
     return;
   }
@@ -1265,7 +1395,8 @@ extern "C" agipc_status agipc_dpcg_setup(agipc_handle h, const agipc_bsr *A, con
   agipc_status ast;
   PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
   if (ast != AGIPC_OK) return ast;
-  ast = pcg_setup(h, A, A_halo, n_ghost_slots, b, nullptr, 1, rel_tol, max_iters, d->B, hst, red);
+  ast = pcg_setup(h, A, A_halo, n_ghost_slots, b, nullptr, 1, rel_tol, max_iters, d->B, hst, red, AGIPC_STORAGE_FULL,
+                  "dpcg_");
   if (ast != AGIPC_OK) return ast;
   d->n = n;
   d->n_gs = n_ghost_slots;
@@ -1299,7 +1430,7 @@ extern "C" agipc_status agipc_dpcg_spmv(agipc_handle h, const double *recvbuf, d
     LAUNCH(h, k_ghost_in, (unsigned)std::min<int64_t>(cdiv(3 * d->n_gs, 256), 4 * h->sm_count), 256, 0, d->n, d->n_gs,
            recvbuf, B.z, (const double *)pold, pnew, (const PcgState *)B.st);
   LAUNCH(h, spmv_kernel(B.spmv_un), (unsigned)B.G1, PCG_THREADS, 0, B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row,
-         B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (d->k & 1), B.parts, B.st, red);
+         B.vr_ptr, B.z, pold, pnew, B.qseg, B.counters + (d->k & 1), B.pqs, B.st, red);
   d->pending = DP_ALPHA;
   return AGIPC_OK;
 }
@@ -1362,6 +1493,177 @@ extern "C" agipc_status agipc_dpcg_finish(agipc_handle h, const double *red, dou
   if (stats->status == AGIPC_ESINGULAR) return set_err(h, AGIPC_ESINGULAR, "dpcg: singular diagonal block");
   if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "dpcg: p^T A p <= 0");
   if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "dpcg: NaN/Inf");
+  if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
+  return AGIPC_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// agipc_dpcg_solve: the split-phase iteration above with the exchanges inside the library
+// (SURVEY 8(e) exchange 4): per iteration
+//   k_ghost_in (ghost z, p)  K1 (rank's p.q partial)  AllReduce(1)  k_dscalars(alpha)
+//   K2 (rank's r.z, r.r partials)  AllReduce(2)  k_dscalars(beta, stop)  pack z  send/recv
+// -- the same kernels in the same order as the split-phase calls driven by dist.py over gloo, so
+// every rank takes the same decisions from the same reduced sums; check_every iterations are one
+// CUDA graph with the NCCL calls captured in it.
+// ------------------------------------------------------------------------------------
+agipc_status comm_check(agipc_handle h, const char *who);                          // comm.cu
+agipc_status comm_allreduce_f64(agipc_handle h, double *buf, int64_t n, cudaStream_t s);
+agipc_status comm_sendrecv_f64(agipc_handle h, int n_peers, const int *peer_rank, const double *sendbuf,
+                               const int64_t *soff, double *recvbuf, const int64_t *roff, cudaStream_t s);
+
+struct DHalo {  // the PCG halo as the graph sees it (stable workspace pointers)
+  int P = 0;
+  std::vector<int> peer;
+  std::vector<int64_t> soff, roff;  // element (double) offsets per peer
+  int64_t n_send = 0;
+  const int32_t *send_idx = nullptr;
+  double *sendbuf = nullptr, *recvbuf = nullptr;
+};
+
+static agipc_status dpcg_enqueue(agipc_handle h, cudaStream_t s, int iters, DPcg *d, const DHalo &X, double *red) {
+  const PcgBufs &B = d->B;
+  for (int k = 0; k < iters; ++k) {
+    double *pold = B.P[k & 1], *pnew = B.P[(k + 1) & 1];
+    if (d->n_gs > 0)
+      k_ghost_in<<<(unsigned)std::min<int64_t>(cdiv(3 * d->n_gs, 256), 4 * h->sm_count), 256, 0, s>>>(
+          d->n, d->n_gs, X.recvbuf, B.z, pold, pnew, B.st);
+    spmv_kernel(B.spmv_un)<<<B.G1, PCG_THREADS, 0, s>>>(B.sptr, B.scol, B.sval, B.s_vrow, B.order, B.v_row, B.vr_ptr, B.z,
+                                                       pold, pnew, B.qseg, B.counters + (k & 1), B.pqs, B.st, red);
+    agipc_status st = comm_allreduce_f64(h, red, 1, s);
+    if (st != AGIPC_OK) return st;
+    k_dscalars<<<1, 1, 0, s>>>(B.st, red, (int)DP_ALPHA);
+    k_update<1, PCG_THREADS><<<B.G2, PCG_THREADS, 0, s>>>(d->n, B.vr_ptr, B.x, B.r, B.z, pnew, B.qseg, B.Dinv,
+                                                           B.counters + ((k + 1) & 1), B.parts, B.st, red, nullptr,
+                                                           nullptr);
+    if ((st = comm_allreduce_f64(h, red, 2, s)) != AGIPC_OK) return st;
+    k_dscalars<<<1, 1, 0, s>>>(B.st, red, (int)DP_UPDATE);
+    if (X.n_send > 0)
+      k_pack3<<<(unsigned)cdiv(3 * X.n_send, 256), 256, 0, s>>>(X.n_send, X.send_idx, B.z, X.sendbuf);
+    if ((st = comm_sendrecv_f64(h, X.P, X.peer.data(), X.sendbuf, X.soff.data(), X.recvbuf, X.roff.data(), s)) !=
+        AGIPC_OK)
+      return st;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(h, AGIPC_ECUDA, "dpcg launch: %s", cudaGetErrorString(e));
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_dpcg_solve(agipc_handle h, const agipc_bsr *A, const agipc_bsr *A_halo,
+                                         int64_t n_ghost_slots, const agipc_halo *slots, const double *b, double *x,
+                                         double rel_tol, int max_iters, int check_every, agipc_pcg_stats *stats) {
+  if (!h) return AGIPC_EINVAL;
+  agipc_status ast = comm_check(h, "dpcg_solve");
+  if (ast != AGIPC_OK) return ast;
+  if (!A || !b || !x || !stats || max_iters < 0 || A->n_rows <= 0 || n_ghost_slots < 0 || !(rel_tol >= 0.0))
+    return set_err(h, AGIPC_EINVAL, "dpcg_solve: bad arguments");
+  if (dpcg_active(h)) return set_err(h, AGIPC_EINVAL, "dpcg_solve: a split-phase distributed solve is in progress");
+  const int P = slots ? slots->n_peers : 0;
+  if (P > 0 && (!slots->peer_rank || !slots->send_ptr || !slots->recv_ptr))
+    return set_err(h, AGIPC_EINVAL, "dpcg_solve: null halo arrays");
+  memset(stats, 0, sizeof(*stats));
+  CU_TRY(h, cudaSetDevice(h->device));
+  if (check_every <= 0) check_every = 16;
+  if (!h->dpcg) h->dpcg = new DPcg();
+  DPcg *d = h->dpcg;
+  cudaStream_t s0 = h->stream;
+  PcgState *hst = (PcgState *)pinned_get(h, sizeof(PcgState), &ast);
+  if (ast != AGIPC_OK) return ast;
+  // halo of the PCG vectors in stable workspace buffers (the graph keeps their addresses)
+  DHalo X;
+  X.P = P;
+  X.soff.assign(P + 1, 0);
+  X.roff.assign(P + 1, 0);
+  for (int q = 0; q < P; ++q) {
+    X.peer.push_back(slots->peer_rank[q]);
+    X.soff[q + 1] = X.soff[q] + 3 * (slots->send_ptr[q + 1] - slots->send_ptr[q]);
+    X.roff[q + 1] = X.roff[q] + 3 * (slots->recv_ptr[q + 1] - slots->recv_ptr[q]);
+  }
+  X.n_send = X.soff[P] / 3;
+  if (X.roff[P] / 3 != n_ghost_slots) return set_err(h, AGIPC_EINVAL, "dpcg_solve: recv ranges != n_ghost_slots");
+  WS(h, red, double, "dpcg_red", 4);
+  WS(h, sidx, int32_t, "dpcg_send_idx", X.n_send + 1);
+  WS(h, sbuf, double, "dpcg_sendbuf", 3 * X.n_send + 3);
+  WS(h, rbuf, double, "dpcg_recvbuf", 3 * n_ghost_slots + 3);
+  X.send_idx = sidx;
+  X.sendbuf = sbuf;
+  X.recvbuf = rbuf;
+  if (X.n_send > 0) {
+    if (!slots->send_idx) return set_err(h, AGIPC_EINVAL, "dpcg_solve: null send_idx");
+    CU_TRY(h, cudaMemcpyAsync(sidx, slots->send_idx + slots->send_ptr[0], sizeof(int32_t) * X.n_send,
+                              cudaMemcpyDeviceToDevice, s0));
+  }
+  ast = pcg_setup(h, A, A_halo, n_ghost_slots, b, nullptr, 1, rel_tol, max_iters, d->B, hst, red, AGIPC_STORAGE_FULL,
+                  "dpcg_");
+  if (ast != AGIPC_OK) return ast;
+  d->n = A->n_rows;
+  d->n_gs = n_ghost_slots;
+  const PcgBufs &B = d->B;
+  // setup sums [r.z, r.r, b.b, singular] over the ranks, then the first halo of z
+  if ((ast = comm_allreduce_f64(h, red, 4, s0)) != AGIPC_OK) return ast;
+  LAUNCH(h, k_dscalars, 1, 1, 0, B.st, (const double *)red, (int)DP_INIT);
+  if (X.n_send > 0) LAUNCH(h, k_pack3, (unsigned)cdiv(3 * X.n_send, 256), 256, 0, X.n_send, (const int32_t *)sidx, B.z, sbuf);
+  if ((ast = comm_sendrecv_f64(h, P, X.peer.data(), sbuf, X.soff.data(), rbuf, X.roff.data(), s0)) != AGIPC_OK)
+    return ast;
+  if (max_iters > 0) {
+    PcgGraph *g = d->g;
+    if (!g) {
+      g = d->g = new PcgGraph();
+      CU_TRY(h, cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+      CU_TRY(h, cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
+      CU_TRY(h, cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming));
+    }
+    int chunk = std::max(2, std::min(check_every, max_iters));
+    chunk += chunk & 1;
+    std::vector<int64_t> key = {(int64_t)h->ws_gen, d->n, d->n_gs, chunk, B.G1, B.G2, B.spmv_un, P,
+                                (int64_t)(intptr_t)h->comm};
+    for (int q = 0; q < P; ++q) {
+      key.push_back(X.peer[q]);
+      key.push_back(X.soff[q + 1]);
+      key.push_back(X.roff[q + 1]);
+    }
+    const bool l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);  // before capture: nodes inherit it
+    if (!g->exec || key != d->gkey) {
+      if (g->exec) {
+        cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+      }
+      cudaGraph_t graph;
+      CU_TRY(h, cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+      agipc_status es = dpcg_enqueue(h, g->stream, chunk, d, X, red);
+      cudaError_t ce = cudaStreamEndCapture(g->stream, &graph);
+      if (es != AGIPC_OK) return es;
+      if (ce != cudaSuccess) return set_err(h, AGIPC_ECUDA, "dpcg capture: %s", cudaGetErrorString(ce));
+      CU_TRY(h, cudaGraphInstantiate(&g->exec, graph, 0));
+      cudaGraphDestroy(graph);
+      d->gkey = key;
+    }
+    CU_TRY(h, cudaEventRecord(g->ev_in, s0));
+    CU_TRY(h, cudaStreamWaitEvent(g->stream, g->ev_in, 0));
+    {
+      ProfScope prof_solve(h, PROF_PCG_SOLVE, g->stream);
+      int launched = 0, it_before = 0;
+      while (true) {
+        CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
+        launched += chunk;
+        CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
+        CU_TRY(h, cudaStreamSynchronize(g->stream));
+        const int ran = hst->it - it_before;
+        h->launches += (2 + (d->n_gs > 0) + (X.n_send > 0) + 2) * (int64_t)ran;
+        it_before = hst->it;
+        if (hst->done || launched >= max_iters) break;  // identical on every rank
+      }
+    }
+    if (l2win) pcg_l2_release(g->stream);
+    CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
+    CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
+  }
+  LAUNCH(h, k_copy_out, (unsigned)cdiv(3 * d->n, 256), 256, 0, 3 * d->n, B.x, x);
+  CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+  CU_TRY(h, cudaStreamSynchronize(s0));
+  dpcg_fill_stats(hst, stats);
+  if (stats->status == AGIPC_ESINGULAR) return set_err(h, AGIPC_ESINGULAR, "dpcg_solve: singular diagonal block");
+  if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "dpcg_solve: p^T A p <= 0");
+  if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "dpcg_solve: NaN/Inf");
   if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
   return AGIPC_OK;
 }

@@ -18,11 +18,11 @@
 #define TP_WARPS 8
 #define TP_WARP_CAP 512
 
-__global__ void k_tp_hist(int64_t n, const int32_t *__restrict__ ti, int64_t n_rows, int *__restrict__ cnt,
-                          int *__restrict__ bad) {
+__global__ void k_tp_hist(int64_t n, const int32_t *__restrict__ ti, const int32_t *__restrict__ tj, int64_t n_rows,
+                          int *__restrict__ cnt, int *__restrict__ bad) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = ti[t];
-    if (i < 0 || i >= n_rows) {
+    const int i = ti[t], j = tj[t];
+    if (i < 0 || i >= n_rows || j < 0) {
       atomicOr(bad, 1);
       continue;
     }
@@ -30,10 +30,11 @@ __global__ void k_tp_hist(int64_t n, const int32_t *__restrict__ ti, int64_t n_r
   }
 }
 
-__global__ void k_tp_scatter(int64_t n, const int32_t *__restrict__ ti, const int64_t *__restrict__ rstart,
+__global__ void k_tp_scatter(int64_t n, int64_t n_rows, const int32_t *__restrict__ ti, const int64_t *__restrict__ rstart,
                              int *__restrict__ cur, int32_t *__restrict__ bucket) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int i = ti[t];
+    if (i < 0 || i >= n_rows) continue;  // flagged by k_tp_hist (EINVAL before any use)
     bucket[rstart[i] + atomicAdd(cur + i, 1)] = (int32_t)t;
   }
 }
@@ -212,11 +213,11 @@ extern "C" agipc_status agipc_triplet_plan(agipc_handle h, int64_t n_rows, int64
   int *flags = cnt + 2 * (n_rows + 1);  // [0] bad index, [1] number of big rows
   CU_TRY(h, cudaMemsetAsync(cnt, 0, sizeof(int) * (2 * (n_rows + 1) + 2), s));
   const unsigned G = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_trip, 256), 16 * h->sm_count));
-  LAUNCH(h, k_tp_hist, G, 256, 0, n_trip, ti, n_rows, cnt, flags);
+  LAUNCH(h, k_tp_hist, G, 256, 0, n_trip, ti, tj, n_rows, cnt, flags);
   agipc_status st = scan_exclusive_i64(h, SCAN_SRC_I32, cnt, n_rows, rstart);
   if (st != AGIPC_OK) return st;
   int32_t *bucket = plan->seg_idx;  // the sorted buckets are seg_idx
-  LAUNCH(h, k_tp_scatter, G, 256, 0, n_trip, ti, (const int64_t *)rstart, cur, bucket);
+  LAUNCH(h, k_tp_scatter, G, 256, 0, n_trip, n_rows, ti, (const int64_t *)rstart, cur, bucket);
   const unsigned GR = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_rows, TP_WARPS), 64 * h->sm_count));
   LAUNCH(h, k_tp_rows<0>, GR, TP_WARPS * 32, 0, n_rows, (const int64_t *)rstart, bucket, tj, rowlen,
          (const int64_t *)nullptr, (int32_t *)nullptr, (int64_t *)nullptr, big, flags + 1);
@@ -224,7 +225,7 @@ extern "C" agipc_status agipc_triplet_plan(agipc_handle h, int64_t n_rows, int64
   if (st != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(hf, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CU_TRY(h, cudaStreamSynchronize(s));
-  if (hf[0]) return set_err(h, AGIPC_EINVAL, "triplet_plan: a row index is outside [0, n_rows)");
+  if (hf[0]) return set_err(h, AGIPC_EINVAL, "triplet_plan: a row index outside [0, n_rows) or a negative column");
   const int nbig = hf[1];
   if (nbig > 0) {
     WS(h, scratch, unsigned long long, "tp_scratch", 2 * n_trip + 64);

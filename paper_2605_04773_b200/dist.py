@@ -1,17 +1,22 @@
 """Multi-GPU partitioned coarsening step (north star).
 
 One process per GPU.  Rank r owns a contiguous range of fine nodes (partition.LocalMesh); every
-step of the path runs in libagipc's kernels on the rank's own rows, and this module only moves
-buffers between ranks with torch.distributed (plumbing):
+step of the path runs in libagipc's kernels on the rank's own rows.  The exchanges:
 
   exchange 1  x_prev / x_cur of the ghost nodes (send/recv), before tagging
   exchange 2  all-gather of the per-rank coarse slot counts -> exclusive scan = global offsets
   exchange 3  column codes of the ghost nodes (send/recv) -> the halo matrix of the coarse rows
   PCG         per iteration: send/recv of z on the ghost slots, all-reduce of [p.q] and [r.z, r.r]
 
-With the NCCL backend the buffers stay on the GPU (NVLink).  With gloo (tests: several processes
-sharing one GPU, or CPU-only host logic) they are staged through host memory; the kernels and
-the numbers are the same."""
+Two transports with the same kernels in the same order:
+  LibComm  (GPU runs, one process per GPU): the library's own NCCL communicator
+           (agipc_comm_init; torch.distributed only broadcasts its 128-byte unique id) -- every
+           exchange is an agipc_* call (agipc_halo_exchange, agipc_comm_allgather_scan,
+           agipc_comm_alltoall_i64) and the PCG is agipc_dpcg_solve, NCCL calls captured in its
+           CUDA graph: no torch collective on the hot path;
+  Comm     (tests: several processes sharing one GPU -- NCCL refuses two ranks on one device --
+           or CPU-only host logic): torch.distributed over gloo staging through host memory,
+           driving the split-phase agipc_dpcg_* calls."""
 from __future__ import annotations
 
 import dataclasses
@@ -20,8 +25,9 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (CoarseBuffers, DeviceMesh, DistPcg, Handle, assemble_coarse, assemble_halo, build_map, coarse_halo,
-               gather_rows, tag_edges)
+from . import (CoarseBuffers, DeviceMesh, DistPcg, Halo, Handle, assemble_coarse, assemble_halo, build_map,
+               coarse_halo, comm_allgather_scan, comm_alltoall_i64, comm_unique_id, dpcg_solve, gather_rows,
+               halo_exchange, tag_edges)
 from .partition import LocalMesh
 
 
@@ -93,6 +99,20 @@ class Comm:
         return {q: t.cpu().numpy() for q, t in recvs.items()}
 
 
+class LibComm:
+    """The library-owned NCCL communicator of handle h (agipc_comm_init).  The process group is used
+    once, to broadcast rank 0's 128-byte unique id (plumbing)."""
+
+    def __init__(self, h: Handle, group=None):
+        self.h = h
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = [comm_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        h.comm_init(uid[0], self.world, self.rank)
+
+
 @dataclasses.dataclass
 class DistCoarse:
     """This rank's share of the coarse system."""
@@ -113,9 +133,10 @@ class DistCoarse:
 class DistCoarseningStep:
     """Rank-local driver of steps 1-4 on a partitioned mesh."""
 
-    def __init__(self, h: Handle, comm: Comm, lm: LocalMesh, device, group_size=32, affine_threshold=32,
+    def __init__(self, h: Handle, comm, lm: LocalMesh, device, group_size=32, affine_threshold=32,
                  theta=5e-5, rel_tol=1e-3, max_iters=10000, check_every=32):
         self.h, self.comm, self.lm = h, comm, lm
+        self.lib = isinstance(comm, LibComm)
         self.group_size, self.affine_threshold, self.theta = group_size, affine_threshold, theta
         self.rel_tol, self.max_iters, self.check_every = rel_tol, max_iters, check_every
         t = lambda a, dt: torch.as_tensor(a).to(device=device, dtype=dt).contiguous()  # noqa: E731
@@ -130,11 +151,32 @@ class DistCoarseningStep:
         self.bufs = CoarseBuffers(device, lm.n_own, 4 * lm.n_own // 8 + 16, lm.bsr_col.shape[0] // 2 + 64)
         self.ghost_code = torch.empty(lm.n_ghost, dtype=torch.int32, device=device)
         self.device = device
+        if self.lib:  # node halo for agipc_halo_exchange: peers ascending, concatenated send lists
+            peers = sorted(set(lm.send_idx) | set(lm.recv_ptr))
+            sp, rp, idx = [0], [0], []
+            for q in peers:
+                si = lm.send_idx.get(q, np.zeros(0, np.int32))
+                idx.append(np.asarray(si, np.int32))
+                sp.append(sp[-1] + len(si))
+                g0, g1 = lm.recv_ptr.get(q, (rp[-1], rp[-1]))
+                assert g0 == rp[-1], "ghost ranges must follow the ascending peer order"
+                rp.append(g1)
+            self.peers = peers
+            self.node_send_all = t(np.concatenate(idx) if idx else np.zeros(0, np.int32), torch.int32)
+            self.node_halo = Halo(peers, sp, self.node_send_all, rp)
+            n_send = sp[-1]
+            self.code_send = torch.empty(max(n_send, 1), dtype=torch.int32, device=device)
+            self.code_halo = Halo(peers, sp, torch.arange(n_send, dtype=torch.int32, device=device), rp)
+            self.node_send_ptr = sp
 
     # -- exchange 1 -------------------------------------------------------------------------
     def halo_positions(self, *xs):
         """Fill the ghost rows of each [n_own+n_ghost, 3] array from the owners."""
         lm = self.lm
+        if self.lib:
+            for x in xs:
+                halo_exchange(self.h, self.node_halo, x, x[lm.n_own:])
+            return
         for x in xs:
             sends = {q: gather_rows(self.h, x, idx) for q, idx in self.send_idx.items()}
             recvs = {q: x[lm.n_own + g0:lm.n_own + g1] for q, (g0, g1) in lm.recv_ptr.items()}
@@ -149,6 +191,8 @@ class DistCoarseningStep:
         cs = assemble_coarse(h, self.dmesh, self.map, info["n_coarse"], self.affine_threshold, self.H_ptr, self.H_col,
                              H_val, g_own, self.bufs)
         n_c = cs.n3 + cs.n12
+        if self.lib:
+            return self._coarsen_lib(cs, info, nf, H_val, Hh_val)
         # exchange 2: counts -> rank-major offsets
         allc = comm.allgather_i64([cs.n_slots, n_c])
         slot_off = int(allc[:comm.rank, 0].sum())
@@ -179,6 +223,43 @@ class DistCoarseningStep:
         return DistCoarse(cs, hrp, hcol, hval, slot_off, coarse_off, allc[:, 0].copy(), base - cs.n_slots, send_slots,
                           rng, info, nf)
 
+    def _coarsen_lib(self, cs, info, nf, H_val, Hh_val) -> DistCoarse:
+        """Exchanges 2 and 3 through the library communicator (device buffers, NCCL)."""
+        h, lm, comm = self.h, self.lm, self.comm
+        n_c = cs.n3 + cs.n12
+        dev = self.device
+        # exchange 2: all-gather exclusive scan of (n_slots, n_coarse) on the device
+        local = torch.tensor([cs.n_slots, n_c], dtype=torch.int64, device=dev)
+        allc, scan = comm_allgather_scan(h, local)
+        # exchange 3: column codes of the sent nodes (concatenated in peer order) and slot counts
+        send_slots, cnt_send = {}, torch.zeros(comm.world, dtype=torch.int64)
+        sp = self.node_send_ptr
+        for k, q in enumerate(self.peers):
+            if sp[k + 1] > sp[k]:
+                code, sl = coarse_halo(h, cs.new_map, cs.n3, n_c, self.node_send_all[sp[k]:sp[k + 1]],
+                                       ghost_code=self.code_send[sp[k]:sp[k + 1]])
+                send_slots[q] = sl
+                cnt_send[q] = sl.shape[0]
+        halo_exchange(h, self.code_halo, self.code_send, self.ghost_code)
+        cnt_recv = comm_alltoall_i64(h, cnt_send.to(dev)).cpu().numpy()
+        sc = scan.cpu().numpy()
+        allc_h = allc.cpu().numpy()
+        base, gptr, sbase, rng = cs.n_slots, [], [], {}
+        for q in self.recv_peers:
+            g0, g1 = lm.recv_ptr[q]
+            m = int(cnt_recv[q])
+            gptr.append(g0)
+            sbase.append(base)
+            rng[q] = (base - cs.n_slots, base - cs.n_slots + m)
+            base += m
+        gptr.append(lm.n_ghost)
+        if not self.recv_peers:
+            gptr = [0]
+        hrp, hcol, hval = assemble_halo(h, self.dmesh, cs.new_map, cs.n3, n_c, self.Hh_ptr, self.Hh_col, Hh_val,
+                                        self.ghost_code, gptr, sbase)
+        return DistCoarse(cs, hrp, hcol, hval, int(sc[0]), int(sc[1]), allc_h[:, 0].copy(), base - cs.n_slots,
+                          send_slots, rng, info, nf)
+
     # -- step 4 -------------------------------------------------------------------------------
     def solve(self, dc: DistCoarse, x=None):
         """Distributed block-Jacobi PCG on H_c y = g_c from y0 = 0 (d_c = -y)."""
@@ -186,42 +267,69 @@ class DistCoarseningStep:
         n = cs.n_slots
         if x is None:
             x = torch.empty((n, 3), dtype=torch.float64, device=self.device)
-        pcg = DistPcg(self.h, cs.row_ptr, cs.col, cs.val, dc.h_row_ptr, dc.h_col, dc.h_val, dc.n_ghost_slots, cs.g_c,
-                      self.rel_tol, self.max_iters)
-        peers_s = sorted(dc.send_slots)
-        tot = sum(int(dc.send_slots[q].shape[0]) for q in peers_s)
-        sendbuf = torch.empty((max(tot, 1), 3), dtype=torch.float64, device=self.device)
-        recvbuf = torch.empty((max(dc.n_ghost_slots, 1), 3), dtype=torch.float64, device=self.device)
-        so, sviews = 0, {}
-        for q in peers_s:
-            m = int(dc.send_slots[q].shape[0])
-            if m:
-                sviews[q] = sendbuf[so:so + m]
-            so += m
-        rviews = {q: recvbuf[a:b] for q, (a, b) in dc.recv_slot_range.items() if b > a}
-        send_all = torch.cat([dc.send_slots[q] for q in peers_s]) if tot else None
-
-        def halo():
-            if send_all is not None:
-                pcg.pack(send_all, sendbuf)
-            comm.exchange(sviews, rviews)
-
-        comm.allreduce_(pcg.red)
-        halo()
-        it = 0
-        while it < self.max_iters:
-            pcg.spmv(recvbuf)
-            comm.allreduce_(pcg.red)
-            pcg.update()
-            comm.allreduce_(pcg.red)
-            halo()
-            it += 1
-            if it % self.check_every == 0 and pcg.status()[0]:
-                break
-        st = pcg.finish(x)
-        return x, st
+        if self.lib:  # agipc_dpcg_solve: halo + all-reduces inside the library's CUDA graph
+            peers = sorted(set(dc.send_slots) | set(dc.recv_slot_range))
+            sp, rp, idx = [0], [0], []
+            for q in peers:
+                sl = dc.send_slots.get(q)
+                idx.append(sl if sl is not None else torch.zeros(0, dtype=torch.int32, device=self.device))
+                sp.append(sp[-1] + (sl.shape[0] if sl is not None else 0))
+                a, b = dc.recv_slot_range.get(q, (rp[-1], rp[-1]))
+                assert a == rp[-1]
+                rp.append(b)
+            send_all = torch.cat(idx) if idx else torch.zeros(0, dtype=torch.int32, device=self.device)
+            slots = Halo(peers, sp, send_all, rp)
+            return dpcg_solve(self.h, cs.row_ptr, cs.col, cs.val, dc.h_row_ptr, dc.h_col, dc.h_val, dc.n_ghost_slots,
+                              slots, cs.g_c, x, self.rel_tol, self.max_iters, self.check_every)
+        return split_phase_solve(self.h, comm, cs.row_ptr, cs.col, cs.val, dc.h_row_ptr, dc.h_col, dc.h_val,
+                                 dc.n_ghost_slots, dc.send_slots, dc.recv_slot_range, cs.g_c, x, self.rel_tol,
+                                 self.max_iters, self.check_every)
 
     def __call__(self, x_prev, x_cur, g_own, H_val, Hh_val, count=False):
         dc = self.coarsen(x_prev, x_cur, g_own, H_val, Hh_val, count)
         x, st = self.solve(dc)
         return dc, x, st
+
+
+def split_phase_solve(h: Handle, comm: Comm, row_ptr, col, val, h_row_ptr, h_col, h_val, n_ghost_slots: int,
+                      send_slots: dict, recv_slot_range: dict, b, x, rel_tol: float, max_iters: int, check_every: int):
+    """The distributed PCG driven from the host over a torch.distributed Comm (the gloo transport of
+    the tests): the split-phase agipc_dpcg_* calls with the all-reduces and the z halo in between --
+    the kernel sequence agipc_dpcg_solve captures with NCCL.  Returns (x, stats); a library error
+    (e.g. ESINGULAR on any rank: the setup sums carry the flag) raises on every rank alike."""
+    dev = b.device
+    pcg = DistPcg(h, row_ptr, col, val, h_row_ptr, h_col, h_val, n_ghost_slots, b, rel_tol, max_iters)
+    peers_s = sorted(send_slots)
+    tot = sum(int(send_slots[q].shape[0]) for q in peers_s)
+    sendbuf = torch.empty((max(tot, 1), 3), dtype=torch.float64, device=dev)
+    recvbuf = torch.empty((max(n_ghost_slots, 1), 3), dtype=torch.float64, device=dev)
+    so, sviews = 0, {}
+    for q in peers_s:
+        m = int(send_slots[q].shape[0])
+        if m:
+            sviews[q] = sendbuf[so:so + m]
+        so += m
+    rviews = {q: recvbuf[a:b_] for q, (a, b_) in recv_slot_range.items() if b_ > a}
+    send_all = torch.cat([send_slots[q] for q in peers_s]) if tot else None
+
+    def halo():
+        if send_all is not None:
+            pcg.pack(send_all, sendbuf)
+        comm.exchange(sviews, rviews)
+
+    comm.allreduce_(pcg.red)
+    halo()
+    it = 0
+    while it < max_iters:
+        pcg.spmv(recvbuf)  # consumes the reduced sums of the previous call (k_dscalars) first
+        comm.allreduce_(pcg.red)
+        pcg.update()
+        comm.allreduce_(pcg.red)
+        halo()
+        it += 1
+        # the done flag is only read after the first spmv has applied the reduced setup sums, so
+        # every rank sees the same flag (a singular block on one rank stops all of them)
+        if it % check_every == 0 and pcg.status()[0]:
+            break
+    st = pcg.finish(x)
+    return x, st

@@ -188,3 +188,36 @@ def comm_allgather_obj(comm, obj):
     out = [None] * comm.world
     dist.all_gather_object(out, obj)
     return out
+
+
+def singular_worker(rank, world, port, out_dir):
+    """a singular diagonal block on ONE rank must stop every rank (no hang)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_04773_b200 as P
+    from paper_2605_04773_b200.dist import Comm, split_phase_solve
+    try:
+        _init(rank, world, port)
+        torch.cuda.set_device(0)
+        comm = Comm()
+        h = P.Handle(0)
+        n = 6
+        d = torch.device("cuda:0")
+        rp = torch.arange(n + 1, dtype=torch.int64, device=d)
+        col = torch.arange(n, dtype=torch.int32, device=d)
+        val = torch.eye(3, dtype=torch.float64, device=d).repeat(n, 1, 1) * (rank + 2.0)
+        if rank == world - 1:
+            val[2] = 0.0
+        b = torch.ones((n, 3), dtype=torch.float64, device=d)
+        x = torch.empty_like(b)
+        try:
+            split_phase_solve(h, comm, rp, col, val, None, None, None, 0, {}, {}, b, x, 1e-8, 1000, 4)
+            status = "ok"
+        except P.AgipcError as e:
+            status = P._status_name(e.status)
+        dist.barrier()
+        dist.destroy_process_group()
+        open(os.path.join(out_dir, f"ok{rank}"), "w").write(status)
+    except Exception:
+        open(os.path.join(out_dir, f"err{rank}"), "w").write(traceback.format_exc())
+        raise

@@ -23,3 +23,15 @@ def test_distributed_step_matches_segmented_oracle(gpu, tmp_path, n, R, thr, kin
     errs = [f.read_text() for f in tmp_path.glob("err*")]
     assert not errs, errs
     assert sorted(os.listdir(tmp_path)) == [f"ok{r}" for r in range(R)]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("R", [2, 3])
+def test_singular_block_on_one_rank_stops_every_rank(gpu, tmp_path, R):
+    """the singular flag travels with the setup sums (red[3]), so every rank
+    returns ESINGULAR instead of the other ranks waiting in the next all-reduce."""
+    from dist_worker import singular_worker
+    mp.start_processes(singular_worker, args=(R, free_port(), str(tmp_path)), nprocs=R, start_method="spawn")
+    errs = [f.read_text() for f in tmp_path.glob("err*")]
+    assert not errs, errs
+    assert [(tmp_path / f"ok{r}").read_text() for r in range(R)] == ["AGIPC_ESINGULAR"] * R

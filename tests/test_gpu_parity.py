@@ -391,6 +391,68 @@ def test_full_size_path(P, h, cfg):
     assert np.array_equal(d.cpu().numpy(), -oracle.prolongate(oa["new_map"], oa["n3"], m.X, xc))
 
 
+def test_newton_step_bitwise_reproducible(P, gpu):
+    """with AGIPC_OPT_DETERMINISTIC no fp64 atomics remain on the path -- the
+    large-row chunks write partials that a fixed-order reduction sums, K1 keeps p.q per slice --
+    so two runs of the same Newton step give bitwise-equal H_c, g_c, PCG iterate and iteration
+    count (C3 walls at 60^3: hundreds of 12-DoF aggregates).  The deterministic H_c also passes
+    the oracle contract (checked at C1 with 12-DoF rows below)."""
+    from paper_2605_04773_b200.step import CoarseningStep
+    c = synth.config_c3(n=60)
+    m = c["mesh"]
+    H = synth.fine_hessian(m, E=c["E"])
+    g = synth.fine_gradient(m.n_nodes)
+    runs = []
+    for _ in range(2):
+        hh = P.Handle(0)
+        hh.set_option(P.OPT_DETERMINISTIC, 1)
+        st = CoarseningStep(hh, dmesh(P, m), dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32),
+                            dev(H, torch.float64), rel_tol=1e-6)
+        nf, info, cs = st.coarsen(dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64),
+                                  dev(g, torch.float64))
+        assert cs.n12 > 0
+        x, s = st.solve(cs)
+        runs.append((cs.val.clone(), cs.g_c.clone(), x.clone(), s["iters"]))
+    (v0, g0, x0, i0), (v1, g1, x1, i1) = runs
+    assert torch.equal(v0, v1) and torch.equal(g0, g1)
+    assert i0 == i1 and torch.equal(x0, x1)
+
+
+@pytest.mark.parametrize("thr", [32, 5, 10 ** 9])
+def test_assemble_deterministic_option_matches_oracle(P, gpu, thr):
+    hd = P.Handle(0)
+    hd.set_option(P.OPT_DETERMINISTIC, 1)
+    for n, p in ((10, 0.6), (14, 0.4)):
+        m = synth.kuhn_grid(n)
+        dm = dmesh(P, m)
+        H = synth.fine_hessian(m)
+        g = synth.fine_gradient(m.n_nodes)
+        _, _, om = check_map(P, hd, m, dm, synth.random_tags(m, p, 3), 32)
+        check_assemble(P, hd, m, dm, om, H, g, thr)
+
+
+def test_assemble_sign_flip_mutation_fails_parity(P, h):
+    """SPEC S:609 mutation check: a restriction with one flipped sign (here: the assembled coarse
+    values of one 12-DoF row negated, i.e. U with -w_f for that slot) must fail the oracle contract
+    -- the parity check is sharp enough to see a sign error in the restriction."""
+    m = synth.kuhn_grid(10)
+    dm = dmesh(P, m)
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    om = oracle.build_map(m.adj_ptr, m.adj_nbr, synth.random_tags(m, 0.6, 2), 32)
+    cs, oa = check_assemble(P, h, m, dm, om, H, g, 5)
+    assert oa["n12"] > 0
+    val = cs.val.cpu().numpy().copy()
+    r = oa["n3"] + 1  # a 12-DoF slot row (p = 1)
+    k0, k1 = oa["row_ptr"][r], oa["row_ptr"][r + 1]
+    val[k0:k1] *= -1.0
+    dv = np.abs(val - oa["val"])
+    assert (dv > 1e-12 * oa["bound"]).any()
+    gc = cs.g_c.cpu().numpy().copy()
+    gc[r] *= -1.0
+    assert (np.abs(gc - oa["g_c"]) > 1e-12 * oa["g_bound"]).any()
+
+
 # ------------------------------------------------------------------------------------------
 # NEXT#4: shells and rods in step 1 (bit-exact norms and tags; accumulation into tet tags)
 # ------------------------------------------------------------------------------------------
