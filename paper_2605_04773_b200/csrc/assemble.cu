@@ -588,18 +588,26 @@ __global__ void __launch_bounds__(1024) k_group_unique_big(const AsmScal *sc, co
 }
 
 // Mirror positions: for every pair with an origin (a small row a meeting the large column b),
-// the column position of a inside b's final row (independent binary searches, thread per pair).
+// the BLOCK INDEX of (slot(b, 0), a) in the final coarse BSR -- row start + column position of a
+// inside b's row -- and b's slot-row length, so the numeric pass writes the mirrored block
+// (slot(b, q), slot(a, p)) at mirpos + q * rowlen(b) + p with no further lookup (independent
+// binary searches, thread per pair; runs after the slot row pointer scan).  Heads of runs with a
+// small column keep the -1 written by the symbolic pass.
 __global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
                              const long long *__restrict__ porig, const int32_t *__restrict__ gbuf,
                              const long long *__restrict__ nb_off, const int32_t *__restrict__ nb_cnt,
-                             const int32_t *__restrict__ f12, int32_t *__restrict__ mir) {
+                             const int32_t *__restrict__ f12, const int32_t *__restrict__ rowlen,
+                             const int64_t *__restrict__ crp, long long *__restrict__ mirpos,
+                             int32_t *__restrict__ mirrl) {
   const long long np = min(sc->pair_count, cap);
+  const long long n3 = sc->n3;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
     const long long o = porig[p];
     if (o < 0) continue;
     const int2 q = pairs[p];
     const int idx = lower_bound_dev<int32_t>(gbuf + nb_off[q.x], nb_cnt[q.x], (int32_t)q.y);
-    mir[o] = colpos(idx, f12[q.x]);
+    mirpos[o] = crp[slot_of(q.x, 0, n3)] + colpos(idx, f12[q.x]);
+    mirrl[o] = rowlen[q.x];
   }
 }
 
@@ -680,7 +688,8 @@ struct WarpArgs {
   int32_t *rowlen;
   int2 *pairs;
   long long *porig;
-  int32_t *mir;                // mirror positions (k_mirror_pos), indexed like mkeys from mir_base
+  long long *mirpos;           // mirror block positions (k_mirror_pos), indexed like mkeys from
+  int32_t *mirrl;              //   mir_base; -1 = the run's column is small (no mirror)
   long long mir_base;
   long long pair_cap;
   AsmScal *scw;
@@ -754,6 +763,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const int U12 = __popc((__ballot_sync(FULL_MASK, head && bs >= n3) & smask) >> (sg * SEG));
       if (segv && sl == 0) A.rowlen[a] = U + 3 * U12;
       const bool emit = head && !A.is_small[bs];  // transposed pair (large column, small node)
+      if (head && !emit) A.mirpos[A.mir_base + wi * SEG + sl] = -1;
       pairs_push(emit, make_int2(bs, a), A.mir_base + wi * SEG + sl, s_pb[w], npb, A.pairs, A.porig, A.pair_cap,
                  A.scw);
       continue;
@@ -773,8 +783,13 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
 #pragma unroll
     for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
     const int ncb_b = valid ? ncb_of(bs, n3) : 1;
-    long long mbase = -1;  // position of column a in the large row bs (B_ji = B_ij^T, reading R22)
-    if (tail && !A.is_small[bs]) mbase = A.mir[A.mir_base + wi * SEG + hl];  // k_mirror_pos
+    // mirrored block (slot(bs, q), slot(a, p)) at mbase + q * mrl + p (B_ji = B_ij^T, reading R22)
+    long long mbase = -1;
+    int mrl = 0;
+    if (tail) {
+      mbase = A.mirpos[A.mir_base + wi * SEG + hl];  // k_mirror_pos (-1: small column)
+      mrl = A.mirrl[A.mir_base + wi * SEG + hl];
+    }
     // park B and the affine coordinates once; a run of one entry (the common case) never reads
     // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
     const int h0 = sg * SEG + hl;
@@ -820,7 +835,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
 #pragma unroll
         for (int x = 0; x < 9; ++x) dst[x] = v[x];
         if (mbase >= 0) {
-          double *mt = A.cval + 9 * (A.crp[slot_of(bs, q, n3)] + mbase + p);
+          double *mt = A.cval + 9 * (mbase + (long long)q * mrl + p);
 #pragma unroll
           for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -925,6 +940,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
       run_base += __shfl_sync(FULL_MASK, incl, 31);
       if (!NUMERIC) {
         const bool emit = head && !A.is_small[b];  // transposed pair (large column, small node)
+        if (head && !emit) A.mirpos[mir0 + e] = -1;
         pairs_push(emit, make_int2(b, a), mir0 + e, s_pb[w], npb, A.pairs, A.porig,
                    A.pair_cap, A.scw);
         continue;
@@ -974,8 +990,12 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
         const int ncb_b = valid ? ncb_of(b, n3) : 1;
         const int Q = __ballot_sync(FULL_MASK, valid && ncb_b == 4) ? 4 : 1;
         const int he = hl < 0 ? carry_he : e0 + hl;  // sorted position of my run's head
-        long long mbase = -1;  // position of column a in the large row b (B_ji = B_ij^T, reading R22)
-        if (tail && !A.is_small[b]) mbase = A.mir[mir0 + he];  // k_mirror_pos
+        long long mbase = -1;  // mirrored block of (b, a): mbase + q * mrl + p (R22, k_mirror_pos)
+        int mrl = 0;
+        if (tail) {
+          mbase = A.mirpos[mir0 + he];
+          mrl = A.mirrl[mir0 + he];
+        }
         const int last_he = __shfl_sync(FULL_MASK, he, 31);
         const bool cont = valid && !tail && l == 31;  // my run continues into the next window
         const int last_cp = __shfl_sync(FULL_MASK, cp, 31);
@@ -1004,7 +1024,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
 #pragma unroll
             for (int x = 0; x < 9; ++x) dst[x] = v[x];
             if (mbase >= 0) {
-              double *mt = A.cval + 9 * (A.crp[slot_of(b, q, n3)] + mbase + p);
+              double *mt = A.cval + 9 * (mbase + (long long)q * mrl + p);
 #pragma unroll
               for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -1109,10 +1129,18 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
         const int b = lst[t];
         const int cp = colpos(t, first12);
         const int ncb_b = ncb_of(b, n3);
-        for (int q = 0; q < ncb_b; ++q) ccol[rs + cp + q] = slot_of(b, q, n3);
+        // blocks of a small column are written exactly once by the small row's mirror (R22);
+        // only the blocks the large-row chunks accumulate into need zeroing
+        const bool zero = !is_small[b];
+        for (int q = 0; q < ncb_b; ++q) {
+          ccol[rs + cp + q] = slot_of(b, q, n3);
+          if (zero) {
+            double *v = cval + 9 * (rs + cp + q);
+#pragma unroll
+            for (int x = 0; x < 9; ++x) v[x] = 0.0;
+          }
+        }
       }
-      double *v = cval + 9 * rs;
-      for (int x = l; x < 9 * rl; x += 32) v[x] = 0.0;
     }
   }
 }
@@ -1331,6 +1359,208 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
         if (l < s) {
           const int i = tab.ci[l];
           const double wi = wgt(A.X, i, NCB, pp);
+          g0 = wi * A.g_f[3 * (int64_t)i];
+          g1 = wi * A.g_f[3 * (int64_t)i + 1];
+          g2 = wi * A.g_f[3 * (int64_t)i + 2];
+        }
+        g0 = warp_sum(g0);
+        g1 = warp_sum(g1);
+        g2 = warp_sum(g2);
+        if (l == 0) {
+          double *gc = A.g_c + 3 * (int64_t)slot_of(a, pp, n3);
+          atomicAdd(gc, g0);
+          atomicAdd(gc + 1, g1);
+          atomicAdd(gc + 2, g2);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Large rows, FACTORISED accumulation (the default atomic path): one warp per 32-children chunk,
+// lane c = child c walks its own fine row.  Eq 4 with w_i = X_bar_i, w_j = X_bar_j:
+//   H_c(a, a)[p][q] = sum_i w_i[p] C_i[q],   C_i[q] = sum_{j in a} w_j[q] B_ij
+// so a diagonal entry costs 36 FMAs (C_i += w_j (x) B_ij) instead of the 144 of the direct
+// (p, q) expansion, and the 144 (p, q, x) sums over the chunk's children are 144 warp
+// reductions per CHUNK (lane o mod 32 keeps output o for the atomics).  Interface entries
+// (large-large, b != a) go to a per-warp shared list and are summed per column aggregate after
+// the children loop, as in k_num_large_atomic.  Small columns: mirrored by the small rows (R22).
+#define ITF_F 256
+template <int NCB>
+__global__ void __launch_bounds__(128, 4) k_num_large_fact(LargeArgs A) {
+  __shared__ ChildTab s_tab[4];
+  __shared__ double s_wc[4][32][3];  // X_bar of the chunk's children (w_i)
+  __shared__ long long s_ik[4][ITF_F];  // interface entries: block, child, column aggregate, column node
+  __shared__ int s_ic[4][ITF_F];
+  __shared__ int s_ib[4][ITF_F];
+  __shared__ int s_ij[4][ITF_F];
+  __shared__ int s_icnt[4];
+  const int w = threadIdx.x >> 5, l = lane_id();
+  constexpr int LPB = NCB == 4 ? 8 : 1, G = 32 / LPB;  // interface lanes: (group, p, q half)
+  const int gq = l / LPB, p = NCB == 4 ? (l >> 1) & 3 : 0, q0 = NCB == 4 ? (l & 1) * 2 : 0;
+  const long long n3 = A.sc->n3;
+  ChildTab &tab = s_tab[w];
+  const int64_t n_tasks = A.task_ptr[A.n_c];
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
+    const int a = A.task_node[t];
+    if (ncb_of(a, n3) != NCB) continue;
+    const int chunk = (int)(t - A.task_ptr[a]);
+    const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
+    load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+    double wc[3] = {0.0, 0.0, 0.0};
+    if (l < s) {
+      const int64_t ci = tab.ci[l];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        wc[d] = __ldg(A.X + 3 * ci + d);
+        s_wc[w][l][d] = wc[d];
+      }
+    }
+    if (l == 0) s_icnt[w] = 0;
+    __syncwarp();
+    const int32_t *lst = A.gbuf + A.nb_off[a];
+    const int U = A.nb_cnt[a];
+    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
+    // ---- lane = child: C[q][x] = sum over the child's diagonal entries of w_j[q] B_ij[x] ----
+    double C[NCB][9];
+#pragma unroll
+    for (int q = 0; q < NCB; ++q)
+#pragma unroll
+      for (int x = 0; x < 9; ++x) C[q][x] = 0.0;
+    if (l < s) {
+      const long long k0 = tab.rb[l], k1 = k0 + (tab.off[l + 1] - tab.off[l]);
+#pragma unroll 2
+      for (long long k = k0; k < k1; ++k) {
+        const int j = __ldg(A.col + k);
+        const int b = __ldg(A.nm + j);
+        if (b == a) {
+          double Bv[9];
+#pragma unroll
+          for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * k + x);
+          double wj[NCB];
+#pragma unroll
+          for (int q = 0; q < NCB; ++q) wj[q] = (NCB == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)j + q);
+#pragma unroll
+          for (int q = 0; q < NCB; ++q)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) C[q][x] += wj[q] * Bv[x];
+        } else if (!__ldg(A.fcls + j)) {  // large-large interface entry
+          const int pos = atomicAdd(&s_icnt[w], 1);
+          if (pos < ITF_F) {
+            s_ik[w][pos] = k;
+            s_ic[w][pos] = l;
+            s_ib[w][pos] = b;
+            s_ij[w][pos] = j;
+          } else {  // list full (never at the synthetic configurations): direct fp64 atomics
+            const int ncb_b = ncb_of(b, n3);
+            const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b), first12);
+            for (int pp = 0; pp < NCB; ++pp) {
+              const double wi = (NCB == 1 || pp == 3) ? 1.0 : wc[pp];
+              const long long rs = A.crp[slot_of(a, pp, n3)];
+              for (int qq = 0; qq < ncb_b; ++qq) {
+                const double cf = wi * ((ncb_b == 1 || qq == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)j + qq));
+                for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cp + qq) + x, cf * __ldg(A.val + 9 * k + x));
+              }
+            }
+          }
+        }
+      }
+    }
+    // ---- H[p][q][x] = sum_c w_c[p] C_c[q][x]: 144 warp sums, lane (o mod 32) keeps output o ----
+    constexpr int NO = NCB * NCB * 9, NR = (NO + 31) / 32;
+    double hacc[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) hacc[r] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NCB; ++q)
+#pragma unroll
+      for (int x = 0; x < 9; ++x)
+#pragma unroll
+        for (int pp = 0; pp < NCB; ++pp) {
+          double v = (NCB == 1 || pp == 3) ? C[q][x] : wc[pp] * C[q][x];
+          v = warp_sum(v);
+          const int o = (pp * NCB + q) * 9 + x;
+          if (l == (o & 31)) hacc[o >> 5] = v;
+        }
+    {
+      const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, a), first12);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int o = l + 32 * r;
+        if (o < NO) {
+          const int pp = o / (9 * NCB), qq = (o / 9) % NCB, x = o % 9;
+          atomicAdd(A.cval + 9 * (A.crp[slot_of(a, pp, n3)] + cpa + qq) + x, hacc[r]);
+        }
+      }
+    }
+    // ---- interface entries: one pass per distinct column aggregate b0 ----
+    __syncwarp();
+    const int icnt = min(s_icnt[w], ITF_F);
+    int left = icnt;
+    while (left > 0) {
+      int f = -1;
+      for (int d0 = 0; d0 < icnt && f < 0; d0 += 32) {
+        const unsigned mb = __ballot_sync(FULL_MASK, d0 + l < icnt && s_ib[w][d0 + l] >= 0);
+        if (mb) f = d0 + __ffs(mb) - 1;
+      }
+      const int b0 = s_ib[w][f];
+      const int ncb_b = ncb_of(b0, n3);
+      constexpr int QI = NCB == 4 ? 2 : 4;
+      double ac[QI][9];
+#pragma unroll
+      for (int qq = 0; qq < QI; ++qq)
+#pragma unroll
+        for (int x = 0; x < 9; ++x) ac[qq][x] = 0.0;
+      for (int d = f + gq; d < icnt; d += G) {
+        if (s_ib[w][d] != b0) continue;
+        const long long kk = s_ik[w][d];
+        const int jj = s_ij[w][d];
+        const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_ic[w][d]][p];
+        double Bv[9];
+#pragma unroll
+        for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * kk + x);
+#pragma unroll
+        for (int qq = 0; qq < QI; ++qq) {
+          const int q = q0 + qq;
+          const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)jj + q)) : 0.0;
+#pragma unroll
+          for (int x = 0; x < 9; ++x) ac[qq][x] += c * Bv[x];
+        }
+      }
+      __syncwarp();
+      int done_n = 0;
+      for (int d0 = f; d0 < icnt; d0 += 32) {
+        const bool mine = d0 + l < icnt && s_ib[w][d0 + l] == b0;
+        done_n += __popc(__ballot_sync(FULL_MASK, mine));
+        if (mine) s_ib[w][d0 + l] = -1;
+      }
+      __syncwarp();
+      left -= done_n;
+#pragma unroll
+      for (int o = LPB; o < 32; o <<= 1)
+#pragma unroll
+        for (int qq = 0; qq < QI; ++qq)
+#pragma unroll
+          for (int x = 0; x < 9; ++x) ac[qq][x] += __shfl_xor_sync(FULL_MASK, ac[qq][x], o);
+      const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b0), first12);
+      if (gq == 0) {
+        const long long rs = A.crp[slot_of(a, p, n3)];
+#pragma unroll
+        for (int qq = 0; qq < QI; ++qq)
+          if (q0 + qq < ncb_b) {
+            double *dst = A.cval + 9 * (rs + cp + q0 + qq);
+#pragma unroll
+            for (int x = 0; x < 9; ++x) atomicAdd(dst + x, ac[qq][x]);
+          }
+      }
+    }
+    if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
+      for (int pp = 0; pp < NCB; ++pp) {
+        double g0 = 0, g1 = 0, g2 = 0;
+        if (l < s) {
+          const int i = tab.ci[l];
+          const double wi = (NCB == 1 || pp == 3) ? 1.0 : wc[pp];
           g0 = wi * A.g_f[3 * (int64_t)i];
           g1 = wi * A.g_f[3 * (int64_t)i + 1];
           g2 = wi * A.g_f[3 * (int64_t)i + 2];
@@ -1761,7 +1991,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WA.n_w = n_w16; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
   WA.is_small = is_small; WA.rp = H->row_ptr; WA.col = H->col; WA.val = H->val; WA.nm = out->new_map;
   WA.X = mesh->x_rest; WA.g_f = gfp; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
-  WA.porig = porig; WA.mir = nullptr; WA.mir_base = 0;
+  WA.porig = porig; WA.mirpos = nullptr; WA.mirrl = nullptr; WA.mir_base = 0;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
   WA.mkeys = nullptr; WA.e_off = nullptr;
@@ -1769,13 +1999,16 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WB.n_w = n_w32; WB.wlist = w32;
   // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys
   const long long mir_mid = 16 * n_w16 + 32 * n_w32;
-  WS(h, mir, int32_t, "asm_mirror", mir_mid + nnzb_f + 1);
+  WS(h, mirpos, long long, "asm_mirror_pos", mir_mid + nnzb_f + 1);
+  WS(h, mirrl, int32_t, "asm_mirror_rl", mir_mid + nnzb_f + 1);
   {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
     WS(h, skeys, long long, "asm_small_keys", 16 * n_w16 + 32 * n_w32 + 1);
     WA.mkeys = skeys;
     WB.mkeys = skeys + 16 * n_w16;
-    WA.mir = mir;
-    WB.mir = mir;
+    WA.mirpos = mirpos;
+    WA.mirrl = mirrl;
+    WB.mirpos = mirpos;
+    WB.mirrl = mirrl;
     WB.mir_base = 16 * n_w16;
   }
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
@@ -1811,9 +2044,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
          big_list, sc, f12);
   LAUNCH(h, k_group_unique_big, (unsigned)h->sm_count, 1024, 0, sc, big_list, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen,
          f12);
-  LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, (const int2 *)pairs,
-         (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
-         (const int32_t *)f12, mir);
+
 
   // ---- C. slot row pointer (upper bound 4 n_c slots; entries past n_slots are 0) ----
   const int64_t slot_bound = 4 * n_c;
@@ -1824,6 +2055,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, rl, slot_bound, crp_ws)) != AGIPC_OK) return st;
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, recmax, task_bound, rec_off)) != AGIPC_OK) return st;
   LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound);
+  LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, (const AsmScal *)sc, pair_cap, (const int2 *)pairs,
+         (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
+         (const int32_t *)f12, (const int32_t *)rowlen, (const int64_t *)crp_ws, mirpos, mirrl);
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
   CU_TRY(h, cudaStreamSynchronize(st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
@@ -1858,9 +2092,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
-  if (!h->opt_deterministic) {
-    // 2 diagonal blocks per group in flight: 3 or 4 (at 3 CTAs/SM) measured slower, 1.63 / 1.61 vs
-    // 1.51 ms numeric at C3 (profiles/r01h/bench_nb*.jsonl)
+  static const int large_variant = getenv("AGIPC_LARGE_DIRECT") ? atoi(getenv("AGIPC_LARGE_DIRECT")) : 0;
+  if (!h->opt_deterministic && !large_variant) {  // factorised (default)
+    LAUNCH(h, k_num_large_fact<4>, glarge, 128, 0, LA);
+    if (hsc->n_large3 > 0) LAUNCH(h, k_num_large_fact<1>, glarge, 128, 0, LA);
+  } else if (!h->opt_deterministic) {  // round-1 direct (p, q) expansion, for A/B runs
     LAUNCH(h, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
     if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
   } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)

@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(MAP_THREADS)
   // flush the warp's buffered cross edges with ONE global atomic (a single counter shared by
   // the whole grid is the contended resource)
   auto flush = [&]() {
+    __syncwarp();  // the lanes' s_cross writes are visible before other lanes read them
     unsigned long long cb = 0;
     if (lane == 0) cb = atomicAdd(cross_count, (unsigned long long)nx);
     cb = __shfl_sync(FULL_MASK, cb, 0);

@@ -378,14 +378,14 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     if (!zero_x0 && ax) {  // (A x)_row precomputed from upper storage (k_ax_upper)
       y0 = ax[3 * row]; y1 = ax[3 * row + 1]; y2 = ax[3 * row + 2];
-    } else if (!zero_x0) {  // (A x)_row, one warp, flat over the row's values
-      const int64_t k0 = rp[row], ne = 9 * (rp[row + 1] - k0);
-      for (int64_t e = l; e < ne; e += 32) {
-        const int blk = (int)(e / 9), rem = (int)(e - 9 * (int64_t)blk), ii = rem / 3, jj = rem - 3 * ii;
-        const double prod = val[9 * k0 + e] * x[3 * (int64_t)col[k0 + blk] + jj];
-        y0 += ii == 0 ? prod : 0.0;
-        y1 += ii == 1 ? prod : 0.0;
-        y2 += ii == 2 ? prod : 0.0;
+    } else if (!zero_x0) {  // (A x)_row, one warp, lane per block (consecutive 72-B blocks)
+      for (int64_t k = rp[row] + l; k < rp[row + 1]; k += 32) {
+        const double *B = val + 9 * k;
+        const int64_t c = 3 * (int64_t)col[k];
+        const double x0 = x[c], x1 = x[c + 1], x2 = x[c + 2];
+        y0 += B[0] * x0 + B[1] * x1 + B[2] * x2;
+        y1 += B[3] * x0 + B[4] * x1 + B[5] * x2;
+        y2 += B[6] * x0 + B[7] * x1 + B[8] * x2;
       }
       y0 = warp_sum(y0);
       y1 = warp_sum(y1);
@@ -574,25 +574,33 @@ __global__ void __launch_bounds__(PCG_THREADS) k_spmv_flat(int64_t n, const int6
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double beta = st->beta;
-  const int l = lane_id();
+  const int l = lane_id(), sl = l & 15;  // half-warp per row, lane per block (consecutive 72-B blocks)
   double pq = 0.0;
-  const int64_t W = (int64_t)gridDim.x * PCG_WARPS;
-  for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + (threadIdx.x >> 5); row < n; row += W) {
-    const int64_t k0 = rp[row], ne = 9 * (rp[row + 1] - k0);
-    const double *v = val + 9 * k0;
+  const int64_t W = 2 * (int64_t)gridDim.x * PCG_WARPS;
+  for (int64_t row = 2 * ((int64_t)blockIdx.x * PCG_WARPS + (threadIdx.x >> 5)) + (l >> 4); row - (l >> 4) < n;
+       row += W) {
+    const bool rv = row < n;
+    const int64_t k0 = rv ? rp[row] : 0, k1 = rv ? rp[row + 1] : 0;
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    for (int64_t e = l; e < ne; e += 32) {
-      const int blk = (int)(e / 9), rem = (int)(e - 9 * (int64_t)blk), ii = rem / 3, jj = rem - 3 * ii;
-      const int64_t c = 3 * (int64_t)__ldg(col + k0 + blk) + jj;
-      const double prod = __ldcs(v + e) * (__ldg(z + c) + beta * __ldg(pold + c));
-      y0 += ii == 0 ? prod : 0.0;
-      y1 += ii == 1 ? prod : 0.0;
-      y2 += ii == 2 ? prod : 0.0;
+    for (int64_t k = k0 + sl; k < k1; k += 16) {
+      const double *B = val + 9 * k;
+      const int64_t c = 3 * (int64_t)__ldg(col + k);
+      double m[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) m[e] = __ldcs(B + e);
+      const double x0 = __ldg(z + c) + beta * __ldg(pold + c), x1 = __ldg(z + c + 1) + beta * __ldg(pold + c + 1),
+                   x2 = __ldg(z + c + 2) + beta * __ldg(pold + c + 2);
+      y0 += m[0] * x0 + m[1] * x1 + m[2] * x2;
+      y1 += m[3] * x0 + m[4] * x1 + m[5] * x2;
+      y2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
     }
-    y0 = warp_sum(y0);
-    y1 = warp_sum(y1);
-    y2 = warp_sum(y2);
-    if (l == 0) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {  // sums over the half-warp (fixed order)
+      y0 += __shfl_xor_sync(FULL_MASK, y0, o);
+      y1 += __shfl_xor_sync(FULL_MASK, y1, o);
+      y2 += __shfl_xor_sync(FULL_MASK, y2, o);
+    }
+    if (sl == 0 && rv) {
       const int64_t i = 3 * row;
       const double pn0 = z[i] + beta * pold[i], pn1 = z[i + 1] + beta * pold[i + 1], pn2 = z[i + 2] + beta * pold[i + 2];
       pnew[i] = pn0; pnew[i + 1] = pn1; pnew[i + 2] = pn2;
@@ -1060,7 +1068,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_kernel(B.spmv_un), PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
   }
-  if (B.flat) B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
+  if (B.flat) B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 2 * PCG_WARPS), 8 * (int64_t)h->sm_count));
   // K2: 2 CTAs of 256 threads per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl,
   // upd_nt.jsonl: 3-8 CTAs per SM, 2 slots per pass or 512-thread CTAs are not faster)
   B.upd_u = 1;
