@@ -194,10 +194,7 @@ agipc_status agipc_set_option(agipc_handle h, int option, int64_t value) {
       CU_TRY(h, cudaSetDevice(h->device));
       int max_persist = 0;
       CU_TRY(h, cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device));
-      size_t v = std::min((size_t)value, (size_t)std::max(0, max_persist));
-      // the one place the library changes a device-wide limit, on the caller's request
-      if (v > 0) CU_TRY(h, cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, v));
-      h->opt_l2_persist = v;
+      h->opt_l2_persist = std::min((size_t)value, (size_t)std::max(0, max_persist));
       return AGIPC_OK;
     }
   }

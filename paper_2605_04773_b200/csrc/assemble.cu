@@ -716,15 +716,37 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   ChildTab &tab = s_tab[w * NSEG + sg];
   const long long n3 = A.sc->n3;
   const int64_t n_units = (A.n_w + NSEG - 1) / NSEG;
-  for (int64_t u = (int64_t)blockIdx.x * 8 + w; u < n_units; u += (int64_t)gridDim.x * 8) {
+  const int64_t ustride = (int64_t)gridDim.x * 8;
+  // software pipeline over units: the node id, its child count and the lane's child of the NEXT
+  // unit are loaded while this unit is processed (the wlist -> child_ptr -> child_list chain is
+  // off the critical path; profiles/r02d stall-by-line)
+  int a_nx = 0, s_nx = 0, ci_nx = 0;
+  {
+    const int64_t u0 = (int64_t)blockIdx.x * 8 + w, wi0 = u0 * NSEG + sg;
+    if (u0 < n_units && wi0 < A.n_w) {
+      a_nx = A.wlist[wi0];
+      s_nx = A.size_new[a_nx];
+      if (sl < s_nx) ci_nx = A.child_list[A.child_ptr[a_nx] + sl];
+    }
+  }
+  for (int64_t u = (int64_t)blockIdx.x * 8 + w; u < n_units; u += ustride) {
     const int64_t wi = u * NSEG + sg;
     const bool segv = wi < A.n_w;
-    const int a = segv ? A.wlist[wi] : 0;
-    const int s = segv ? A.size_new[a] : 0;
+    const int a = segv ? a_nx : 0;
+    const int s = segv ? s_nx : 0;
+    const int ci_cur = ci_nx;
+    {
+      const int64_t wn = (u + ustride) * NSEG + sg;
+      if (u + ustride < n_units && wn < A.n_w) {
+        a_nx = A.wlist[wn];
+        s_nx = A.size_new[a_nx];
+        ci_nx = sl < s_nx ? A.child_list[A.child_ptr[a_nx] + sl] : 0;
+      }
+    }
     // children of the node and the offsets of their rows (segment-local scan)
     int len = 0;
     if (sl < s) {
-      const int ci = A.child_list[A.child_ptr[a] + sl];
+      const int ci = ci_cur;
       const long long rb = A.rp[ci];
       tab.ci[sl] = ci;
       tab.rb[sl] = rb;
@@ -889,10 +911,38 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
   ChildTab &tab = s_tab[w];
   long long *key = s_key[w];
   const long long n3 = A.sc->n3;
-  for (int64_t wi = (int64_t)blockIdx.x * MID_WARPS + w; wi < A.n_w; wi += (int64_t)gridDim.x * MID_WARPS) {
-    const int a = A.wlist[wi];
-    const int s = A.size_new[a];
-    const int T = load_children(tab, A.child_list, A.child_ptr[a], s, A.rp);  // T <= MID_CAP
+  const int64_t wstride = (int64_t)gridDim.x * MID_WARPS;
+  // software pipeline: the next node's id, child count and the lane's child are loaded while
+  // this node is processed (as in k_small_warp)
+  int a_nx = 0, s_nx = 0, ci_nx = 0;
+  {
+    const int64_t w0 = (int64_t)blockIdx.x * MID_WARPS + w;
+    if (w0 < A.n_w) {
+      a_nx = A.wlist[w0];
+      s_nx = A.size_new[a_nx];
+      if (l < s_nx) ci_nx = A.child_list[A.child_ptr[a_nx] + l];
+    }
+  }
+  for (int64_t wi = (int64_t)blockIdx.x * MID_WARPS + w; wi < A.n_w; wi += wstride) {
+    const int a = a_nx;
+    const int s = s_nx;
+    int len = 0;
+    if (l < s) {  // load_children with the prefetched child
+      const long long b0 = A.rp[ci_nx];
+      tab.ci[l] = ci_nx;
+      tab.rb[l] = b0;
+      len = (int)(A.rp[ci_nx + 1] - b0);
+    }
+    if (wi + wstride < A.n_w) {
+      a_nx = A.wlist[wi + wstride];
+      s_nx = A.size_new[a_nx];
+      ci_nx = l < s_nx ? A.child_list[A.child_ptr[a_nx] + l] : 0;
+    }
+    const int incl_c = warp_incl_scan(len);
+    tab.off[l + 1] = incl_c;
+    if (l == 0) tab.off[0] = 0;
+    __syncwarp();
+    const int T = __shfl_sync(FULL_MASK, incl_c, 31);  // T <= MID_CAP
     long long *gkeys = A.mkeys + A.e_off[wi];
     const long long mir0 = A.mir_base + A.e_off[wi];  // this node's mirror-position slots
     if (NUMERIC) {  // the symbolic pass left the sorted keys of this node in global memory
@@ -1180,12 +1230,35 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
   const long long n3 = A.sc->n3;
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
-  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
-    const int a = A.task_node[t];
+  const int64_t tstride = (int64_t)gridDim.x * 4;
+  // software pipeline: the next task's node, chunk size and the lane's child are loaded while
+  // this task is processed (task_node -> task_ptr / child_ptr -> child_list off the critical path)
+  int a_nx = 0, s_nx = 0, ci_nx = 0;
+  auto prefetch = [&](int64_t tn) {
+    if (tn < n_tasks) {
+      a_nx = A.task_node[tn];
+      const int ch = (int)(tn - A.task_ptr[a_nx]);
+      s_nx = min(LARGE_CHUNK, A.size_new[a_nx] - ch * LARGE_CHUNK);
+      ci_nx = l < s_nx ? A.child_list[A.child_ptr[a_nx] + (int64_t)ch * LARGE_CHUNK + l] : 0;
+    }
+  };
+  prefetch((int64_t)blockIdx.x * 4 + w);
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += tstride) {
+    const int a = a_nx, s = s_nx, ci_c = ci_nx;
+    prefetch(t + tstride);
     if (ncb_of(a, n3) != NCB) continue;
-    const int chunk = (int)(t - A.task_ptr[a]);
-    const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
-    const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+    int len = 0;
+    if (l < s) {  // load_children with the prefetched child
+      const long long b0 = A.rp[ci_c];
+      tab.ci[l] = ci_c;
+      tab.rb[l] = b0;
+      len = (int)(A.rp[ci_c + 1] - b0);
+    }
+    const int incl_c = warp_incl_scan(len);
+    tab.off[l + 1] = incl_c;
+    if (l == 0) tab.off[0] = 0;
+    __syncwarp();
+    const int T = __shfl_sync(FULL_MASK, incl_c, 31);
     if (l < s) {
       const int64_t ci = tab.ci[l];
       s_wc[w][l][0] = __ldg(A.X + 3 * ci);
@@ -1359,208 +1432,6 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
         if (l < s) {
           const int i = tab.ci[l];
           const double wi = wgt(A.X, i, NCB, pp);
-          g0 = wi * A.g_f[3 * (int64_t)i];
-          g1 = wi * A.g_f[3 * (int64_t)i + 1];
-          g2 = wi * A.g_f[3 * (int64_t)i + 2];
-        }
-        g0 = warp_sum(g0);
-        g1 = warp_sum(g1);
-        g2 = warp_sum(g2);
-        if (l == 0) {
-          double *gc = A.g_c + 3 * (int64_t)slot_of(a, pp, n3);
-          atomicAdd(gc, g0);
-          atomicAdd(gc + 1, g1);
-          atomicAdd(gc + 2, g2);
-        }
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// Large rows, FACTORISED accumulation (the default atomic path): one warp per 32-children chunk,
-// lane c = child c walks its own fine row.  Eq 4 with w_i = X_bar_i, w_j = X_bar_j:
-//   H_c(a, a)[p][q] = sum_i w_i[p] C_i[q],   C_i[q] = sum_{j in a} w_j[q] B_ij
-// so a diagonal entry costs 36 FMAs (C_i += w_j (x) B_ij) instead of the 144 of the direct
-// (p, q) expansion, and the 144 (p, q, x) sums over the chunk's children are 144 warp
-// reductions per CHUNK (lane o mod 32 keeps output o for the atomics).  Interface entries
-// (large-large, b != a) go to a per-warp shared list and are summed per column aggregate after
-// the children loop, as in k_num_large_atomic.  Small columns: mirrored by the small rows (R22).
-#define ITF_F 256
-template <int NCB>
-__global__ void __launch_bounds__(128, 4) k_num_large_fact(LargeArgs A) {
-  __shared__ ChildTab s_tab[4];
-  __shared__ double s_wc[4][32][3];  // X_bar of the chunk's children (w_i)
-  __shared__ long long s_ik[4][ITF_F];  // interface entries: block, child, column aggregate, column node
-  __shared__ int s_ic[4][ITF_F];
-  __shared__ int s_ib[4][ITF_F];
-  __shared__ int s_ij[4][ITF_F];
-  __shared__ int s_icnt[4];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  constexpr int LPB = NCB == 4 ? 8 : 1, G = 32 / LPB;  // interface lanes: (group, p, q half)
-  const int gq = l / LPB, p = NCB == 4 ? (l >> 1) & 3 : 0, q0 = NCB == 4 ? (l & 1) * 2 : 0;
-  const long long n3 = A.sc->n3;
-  ChildTab &tab = s_tab[w];
-  const int64_t n_tasks = A.task_ptr[A.n_c];
-  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
-    const int a = A.task_node[t];
-    if (ncb_of(a, n3) != NCB) continue;
-    const int chunk = (int)(t - A.task_ptr[a]);
-    const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
-    load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
-    double wc[3] = {0.0, 0.0, 0.0};
-    if (l < s) {
-      const int64_t ci = tab.ci[l];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        wc[d] = __ldg(A.X + 3 * ci + d);
-        s_wc[w][l][d] = wc[d];
-      }
-    }
-    if (l == 0) s_icnt[w] = 0;
-    __syncwarp();
-    const int32_t *lst = A.gbuf + A.nb_off[a];
-    const int U = A.nb_cnt[a];
-    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
-    // ---- lane = child: C[q][x] = sum over the child's diagonal entries of w_j[q] B_ij[x] ----
-    double C[NCB][9];
-#pragma unroll
-    for (int q = 0; q < NCB; ++q)
-#pragma unroll
-      for (int x = 0; x < 9; ++x) C[q][x] = 0.0;
-    if (l < s) {
-      const long long k0 = tab.rb[l], k1 = k0 + (tab.off[l + 1] - tab.off[l]);
-#pragma unroll 2
-      for (long long k = k0; k < k1; ++k) {
-        const int j = __ldg(A.col + k);
-        const int b = __ldg(A.nm + j);
-        if (b == a) {
-          double Bv[9];
-#pragma unroll
-          for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * k + x);
-          double wj[NCB];
-#pragma unroll
-          for (int q = 0; q < NCB; ++q) wj[q] = (NCB == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)j + q);
-#pragma unroll
-          for (int q = 0; q < NCB; ++q)
-#pragma unroll
-            for (int x = 0; x < 9; ++x) C[q][x] += wj[q] * Bv[x];
-        } else if (!__ldg(A.fcls + j)) {  // large-large interface entry
-          const int pos = atomicAdd(&s_icnt[w], 1);
-          if (pos < ITF_F) {
-            s_ik[w][pos] = k;
-            s_ic[w][pos] = l;
-            s_ib[w][pos] = b;
-            s_ij[w][pos] = j;
-          } else {  // list full (never at the synthetic configurations): direct fp64 atomics
-            const int ncb_b = ncb_of(b, n3);
-            const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b), first12);
-            for (int pp = 0; pp < NCB; ++pp) {
-              const double wi = (NCB == 1 || pp == 3) ? 1.0 : wc[pp];
-              const long long rs = A.crp[slot_of(a, pp, n3)];
-              for (int qq = 0; qq < ncb_b; ++qq) {
-                const double cf = wi * ((ncb_b == 1 || qq == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)j + qq));
-                for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cp + qq) + x, cf * __ldg(A.val + 9 * k + x));
-              }
-            }
-          }
-        }
-      }
-    }
-    // ---- H[p][q][x] = sum_c w_c[p] C_c[q][x]: 144 warp sums, lane (o mod 32) keeps output o ----
-    constexpr int NO = NCB * NCB * 9, NR = (NO + 31) / 32;
-    double hacc[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) hacc[r] = 0.0;
-#pragma unroll
-    for (int q = 0; q < NCB; ++q)
-#pragma unroll
-      for (int x = 0; x < 9; ++x)
-#pragma unroll
-        for (int pp = 0; pp < NCB; ++pp) {
-          double v = (NCB == 1 || pp == 3) ? C[q][x] : wc[pp] * C[q][x];
-          v = warp_sum(v);
-          const int o = (pp * NCB + q) * 9 + x;
-          if (l == (o & 31)) hacc[o >> 5] = v;
-        }
-    {
-      const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, a), first12);
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int o = l + 32 * r;
-        if (o < NO) {
-          const int pp = o / (9 * NCB), qq = (o / 9) % NCB, x = o % 9;
-          atomicAdd(A.cval + 9 * (A.crp[slot_of(a, pp, n3)] + cpa + qq) + x, hacc[r]);
-        }
-      }
-    }
-    // ---- interface entries: one pass per distinct column aggregate b0 ----
-    __syncwarp();
-    const int icnt = min(s_icnt[w], ITF_F);
-    int left = icnt;
-    while (left > 0) {
-      int f = -1;
-      for (int d0 = 0; d0 < icnt && f < 0; d0 += 32) {
-        const unsigned mb = __ballot_sync(FULL_MASK, d0 + l < icnt && s_ib[w][d0 + l] >= 0);
-        if (mb) f = d0 + __ffs(mb) - 1;
-      }
-      const int b0 = s_ib[w][f];
-      const int ncb_b = ncb_of(b0, n3);
-      constexpr int QI = NCB == 4 ? 2 : 4;
-      double ac[QI][9];
-#pragma unroll
-      for (int qq = 0; qq < QI; ++qq)
-#pragma unroll
-        for (int x = 0; x < 9; ++x) ac[qq][x] = 0.0;
-      for (int d = f + gq; d < icnt; d += G) {
-        if (s_ib[w][d] != b0) continue;
-        const long long kk = s_ik[w][d];
-        const int jj = s_ij[w][d];
-        const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_ic[w][d]][p];
-        double Bv[9];
-#pragma unroll
-        for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * kk + x);
-#pragma unroll
-        for (int qq = 0; qq < QI; ++qq) {
-          const int q = q0 + qq;
-          const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : __ldg(A.X + 3 * (int64_t)jj + q)) : 0.0;
-#pragma unroll
-          for (int x = 0; x < 9; ++x) ac[qq][x] += c * Bv[x];
-        }
-      }
-      __syncwarp();
-      int done_n = 0;
-      for (int d0 = f; d0 < icnt; d0 += 32) {
-        const bool mine = d0 + l < icnt && s_ib[w][d0 + l] == b0;
-        done_n += __popc(__ballot_sync(FULL_MASK, mine));
-        if (mine) s_ib[w][d0 + l] = -1;
-      }
-      __syncwarp();
-      left -= done_n;
-#pragma unroll
-      for (int o = LPB; o < 32; o <<= 1)
-#pragma unroll
-        for (int qq = 0; qq < QI; ++qq)
-#pragma unroll
-          for (int x = 0; x < 9; ++x) ac[qq][x] += __shfl_xor_sync(FULL_MASK, ac[qq][x], o);
-      const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b0), first12);
-      if (gq == 0) {
-        const long long rs = A.crp[slot_of(a, p, n3)];
-#pragma unroll
-        for (int qq = 0; qq < QI; ++qq)
-          if (q0 + qq < ncb_b) {
-            double *dst = A.cval + 9 * (rs + cp + q0 + qq);
-#pragma unroll
-            for (int x = 0; x < 9; ++x) atomicAdd(dst + x, ac[qq][x]);
-          }
-      }
-    }
-    if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
-      for (int pp = 0; pp < NCB; ++pp) {
-        double g0 = 0, g1 = 0, g2 = 0;
-        if (l < s) {
-          const int i = tab.ci[l];
-          const double wi = (NCB == 1 || pp == 3) ? 1.0 : wc[pp];
           g0 = wi * A.g_f[3 * (int64_t)i];
           g1 = wi * A.g_f[3 * (int64_t)i + 1];
           g2 = wi * A.g_f[3 * (int64_t)i + 2];
@@ -2092,11 +1963,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
-  static const int large_variant = getenv("AGIPC_LARGE_DIRECT") ? atoi(getenv("AGIPC_LARGE_DIRECT")) : 0;
-  if (!h->opt_deterministic && !large_variant) {  // factorised (default)
-    LAUNCH(h, k_num_large_fact<4>, glarge, 128, 0, LA);
-    if (hsc->n_large3 > 0) LAUNCH(h, k_num_large_fact<1>, glarge, 128, 0, LA);
-  } else if (!h->opt_deterministic) {  // round-1 direct (p, q) expansion, for A/B runs
+  // (a factorised variant -- lane per child, C_i[q] = sum_j w_j[q] B_ij, then sum_i w_i[p] C_i[q] --
+  // cuts the FMAs 4x but measured 2.03 vs 0.54 ms at C3: divergent per-lane row walks, 17% warps
+  // active; profiles/r02f)
+  if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
     LAUNCH(h, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
     if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
   } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)

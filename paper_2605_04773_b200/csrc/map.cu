@@ -456,7 +456,6 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         if (active[r]) A.mk[v[r]] = s_w[w] + local[r];
       __syncthreads();
     }
-    if (gtid == 0) A.ne[1 - cur] = 0;
     gsync();
     // ---- P3: scan the tile counts (every CTA, shared memory), remap, compose, reset ----
     {
@@ -481,25 +480,24 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       __syncthreads();
     }
     const int64_t n2 = s_total;
-    int2 *Eo = A.E[1 - cur];
     bool hit = false;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne; base += gstride) {
-      const int64_t e = base + threadIdx.x;
-      int2 o = make_int2(0, 0);
-      bool keep = false;
-      if (e < ne) {
-        const int2 uv = E[e];
-        o.x = s_pref[uv.x / TN] + A.mk[uv.x];
-        o.y = s_pref[uv.y / TN] + A.mk[uv.y];
-        keep = o.x != o.y;
-        if (keep && o.x / gs == o.y / gs) {  // P1 of the next level
-          atomicOr(A.h + o.x, 1u << (o.y - (o.y / gs) * gs));
-          atomicOr(A.h + o.y, 1u << (o.x - (o.x / gs) * gs));
-          hit = true;
-        }
+    // remap in place (each edge is read and written by one thread): a merged edge becomes dead
+    // (-1, -1) instead of being compacted away -- no CTA-wide compaction (two barriers and a
+    // global atomic) on the per-level critical path; later levels skip dead entries
+    int2 *Ew = A.E[cur];
+    for (int64_t e = gtid; e < ne; e += gstride) {
+      const int2 uv = E[e];
+      if (uv.x < 0) continue;
+      int2 o;
+      o.x = s_pref[uv.x / TN] + A.mk[uv.x];
+      o.y = s_pref[uv.y / TN] + A.mk[uv.y];
+      const bool keep = o.x != o.y;
+      if (keep && o.x / gs == o.y / gs) {  // P1 of the next level
+        atomicOr(A.h + o.x, 1u << (o.y - (o.y / gs) * gs));
+        atomicOr(A.h + o.y, 1u << (o.x - (o.x / gs) * gs));
+        hit = true;
       }
-      const unsigned long long pos = cta_compact(keep, A.ne + (1 - cur), s_cw, &s_cbase);
-      if (keep) Eo[pos] = o;
+      Ew[e] = keep ? o : make_int2(-1, -1);
     }
     if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
     for (int64_t c = gtid; c < n1; c += 2 * gstride) {  // two independent gathers in flight
@@ -519,7 +517,6 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
     }
     gsync();
     n = n2;
-    cur = 1 - cur;
     if (A.max_levels > 0 && level >= A.max_levels) {
       if (gtid == 0) {
         A.ctrl[2] = level;

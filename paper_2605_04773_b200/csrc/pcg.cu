@@ -54,6 +54,7 @@ struct PcgGraph {
   uint64_t ws_gen = 0;
   bool flat = false;
   int64_t n_flat = -1;
+  bool l2on = false;  // captured with the persisting access-policy window
   std::vector<cudaEvent_t> ev;  // profiling: 3 events per iteration of the chunk
 };
 
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(PCG_THREADS, MINB) k_spmv_sell(const int64_t *
 // the per-solve re-layout of the 1.1 GB fine matrix (two extra passes) costs more than the tiling
 // gains.  Static row -> warp assignment, so the p.q partials (and the solve) are reproducible.
 // ------------------------------------------------------------------------------------
+template <int SW>
 __global__ void __launch_bounds__(PCG_THREADS) k_spmv_flat(int64_t n, const int64_t *__restrict__ rp,
                                                          const int32_t *__restrict__ col,
                                                          const double *__restrict__ val,
@@ -574,15 +576,16 @@ __global__ void __launch_bounds__(PCG_THREADS) k_spmv_flat(int64_t n, const int6
   if (*(volatile int *)&st->done) return;
   __shared__ double s_red[PCG_WARPS];
   const double beta = st->beta;
-  const int l = lane_id(), sl = l & 15;  // half-warp per row, lane per block (consecutive 72-B blocks)
+  // SW-lane segment per row, lane per block (consecutive 72-B blocks); 32 / SW rows per warp
+  constexpr int RPW = 32 / SW;
+  const int l = lane_id(), sl = l % SW, sg = l / SW;
   double pq = 0.0;
-  const int64_t W = 2 * (int64_t)gridDim.x * PCG_WARPS;
-  for (int64_t row = 2 * ((int64_t)blockIdx.x * PCG_WARPS + (threadIdx.x >> 5)) + (l >> 4); row - (l >> 4) < n;
-       row += W) {
+  const int64_t W = RPW * (int64_t)gridDim.x * PCG_WARPS;
+  for (int64_t row = RPW * ((int64_t)blockIdx.x * PCG_WARPS + (threadIdx.x >> 5)) + sg; row - sg < n; row += W) {
     const bool rv = row < n;
     const int64_t k0 = rv ? rp[row] : 0, k1 = rv ? rp[row + 1] : 0;
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    for (int64_t k = k0 + sl; k < k1; k += 16) {
+    for (int64_t k = k0 + sl; k < k1; k += SW) {
       const double *B = val + 9 * k;
       const int64_t c = 3 * (int64_t)__ldg(col + k);
       double m[9];
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_spmv_flat(int64_t n, const int6
       y2 += m[6] * x0 + m[7] * x1 + m[8] * x2;
     }
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {  // sums over the half-warp (fixed order)
+    for (int o = SW / 2; o > 0; o >>= 1) {  // sums over the segment (fixed order)
       y0 += __shfl_xor_sync(FULL_MASK, y0, o);
       y1 += __shfl_xor_sync(FULL_MASK, y1, o);
       y2 += __shfl_xor_sync(FULL_MASK, y2, o);
@@ -930,39 +933,47 @@ struct PcgBufs {
 };
 
 
-// L2 residency of the PCG vectors (B200: 126 MB L2), opt-in (agipc_set_option
-// AGIPC_OPT_L2_PERSIST sets the device's persisting-L2 limit once, on the caller's request): the
-// matrix is streamed with evict-first loads; the vector arena gets a persisting access-policy
-// window on the solve stream (the captured kernel nodes inherit it).  Returns whether a window
-// was set (the persisting lines are then released after the solve).
-static bool pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size_t bytes) {
+// L2 residency of the PCG vectors (B200: 126 MB L2), opt-in (agipc_set_option AGIPC_OPT_L2_PERSIST):
+// the matrix is streamed with evict-first loads; when the whole vector arena fits in the requested
+// persisting size, the solve stream gets a persisting access-policy window over it (the captured
+// kernel nodes inherit it) and the device's persisting carve-out is set to the arena for the
+// solve and restored afterwards (pcg_l2_release).  A window larger than the carve-out thrashes and
+// a carve-out without a window only shrinks the normal L2 (C4, 1.1M slots: SpMV 386 -> 273 us,
+// K2 107 -> 54 us without either, profiles/r02f), so neither is set then.
+struct L2Win {
+  bool on = false;
+  size_t prev_limit = 0;
+};
+
+static L2Win pcg_l2_window(agipc_handle h, cudaStream_t s, const void *base, size_t bytes) {
+  L2Win r;
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
-  const bool on = h->opt_l2_persist > 0 && base && bytes > 0;
-  if (on) {
-    int max_win = 0;
-    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
-    if (max_win <= 0) {
-      cudaGetLastError();
-      return false;
-    }
-    const size_t win = std::min(bytes, (size_t)max_win);
-    const size_t persist = std::min(win, h->opt_l2_persist);
+  int max_win = 0;
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+  const bool on = h->opt_l2_persist > 0 && base && bytes > 0 && bytes <= h->opt_l2_persist && max_win > 0 &&
+                  bytes <= (size_t)max_win;
+  if (on && cudaDeviceGetLimit(&r.prev_limit, cudaLimitPersistingL2CacheSize) == cudaSuccess &&
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) == cudaSuccess) {
     v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
-    v.accessPolicyWindow.num_bytes = win;
-    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)win);
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = 1.0f;
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    r.on = true;
   }
+  cudaGetLastError();
   if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
-  return on;
+  return r;
 }
 
-static void pcg_l2_release(cudaStream_t s) {
+static void pcg_l2_release(cudaStream_t s, const L2Win &w) {
+  if (!w.on) return;
   cudaStreamAttrValue v;
   memset(&v, 0, sizeof(v));
   if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
   if (cudaCtxResetPersistingL2Cache() != cudaSuccess) cudaGetLastError();
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, w.prev_limit) != cudaSuccess) cudaGetLastError();
 }
 
 // iteration j reads p_old = P[j&1] and writes p_new = P[(j+1)&1] (the chunk length is even)
@@ -973,7 +984,7 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
     const bool sample = ev && (k % PROF_EVERY) == 0;  // sampled kernel timing (low overhead)
     if (sample) cudaEventRecordWithFlags(ev[3 * k], s, cudaEventRecordExternal);
     if (B.flat)
-      k_spmv_flat<<<B.G1, PCG_THREADS, 0, s>>>(B.n, B.A_rp, B.A_col, B.A_val, B.z, pold, pnew, B.qseg, B.parts, B.st,
+      k_spmv_flat<8><<<B.G1, PCG_THREADS, 0, s>>>(B.n, B.A_rp, B.A_col, B.A_val, B.z, pold, pnew, B.qseg, B.parts, B.st,
                                                nullptr);
     else if (B.sym)
       k_spmv_sym<<<B.G1, PCG_THREADS, 3 * sizeof(double) * B.win, s>>>(
@@ -1068,7 +1079,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_kernel(B.spmv_un), PCG_THREADS, 0));
     B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(B.ns_bound, PCG_WARPS), (int64_t)std::max(1, occ) * h->sm_count));
   }
-  if (B.flat) B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 2 * PCG_WARPS), 8 * (int64_t)h->sm_count));
+  if (B.flat) B.G1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 4 * PCG_WARPS), 8 * (int64_t)h->sm_count));
   // K2: 2 CTAs of 256 threads per SM, 1 slot per thread pass (profiles/r01h/update_exp.jsonl,
   // upd_nt.jsonl: 3-8 CTAs per SM, 2 slots per pass or 512-thread CTAs are not faster)
   B.upd_u = 1;
@@ -1182,14 +1193,14 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     }
     int chunk = std::max(2, std::min(check_every, max_iters));
     chunk += chunk & 1;  // even: the p ping-pong parity is the same at every graph launch
-    const bool l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);
+    const L2Win l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);
     const void *key[8] = {B.flat ? (const void *)B.A_val : B.sval, B.flat ? (const void *)B.A_col : B.scol, B.x, B.qseg,
                           B.Dinv, B.flat ? (const void *)B.A_rp : B.sptr, B.P[0], B.parts};
     // ws_gen changes whenever any named buffer moved (every pointer baked into the graph is one)
     bool same = g->exec && g->ws_gen == h->ws_gen && g->n == n && g->ns == B.ns_bound && g->chunk == chunk && g->grid1 == B.G1 &&
                 g->grid2 == B.G2 && g->prof == h->prof && g->sym == B.sym && g->win == B.win && g->yext == B.yext &&
                 g->all_red == B.all_red && g->upd_u == B.upd_u &&
-                g->spmv_un == B.spmv_un && g->flat == B.flat && g->n_flat == B.n;
+                g->spmv_un == B.spmv_un && g->flat == B.flat && g->n_flat == B.n && g->l2on == l2win.on;
     for (int i = 0; i < 8 && same; ++i) same = g->key[i] == key[i];
     if (!same) {
       if (g->exec) {
@@ -1224,6 +1235,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
       g->ws_gen = h->ws_gen;
       g->flat = B.flat;
       g->n_flat = B.n;
+      g->l2on = l2win.on;
       for (int i = 0; i < 8; ++i) g->key[i] = key[i];
     }
     CU_TRY(h, cudaEventRecord(g->ev_in, s0));
@@ -1253,7 +1265,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
     }
     // the solve's vectors were persisting L2 lines; release them so the next Newton step's
     // coarsen/assemble kernels get the whole L2 (the loop above has synchronised the solve)
-    if (l2win) pcg_l2_release(g->stream);
+    pcg_l2_release(g->stream, l2win);
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
     CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
   }
@@ -1622,14 +1634,14 @@ extern "C" agipc_status agipc_dpcg_solve(agipc_handle h, const agipc_bsr *A, con
     }
     int chunk = std::max(2, std::min(check_every, max_iters));
     chunk += chunk & 1;
+    const L2Win l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);  // before capture: nodes inherit it
     std::vector<int64_t> key = {(int64_t)h->ws_gen, d->n, d->n_gs, chunk, B.G1, B.G2, B.spmv_un, P,
-                                (int64_t)(intptr_t)h->comm};
+                                (int64_t)(intptr_t)h->comm, (int64_t)l2win.on};
     for (int q = 0; q < P; ++q) {
       key.push_back(X.peer[q]);
       key.push_back(X.soff[q + 1]);
       key.push_back(X.roff[q + 1]);
     }
-    const bool l2win = pcg_l2_window(h, g->stream, B.arena, B.arena_bytes);  // before capture: nodes inherit it
     if (!g->exec || key != d->gkey) {
       if (g->exec) {
         cudaGraphExecDestroy(g->exec);
@@ -1661,7 +1673,7 @@ extern "C" agipc_status agipc_dpcg_solve(agipc_handle h, const agipc_bsr *A, con
         if (hst->done || launched >= max_iters) break;  // identical on every rank
       }
     }
-    if (l2win) pcg_l2_release(g->stream);
+    pcg_l2_release(g->stream, l2win);
     CU_TRY(h, cudaEventRecord(g->ev_out, g->stream));
     CU_TRY(h, cudaStreamWaitEvent(s0, g->ev_out, 0));
   }

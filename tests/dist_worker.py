@@ -172,7 +172,7 @@ def gpu_worker(rank, world, port, out_dir, n, thr, kind):
         step.rel_tol = 1e-3
         _, st3 = step.solve(dc)
         from pcg_band import oracle_iteration_band  # reading R25
-        lo, hi = oracle_iteration_band(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], 1e-3)
+        lo, hi = oracle_iteration_band(oa["row_ptr"], oa["col"], oa["val"], oa["g_c"], 1e-3, n_pert=16, slack=4)
         assert lo <= st3["iters"] <= hi, (st3, lo, hi)
         ref = {"iters": (lo, hi)}
         dist.barrier()

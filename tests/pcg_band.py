@@ -11,10 +11,13 @@ import numpy as np
 import oracle
 
 
-def oracle_iteration_band(row_ptr, col, val, b, tol, n_pert=8, rel=1e-15, max_iters=20000):
+def oracle_iteration_band(row_ptr, col, val, b, tol, n_pert=8, rel=1e-15, max_iters=20000, slack=2):
+    """slack: iterations added on both sides (2; the distributed solve uses 4: its p.q, r.z and
+    r.r are partial sums per rank added in rank order, a further rounding order, and its halo
+    coarse blocks are summed with atomics -- reading R25)."""
     its = [oracle.pcg(row_ptr, col, val, b, rel_tol=tol, max_iters=max_iters)["iters"]]
     for s in range(n_pert):
         e = rel * np.random.default_rng([s, 99]).standard_normal(val.shape[0])
         its.append(oracle.pcg(row_ptr, col, val * (1.0 + e[:, None, None]), b, rel_tol=tol,
                               max_iters=max_iters)["iters"])
-    return min(its) - 2, max(its) + 2
+    return min(its) - slack, max(its) + slack
