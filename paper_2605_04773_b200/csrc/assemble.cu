@@ -440,11 +440,32 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
   int npb = 0;
   ChildTab &tab = s_tab[w];
   const int64_t n_tasks = A.task_ptr[A.n_c];
-  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += (int64_t)gridDim.x * 4) {
-    const int a = A.task_node[t];
-    const int chunk = (int)(t - A.task_ptr[a]);
-    const int s = min(LARGE_CHUNK, A.size_new[a] - chunk * LARGE_CHUNK);
-    const int T = load_children(tab, A.child_list, A.child_ptr[a] + (int64_t)chunk * LARGE_CHUNK, s, A.rp);
+  const int64_t tstride = (int64_t)gridDim.x * 4;
+  int a_nx = 0, s_nx = 0, ci_nx = 0, ch_nx = 0;  // next task prefetched (as in k_num_large_atomic)
+  auto prefetch = [&](int64_t tn) {
+    if (tn < n_tasks) {
+      a_nx = A.task_node[tn];
+      ch_nx = (int)(tn - A.task_ptr[a_nx]);
+      s_nx = min(LARGE_CHUNK, A.size_new[a_nx] - ch_nx * LARGE_CHUNK);
+      ci_nx = l < s_nx ? A.child_list[A.child_ptr[a_nx] + (int64_t)ch_nx * LARGE_CHUNK + l] : 0;
+    }
+  };
+  prefetch((int64_t)blockIdx.x * 4 + w);
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += tstride) {
+    const int a = a_nx, chunk = ch_nx, s = s_nx, ci_c = ci_nx;
+    prefetch(t + tstride);
+    int len = 0;
+    if (l < s) {
+      const long long b0 = A.rp[ci_c];
+      tab.ci[l] = ci_c;
+      tab.rb[l] = b0;
+      len = (int)(A.rp[ci_c + 1] - b0);
+    }
+    const int incl_c = warp_incl_scan(len);
+    tab.off[l + 1] = incl_c;
+    if (l == 0) tab.off[0] = 0;
+    __syncwarp();
+    const int T = __shfl_sync(FULL_MASK, incl_c, 31);
     int nseen = 0, nitf = 0;
     for (int e0 = 0; e0 < T; e0 += 32) {
       const int e = e0 + l;

@@ -174,13 +174,20 @@ __global__ void __launch_bounds__(MAP_THREADS)
     __syncwarp();
     if (nn > 0) {
       const long long E0 = s_ptr[w][0], E1 = s_ptr[w][nn];
+      // software pipeline: the next 32 entries' neighbour / tag loads are issued before this
+      // batch's row search, hash OR and ballots
+      int u_nx = 0, t_nx = 0;
+      if (E0 + lane < E1) {
+        u_nx = __ldg(adj_nbr + E0 + lane);
+        t_nx = __ldg(tags + E0 + lane);
+      }
       for (long long eb = E0; eb < E1; eb += 32) {
         const long long e = eb + lane;
         const bool valid = e < E1;
-        int u = 0, t = 0;
-        if (valid) {
-          u = __ldg(adj_nbr + e);
-          t = __ldg(tags + e);
+        const int u = u_nx, t = t_nx;
+        if (e + 32 < E1) {
+          u_nx = __ldg(adj_nbr + e + 32);
+          t_nx = __ldg(tags + e + 32);
         }
         int lo = 0, hi = nn;  // row r: s_ptr[r] <= e < s_ptr[r+1]
         while (hi - lo > 1) {

@@ -1,0 +1,17 @@
+# r02i: software-pipelined unit loops in k_small_warp / k_mid_warp / k_num_large_atomic
+set -x
+python __graft_entry__.py build 2>&1 | tail -2
+mkdir -p gpurun_out/r02i
+export AGIPC_SKIP_FULL_CONFIGS=1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_comm_gpu.py -q -x --timeout 600 --timeout-method thread 2>&1 | tail -3
+for i in 1 2; do timeout 600 python bench.py --steps 10 --warmup 3 --no-next --no-e2e --no-cpu-baseline --no-big > gpurun_out/r02i/bench$i.json 2>> gpurun_out/r02i/bench.err; done
+python - <<'PY'
+import json
+for i in (1, 2):
+    d = json.load(open(f"gpurun_out/r02i/bench{i}.json"))
+    print({k: d[k] for k in ("value", "ms_per_step", "pcg_iters_per_s")}, d["roofline"]["frac"], d["phase_ms_per_step"])
+PY
+B="python bench.py --steps 1 --warmup 1 --no-next --no-e2e --no-cpu-baseline --no-big"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02i/launches.csv \
+  $B > gpurun_out/r02i/launches_bench.log 2>&1
+python profiles/summarize_launches.py gpurun_out/r02i/launches.csv gpurun_out/r02i/launches_summary.csv | head -24
