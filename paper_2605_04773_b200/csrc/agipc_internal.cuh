@@ -77,6 +77,8 @@ struct agipc_handle_s {
   cudaEvent_t values_event = nullptr;  // agipc_set_values_event (one-shot, consumed by assemble)
   struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)
   struct Comm *comm = nullptr;  // NCCL communicator (comm.cu, agipc_comm_init)
+  cudaStream_t aux = nullptr;   // second stream for independent kernels of one call (fork / join)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;
   std::vector<ProfPending> prof_pending;
@@ -152,6 +154,24 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
                        cudaGetErrorString(_e));                                              \
     }                                                                                        \
   } while (0)
+
+// LAUNCH on an explicit stream (the handle's aux stream of a fork / join region)
+#define LAUNCH_S(h, strm, kernel, grid, block, smem, ...)                                     \
+  do {                                                                                       \
+    if ((grid) > 0) {                                                                        \
+      kernel<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);                              \
+      (h)->launches += 1;                                                                    \
+      cudaError_t _e = cudaGetLastError();                                                   \
+      if (_e != cudaSuccess)                                                                 \
+        return set_err((h), AGIPC_ECUDA, "launch %s failed: %s", #kernel,                    \
+                       cudaGetErrorString(_e));                                              \
+    }                                                                                        \
+  } while (0)
+
+// Fork: work enqueued on h->aux after this starts once everything before on h->stream is done.
+agipc_status aux_fork(agipc_handle h);
+// Join: h->stream waits for everything enqueued on h->aux so far.
+agipc_status aux_join(agipc_handle h);
 
 #define WS(h, var, type, name, count)                                                        \
   type *var = nullptr;                                                                       \

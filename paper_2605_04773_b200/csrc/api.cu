@@ -60,6 +60,23 @@ void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st, b
   return b.ptr;
 }
 
+agipc_status aux_fork(agipc_handle h) {
+  if (!h->aux) {
+    CU_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    CU_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CU_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  }
+  CU_TRY(h, cudaEventRecord(h->ev_fork, h->stream));
+  CU_TRY(h, cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+  return AGIPC_OK;
+}
+
+agipc_status aux_join(agipc_handle h) {
+  CU_TRY(h, cudaEventRecord(h->ev_join, h->aux));
+  CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  return AGIPC_OK;
+}
+
 void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st) {
   if (h->pinned_bytes < bytes) {
     if (h->pinned) {
@@ -158,6 +175,12 @@ agipc_status agipc_destroy(agipc_handle h) {
   comm_free(h);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pcg) pcg_graph_free(h->pcg);
+  if (h->aux) {
+    cudaStreamSynchronize(h->aux);
+    cudaStreamDestroy(h->aux);
+    cudaEventDestroy(h->ev_fork);
+    cudaEventDestroy(h->ev_join);
+  }
   if (h->dpcg) dpcg_free(h->dpcg);
   prof_flush(h);
   for (auto e : h->prof_pool) cudaEventDestroy(e);

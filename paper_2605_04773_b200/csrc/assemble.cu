@@ -1905,6 +1905,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   }
   const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
   const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
+  // the large-row symbolic pass runs on the aux stream next to the small / mid rows' (both
+  // latency-bound at partial occupancy; they only share the atomic pair counter)
+  if ((st = aux_fork(h)) != AGIPC_OK) return st;
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
   WM = WA;
@@ -1924,7 +1927,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
   LA.recmax = recmax; LA.rec_off = rec_off; LA.rec_b = nullptr; LA.rec_v = nullptr; LA.part = nullptr;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
-  LAUNCH(h, k_sym_large, glarge, 128, 0, LA);
+  LAUNCH_S(h, h->aux, k_sym_large, glarge, 128, 0, LA);
+  if ((st = aux_join(h)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
   LAUNCH(h, k_pair_count, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, gcnt);
   LAUNCH(h, k_pow2, gC, 256, 0, n_c, gcnt, gpad);
@@ -1977,10 +1981,15 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
   LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
          out->val);
+  // the 12-DoF chunks (aux stream) and the small / mid rows (handle stream) write disjoint
+  // blocks -- (large, large) by the chunks, own rows and the mirrored (large, small) blocks by the
+  // small rows -- and are both latency-bound at partial occupancy: run them side by side
+  if ((st = aux_fork(h)) != AGIPC_OK) return st;
   WM.crp = out->row_ptr; WM.ccol = out->col; WM.cval = out->val;
   if (n_small > 0) LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
   WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
   WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
+  // (5 CTAs/SM at 48 registers measured slower: 1.35 vs 1.26 ms numeric at C3, profiles/r02k)
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   LA.crp = out->row_ptr; LA.cval = out->val;
@@ -1988,8 +1997,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   // cuts the FMAs 4x but measured 2.03 vs 0.54 ms at C3: divergent per-lane row walks, 17% warps
   // active; profiles/r02f)
   if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
-    LAUNCH(h, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
-    if (hsc->n_large3 > 0) LAUNCH(h, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
+    LAUNCH_S(h, h->aux, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
+    if (hsc->n_large3 > 0) LAUNCH_S(h, h->aux, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
   } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)
     // sizes vary between Newton steps: ask for 1.5x so that the buffers rarely grow
     WS(h, part, double, "asm_large_part", PART_STRIDE * (3 * hsc->n_tasks / 2 + 64));
@@ -1998,9 +2007,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     LA.part = part;
     LA.rec_b = rec_b;
     LA.rec_v = rec_v;
-    LAUNCH(h, k_num_large<4>, glarge, 128, 0, LA);
-    if (hsc->n_large3 > 0) LAUNCH(h, k_num_large<1>, glarge, 128, 0, LA);
-    LAUNCH(h, k_large_reduce, (unsigned)std::min<int64_t>(n_c, 16 * h->sm_count), 128, 0, LA, (const int32_t *)f12);
+    LAUNCH_S(h, h->aux, k_num_large<4>, glarge, 128, 0, LA);
+    if (hsc->n_large3 > 0) LAUNCH_S(h, h->aux, k_num_large<1>, glarge, 128, 0, LA);
+    LAUNCH_S(h, h->aux, k_large_reduce, (unsigned)std::min<int64_t>(n_c, 16 * h->sm_count), 128, 0, LA,
+             (const int32_t *)f12);
   }
-  return AGIPC_OK;
+  return aux_join(h);
 }
