@@ -339,7 +339,14 @@ struct TailArgs {
   long long *level_n;      // [64]
   unsigned *bar;           // software grid barrier counter (zeroed before launch); nullptr =
                            // cooperative launch + cg grid.sync()
+  unsigned long long *trace;  // AGIPC_TAIL_TRACE: CTA 0's %globaltimer at 7 points of each level
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Grid barrier of a persistent kernel whose CTAs are all resident (one per SM, checked by the
 // occupancy query before launch): a monotone arrival counter, barrier i completes when it reaches
@@ -421,6 +428,8 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       break;
     }
     // ---- P2: Alg S1/S2 per tile (closure, election, tile-local rank); clears the hashes ----
+    unsigned long long *tr = (A.trace && level <= 64 && blockIdx.x == 0 && threadIdx.x == 0) ? A.trace + 8 * (level - 1) : nullptr;
+    if (tr) tr[0] = gtimer();
     const int64_t ntiles = (n + TN - 1) / TN;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       // a warp takes TAIL_SUB consecutive blocks of gpw groups (all hashes loaded up front)
@@ -438,9 +447,22 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       for (int r = 0; r < TAIL_SUB; ++r) {
         if (active[r]) A.h[v[r]] = 0u;
         uint32_t x = hv[r];
-        for (int k = 0; k < gs; ++k) {
-          const uint32_t tt = __shfl_sync(FULL_MASK, x, (base_lane + k) & 31);
-          if ((x >> k) & 1u) x |= tt;
+        // most groups of the later levels have no intra-group edge: every lane is its own
+        // component and the closure is the identity -- skip it warp-uniformly
+        const unsigned nonisol = __ballot_sync(FULL_MASK, active[r] && x != (1u << lig));
+        if (nonisol) {
+          if (gs == 32) {  // Warshall over the non-isolated lanes only (an isolated vertex joins nothing)
+            for (unsigned m = nonisol; m; m &= m - 1u) {
+              const int k = __ffs(m) - 1;
+              const uint32_t tt = __shfl_sync(FULL_MASK, x, k);
+              if ((x >> k) & 1u) x |= tt;
+            }
+          } else {
+            for (int k = 0; k < gs; ++k) {
+              const uint32_t tt = __shfl_sync(FULL_MASK, x, (base_lane + k) & 31);
+              if ((x >> k) & 1u) x |= tt;
+            }
+          }
         }
         const bool elected = active[r] && ((x & ((1u << lig) - 1u)) == 0u);
         const unsigned bal = __ballot_sync(FULL_MASK, elected);
@@ -463,7 +485,9 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         if (active[r]) A.mk[v[r]] = s_w[w] + local[r];
       __syncthreads();
     }
+    if (tr) tr[1] = gtimer();
     gsync();
+    if (tr) tr[2] = gtimer();
     // ---- P3: scan the tile counts (every CTA, shared memory), remap, compose, reset ----
     {
       const int64_t per = (ntiles + TAIL_THREADS - 1) / TAIL_THREADS;
@@ -487,6 +511,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       __syncthreads();
     }
     const int64_t n2 = s_total;
+    if (tr) tr[3] = gtimer();
     bool hit = false;
     // remap in place (each edge is read and written by one thread): a merged edge becomes dead
     // (-1, -1) instead of being compacted away -- no CTA-wide compaction (two barriers and a
@@ -507,6 +532,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       Ew[e] = keep ? o : make_int2(-1, -1);
     }
     if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
+    if (tr) tr[4] = gtimer();
     for (int64_t c = gtid; c < n1; c += 2 * gstride) {  // two independent gathers in flight
       const int64_t c1 = c + gstride;
       const bool two = c1 < n1;
@@ -522,7 +548,9 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       A.ctrl[3] = 1;
       if (level <= 64) A.level_n[level - 1] = n2;
     }
+    if (tr) tr[5] = gtimer();
     gsync();
+    if (tr) tr[6] = gtimer();
     n = n2;
     if (A.max_levels > 0 && level >= A.max_levels) {
       if (gtid == 0) {
@@ -643,6 +671,14 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     A.ctrl = sc->ctrl;
     A.nvals = sc->nvals;
     A.level_n = sc->level_n;
+    static const bool trace_on = getenv("AGIPC_TAIL_TRACE") != nullptr;
+    unsigned long long *trace = nullptr;
+    if (trace_on) {
+      WS(h, trw, unsigned long long, "map_tail_trace", 8 * 64);
+      CU_TRY(h, cudaMemsetAsync(trw, 0, sizeof(unsigned long long) * 8 * 64, s0));
+      trace = trw;
+    }
+    A.trace = trace;
     const size_t smem = sizeof(int32_t) * (size_t)tiles_max;
     if (smem > 200 * 1024) return set_err(h, AGIPC_ERANGE, "build_map: %lld nodes exceed the tail kernel", (long long)N);
     if (smem > h->tail_smem) {  // host-side attribute + residency check once per size (they cost
@@ -681,6 +717,22 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   if (st != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(hs, sc, sizeof(MapScalars), cudaMemcpyDeviceToHost, s0));
   CU_TRY(h, cudaStreamSynchronize(s0));
+  if (getenv("AGIPC_TAIL_TRACE") && max_levels != 1) {  // per-phase time of the tail levels (CTA 0)
+    unsigned long long t[8 * 64];
+    if (cudaMemcpy(t, h->ws["map_tail_trace"].ptr, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      double acc[6] = {0, 0, 0, 0, 0, 0};
+      int nl = 0;
+      for (int lv = 0; lv < 64; ++lv) {
+        const unsigned long long *r = t + 8 * lv;
+        if (!r[0] || !r[6]) continue;
+        ++nl;
+        for (int k = 0; k < 6; ++k) acc[k] += 1e-3 * (double)(r[k + 1] - r[k]);
+      }
+      fprintf(stderr, "libagipc[tail-trace] levels %d, mean us per level: P2 closure %.2f | barrier %.2f | "
+              "tile scan %.2f | edges %.2f | compose %.2f | barrier %.2f\n", nl, acc[0] / nl, acc[1] / nl,
+              acc[2] / nl, acc[3] / nl, acc[4] / nl, acc[5] / nl);
+    }
+  }
   info->n_cross_edges = (int64_t)hs->cross;
   info->n_coarse = hs->nvals[0];
   if (max_levels == 1) {
