@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     ap.add_argument("--partitioned", action="store_true", help="use the partitioned path even at N=1")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: ONE --side^3 box (272 = C5) cut into N slabs (partitioned path at any N)")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row measurements")
     ap.add_argument("--no-big", action="store_true", help="skip the single-GPU C4 (5M) and C5 (20M) lines")
     ap.add_argument("--big-steps", type=int, default=2, help="timed steps of the C4 / C5 lines")
@@ -437,11 +439,13 @@ def run_agipc(args, world, rank, local_rank):
     emit(out)
 
 
-def measure_big_configs(P, h, dev, steps, warmup=1):
+def measure_big_configs(P, h, dev, steps, warmup=2):
     """BASELINE.json configs[3] and [4] on ONE B200 (their 1-GPU points; the multi-GPU runs use the
     partitioned path): C4 = 27 objects x 57^3 nodes with contact blocks, per-object E, twist
     iterates; C5 = the 272^3 grid (20,123,648 nodes) with the C3 strain-wall rule.  Per config:
-    coarsen+assemble ms per Newton step, the coarse PCG to 1e-3 (iterations/s), the full step."""
+    coarsen+assemble ms per Newton step, the coarse PCG to 1e-3 (iterations/s), the full step.
+    Two warm-up steps: C5 alternates two wall phases and the first step of each grows the
+    workspace (1063 / 252 ms, then 40-47 ms, profiles/r02m/probe_c5.txt)."""
     import torch
     import synth
     from paper_2605_04773_b200.step import CoarseningStep
@@ -532,20 +536,35 @@ def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=
     byt = N * (4 + 24 + 24) + cs.n_slots * 24   # new_map, X_bar, d_f written, coarse vector
     out["prolongate"] = {"ms": round(ms, 4), "gbs": round(byt / (ms * 1e-3) / 1e9, 1),
                          "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 3), "bytes": int(byt)}
-    t_ref, its = [], 0
-    for _ in range(2):
-        flush.zero_()
-        P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, y_c, 1.0, yf)
-        a, b = ev(), ev()
-        a.record()
-        _, st = P.pcg_solve(h, Hrp, Hcol, Hval, gd, yf, 1e-3, 10, 10)
-        b.record()
-        torch.cuda.synchronize()
-        t_ref.append(a.elapsed_time(b))
-        its = st["iters"]
-    out["post_coarsening_pcg"] = {"ms_per_solve": round(min(t_ref), 3), "iters": its,
-                                  "note": "fine block-Jacobi PCG from d_f, <= 10 iterations, incl. the per-solve "
-                                          "SELL re-layout of the 1.1 GB fine matrix"}
+    def fine_solves(reps):
+        ts, it = [], 0
+        for _ in range(reps):
+            flush.zero_()
+            P.prolongate(h, dm, cs.new_map, cs.n3, cs.n_slots, y_c, 1.0, yf)
+            a, b = ev(), ev()
+            a.record()
+            _, st = P.pcg_solve(h, Hrp, Hcol, Hval, gd, yf, 1e-3, 10, 10)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+            it = st["iters"]
+        return ts, it
+    t_flat, _ = fine_solves(2)
+    h.pcg_set_static(Hrp, Hcol)   # the fine pattern is static: one SELL layout per run
+    try:
+        t_ref, its = fine_solves(3)
+        h.profile(True)
+        fine_solves(1)
+        fprof = h.profile_read()
+        h.profile(False)
+    finally:
+        h.pcg_set_static()
+    out["post_coarsening_pcg"] = {"ms_per_solve": round(min(t_ref[1:]), 3), "iters": its,
+                                  "first_solve_ms": round(t_ref[0], 3), "flat_ms_per_solve": round(min(t_flat), 3),
+                                  "phases_ms": {k: round(v[1], 4) for k, v in fprof.items() if v[1] > 0},
+                                  "note": "fine block-Jacobi PCG from d_f, <= 10 iterations, on the registered static "
+                                          "pattern (values refilled into the SELL layout each solve; first_solve_ms "
+                                          "includes the one-time layout build, flat_ms_per_solve = unregistered BSR)"}
     sh = synth.sheet(1000, seed=3)
     t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(y_c.device, dt)  # noqa: E731
     X = t(sh["X"], torch.float64)
@@ -599,22 +618,43 @@ def measure_next_rows(P, h, step, cs, y_c, gd, dm, Hrp, Hcol, Hval, flush, reps=
 
 
 # --------------------------------------------------------------------------------------
-def build_partition(n, world, rank):
-    """Rank r's slab of the n x n x (world n) box plus its ghost planes; H_f on the sub-box."""
+def build_partition(n, world, rank, strong=False):
+    """Rank r's slab plus its ghost planes; H_f on the sub-box.  Weak (default): slabs of n^3
+    nodes, the box n x n x (world n).  Strong: ONE n^3 box (n = 272: C5) cut into `world` slabs
+    of n x n x n/world nodes; its displacements and g_f are drawn per global lexicographic node
+    (i n + j) n + k, so every N solves the same physical problem (only the slab-major numbering,
+    hence the coarse groups, depends on N).  At N = 1 the box is built by the C generator
+    (synth.kuhn_grid: the same Morton numbering as one slab)."""
     import synth
     from paper_2605_04773_b200 import partition as pt
     t0 = time.time()
-    b = pt.slab_bounds(n, world)
-    S, gid = synth.kuhn_box(n, slabs=world, z_lo=max(0, rank * n - 1), z_hi=min(world * n - 1, (rank + 1) * n))
+    t = n // world if strong else n
+    if strong:
+        assert n % world == 0, "--strong: the grid side must be a multiple of the rank count"
+    b = pt.slab_bounds(n, world, t)
+    if strong and world == 1:
+        S = synth.kuhn_grid(n)
+        gid = np.arange(S.n_nodes, dtype=np.int64)
+    else:
+        nz = world * t
+        S, gid = synth.kuhn_box(n, slabs=world, z_lo=max(0, rank * t - 1), z_hi=min(nz - 1, (rank + 1) * t), t=t)
     lm = pt.local_mesh(S, gid, b[rank], b[rank + 1], b, rank)
     H = synth.fine_hessian(S, E=1e5)
-    Hl = np.ascontiguousarray(H[lm.loc_src])
+    if lm.loc_src.shape[0] == H.shape[0] and np.array_equal(lm.loc_src, np.arange(H.shape[0])):
+        Hl = H                                  # one rank owns everything: no 2nd copy (C5: 21.7 GB)
+    else:
+        Hl = np.ascontiguousarray(H[lm.loc_src])
     Hh = np.ascontiguousarray(H[lm.halo_src])
     del H
     lid = np.searchsorted(gid, lm.gid)          # sub-box node of every local node
-    ijk = S.ijk[lid]
-    g = synth.slab_gradient(lm.gid[:lm.n_own])
-    disp = [synth.slab_walls(ijk, lm.gid, n, k) for k in range(10)]
+    ijk = S.ijk[lid].astype(np.int64)
+    if strong:
+        key = (ijk[:, 0] * n + ijk[:, 1]) * n + ijk[:, 2]
+        g = synth.slab_gradient(key[:lm.n_own])
+        disp = [synth.slab_walls(ijk, key, n, k) for k in range(10)]
+    else:
+        g = synth.slab_gradient(lm.gid[:lm.n_own])
+        disp = [synth.slab_walls(ijk, lm.gid, n, k) for k in range(10)]
     return lm, Hl, Hh, g, disp, time.time() - t0
 
 
@@ -630,7 +670,7 @@ def run_partitioned(args, world, rank, local_rank):
     torch.cuda.set_device(dev_i)
     dev = torch.device("cuda", dev_i)
     tcomm = Comm()  # once-per-mesh set-up (halo requests) over the process group
-    lm, Hl, Hh, g, disp, gen_s = build_partition(args.side, world, rank)
+    lm, Hl, Hh, g, disp, gen_s = build_partition(args.side, world, rank, args.strong)
     pt.exchange_requests(lm, world, tcomm.alltoall_i64)
     h = P.Handle(dev_i)
     h.set_option(P.OPT_L2_PERSIST, 128 << 20)
@@ -739,13 +779,19 @@ def run_partitioned(args, world, rank, local_rank):
         return
     out = {
         "metric": METRIC, "value": round(coarsen_ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": False,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"partitioned C3: one {args.side}x{args.side}x{world * args.side} Kuhn tet box "
-                               f"({world * args.side ** 3:,} nodes, slab-major Morton), rank r owns slab r "
-                               f"({args.side ** 3:,} nodes); strain walls k = step mod 10, theta=5e-5, E=1e5, "
+        "config": {"workload": (f"strong scaling: one {args.side}^3 Kuhn tet box ({args.side ** 3:,} nodes) cut into "
+                                f"{world} slab(s) of {args.side}x{args.side}x{args.side // world} nodes (slab-major "
+                                f"Morton), rank r owns slab r" if args.strong else
+                                f"partitioned C3: one {args.side}x{args.side}x{world * args.side} Kuhn tet box "
+                                f"({world * args.side ** 3:,} nodes, slab-major Morton), rank r owns slab r "
+                                f"({args.side ** 3:,} nodes)") +
+                               "; strain walls k = step mod 10, theta=5e-5, E=1e5, "
                                "gs=32, affine_threshold=32, distributed block-Jacobi PCG to 1e-3 from x0=0",
-                   "nodes": world * args.side ** 3, "nodes_per_rank": args.side ** 3,
+                   "nodes": args.side ** 3 if args.strong else world * args.side ** 3,
+                   "nodes_per_rank": lm.n_own, "comm_ranks": world,
                    "l2": "flushed between steps (256 MB write); per-rank fine BSR 1.1 GB > L2",
                    "parallelism": f"{world} ranks, partitioned",
                    "transport": ("libagipc NCCL communicator (agipc_comm_init; exchanges and the PCG "
@@ -795,7 +841,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-    if world > 1 or args.partitioned:
+    if world > 1 or args.partitioned or args.strong:
         import torch
         import torch.distributed as dist
         dev_i = local_rank % max(1, torch.cuda.device_count())

@@ -264,6 +264,14 @@ AGIPC_API agipc_status agipc_pcg_solve(agipc_handle h, const agipc_bsr *A, const
                                        int zero_x0, double rel_tol, int max_iters, int check_every,
                                        agipc_pcg_stats *stats);
 
+/* agipc_pcg_set_static: register A's pattern (row_ptr, col, n_rows, nnzb) as STATIC -- the caller
+ * promises that the contents behind these two pointers do not change while it is registered (the
+ * fine mesh topology is static).  Solves on a matrix with exactly these pointers and sizes
+ * keep the SELL layout of the first such solve (segments, sorted windows, slices) and only refill
+ * the values: NEXT#1's post-coarsening fine solve every Newton step.  A = NULL clears.
+ * Without a registration, solves of at most 32 iterations stream the BSR as it is (no re-layout). */
+AGIPC_API agipc_status agipc_pcg_set_static(agipc_handle h, const agipc_bsr *A);
+
 /* ---- NEXT#2: symmetric (diagonal + upper-triangular) storage -----------------------------
  * "both FEM elasticity and IPC contact/friction Hessians are symmetric, so we store and
  * accumulate only the diagonal and upper-triangular entries ... This reduces memory traffic ...

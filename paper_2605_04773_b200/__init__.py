@@ -92,7 +92,8 @@ EXPORTS = ["agipc_create", "agipc_destroy", "agipc_set_stream", "agipc_last_erro
            "agipc_tag_rods", "agipc_triplet_plan", "agipc_triplet_reduce", "agipc_bsr_upper", "agipc_pcg_solve_sym",
            "agipc_bsr_expand_upper", "agipc_set_values_event", "agipc_set_option", "agipc_workspace_size",
            "agipc_set_workspace", "agipc_comm_unique_id", "agipc_comm_init", "agipc_comm_info",
-           "agipc_comm_allgather_scan", "agipc_comm_alltoall_i64", "agipc_halo_exchange", "agipc_dpcg_solve"]
+           "agipc_comm_allgather_scan", "agipc_comm_alltoall_i64", "agipc_halo_exchange", "agipc_dpcg_solve",
+           "agipc_pcg_set_static"]
 
 OPT_CHECK_SYMMETRY, OPT_L2_PERSIST, OPT_COMM_ALWAYS, OPT_DETERMINISTIC = 1, 2, 3, 4  # include/agipc.h AGIPC_OPT_*
 
@@ -146,6 +147,7 @@ def lib():
         L.agipc_dpcg_status.argtypes = [P, C.POINTER(i32), C.POINTER(_PcgStats)]
         L.agipc_dpcg_finish.argtypes = [P, P, P, C.POINTER(_PcgStats)]
         L.agipc_set_option.argtypes = [P, i32, i64]
+        L.agipc_pcg_set_static.argtypes = [P, C.POINTER(_Bsr)]
         L.agipc_workspace_size.argtypes = [P, i64, i64, i64, i64, C.POINTER(C.c_size_t)]
         L.agipc_set_workspace.argtypes = [P, P, C.c_size_t]
         L.agipc_comm_unique_id.argtypes = [P]
@@ -229,6 +231,16 @@ class Handle:
     def set_option(self, option: int, value: int):
         """agipc_set_option (OPT_CHECK_SYMMETRY, OPT_L2_PERSIST)."""
         self._check(lib().agipc_set_option(self._h, int(option), int(value)))
+
+    def pcg_set_static(self, row_ptr=None, col=None):
+        """agipc_pcg_set_static: solves on exactly this (row_ptr, col) keep their SELL layout and
+        only refill values (the fine pattern is static).  No arguments clears."""
+        if row_ptr is None:
+            self._check(lib().agipc_pcg_set_static(self._h, None))
+            return
+        self._static_pattern = (row_ptr, col)  # the library holds the pointers: keep them alive
+        bsr = _Bsr(row_ptr.shape[0] - 1, col.shape[0], _p(row_ptr), _p(col), None)
+        self._check(lib().agipc_pcg_set_static(self._h, C.byref(bsr)))
 
     def workspace_size(self, n_nodes=0, n_tets=0, nnz_adj=0, nnzb_fine=0) -> int:
         """agipc_workspace_size: bytes of caller-owned scratch to register (set_workspace)."""

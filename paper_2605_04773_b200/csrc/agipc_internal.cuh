@@ -73,6 +73,14 @@ struct agipc_handle_s {
   void *pinned = nullptr;  // small pinned host buffer for D2H of scalars
   size_t pinned_bytes = 0;
   PcgGraph *pcg = nullptr;
+  PcgGraph *pcg_static = nullptr;  // graph of solves on the registered static pattern
+  struct StaticPattern {           // agipc_pcg_set_static: SELL layout kept across solves
+    const void *rp = nullptr, *col = nullptr;
+    int64_t n = -1, nnzb = -1;
+    bool built = false;
+    long long nv = 0, ns = 0, sell_blocks = 0;
+    const void *bufs[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  } spat;
   size_t tail_smem = 0;
   cudaEvent_t values_event = nullptr;  // agipc_set_values_event (one-shot, consumed by assemble)
   struct DPcg *dpcg = nullptr;  // distributed PCG in progress (pcg.cu)

@@ -175,6 +175,7 @@ agipc_status agipc_destroy(agipc_handle h) {
   comm_free(h);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->pcg) pcg_graph_free(h->pcg);
+  if (h->pcg_static) pcg_graph_free(h->pcg_static);
   if (h->aux) {
     cudaStreamSynchronize(h->aux);
     cudaStreamDestroy(h->aux);

@@ -692,6 +692,7 @@ __device__ __forceinline__ double seg_sum(double v) {
 
 struct WarpArgs {
   int64_t n_w;
+  long long *msrc;             // small nodes: (fine block << 5 | child index) per sorted key
   long long *mkeys;            // mid nodes: sorted (column, entry) keys, written by the symbolic
   const int64_t *e_off;        //   pass at e_off[wi], reused by the numeric pass (no second sort)
   const int32_t *wlist;        // small nodes handled by this kernel
@@ -726,7 +727,7 @@ struct WarpArgs {
 template <int SEG, bool NUMERIC>
 __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   constexpr int NSEG = 32 / SEG;
-  __shared__ ChildTab s_tab[8 * NSEG];
+  __shared__ ChildTab s_tab[NUMERIC ? 1 : 8 * NSEG];
   // numeric: per-lane parked block B_ij (9), X_bar of its row child (3) and of its column node (3)
   __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][15];
   __shared__ PairBuf s_pb[NUMERIC ? 1 : 8];  // symbolic: buffered pairs
@@ -734,20 +735,26 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   const int w = threadIdx.x >> 5, l = lane_id();
   const int sg = l / SEG, sl = l % SEG;
   const unsigned smask = SEG == 32 ? FULL_MASK : (((1u << SEG) - 1u) << (sg * SEG));
-  ChildTab &tab = s_tab[w * NSEG + sg];
   const long long n3 = A.sc->n3;
   const int64_t n_units = (A.n_w + NSEG - 1) / NSEG;
   const int64_t ustride = (int64_t)gridDim.x * 8;
   // software pipeline over units: the node id, its child count and the lane's child of the NEXT
   // unit are loaded while this unit is processed (the wlist -> child_ptr -> child_list chain is
-  // off the critical path; profiles/r02d stall-by-line)
+  // off the critical path; profiles/r02d stall-by-line).  The numeric pass also prefetches the
+  // next unit's sorted key and source entry (written by the symbolic pass), so its only
+  // dependent loads are the fine block itself and the output positions.
   int a_nx = 0, s_nx = 0, ci_nx = 0;
+  long long key_nx = 0, m_nx = -1;
   {
     const int64_t u0 = (int64_t)blockIdx.x * 8 + w, wi0 = u0 * NSEG + sg;
     if (u0 < n_units && wi0 < A.n_w) {
       a_nx = A.wlist[wi0];
       s_nx = A.size_new[a_nx];
       if (sl < s_nx) ci_nx = A.child_list[A.child_ptr[a_nx] + sl];
+      if (NUMERIC) {
+        key_nx = A.mkeys[wi0 * SEG + sl];
+        m_nx = A.msrc[wi0 * SEG + sl];
+      }
     }
   }
   for (int64_t u = (int64_t)blockIdx.x * 8 + w; u < n_units; u += ustride) {
@@ -756,52 +763,56 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
     const int a = segv ? a_nx : 0;
     const int s = segv ? s_nx : 0;
     const int ci_cur = ci_nx;
+    const long long key_cur = key_nx, m_cur = m_nx;
     {
       const int64_t wn = (u + ustride) * NSEG + sg;
       if (u + ustride < n_units && wn < A.n_w) {
         a_nx = A.wlist[wn];
         s_nx = A.size_new[a_nx];
         ci_nx = sl < s_nx ? A.child_list[A.child_ptr[a_nx] + sl] : 0;
+        if (NUMERIC) {
+          key_nx = A.mkeys[wn * SEG + sl];
+          m_nx = A.msrc[wn * SEG + sl];
+        }
       }
     }
-    // children of the node and the offsets of their rows (segment-local scan)
-    int len = 0;
-    if (sl < s) {
-      const int ci = ci_cur;
-      const long long rb = A.rp[ci];
-      tab.ci[sl] = ci;
-      tab.rb[sl] = rb;
-      len = (int)(A.rp[ci + 1] - rb);
-    }
-    const int incl = seg_incl_scan<SEG>(len, sl);
-    tab.off[sl + 1] = incl;
-    if (sl == 0) tab.off[0] = 0;
-    __syncwarp();
-    const int T = __shfl_sync(FULL_MASK, incl, SEG - 1, SEG);
-    int b = INT_MAX, i = 0, j = 0;
-    long long k = 0;
-    if (sl < T) {
-      int c;
-      entry_of(tab, s, sl, c, k);
-      i = tab.ci[c];
-      j = A.col[k];
-      if (!NUMERIC) b = A.nm[j];
-    }
-    // sorted (column, entry) keys: computed by the symbolic pass and kept at wi * SEG + sl for
-    // the numeric pass (no second new_map gather and sort)
-    long long key;
-    if (!NUMERIC) {
-      key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
-      if (segv) A.mkeys[wi * SEG + sl] = key;
-    } else {
-      key = segv ? A.mkeys[wi * SEG + sl] : (((long long)INT_MAX << 5) | sl);
-    }
-    const int bs = (int)(key >> 5), src = (int)(key & 31);
-    const long long prevk = __shfl_up_sync(FULL_MASK, key, 1, SEG);
-    const bool valid = sl < T;
-    const bool head = valid && (sl == 0 || (prevk >> 5) != bs);
-    const unsigned hb = (__ballot_sync(FULL_MASK, head) & smask) >> (sg * SEG);  // segment-local bits
-    if (!NUMERIC) {
+    if constexpr (!NUMERIC) {
+      ChildTab &tab = s_tab[w * NSEG + sg];
+      // children of the node and the offsets of their rows (segment-local scan)
+      int len = 0;
+      if (sl < s) {
+        const int ci = ci_cur;
+        const long long rb = A.rp[ci];
+        tab.ci[sl] = ci;
+        tab.rb[sl] = rb;
+        len = (int)(A.rp[ci + 1] - rb);
+      }
+      const int incl = seg_incl_scan<SEG>(len, sl);
+      tab.off[sl + 1] = incl;
+      if (sl == 0) tab.off[0] = 0;
+      __syncwarp();
+      const int T = __shfl_sync(FULL_MASK, incl, SEG - 1, SEG);
+      int b = INT_MAX, c = 0;
+      long long k = 0;
+      if (sl < T) {
+        entry_of(tab, s, sl, c, k);
+        b = A.nm[A.col[k]];
+      }
+      // sorted (column, entry) keys and, per sorted position, its fine block and child index:
+      // kept at wi * SEG + sl for the numeric pass (no second new_map gather, sort or row walk)
+      const long long key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
+      const int src = (int)(key & 31);
+      const long long ksrc = __shfl_sync(FULL_MASK, k, src, SEG);
+      const int csrc = __shfl_sync(FULL_MASK, c, src, SEG);
+      if (segv) {
+        A.mkeys[wi * SEG + sl] = key;
+        A.msrc[wi * SEG + sl] = sl < T ? ((ksrc << 5) | csrc) : -1;
+      }
+      const int bs = (int)(key >> 5);
+      const long long prevk = __shfl_up_sync(FULL_MASK, key, 1, SEG);
+      const bool valid = sl < T;
+      const bool head = valid && (sl == 0 || (prevk >> 5) != bs);
+      const unsigned hb = (__ballot_sync(FULL_MASK, head) & smask) >> (sg * SEG);  // segment-local bits
       const int U = __popc(hb);
       const int U12 = __popc((__ballot_sync(FULL_MASK, head && bs >= n3) & smask) >> (sg * SEG));
       if (segv && sl == 0) A.rowlen[a] = U + 3 * U12;
@@ -809,106 +820,116 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       if (head && !emit) A.mirpos[A.mir_base + wi * SEG + sl] = -1;
       pairs_push(emit, make_int2(bs, a), A.mir_base + wi * SEG + sl, s_pb[w], npb, A.pairs, A.porig, A.pair_cap,
                  A.scw);
-      continue;
-    }
-    // numeric: column position of every run, run membership, run tails
-    const int ncb_a = segv ? ncb_of(a, n3) : 1;
-    const int wgt_b = head ? ncb_of(bs, n3) : 0;
-    const int cp_incl = seg_incl_scan<SEG>(wgt_b, sl);
-    const int hl = valid ? 31 - __clz(hb & ((2u << sl) - 1u)) : sl;  // my run's head (segment lane)
-    const int cp = __shfl_sync(FULL_MASK, cp_incl - wgt_b, hl, SEG);
-    const bool tail = valid && (sl == T - 1 || ((hb >> (sl + 1)) & 1u));
-    const int Q = __ballot_sync(FULL_MASK, valid && bs >= n3) ? 4 : 1;        // warp-uniform loop bounds
-    const int PA = __ballot_sync(FULL_MASK, segv && ncb_a == 4) ? 4 : 1;
-    const int si = __shfl_sync(FULL_MASK, i, src, SEG), sj = __shfl_sync(FULL_MASK, j, src, SEG);
-    const long long sk = __shfl_sync(FULL_MASK, k, src, SEG);
-    double B[9];
+      __syncwarp();
+    } else {
+      const long long key = segv ? key_cur : (((long long)INT_MAX << 5) | sl);
+      const long long m = segv ? m_cur : -1;
+      const bool valid = m >= 0;
+      const int bs = (int)(key >> 5);
+      const long long prevk = __shfl_up_sync(FULL_MASK, key, 1, SEG);
+      const bool head = valid && (sl == 0 || (prevk >> 5) != bs);
+      const unsigned hb = (__ballot_sync(FULL_MASK, head) & smask) >> (sg * SEG);  // segment-local bits
+      const int T = __popc((__ballot_sync(FULL_MASK, valid) & smask) >> (sg * SEG));  // valid = prefix
+      const long long sk = valid ? (m >> 5) : 0;
+      const int si = __shfl_sync(FULL_MASK, ci_cur, (int)(m & 31), SEG);  // child c sits on lane c
+      // column position of every run, run membership, run tails
+      const int ncb_a = segv ? ncb_of(a, n3) : 1;
+      const int wgt_b = head ? ncb_of(bs, n3) : 0;
+      const int cp_incl = seg_incl_scan<SEG>(wgt_b, sl);
+      const int hl = valid ? 31 - __clz(hb & ((2u << sl) - 1u)) : sl;  // my run's head (segment lane)
+      const int cp = __shfl_sync(FULL_MASK, cp_incl - wgt_b, hl, SEG);
+      const bool tail = valid && (sl == T - 1 || ((hb >> (sl + 1)) & 1u));
+      const int Q = __ballot_sync(FULL_MASK, valid && bs >= n3) ? 4 : 1;        // warp-uniform loop bounds
+      const int PA = __ballot_sync(FULL_MASK, segv && ncb_a == 4) ? 4 : 1;
+      const int ncb_b = valid ? ncb_of(bs, n3) : 1;
+      const int sj = (valid && ncb_b == 4) ? A.col[sk] : 0;  // the column node (affine weights only)
+      double B[9];
 #pragma unroll
-    for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
-    const int ncb_b = valid ? ncb_of(bs, n3) : 1;
-    // mirrored block (slot(bs, q), slot(a, p)) at mbase + q * mrl + p (B_ji = B_ij^T, reading R22)
-    long long mbase = -1;
-    int mrl = 0;
-    if (tail) {
-      mbase = A.mirpos[A.mir_base + wi * SEG + hl];  // k_mirror_pos (-1: small column)
-      mrl = A.mirrl[A.mir_base + wi * SEG + hl];
-    }
-    // park B and the affine coordinates once; a run of one entry (the common case) never reads
-    // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
-    const int h0 = sg * SEG + hl;
-    const bool multi = __ballot_sync(FULL_MASK, tail && h0 != l) != 0u;  // warp-uniform
-    if (multi) {
-#pragma unroll
-      for (int x = 0; x < 9; ++x) s_v[w][l][x] = B[x];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        s_v[w][l][9 + c] = (valid && ncb_a == 4) ? __ldg(A.X + 3 * (int64_t)si + c) : 0.0;
-        s_v[w][l][12 + c] = (valid && ncb_b == 4) ? __ldg(A.X + 3 * (int64_t)sj + c) : 0.0;
+      for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
+      // mirrored block (slot(bs, q), slot(a, p)) at mbase + q * mrl + p (B_ji = B_ij^T, reading R22)
+      long long mbase = -1;
+      int mrl = 0;
+      if (tail) {
+        mbase = A.mirpos[A.mir_base + wi * SEG + hl];  // k_mirror_pos (-1: small column)
+        mrl = A.mirrl[A.mir_base + wi * SEG + hl];
       }
-    }
-    __syncwarp();
-    for (int p = 0; p < PA; ++p) {
-      const bool pv = p < ncb_a;
-      const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
-      for (int q = 0; q < Q; ++q) {
-        if (!(tail && pv && q < ncb_b)) continue;
-        // coef = w_i[p] w_j[q] (Eq 4), the same product order as the oracle's weights
-        const double coef = wgt(A.X, si, ncb_a, p) * wgt(A.X, sj, ncb_b, q);
-        double v[9];
-        if (h0 == l) {
+      // park B and the affine coordinates once; a run of one entry (the common case) never reads
+      // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
+      const int h0 = sg * SEG + hl;
+      const bool multi = __ballot_sync(FULL_MASK, tail && h0 != l) != 0u;  // warp-uniform
+      if (multi) {
 #pragma unroll
-          for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
-        } else {
-          for (int t = h0; t <= l; ++t) {
-            const double wit = (ncb_a == 4 && p < 3) ? s_v[w][t][9 + p] : 1.0;
-            const double wjt = (ncb_b == 4 && q < 3) ? s_v[w][t][12 + q] : 1.0;
-            const double ct = wit * wjt;
-            if (t == h0) {
+        for (int x = 0; x < 9; ++x) s_v[w][l][x] = B[x];
 #pragma unroll
-              for (int x = 0; x < 9; ++x) v[x] = ct * s_v[w][t][x];
-            } else {
+        for (int c = 0; c < 3; ++c) {
+          s_v[w][l][9 + c] = (valid && ncb_a == 4) ? __ldg(A.X + 3 * (int64_t)si + c) : 0.0;
+          s_v[w][l][12 + c] = (valid && ncb_b == 4) ? __ldg(A.X + 3 * (int64_t)sj + c) : 0.0;
+        }
+      }
+      __syncwarp();
+      for (int p = 0; p < PA; ++p) {
+        const bool pv = p < ncb_a;
+        const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
+        for (int q = 0; q < Q; ++q) {
+          if (!(tail && pv && q < ncb_b)) continue;
+          // coef = w_i[p] w_j[q] (Eq 4), the same product order as the oracle's weights
+          const double coef = wgt(A.X, si, ncb_a, p) * wgt(A.X, sj, ncb_b, q);
+          double v[9];
+          if (h0 == l) {
 #pragma unroll
-              for (int x = 0; x < 9; ++x) v[x] += ct * s_v[w][t][x];
+            for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+          } else {
+            for (int t = h0; t <= l; ++t) {
+              const double wit = (ncb_a == 4 && p < 3) ? s_v[w][t][9 + p] : 1.0;
+              const double wjt = (ncb_b == 4 && q < 3) ? s_v[w][t][12 + q] : 1.0;
+              const double ct = wit * wjt;
+              if (t == h0) {
+#pragma unroll
+                for (int x = 0; x < 9; ++x) v[x] = ct * s_v[w][t][x];
+              } else {
+#pragma unroll
+                for (int x = 0; x < 9; ++x) v[x] += ct * s_v[w][t][x];
+              }
             }
           }
-        }
-        const long long pos = rs + cp + q;
-        A.ccol[pos] = slot_of(bs, q, n3);
-        double *dst = A.cval + 9 * pos;
+          const long long pos = rs + cp + q;
+          A.ccol[pos] = slot_of(bs, q, n3);
+          double *dst = A.cval + 9 * pos;
 #pragma unroll
-        for (int x = 0; x < 9; ++x) dst[x] = v[x];
-        if (mbase >= 0) {
-          double *mt = A.cval + 9 * (mbase + (long long)q * mrl + p);
+          for (int x = 0; x < 9; ++x) dst[x] = v[x];
+          if (mbase >= 0) {
+            double *mt = A.cval + 9 * (mbase + (long long)q * mrl + p);
 #pragma unroll
-          for (int r = 0; r < 3; ++r)
+            for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
+              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
+          }
         }
       }
-    }
-    __syncwarp();
-    if (A.g_f) {  // g_c[slot(a,p)] = sum over the children of w_i[p] g_f[i]
-      for (int p = 0; p < PA; ++p) {
-        double g0 = 0, g1 = 0, g2 = 0;
-        if (sl < s && p < ncb_a) {
-          const int ci = tab.ci[sl];
-          const double wc = wgt(A.X, ci, ncb_a, p);
-          g0 = wc * A.g_f[3 * (int64_t)ci];
-          g1 = wc * A.g_f[3 * (int64_t)ci + 1];
-          g2 = wc * A.g_f[3 * (int64_t)ci + 2];
-        }
-        g0 = seg_sum<SEG>(g0);
-        g1 = seg_sum<SEG>(g1);
-        g2 = seg_sum<SEG>(g2);
-        if (segv && sl == 0 && p < ncb_a) {
-          double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
-          gc[0] = g0;
-          gc[1] = g1;
-          gc[2] = g2;
+      __syncwarp();
+      if (A.g_f) {  // g_c[slot(a,p)] = sum over the children of w_i[p] g_f[i]
+        for (int p = 0; p < PA; ++p) {
+          double g0 = 0, g1 = 0, g2 = 0;
+          if (sl < s && p < ncb_a) {
+            const int ci = ci_cur;
+            const double wc = wgt(A.X, ci, ncb_a, p);
+            g0 = wc * A.g_f[3 * (int64_t)ci];
+            g1 = wc * A.g_f[3 * (int64_t)ci + 1];
+            g2 = wc * A.g_f[3 * (int64_t)ci + 2];
+          }
+          g0 = seg_sum<SEG>(g0);
+          g1 = seg_sum<SEG>(g1);
+          g2 = seg_sum<SEG>(g2);
+          if (segv && sl == 0 && p < ncb_a) {
+            double *gc = A.g_c + 3 * (int64_t)slot_of(a, p, n3);
+            gc[0] = g0;
+            gc[1] = g1;
+            gc[2] = g2;
+          }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (!NUMERIC) pairs_flush(s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
 }
@@ -1886,7 +1907,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WA.porig = porig; WA.mirpos = nullptr; WA.mirrl = nullptr; WA.mir_base = 0;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
-  WA.mkeys = nullptr; WA.e_off = nullptr;
+  WA.mkeys = nullptr; WA.e_off = nullptr; WA.msrc = nullptr;
   WarpArgs WB = WA, WM;
   WB.n_w = n_w32; WB.wlist = w32;
   // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys
@@ -1895,8 +1916,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, mirrl, int32_t, "asm_mirror_rl", mir_mid + nnzb_f + 1);
   {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
     WS(h, skeys, long long, "asm_small_keys", 16 * n_w16 + 32 * n_w32 + 1);
+    WS(h, ssrc, long long, "asm_small_src", 16 * n_w16 + 32 * n_w32 + 1);
     WA.mkeys = skeys;
     WB.mkeys = skeys + 16 * n_w16;
+    WA.msrc = ssrc;
+    WB.msrc = ssrc + 16 * n_w16;
     WA.mirpos = mirpos;
     WA.mirrl = mirrl;
     WB.mirpos = mirpos;

@@ -289,7 +289,10 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
                             const int64_t *__restrict__ vr_ptr,
                             const int32_t *__restrict__ perm, const int32_t *__restrict__ v_row,
                             const int32_t *__restrict__ v_len, const int64_t *__restrict__ sptr,
-                            int32_t *__restrict__ scol, double *__restrict__ sval, int32_t *__restrict__ s_vrow) {
+                            int32_t *__restrict__ scol, double *__restrict__ sval, int32_t *__restrict__ s_vrow,
+                            const double *__restrict__ x0, double *__restrict__ qx) {
+  // x0 != nullptr: also the virtual row's part of A x0 into qx[v] (k_init sums a row's parts:
+  // the initial residual r = b - A x0 without a second pass over the matrix)
   const long long ns = st->ns, nv = st->nv;
   const int l = lane_id();
   for (long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < ns;
@@ -313,10 +316,12 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
     const double *vs = halo ? hval : val;
     const long long base = sptr[s];
     const int L = (int)((sptr[s + 1] - base) / 32);
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     for (int j = 0; j < L; ++j) {
       const long long t = base + 32LL * j;
       const bool real = j < len;
-      scol[t + l] = real ? cs[k0 + j] : row;
+      const int c = real ? cs[k0 + j] : row;
+      scol[t + l] = c;
       double *dst = sval + 9 * t;  // tile of the block column (see blk_load for the layout)
       const double *src = vs + 9 * (k0 + j);
       double v[9];
@@ -326,6 +331,17 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
       for (int pp = 0; pp < 4; ++pp)  // one 16-B store per component pair: 512 B per warp
         *reinterpret_cast<double2 *>(dst + tile_off(2 * pp, l)) = make_double2(v[2 * pp], v[2 * pp + 1]);
       dst[tile_off(8, l)] = v[8];
+      if (x0 && real) {
+        const double a0 = x0[3 * (int64_t)c], a1 = x0[3 * (int64_t)c + 1], a2 = x0[3 * (int64_t)c + 2];
+        y0 += v[0] * a0 + v[1] * a1 + v[2] * a2;
+        y1 += v[3] * a0 + v[4] * a1 + v[5] * a2;
+        y2 += v[6] * a0 + v[7] * a1 + v[8] * a2;
+      }
+    }
+    if (x0 && v >= 0) {
+      qx[3 * (int64_t)v] = y0;
+      qx[3 * (int64_t)v + 1] = y1;
+      qx[3 * (int64_t)v + 2] = y2;
     }
   }
 }
@@ -371,7 +387,9 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
                                                       const double *__restrict__ Dinv, double *__restrict__ r,
                                                       double *__restrict__ z, double *__restrict__ p, double *parts,
                                                       PcgState *st, int zero_x0, double *red,
-                                                      const double *__restrict__ ax) {
+                                                      const double *__restrict__ ax,
+                                                      const int64_t *__restrict__ vr_ptr = nullptr,
+                                                      const double *__restrict__ qx = nullptr) {
   __shared__ double s_red[PCG_WARPS];
   const int w = threadIdx.x >> 5, l = lane_id();
   double rz = 0.0, rr = 0.0, bb = 0.0;
@@ -379,6 +397,15 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     if (!zero_x0 && ax) {  // (A x)_row precomputed from upper storage (k_ax_upper)
       y0 = ax[3 * row]; y1 = ax[3 * row + 1]; y2 = ax[3 * row + 2];
+    } else if (!zero_x0 && qx) {  // (A x)_row = sum of its virtual rows' parts (k_sell_fill)
+      for (int64_t v = vr_ptr[row] + l; v < vr_ptr[row + 1]; v += 32) {
+        y0 += qx[3 * v];
+        y1 += qx[3 * v + 1];
+        y2 += qx[3 * v + 2];
+      }
+      y0 = warp_sum(y0);
+      y1 = warp_sum(y1);
+      y2 = warp_sum(y2);
     } else if (!zero_x0) {  // (A x)_row, one warp, lane per block (consecutive 72-B blocks)
       for (int64_t k = rp[row] + l; k < rp[row + 1]; k += 32) {
         const double *B = val + 9 * k;
@@ -1013,7 +1040,7 @@ static agipc_status enqueue_iters(agipc_handle h, cudaStream_t s, int iters, int
 static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bsr *Ah, int64_t n_gs, const double *b,
                               const double *x, int zero_x0, double rel_tol, int max_iters, PcgBufs &B,
                               PcgState *hst, double *red, int storage = AGIPC_STORAGE_FULL,
-                              const char *pfx = "pcg_", bool flat = false) {
+                              const char *pfx = "pcg_", bool flat = false, bool stat = false) {
 #define PN(x) (std::string(pfx) + (x)).c_str()  // the distributed solve has its own buffers
   const int64_t n = A->n_rows;
   B.sym = storage != AGIPC_STORAGE_FULL;
@@ -1087,11 +1114,21 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
   const int Gi = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, PCG_WARPS), 8 * (int64_t)h->sm_count));
   const int Gp = std::max(std::max(B.G1, B.G2), Gi);
   WS(h, parts, double, PN("parts"), 3 * Gp); B.parts = parts;
+  // static pattern (agipc_pcg_set_static): the SELL layout of the previous solve on the same
+  // row_ptr / col is reused when its buffers are still in place; only the values are refilled
+  const void *pat_bufs[8] = {B.vr_ptr, B.v_row, B.v_len, B.perm, B.sptr, B.s_vrow, B.order, nullptr};
+  bool reuse = stat && h->spat.built;
+  for (int i = 0; i < 7 && reuse; ++i) reuse = h->spat.bufs[i] == pat_bufs[i];
   PcgState init;
   memset(&init, 0, sizeof(init));
   init.tol = rel_tol;
   init.max_iters = max_iters;
   init.status = AGIPC_OK;
+  if (reuse) {
+    init.nv = h->spat.nv;
+    init.ns = h->spat.ns;
+    init.sell_blocks = h->spat.sell_blocks;
+  }
   *hst = init;
   ProfScope prof_setup(h, PROF_PCG_SETUP, s0);
   CU_TRY(h, cudaMemcpyAsync(stp, hst, sizeof(PcgState), cudaMemcpyHostToDevice, s0));
@@ -1114,30 +1151,41 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
     return AGIPC_OK;
   }
-  // SELL layout (once per solve)
+  // SELL layout (once per solve, or once per static pattern)
   const int64_t *hrp = Ah ? Ah->row_ptr : nullptr;
-  LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, nseg);
-  agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
-  if (sst != AGIPC_OK) return sst;
-  LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
-  CU_TRY(h, cudaFuncSetAttribute(k_window_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(unsigned long long) * SORT_WIN)));
-  LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, B.win), 1024, sizeof(unsigned long long) * B.win, stp, B.v_len,
-         B.perm, B.win);
-  LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
-  sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
-  if (sst != AGIPC_OK) return sst;
-  LAUNCH(h, k_sell_scalars, 1, 1, 0, B.ns_bound, B.sptr, stp);
-  LAUNCH(h, k_slice_order, 1, 1024, 0, stp, slen, B.order);
+  // A x0 of a full-storage, halo-free solve from x0 != 0 rides on the value fill
+  const bool fuse_ax = !zero_x0 && !Ah && !B.sym && storage == AGIPC_STORAGE_FULL;
+  if (!reuse) {
+    LAUNCH(h, k_seg_count, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, nseg);
+    agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, nseg, n, B.vr_ptr);
+    if (sst != AGIPC_OK) return sst;
+    LAUNCH(h, k_seg_fill, (unsigned)cdiv(n, 256), 256, 0, n, rb, re, hrp, B.vr_ptr, B.v_row, B.v_len, stp);
+    CU_TRY(h, cudaFuncSetAttribute(k_window_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(unsigned long long) * SORT_WIN)));
+    LAUNCH(h, k_window_sort, (unsigned)cdiv(nv_bound, B.win), 1024, sizeof(unsigned long long) * B.win, stp, B.v_len,
+           B.perm, B.win);
+    LAUNCH(h, k_slice_len, (unsigned)cdiv(B.ns_bound, 256), 256, 0, B.ns_bound, stp, B.perm, B.v_len, slen);
+    sst = scan_exclusive_i64(h, SCAN_SRC_I32, slen, B.ns_bound, B.sptr);
+    if (sst != AGIPC_OK) return sst;
+    LAUNCH(h, k_sell_scalars, 1, 1, 0, B.ns_bound, B.sptr, stp);
+    LAUNCH(h, k_slice_order, 1, 1024, 0, stp, slen, B.order);
+    CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
+    CU_TRY(h, cudaStreamSynchronize(s0));
+    if (stat) {
+      h->spat.built = true;
+      h->spat.nv = hst->nv;
+      h->spat.ns = hst->ns;
+      h->spat.sell_blocks = hst->sell_blocks;
+      for (int i = 0; i < 8; ++i) h->spat.bufs[i] = pat_bufs[i];
+    }
+  }
   CU_TRY(h, cudaMemsetAsync(B.counters, 0, 2 * sizeof(int), s0));
-  CU_TRY(h, cudaMemcpyAsync(hst, stp, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
-  CU_TRY(h, cudaStreamSynchronize(s0));
   const long long sell_blocks = hst->sell_blocks;
   WS(h, scol, int32_t, PN("scol"), sell_blocks + 32); B.scol = scol;
   WS(h, sval, double, PN("sval"), 9 * sell_blocks + 288); B.sval = sval;
   LAUNCH(h, k_sell_fill, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(hst->ns, 8), 16 * h->sm_count)), 256,
          0, stp, rb, re, A->col, A->val, hrp, Ah ? Ah->col : nullptr, Ah ? Ah->val : nullptr, B.vr_ptr, B.perm,
-         B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow);
+         B.v_row, B.v_len, B.sptr, B.scol, B.sval, B.s_vrow, fuse_ax ? (const double *)B.x : nullptr, B.qseg);
   const double *ax = nullptr;
   if (B.sym) {
     CU_TRY(h, cudaMemsetAsync(B.ytin, 0, sizeof(double) * 3 * n, s0));  // straddling rows keep 0
@@ -1151,7 +1199,7 @@ static agipc_status pcg_setup(agipc_handle h, const agipc_bsr *A, const agipc_bs
     }
   }
   LAUNCH(h, k_init, (unsigned)Gi, PCG_THREADS, 0, n, A->row_ptr, A->col, A->val, b, B.x, B.Dinv, B.r, B.z, B.P[0],
-         parts, stp, zero_x0, red, ax);
+         parts, stp, zero_x0, red, ax, (const int64_t *)B.vr_ptr, fuse_ax ? (const double *)B.qseg : nullptr);
   return AGIPC_OK;
 #undef PN
 }
@@ -1176,17 +1224,21 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
   PcgBufs B;
   // short solves (NEXT#1: <= 10 post-coarsening fine iterations) stream the caller's BSR
   // flat instead of re-laying it out; AGIPC_PCG_FLAT=0/1 forces a variant (A/B runs)
-  bool flat = storage == AGIPC_STORAGE_FULL && max_iters <= 32;
+  const bool stat = storage == AGIPC_STORAGE_FULL && h->spat.rp == A->row_ptr && h->spat.col == A->col &&
+                    h->spat.n == n && h->spat.nnzb == A->nnzb;
+  bool flat = storage == AGIPC_STORAGE_FULL && max_iters <= 32 && !stat;
   if (const char *e = getenv("AGIPC_PCG_FLAT")) flat = storage == AGIPC_STORAGE_FULL && atoi(e) != 0;
-  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr, storage, "pcg_", flat);
+  ast = pcg_setup(h, A, nullptr, 0, b, x, zero_x0, rel_tol, max_iters, B, hst, nullptr, storage,
+                  stat && !flat ? "pcgs_" : "pcg_", flat, stat && !flat);
   if (ast != AGIPC_OK) return ast;
   if (max_iters == 0) {
     CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s0));
     CU_TRY(h, cudaStreamSynchronize(s0));
   } else {
-    PcgGraph *g = h->pcg;
+    PcgGraph *&gslot = (stat && !flat) ? h->pcg_static : h->pcg;  // one cached graph per kind
+    PcgGraph *g = gslot;
     if (!g) {
-      g = h->pcg = new PcgGraph();
+      g = gslot = new PcgGraph();
       CU_TRY(h, cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
       CU_TRY(h, cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
       CU_TRY(h, cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming));
@@ -1279,6 +1331,19 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
   if (stats->status == AGIPC_EINDEFINITE) return set_err(h, AGIPC_EINDEFINITE, "pcg_solve: p^T A p <= 0");
   if (stats->status == AGIPC_EBREAKDOWN) return set_err(h, AGIPC_EBREAKDOWN, "pcg_solve: NaN/Inf");
   if (stats->status == AGIPC_NOT_CONVERGED) return AGIPC_NOT_CONVERGED;
+  return AGIPC_OK;
+}
+
+extern "C" agipc_status agipc_pcg_set_static(agipc_handle h, const agipc_bsr *A) {
+  if (!h) return AGIPC_EINVAL;
+  h->spat = agipc_handle_s::StaticPattern();
+  if (A) {
+    if (!A->row_ptr || !A->col || A->n_rows < 0 || A->nnzb < 0) return set_err(h, AGIPC_EINVAL, "pcg_set_static: bad matrix");
+    h->spat.rp = A->row_ptr;
+    h->spat.col = A->col;
+    h->spat.n = A->n_rows;
+    h->spat.nnzb = A->nnzb;
+  }
   return AGIPC_OK;
 }
 

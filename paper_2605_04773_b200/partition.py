@@ -91,18 +91,21 @@ def local_mesh(mesh, gid, lo, hi, bounds, rank) -> LocalMesh:
     adj_nbr = loc_of[mesh.adj_nbr[keep]].astype(np.int32)
     adj_ptr = np.zeros(n_own + 1, np.int64)
     np.cumsum(np.bincount(r_loc, minlength=n_own), out=adj_ptr[1:])
-    # tet slots: (u->v) exists locally iff both ends are owned
-    key = r_loc * (n_own + 1) + adj_nbr
+    # tet slots: (u->v) exists locally iff both ends are owned.  The local slots are the kept
+    # global slots in order, so a mesh tet-slot table translates by the rank of each kept slot
+    # (checked edge by edge; otherwise the slots are found by search)
     ts = np.full((tets.shape[0], 12), -1, np.int32)
-    for e, (a, b) in enumerate(TET_EDGES):
-        u = tets[:, a].astype(np.int64)
-        v = tets[:, b].astype(np.int64)
-        ok = (u < n_own) & (v < n_own)
-        for col, (x, y) in ((2 * e, (u, v)), (2 * e + 1, (v, u))):
-            q = x[ok] * (n_own + 1) + y[ok]
-            pos = np.searchsorted(key, q)
-            assert np.all(key[np.minimum(pos, key.shape[0] - 1)] == q)
-            ts[np.nonzero(ok)[0], col] = pos
+    if not _translate_tet_slots(mesh, tet_own, tets, n_own, rows_m, keep, ts):
+        key = r_loc * (n_own + 1) + adj_nbr
+        for e, (a, b) in enumerate(TET_EDGES):
+            u = tets[:, a].astype(np.int64)
+            v = tets[:, b].astype(np.int64)
+            ok = (u < n_own) & (v < n_own)
+            for col, (x, y) in ((2 * e, (u, v)), (2 * e + 1, (v, u))):
+                q = x[ok] * (n_own + 1) + y[ok]
+                pos = np.searchsorted(key, q)
+                assert np.all(key[np.minimum(pos, key.shape[0] - 1)] == q)
+                ts[np.nonzero(ok)[0], col] = pos
     # fine BSR split into owned / ghost columns
     brow = np.repeat(np.arange(Nm), np.diff(mesh.bsr_ptr))
     bo = own[brow]
@@ -128,6 +131,32 @@ def local_mesh(mesh, gid, lo, hi, bounds, rank) -> LocalMesh:
                      loc_src=loc_src, hbsr_ptr=hbsr_ptr, hbsr_col=hbsr_col, halo_src=halo_src,
                      ghost_owner=ghost_owner, peers=sorted(recv_ptr), recv_ptr=recv_ptr, send_idx={},
                      slot_src=slot_src)
+
+
+def _translate_tet_slots(mesh, tet_own, tets, n_own, rows_m, keep, ts) -> bool:
+    """ts[:, col] = local slot of the mesh's tet slot when both ends are owned.  Returns False
+    (ts untouched) if the mesh has no complete tet-slot table in TET_EDGES order."""
+    mts = getattr(mesh, "tet_slots", None)
+    if mts is None or mts.shape[1] != 12:
+        return False
+    mts = mts[tet_own]
+    if mts.shape[0] != tets.shape[0] or np.any(mts < 0):
+        return False
+    rank_of = np.cumsum(keep, dtype=np.int64) - 1
+    # convention check on (up to) 65536 evenly spaced tets: column 2e is u->v of TET_EDGES[e]
+    smp = np.unique(np.linspace(0, mts.shape[0] - 1, min(mts.shape[0], 65536)).astype(np.int64))
+    tm = mesh.tets[np.nonzero(tet_own)[0][smp]]
+    out = np.full_like(ts, -1)
+    for e, (a, b) in enumerate(TET_EDGES):
+        ok = (tets[:, a] < n_own) & (tets[:, b] < n_own)
+        for col, (x, y) in ((2 * e, (a, b)), (2 * e + 1, (b, a))):
+            g = mts[:, col]
+            gs = g[smp].astype(np.int64)
+            if not (np.array_equal(rows_m[gs], tm[:, x]) and np.array_equal(mesh.adj_nbr[gs], tm[:, y])):
+                return False
+            out[ok, col] = rank_of[g[ok]]
+    ts[:] = out
+    return True
 
 
 def send_lists_from_requests(lm: LocalMesh, requests: dict):
@@ -169,5 +198,7 @@ def exchange_requests(lm: LocalMesh, world: int, exchange):
     return lm
 
 
-def slab_bounds(n: int, R: int):
-    return [r * n ** 3 for r in range(R + 1)]
+def slab_bounds(n: int, R: int, t: int | None = None):
+    """Owned global id ranges of R slabs of n x n x t nodes (t = n: cubes)."""
+    t = n if t is None else t
+    return [r * n * n * t for r in range(R + 1)]

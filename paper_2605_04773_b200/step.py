@@ -40,6 +40,8 @@ class CoarseningStep:
         self.bufs = CoarseBuffers(dev, mesh.n_nodes, 4 * mesh.n_nodes // 8 + 16, H_col.shape[0] // 2 + 64)
         self.x = None
         self.refine_iters = refine_iters
+        if refine_iters > 0:  # the fine solve of every Newton step reuses one SELL layout of H_f
+            h.pcg_set_static(H_row_ptr, H_col)
         self.y_f = torch.empty((mesh.n_nodes, 3), dtype=torch.float64, device=dev)
 
     def coarsen(self, x_prev, x_cur, g_fine, count=False, hessian_ready=None):

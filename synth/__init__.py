@@ -467,23 +467,26 @@ def config_c3(n: int = 100, k: int = 0):
 # R = 1 this is exactly kuhn_grid(n).
 # ----------------------------------------------------------------------------
 
-def kuhn_box(n: int, slabs: int = 1, z_lo: int = 0, z_hi: int | None = None, side: float = 1.0):
+def kuhn_box(n: int, slabs: int = 1, z_lo: int = 0, z_hi: int | None = None, side: float = 1.0,
+             t: int | None = None):
     """Kuhn 6-tet grid over nodes (i, j, k), 0 <= i, j < n, z_lo <= k <= z_hi (default: the
-    whole box, k < slabs*n).  Returns (mesh, gid): gid[v] = global slab-major Morton id of local
-    node v; local ids are ascending in gid (so a sub-box keeps the global order).  Spacing
-    h = side/(n-1); the whole box is centred on the origin."""
-    nz = slabs * n
+    whole box, k < slabs*t) of `slabs` slabs of n x n x t nodes (t = n: cubes).  Returns
+    (mesh, gid): gid[v] = global slab-major Morton id of local node v; local ids are ascending
+    in gid (so a sub-box keeps the global order).  Spacing h = side/(n-1); the whole box is
+    centred on the origin."""
+    t = n if t is None else t
+    nz = slabs * t
     z_hi = nz - 1 if z_hi is None else z_hi
-    assert n >= 2 and 0 <= z_lo < z_hi < nz
+    assert n >= 2 and t >= 1 and 0 <= z_lo < z_hi < nz
     h = side / (n - 1)
     gi = np.arange(n)
     gk = np.arange(z_lo, z_hi + 1)
     I, J, K = np.meshgrid(gi, gi, gk, indexing="ij")
     ijk = np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.int64)
-    s = ijk[:, 2] // n
+    s = ijk[:, 2] // t
     loc = ijk.copy()
-    loc[:, 2] -= s * n
-    gid_all = s * n ** 3 + _morton_rank(n)[_morton_key(loc)]
+    loc[:, 2] -= s * t
+    gid_all = s * (n * n * t) + _morton_rank(n, t)[_morton_key(loc)]
     perm = np.argsort(gid_all, kind="stable")
     gid = gid_all[perm]
     ijk_new = ijk[perm]
@@ -514,16 +517,18 @@ def kuhn_box(n: int, slabs: int = 1, z_lo: int = 0, z_hi: int | None = None, sid
 _MR = {}
 
 
-def _morton_rank(n: int):
-    """Dense rank of every Morton key of the n^3 grid (lookup table, key -> rank)."""
-    if n not in _MR:
+def _morton_rank(n: int, t: int | None = None):
+    """Dense rank of every Morton key of the n x n x t grid (t = n: the cube; lookup table,
+    key -> rank)."""
+    t = n if t is None else t
+    if (n, t) not in _MR:
         g = np.arange(n)
-        I, J, K = np.meshgrid(g, g, g, indexing="ij")
+        I, J, K = np.meshgrid(g, g, np.arange(t), indexing="ij")
         keys = _morton_key(np.stack([I.ravel(), J.ravel(), K.ravel()], axis=1).astype(np.int64))
         tab = np.full(int(keys.max()) + 1, -1, np.int64)
         tab[np.sort(keys)] = np.arange(keys.shape[0])
-        _MR[n] = tab
-    return _MR[n]
+        _MR[(n, t)] = tab
+    return _MR[(n, t)]
 
 
 def slab_walls(ijk: np.ndarray, gid: np.ndarray, n: int, k: int, period: int = 16, rel_amp: float = 1e-2,
@@ -533,23 +538,24 @@ def slab_walls(ijk: np.ndarray, gid: np.ndarray, n: int, k: int, period: int = 1
     for its ghosts.  Returns the displacement [len(gid), 3] (x_prev = X, x_cur = X + disp)."""
     h = 1.0 / (n - 1)
     wall = np.any(ijk % period == (k % period), axis=1)
-    disp = np.zeros((gid.shape[0], 3))
-    blk = gid >> 16
-    for b in np.unique(blk):
-        sel = blk == b
-        xi = np.random.default_rng([seed, 11, k, int(b)]).standard_normal((1 << 16, 3))
-        disp[sel] = xi[gid[sel] & 0xFFFF]
+    disp = _per_block_normals(gid, lambda b: [seed, 11, k, b])
     return (rel_amp * h) * disp * wall[:, None]
+
+
+def _per_block_normals(gid: np.ndarray, seed_of) -> np.ndarray:
+    """xi[v] = row (gid[v] & 0xFFFF) of the N(0,1) [2^16, 3] draw of generator seed_of(gid[v] >> 16)
+    (one pass over the nodes; the blocks' draws are made once each)."""
+    gid = np.asarray(gid, np.int64)
+    ub, inv = np.unique(gid >> 16, return_inverse=True)
+    tab = np.empty((ub.shape[0], 1 << 16, 3))
+    for t, b in enumerate(ub):
+        tab[t] = np.random.default_rng(seed_of(int(b))).standard_normal((1 << 16, 3))
+    return tab[inv.reshape(-1), gid & 0xFFFF]
 
 
 def slab_gradient(gid: np.ndarray, seed: int = 0) -> np.ndarray:
     """g_f ~ N(0,1) per component, drawn per global node id (counter-based like slab_walls)."""
-    g = np.empty((gid.shape[0], 3))
-    blk = gid >> 16
-    for b in np.unique(blk):
-        sel = blk == b
-        g[sel] = np.random.default_rng([seed, 7, int(b)]).standard_normal((1 << 16, 3))[gid[sel] & 0xFFFF]
-    return g
+    return _per_block_normals(gid, lambda b: [seed, 7, b])
 
 
 # ----------------------------------------------------------------------------

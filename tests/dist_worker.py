@@ -85,6 +85,10 @@ def gpu_worker(rank, world, port, out_dir, n, thr, kind):
             gid = np.arange(G.n_nodes)
             b = [int(round(r * G.n_nodes / world)) for r in range(world + 1)]
             H = synth.c4_hessian(sc)
+        elif kind == "thin":  # bench --strong: ONE n^3 cube cut into world slabs of n x n x n/world
+            G, gid = synth.kuhn_box(n, slabs=world, t=n // world)
+            b = pt.slab_bounds(n, world, n // world)
+            H = synth.fine_hessian(G)
         else:
             G, gid = synth.kuhn_box(n, slabs=world)
             b = pt.slab_bounds(n, world)

@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("n,R,thr,kind", [(10, 2, 32, "twist"), (8, 3, 32, "random"), (8, 2, 5, "random"),
                                           (6, 4, 10 ** 9, "random"), (14, 2, 32, "twist"),
-                                          (6, 3, 32, "c4"), (6, 2, 5, "c4")])
+                                          (6, 3, 32, "c4"), (6, 2, 5, "c4"), (12, 3, 32, "thin"),
+                                          (12, 4, 5, "thin")])
 def test_distributed_step_matches_segmented_oracle(gpu, tmp_path, n, R, thr, kind):
     from dist_worker import gpu_worker
     mp.start_processes(gpu_worker, args=(R, free_port(), str(tmp_path), n, thr, kind), nprocs=R,

@@ -322,6 +322,35 @@ def test_post_coarsening_cg_matches_oracle(P, h):
     assert e(ref["x"]) <= e(y0) <= 0.0
 
 
+def test_pcg_static_pattern_refills_values(P, h):
+    """agipc_pcg_set_static: the fine solve keeps its SELL layout across Newton steps (the fine
+    pattern is static) and refills only the values -- new values must take effect, the
+    result must match the oracle, and a rebuilt layout must give the same bits."""
+    c = synth.config_c1()
+    m = c["mesh"]
+    H = synth.fine_hessian(m)
+    g = synth.fine_gradient(m.n_nodes)
+    rp, col = dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32)
+    gd = dev(g, torch.float64)
+    try:
+        h.pcg_set_static(rp, col)
+        out = []
+        for scale in (1.0, 2.0, 1.0):
+            y, s = P.pcg_solve(h, rp, col, dev(scale * H, torch.float64), gd, rel_tol=1e-3, max_iters=10, zero_x0=True)
+            ref = oracle.pcg(m.bsr_ptr, m.bsr_col, scale * H, g, rel_tol=1e-3, max_iters=10)
+            assert s["iters"] == ref["iters"] and s["status"] == ref["status"]
+            assert np.linalg.norm(y.cpu().numpy() - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
+            out.append(y.clone())
+        assert torch.equal(out[0], out[2])
+        assert not torch.allclose(out[0], out[1])
+        h.pcg_set_static()          # clear -> re-register: the layout is rebuilt, same bits
+        h.pcg_set_static(rp, col)
+        y, _ = P.pcg_solve(h, rp, col, dev(H, torch.float64), gd, rel_tol=1e-3, max_iters=10, zero_x0=True)
+        assert torch.equal(y, out[0])
+    finally:
+        h.pcg_set_static()
+
+
 def test_step_with_refinement(P, h):
     from paper_2605_04773_b200.step import CoarseningStep
     c = synth.config_c1()
@@ -331,9 +360,17 @@ def test_step_with_refinement(P, h):
     g = dev(synth.fine_gradient(m.n_nodes), torch.float64)
     st = CoarseningStep(h, dm, dev(m.bsr_ptr, torch.int64), dev(m.bsr_col, torch.int32), dev(H, torch.float64),
                         refine_iters=10)
-    r = st(dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64), g)
-    assert r.y_f is not None and r.refine["iters"] <= 10
-    assert float(torch.sum(r.y_f * g)) > 0      # d_f = -y_f is a descent direction of the fine model
+    h.set_option(P.OPT_DETERMINISTIC, 1)   # bitwise-reproducible H_c, so the two steps compare bitwise
+    try:
+        r = st(dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64), g)
+        assert r.y_f is not None and r.refine["iters"] <= 10
+        assert float(torch.sum(r.y_f * g)) > 0      # d_f = -y_f is a descent direction of the fine model
+        y1 = r.y_f.clone()
+        r = st(dev(c["x_prev"], torch.float64), dev(c["x_cur"], torch.float64), g)  # reused fine layout
+        assert torch.equal(r.y_f, y1)
+    finally:
+        h.set_option(P.OPT_DETERMINISTIC, 0)
+        h.pcg_set_static()
 
 
 # ------------------------------------------------------------------------------------------
