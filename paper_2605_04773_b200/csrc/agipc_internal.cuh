@@ -93,6 +93,16 @@ struct agipc_handle_s {
   std::vector<cudaEvent_t> prof_pool;
   double prof_ms[PROF_N] = {0};
   int64_t prof_n[PROF_N] = {0};
+  // launch trace (env AGIPC_TRACE=<file>, diagnostics only): an event before and after every
+  // LAUNCH on its stream plus the host submit time; written at agipc_destroy
+  bool trace = false;
+  struct TraceRec {
+    const char *name;
+    cudaStream_t s;
+    cudaEvent_t a, b;
+    double host_us;
+  };
+  std::vector<TraceRec> trace_recs;
 };
 
 cudaEvent_t prof_event(agipc_handle h);             // from the pool
@@ -147,13 +157,18 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
                      cudaGetErrorString(_e));                                                \
   } while (0)
 
+void trace_pre(agipc_handle h, const char *name, cudaStream_t s);
+void trace_post(agipc_handle h, cudaStream_t s);
+
 // Every kernel launch goes through LAUNCH so that the handle counts it and errors surface.
 // (one cudaGetLastError after the launch: it also reports an error left pending by an earlier
 // asynchronous call; the host-side cost per launch is on the critical path after every sync)
 #define LAUNCH(h, kernel, grid, block, smem, ...)                                            \
   do {                                                                                       \
     if ((grid) > 0) {                                                                        \
+      if ((h)->trace) trace_pre((h), #kernel, (h)->stream);                                 \
       kernel<<<(grid), (block), (smem), (h)->stream>>>(__VA_ARGS__);                         \
+      if ((h)->trace) trace_post((h), (h)->stream);                                         \
       (h)->launches += 1;                                                                    \
       cudaError_t _e = cudaGetLastError();                                                   \
       if (_e != cudaSuccess)                                                                 \
@@ -166,7 +181,9 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
 #define LAUNCH_S(h, strm, kernel, grid, block, smem, ...)                                     \
   do {                                                                                       \
     if ((grid) > 0) {                                                                        \
+      if ((h)->trace) trace_pre((h), #kernel, (strm));                                      \
       kernel<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);                              \
+      if ((h)->trace) trace_post((h), (strm));                                              \
       (h)->launches += 1;                                                                    \
       cudaError_t _e = cudaGetLastError();                                                   \
       if (_e != cudaSuccess)                                                                 \

@@ -138,6 +138,42 @@ static void prof_flush(agipc_handle h) {
   h->prof_pending.clear();
 }
 
+// ---- launch trace (AGIPC_TRACE=<file>) ----
+#include <chrono>
+static double host_now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void trace_pre(agipc_handle h, const char *name, cudaStream_t s) {
+  if (h->trace_recs.size() >= 200000) return;
+  agipc_handle_s::TraceRec r{name, s, nullptr, nullptr, host_now_us()};
+  r.a = prof_event(h);
+  if (r.a) cudaEventRecord(r.a, s);
+  h->trace_recs.push_back(r);
+}
+void trace_post(agipc_handle h, cudaStream_t s) {
+  if (h->trace_recs.empty() || h->trace_recs.back().b || h->trace_recs.back().s != s) return;
+  auto &r = h->trace_recs.back();
+  r.b = prof_event(h);
+  if (r.b) cudaEventRecord(r.b, s);
+}
+static void trace_dump(agipc_handle h) {
+  const char *path = getenv("AGIPC_TRACE");
+  if (!path || h->trace_recs.empty()) return;
+  cudaDeviceSynchronize();
+  FILE *f = fopen(path, "a");
+  if (!f) return;
+  const auto &r0 = h->trace_recs.front();
+  fprintf(f, "# name stream gpu_start_us gpu_end_us host_submit_us\n");
+  for (auto &r : h->trace_recs) {
+    float t0 = -1.f, t1 = -1.f;
+    if (r0.a && r.a) cudaEventElapsedTime(&t0, r0.a, r.a);
+    if (r0.a && r.b) cudaEventElapsedTime(&t1, r0.a, r.b);
+    fprintf(f, "%s %p %.2f %.2f %.2f\n", r.name, (void *)r.s, 1e3 * t0, 1e3 * t1, r.host_us - r0.host_us);
+  }
+  fclose(f);
+  cudaGetLastError();
+}
+
 static const char *kPhaseNames[PROF_N] = {"tag_edges", "build_map", "assemble_coarse", "pcg_setup",
                                           "pcg_spmv", "pcg_update", "pcg_solve",
                                           "asm_classify", "asm_symbolic", "asm_numeric",
@@ -161,6 +197,7 @@ agipc_status agipc_create(agipc_handle *out, int cuda_device) {
   agipc_handle h = new agipc_handle_s();
   h->device = cuda_device;
   h->sm_count = prop.multiProcessorCount;
+  h->trace = getenv("AGIPC_TRACE") != nullptr;
   *out = h;
   return AGIPC_OK;
 }
@@ -183,6 +220,7 @@ agipc_status agipc_destroy(agipc_handle h) {
     cudaEventDestroy(h->ev_join);
   }
   if (h->dpcg) dpcg_free(h->dpcg);
+  trace_dump(h);
   prof_flush(h);
   for (auto e : h->prof_pool) cudaEventDestroy(e);
   delete h;

@@ -730,6 +730,14 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[NUMERIC ? 1 : 8 * NSEG];
   // numeric: per-lane parked block B_ij (9), X_bar of its row child (3) and of its column node (3)
   __shared__ double s_v[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1][15];
+  // numeric: output descriptors (head lane | tail lane << 6 | q << 12) at column position, per
+  // segment; per head lane its column node and mirror position / row length; per segment
+  // (node, blocks per p, output blocks)
+  __shared__ int s_desc[NUMERIC ? 8 : 1][NUMERIC ? 4 * 32 : 1];
+  __shared__ int s_rbs[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1];
+  __shared__ long long s_rmb[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1];
+  __shared__ int s_rml[NUMERIC ? 8 : 1][NUMERIC ? 32 : 1];
+  __shared__ int s_seg[NUMERIC ? 8 : 1][NUMERIC ? NSEG : 1][3];
   __shared__ PairBuf s_pb[NUMERIC ? 1 : 8];  // symbolic: buffered pairs
   int npb = 0;
   const int w = threadIdx.x >> 5, l = lane_id();
@@ -822,6 +830,11 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
                  A.scw);
       __syncwarp();
     } else {
+      // Output-parallel numeric pass: every valid entry parks its fine block B_ij and the affine
+      // coordinates of its row child / column node in shared memory; every run (one coarse
+      // column b) posts one descriptor per output block q; then the warp's lanes take the output
+      // blocks of ALL its segments round-robin (o = l, l + 32, ...) and sum their run's entries
+      // left to right -- no lane idles through another lane's run or q loop.
       const long long key = segv ? key_cur : (((long long)INT_MAX << 5) | sl);
       const long long m = segv ? m_cur : -1;
       const bool valid = m >= 0;
@@ -832,78 +845,76 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       const int T = __popc((__ballot_sync(FULL_MASK, valid) & smask) >> (sg * SEG));  // valid = prefix
       const long long sk = valid ? (m >> 5) : 0;
       const int si = __shfl_sync(FULL_MASK, ci_cur, (int)(m & 31), SEG);  // child c sits on lane c
-      // column position of every run, run membership, run tails
       const int ncb_a = segv ? ncb_of(a, n3) : 1;
-      const int wgt_b = head ? ncb_of(bs, n3) : 0;
-      const int cp_incl = seg_incl_scan<SEG>(wgt_b, sl);
-      const int hl = valid ? 31 - __clz(hb & ((2u << sl) - 1u)) : sl;  // my run's head (segment lane)
-      const int cp = __shfl_sync(FULL_MASK, cp_incl - wgt_b, hl, SEG);
-      const bool tail = valid && (sl == T - 1 || ((hb >> (sl + 1)) & 1u));
-      const int Q = __ballot_sync(FULL_MASK, valid && bs >= n3) ? 4 : 1;        // warp-uniform loop bounds
-      const int PA = __ballot_sync(FULL_MASK, segv && ncb_a == 4) ? 4 : 1;
+      const int PA = __ballot_sync(FULL_MASK, segv && ncb_a == 4) ? 4 : 1;  // warp-uniform (g_c loop)
       const int ncb_b = valid ? ncb_of(bs, n3) : 1;
+      const int wgt_b = head ? ncb_b : 0;
+      const int cp_incl = seg_incl_scan<SEG>(wgt_b, sl);
+      const int R = __shfl_sync(FULL_MASK, cp_incl, SEG - 1, SEG);  // output blocks per p (row length)
       const int sj = (valid && ncb_b == 4) ? A.col[sk] : 0;  // the column node (affine weights only)
-      double B[9];
 #pragma unroll
-      for (int x = 0; x < 9; ++x) B[x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
-      // mirrored block (slot(bs, q), slot(a, p)) at mbase + q * mrl + p (B_ji = B_ij^T, reading R22)
-      long long mbase = -1;
-      int mrl = 0;
-      if (tail) {
-        mbase = A.mirpos[A.mir_base + wi * SEG + hl];  // k_mirror_pos (-1: small column)
-        mrl = A.mirrl[A.mir_base + wi * SEG + hl];
+      for (int x = 0; x < 9; ++x) s_v[w][l][x] = valid ? __ldg(A.val + 9 * sk + x) : 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        s_v[w][l][9 + c] = (valid && ncb_a == 4) ? __ldg(A.X + 3 * (int64_t)si + c) : 0.0;
+        s_v[w][l][12 + c] = (valid && ncb_b == 4) ? __ldg(A.X + 3 * (int64_t)sj + c) : 0.0;
       }
-      // park B and the affine coordinates once; a run of one entry (the common case) never reads
-      // shared memory, a longer run is summed left to right by its tail lane for every (p, q)
-      const int h0 = sg * SEG + hl;
-      const bool multi = __ballot_sync(FULL_MASK, tail && h0 != l) != 0u;  // warp-uniform
-      if (multi) {
-#pragma unroll
-        for (int x = 0; x < 9; ++x) s_v[w][l][x] = B[x];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          s_v[w][l][9 + c] = (valid && ncb_a == 4) ? __ldg(A.X + 3 * (int64_t)si + c) : 0.0;
-          s_v[w][l][12 + c] = (valid && ncb_b == 4) ? __ldg(A.X + 3 * (int64_t)sj + c) : 0.0;
-        }
+      if (head) {  // run [sl, tl]: descriptors of its output blocks q at column position cp + q
+        const unsigned above = hb & ~((2u << sl) - 1u);
+        const int tl = above ? __ffs(above) - 2 : T - 1;
+        const int cp = cp_incl - wgt_b;
+        for (int q = 0; q < ncb_b; ++q) s_desc[w][sg * 4 * SEG + cp + q] = sl | (tl << 6) | (q << 12);
+        s_rbs[w][l] = bs;
+        // mirrored block (slot(bs, q), slot(a, p)) at mb + q * mrl + p (B_ji = B_ij^T, reading R22)
+        s_rmb[w][l] = A.mirpos[A.mir_base + wi * SEG + sl];  // k_mirror_pos (-1: small column)
+        s_rml[w][l] = A.mirrl[A.mir_base + wi * SEG + sl];
+      }
+      if (sl == 0) {
+        s_seg[w][sg][0] = segv ? a : 0;
+        s_seg[w][sg][1] = segv ? R : 0;
+        s_seg[w][sg][2] = segv ? ncb_a * R : 0;  // output blocks of the segment
       }
       __syncwarp();
-      for (int p = 0; p < PA; ++p) {
-        const bool pv = p < ncb_a;
-        const long long rs = (segv && pv) ? A.crp[slot_of(a, p, n3)] : 0;
-        for (int q = 0; q < Q; ++q) {
-          if (!(tail && pv && q < ncb_b)) continue;
-          // coef = w_i[p] w_j[q] (Eq 4), the same product order as the oracle's weights
-          const double coef = wgt(A.X, si, ncb_a, p) * wgt(A.X, sj, ncb_b, q);
-          double v[9];
-          if (h0 == l) {
+      int tot = 0;
 #pragma unroll
-            for (int x = 0; x < 9; ++x) v[x] = coef * B[x];
+      for (int g = 0; g < NSEG; ++g) tot += s_seg[w][g][2];
+      for (int o = l; o < tot; o += 32) {
+        int g = 0, oo = o;
+#pragma unroll
+        for (int gg = 0; gg < NSEG - 1; ++gg)
+          if (g == gg && oo >= s_seg[w][gg][2]) { oo -= s_seg[w][gg][2]; g = gg + 1; }
+        const int ag = s_seg[w][g][0], Rg = s_seg[w][g][1];
+        const int p = oo / Rg, r = oo - p * Rg;
+        const int d = s_desc[w][g * 4 * SEG + r];
+        const int h0 = g * SEG + (d & 63), t1 = g * SEG + ((d >> 6) & 63), q = d >> 12;
+        const int b = s_rbs[w][h0];
+        const int ncb_ag = ncb_of(ag, n3), ncb_bb = ncb_of(b, n3);
+        // coef = w_i[p] w_j[q] (Eq 4), the same product order as the oracle's weights
+        double v[9];
+        for (int t = h0; t <= t1; ++t) {
+          const double wit = (ncb_ag == 4 && p < 3) ? s_v[w][t][9 + p] : 1.0;
+          const double wjt = (ncb_bb == 4 && q < 3) ? s_v[w][t][12 + q] : 1.0;
+          const double ct = wit * wjt;
+          if (t == h0) {
+#pragma unroll
+            for (int x = 0; x < 9; ++x) v[x] = ct * s_v[w][t][x];
           } else {
-            for (int t = h0; t <= l; ++t) {
-              const double wit = (ncb_a == 4 && p < 3) ? s_v[w][t][9 + p] : 1.0;
-              const double wjt = (ncb_b == 4 && q < 3) ? s_v[w][t][12 + q] : 1.0;
-              const double ct = wit * wjt;
-              if (t == h0) {
 #pragma unroll
-                for (int x = 0; x < 9; ++x) v[x] = ct * s_v[w][t][x];
-              } else {
-#pragma unroll
-                for (int x = 0; x < 9; ++x) v[x] += ct * s_v[w][t][x];
-              }
-            }
+            for (int x = 0; x < 9; ++x) v[x] += ct * s_v[w][t][x];
           }
-          const long long pos = rs + cp + q;
-          A.ccol[pos] = slot_of(bs, q, n3);
-          double *dst = A.cval + 9 * pos;
+        }
+        const long long pos = A.crp[slot_of(ag, p, n3)] + (r - q) + q;
+        A.ccol[pos] = slot_of(b, q, n3);
+        double *dst = A.cval + 9 * pos;
 #pragma unroll
-          for (int x = 0; x < 9; ++x) dst[x] = v[x];
-          if (mbase >= 0) {
-            double *mt = A.cval + 9 * (mbase + (long long)q * mrl + p);
+        for (int x = 0; x < 9; ++x) dst[x] = v[x];
+        const long long mb = s_rmb[w][h0];
+        if (mb >= 0) {
+          double *mt = A.cval + 9 * (mb + (long long)q * s_rml[w][h0] + p);
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
+          for (int rr = 0; rr < 3; ++rr)
 #pragma unroll
-              for (int cc = 0; cc < 3; ++cc) mt[3 * r + cc] = v[3 * cc + r];
-          }
+            for (int cc = 0; cc < 3; ++cc) mt[3 * rr + cc] = v[3 * cc + rr];
         }
       }
       __syncwarp();
@@ -2005,10 +2016,38 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
   LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
          out->val);
-  // the 12-DoF chunks (aux stream) and the small / mid rows (handle stream) write disjoint
-  // blocks -- (large, large) by the chunks, own rows and the mirrored (large, small) blocks by the
-  // small rows -- and are both latency-bound at partial occupancy: run them side by side
-  if ((st = aux_fork(h)) != AGIPC_OK) return st;
+  // the 12-DoF chunks and the small / mid rows write disjoint blocks -- (large, large) by the
+  // chunks, own rows and the mirrored (large, small) blocks by the small rows.  AGIPC_NUM_MODE
+  // (experiments): 0 = chunks on the aux stream next to the small rows, 1 = chunks first then
+  // the small rows on one stream, 2 = small rows first then the chunks
+  static const int num_mode = getenv("AGIPC_NUM_MODE") ? atoi(getenv("AGIPC_NUM_MODE")) : 0;
+  const bool fork = num_mode == 0;
+  cudaStream_t ls = fork ? h->aux : st_;
+  if (fork && (st = aux_fork(h)) != AGIPC_OK) return st;
+  auto launch_large = [&]() -> agipc_status {
+    LA.crp = out->row_ptr; LA.cval = out->val;
+    // (a factorised variant -- lane per child, C_i[q] = sum_j w_j[q] B_ij, then sum_i w_i[p] C_i[q] --
+    // cuts the FMAs 4x but measured 2.03 vs 0.54 ms at C3: divergent per-lane row walks, 17% warps
+    // active; profiles/r02f)
+    if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
+      LAUNCH_S(h, ls, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
+      if (hsc->n_large3 > 0) LAUNCH_S(h, ls, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
+    } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)
+      // sizes vary between Newton steps: ask for 1.5x so that the buffers rarely grow
+      WS(h, part, double, "asm_large_part", PART_STRIDE * (3 * hsc->n_tasks / 2 + 64));
+      WS(h, rec_b, int32_t, "asm_rec_b", 3 * hsc->rec_total / 2 + 64);
+      WS(h, rec_v, double, "asm_rec_v", 144 * (3 * hsc->rec_total / 2 + 64));
+      LA.part = part;
+      LA.rec_b = rec_b;
+      LA.rec_v = rec_v;
+      LAUNCH_S(h, ls, k_num_large<4>, glarge, 128, 0, LA);
+      if (hsc->n_large3 > 0) LAUNCH_S(h, ls, k_num_large<1>, glarge, 128, 0, LA);
+      LAUNCH_S(h, ls, k_large_reduce, (unsigned)std::min<int64_t>(n_c, 16 * h->sm_count), 128, 0, LA,
+               (const int32_t *)f12);
+    }
+    return AGIPC_OK;
+  };
+  if (num_mode == 1 && (st = launch_large()) != AGIPC_OK) return st;
   WM.crp = out->row_ptr; WM.ccol = out->col; WM.cval = out->val;
   if (n_small > 0) LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
   WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
@@ -2016,25 +2055,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   // (5 CTAs/SM at 48 registers measured slower: 1.35 vs 1.26 ms numeric at C3, profiles/r02k)
   if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
-  LA.crp = out->row_ptr; LA.cval = out->val;
-  // (a factorised variant -- lane per child, C_i[q] = sum_j w_j[q] B_ij, then sum_i w_i[p] C_i[q] --
-  // cuts the FMAs 4x but measured 2.03 vs 0.54 ms at C3: divergent per-lane row walks, 17% warps
-  // active; profiles/r02f)
-  if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
-    LAUNCH_S(h, h->aux, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
-    if (hsc->n_large3 > 0) LAUNCH_S(h, h->aux, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
-  } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)
-    // sizes vary between Newton steps: ask for 1.5x so that the buffers rarely grow
-    WS(h, part, double, "asm_large_part", PART_STRIDE * (3 * hsc->n_tasks / 2 + 64));
-    WS(h, rec_b, int32_t, "asm_rec_b", 3 * hsc->rec_total / 2 + 64);
-    WS(h, rec_v, double, "asm_rec_v", 144 * (3 * hsc->rec_total / 2 + 64));
-    LA.part = part;
-    LA.rec_b = rec_b;
-    LA.rec_v = rec_v;
-    LAUNCH_S(h, h->aux, k_num_large<4>, glarge, 128, 0, LA);
-    if (hsc->n_large3 > 0) LAUNCH_S(h, h->aux, k_num_large<1>, glarge, 128, 0, LA);
-    LAUNCH_S(h, h->aux, k_large_reduce, (unsigned)std::min<int64_t>(n_c, 16 * h->sm_count), 128, 0, LA,
-             (const int32_t *)f12);
-  }
-  return aux_join(h);
+  if (num_mode != 1 && (st = launch_large()) != AGIPC_OK) return st;
+  return fork ? aux_join(h) : AGIPC_OK;
 }
