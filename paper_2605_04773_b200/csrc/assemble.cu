@@ -426,6 +426,8 @@ struct LargeArgs {
   int32_t *rec_b;          // [rec_total] column aggregate of each record (-1: unused)
   double *rec_v;           // [rec_total][144] record values, (p*4+q)*9+x
   double *part;            // [n_tasks][PART_STRIDE] diagonal block + g partials of every chunk
+  const int32_t *f12;      // numeric: first 12-DoF entry of every large node's sorted column list
+  const int32_t *dpos;     // numeric: column position of the diagonal block of every large row
 };
 #define PART_STRIDE 160  // 144 diagonal-block values (p*4+q)*9+x + 12 g values p*3+d (+ pad)
 #define LSTAGE 128       // staged diagonal entries per batch of a large-row chunk
@@ -1216,7 +1218,8 @@ __global__ void k_small_lists(int64_t n_c, const int32_t *__restrict__ f16, cons
 __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t *__restrict__ is_small,
                                   const int32_t *__restrict__ gbuf, const long long *__restrict__ nb_off,
                                   const int32_t *__restrict__ nb_cnt, const int32_t *__restrict__ rowlen,
-                                  const int64_t *__restrict__ crp, int32_t *__restrict__ ccol, double *__restrict__ cval) {
+                                  const int64_t *__restrict__ crp, int32_t *__restrict__ ccol, double *__restrict__ cval,
+                                  int32_t *__restrict__ dpos) {
   const int w = threadIdx.x >> 5, l = lane_id();
   const int wpb = blockDim.x >> 5;
   const long long n3 = sc->n3;
@@ -1226,6 +1229,8 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
     const int32_t *lst = gbuf + nb_off[a];
     const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
     const int ncb_a = ncb_of((int)a, n3);
+    if (l == 0) dpos[a] = -1;  // no stored diagonal block (then the chunks accumulate nothing there)
+    __syncwarp();
     for (int p = 0; p < ncb_a; ++p) {
       const long long rs = crp[slot_of((int)a, p, n3)];
       for (int t = l; t < U; t += 32) {
@@ -1235,6 +1240,7 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
         // blocks of a small column are written exactly once by the small row's mirror (R22);
         // only the blocks the large-row chunks accumulate into need zeroing
         const bool zero = !is_small[b];
+        if (b == a && p == 0) dpos[a] = cp;
         for (int q = 0; q < ncb_b; ++q) {
           ccol[rs + cp + q] = slot_of(b, q, n3);
           if (zero) {
@@ -1265,10 +1271,15 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 // by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
 // two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
+#ifndef LSTAGE_A
 #define LSTAGE_A 192
+#endif
+#ifndef LARGE_MINB
+#define LARGE_MINB 4
+#endif
 
 template <int NCB, int NB>
-__global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeArgs A) {
+__global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atomic(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE_A];
   __shared__ int s_i[4][LSTAGE_A];     // child slot c of the entry's row (weights in s_wc)
@@ -1276,6 +1287,7 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
   __shared__ double s_xj[4][LSTAGE_A][3];  // X_bar of the entry's column node (w_j)
   __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
   __shared__ double s_B[4][32][9];       // phase 2: 32 diagonal blocks staged per warp (one per lane)
+  __shared__ int s_ix[4][LSTAGE_A];      // phase 3: staged positions of the current column's entries
   const int w = threadIdx.x >> 5, l = lane_id();
   // lane = (block group, p, q half): NCB = 4 -> 8 lanes per block, 2 q per lane
   constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
@@ -1321,7 +1333,7 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
     __syncwarp();
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
-    const int first12 = lower_bound_dev<int32_t>(lst, U, (int32_t)n3);
+    const int first12 = A.f12[a];
     double acc[QN][9];
 #pragma unroll
     for (int q = 0; q < QN; ++q)
@@ -1421,20 +1433,36 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
         for (int qq = 0; qq < QI; ++qq)
 #pragma unroll
           for (int x = 0; x < 9; ++x) ac[qq][x] = 0.0;
-        for (int d = f + gq; d < icnt; d += G) {
-          if (s_b[w][i0 + d] != b0) continue;
-          const long long kk = s_k[w][i0 + d];
-          const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][i0 + d]][p];
-          double Bv[9];
+        // the entries of b0, compacted in order; their blocks are staged 32 at a time (one
+        // independent 72-B load per lane) before the groups accumulate them
+        int nb = 0;
+        for (int d0 = f; d0 < icnt; d0 += 32) {
+          const bool mine = d0 + l < icnt && s_b[w][i0 + d0 + l] == b0;
+          const unsigned mm = __ballot_sync(FULL_MASK, mine);
+          if (mine) s_ix[w][nb + __popc(mm & ((1u << l) - 1u))] = i0 + d0 + l;
+          nb += __popc(mm);
+        }
+        __syncwarp();
+        for (int s0 = 0; s0 < nb; s0 += 32) {
+          if (s0 + l < nb) {
+            const long long kk = s_k[w][s_ix[w][s0 + l]];
 #pragma unroll
-          for (int x = 0; x < 9; ++x) Bv[x] = __ldg(A.val + 9 * kk + x);
-#pragma unroll
-          for (int qq = 0; qq < QI; ++qq) {
-            const int q = q0 + qq;
-            const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : s_xj[w][i0 + d][q]) : 0.0;
-#pragma unroll
-            for (int x = 0; x < 9; ++x) ac[qq][x] += c * Bv[x];
+            for (int x = 0; x < 9; ++x) s_B[w][l][x] = __ldg(A.val + 9 * kk + x);
           }
+          __syncwarp();
+          const int dn = min(32, nb - s0);
+          for (int dd = gq; dd < dn; dd += G) {
+            const int d = s_ix[w][s0 + dd];
+            const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d]][p];
+#pragma unroll
+            for (int qq = 0; qq < QI; ++qq) {
+              const int q = q0 + qq;
+              const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : s_xj[w][d][q]) : 0.0;
+#pragma unroll
+              for (int x = 0; x < 9; ++x) ac[qq][x] += c * s_B[w][dd][x];
+            }
+          }
+          __syncwarp();
         }
         __syncwarp();
         int done_n = 0;
@@ -1471,8 +1499,8 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : 4) k_num_large_atomic(LargeA
       for (int qq = 0; qq < QN; ++qq)
 #pragma unroll
         for (int x = 0; x < 9; ++x) acc[qq][x] += __shfl_xor_sync(FULL_MASK, acc[qq][x], o);
-    if (gq == 0) {
-      const int cpa = colpos(lower_bound_dev<int32_t>(lst, U, a), first12);
+    const int cpa = A.dpos[a];
+    if (gq == 0 && cpa >= 0) {
       const long long rs = A.crp[slot_of(a, p, n3)];
 #pragma unroll
       for (int qq = 0; qq < QN; ++qq)
@@ -2014,8 +2042,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   ProfScope ps_num(h, PROF_ASM_NUMERIC, st_);
   // ---- D. numeric ----
   if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
+  WS(h, dpos, int32_t, "asm_dpos", n_c);
   LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
-         out->val);
+         out->val, dpos);
+  LA.f12 = f12;
+  LA.dpos = dpos;
   // the 12-DoF chunks and the small / mid rows write disjoint blocks -- (large, large) by the
   // chunks, own rows and the mirrored (large, small) blocks by the small rows.  AGIPC_NUM_MODE
   // (experiments): 0 = chunks on the aux stream next to the small rows, 1 = chunks first then
