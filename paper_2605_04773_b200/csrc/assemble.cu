@@ -955,6 +955,69 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
 #define MID_WARPS 4
 #define MID_CAP 1024
 
+// Bitonic sort (ascending) of 32 R 64-bit keys held lane-major in registers: key i = lane R + r.
+// Partner distances j < R stay inside a lane (compile-time register pairs), j >= R are one
+// shuffle with lane ^ (j / R) -- no shared-memory round trips or warp barriers per stage.
+template <int R>
+__device__ __forceinline__ void warp_reg_bitonic(long long (&k)[R]) {
+  const int l = lane_id();
+#pragma unroll
+  for (int kq = 2; kq <= 32 * R; kq <<= 1) {
+#pragma unroll
+    for (int j = kq >> 1; j > 0; j >>= 1) {
+      if (j >= R) {
+        const int lj = j / R;
+        const bool lower = (l & lj) == 0;  // my element is the lower index of its pair
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool up = ((l * R + r) & kq) == 0;
+          const long long o = __shfl_xor_sync(FULL_MASK, k[r], lj);
+          k[r] = (lower == up) ? min(k[r], o) : max(k[r], o);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & j) == 0) {
+            const bool up = ((l * R + r) & kq) == 0;
+            const long long x = k[r], y = k[r | j];
+            const bool sw = (x > y) == up;
+            k[r] = sw ? y : x;
+            k[r | j] = sw ? x : y;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Mid-node symbolic keys ((column << 10) | entry) of T <= 32 R entries, sorted in registers and
+// stored to shared memory (run counting) and to global memory (reused by the numeric pass).
+template <int R>
+__device__ __forceinline__ void mid_keys_sorted(const WarpArgs &A, const ChildTab &tab, int s, int T, long long *key,
+                                                long long *gkeys) {
+  const int l = lane_id();
+  long long k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = l * R + r;
+    k[r] = LLONG_MAX;
+    if (e < T) {
+      int c;
+      long long kk;
+      entry_of(tab, s, e, c, kk);
+      k[r] = ((long long)A.nm[A.col[kk]] << 10) | e;
+    }
+  }
+  warp_reg_bitonic<R>(k);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = l * R + r;
+    key[e] = k[r];
+    if (e < T) gkeys[e] = k[r];
+  }
+  __syncwarp();
+}
+
 template <bool NUMERIC>
 __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
   __shared__ ChildTab s_tab[MID_WARPS];
@@ -1003,6 +1066,11 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
     if (NUMERIC) {  // the symbolic pass left the sorted keys of this node in global memory
       for (int e = l; e < T; e += 32) key[e] = gkeys[e];
       __syncwarp();
+    } else if (T <= 512) {  // register sort (T > 32 here: at least 2 keys per lane)
+      if (T <= 64) mid_keys_sorted<2>(A, tab, s, T, key, gkeys);
+      else if (T <= 128) mid_keys_sorted<4>(A, tab, s, T, key, gkeys);
+      else if (T <= 256) mid_keys_sorted<8>(A, tab, s, T, key, gkeys);
+      else mid_keys_sorted<16>(A, tab, s, T, key, gkeys);
     } else {
     const int P = next_pow2(T);
     for (int e = l; e < P; e += 32) {
