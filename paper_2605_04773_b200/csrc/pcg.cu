@@ -282,6 +282,9 @@ __global__ void k_sell_scalars(int64_t ns_bound, const int64_t *__restrict__ spt
 __host__ __device__ __forceinline__ int tile_off(int e, int l) { return e < 8 ? 64 * (e >> 1) + 2 * l + (e & 1) : 256 + l; }
 
 // warp per slice: block-column tiles (tile_off); padding = zero blocks pointing at the row itself
+#ifndef FILL_PIPE
+#define FILL_PIPE 1
+#endif
 __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, const int64_t *__restrict__ re,
                             const int32_t *__restrict__ col,
                             const double *__restrict__ val, const int64_t *__restrict__ hrp,
@@ -317,6 +320,45 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
     const long long base = sptr[s];
     const int L = (int)((sptr[s + 1] - base) / 32);
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+#if FILL_PIPE
+    // software pipeline: block j + 1 (and its column / x0 entry) is loaded before block j is
+    // stored, so every lane keeps two independent 72-B reads in flight
+    double vn[9];
+    int cn = row;
+    {
+      const bool real = 0 < len;
+      if (real) cn = cs[k0];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) vn[e] = real ? vs[9 * k0 + e] : 0.0;
+    }
+    for (int j = 0; j < L; ++j) {
+      const long long t = base + 32LL * j;
+      const bool real = j < len;
+      const int c = cn;
+      double v[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) v[e] = vn[e];
+      if (j + 1 < L) {
+        const bool rn = j + 1 < len;
+        cn = rn ? cs[k0 + j + 1] : row;
+        const double *src = vs + 9 * (k0 + j + 1);
+#pragma unroll
+        for (int e = 0; e < 9; ++e) vn[e] = rn ? src[e] : 0.0;
+      }
+      scol[t + l] = c;
+      double *dst = sval + 9 * t;  // tile of the block column (see blk_load for the layout)
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp)  // one 16-B store per component pair: 512 B per warp
+        *reinterpret_cast<double2 *>(dst + tile_off(2 * pp, l)) = make_double2(v[2 * pp], v[2 * pp + 1]);
+      dst[tile_off(8, l)] = v[8];
+      if (x0 && real) {
+        const double a0 = x0[3 * (int64_t)c], a1 = x0[3 * (int64_t)c + 1], a2 = x0[3 * (int64_t)c + 2];
+        y0 += v[0] * a0 + v[1] * a1 + v[2] * a2;
+        y1 += v[3] * a0 + v[4] * a1 + v[5] * a2;
+        y2 += v[6] * a0 + v[7] * a1 + v[8] * a2;
+      }
+    }
+#else
     for (int j = 0; j < L; ++j) {
       const long long t = base + 32LL * j;
       const bool real = j < len;
@@ -338,6 +380,7 @@ __global__ void k_sell_fill(const PcgState *st, const int64_t *__restrict__ rb, 
         y2 += v[6] * a0 + v[7] * a1 + v[8] * a2;
       }
     }
+#endif
     if (x0 && v >= 0) {
       qx[3 * (int64_t)v] = y0;
       qx[3 * (int64_t)v + 1] = y1;
@@ -393,20 +436,41 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
   __shared__ double s_red[PCG_WARPS];
   const int w = threadIdx.x >> 5, l = lane_id();
   double rz = 0.0, rr = 0.0, bb = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + w; row < n; row += (int64_t)gridDim.x * PCG_WARPS) {
-    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-    if (!zero_x0 && ax) {  // (A x)_row precomputed from upper storage (k_ax_upper)
-      y0 = ax[3 * row]; y1 = ax[3 * row + 1]; y2 = ax[3 * row + 2];
-    } else if (!zero_x0 && qx) {  // (A x)_row = sum of its virtual rows' parts (k_sell_fill)
-      for (int64_t v = vr_ptr[row] + l; v < vr_ptr[row + 1]; v += 32) {
-        y0 += qx[3 * v];
-        y1 += qx[3 * v + 1];
-        y2 += qx[3 * v + 2];
+  auto finish_row = [&](int64_t row, double y0, double y1, double y2) {
+    if (zero_x0) {
+      x[3 * row] = 0.0; x[3 * row + 1] = 0.0; x[3 * row + 2] = 0.0;
+    }
+    double b0 = b[3 * row], b1 = b[3 * row + 1], b2 = b[3 * row + 2];
+    double r0 = b0 - y0, r1 = b1 - y1, r2 = b2 - y2;
+    double z0, z1, z2;
+    dinv_apply(Dinv + 9 * row, r0, r1, r2, z0, z1, z2);
+    r[3 * row] = r0; r[3 * row + 1] = r1; r[3 * row + 2] = r2;
+    z[3 * row] = z0; z[3 * row + 1] = z1; z[3 * row + 2] = z2;
+    p[3 * row] = 0.0; p[3 * row + 1] = 0.0; p[3 * row + 2] = 0.0;
+    rz += r0 * z0 + r1 * z1 + r2 * z2;
+    rr += r0 * r0 + r1 * r1 + r2 * r2;
+    bb += b0 * b0 + b1 * b1 + b2 * b2;
+  };
+  if (zero_x0 || ax || qx) {  // thread per row: (A x0)_row is 0, precomputed, or the sum of the
+    // row's virtual-row parts (usually one) -- every row independent, no warp reduction
+    const int64_t tstride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += tstride) {
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+      if (!zero_x0 && ax) {  // (A x)_row precomputed from upper storage (k_ax_upper)
+        y0 = ax[3 * row]; y1 = ax[3 * row + 1]; y2 = ax[3 * row + 2];
+      } else if (!zero_x0) {  // (A x)_row = sum of its virtual rows' parts (k_sell_fill)
+        for (int64_t v = vr_ptr[row]; v < vr_ptr[row + 1]; ++v) {
+          y0 += qx[3 * v];
+          y1 += qx[3 * v + 1];
+          y2 += qx[3 * v + 2];
+        }
       }
-      y0 = warp_sum(y0);
-      y1 = warp_sum(y1);
-      y2 = warp_sum(y2);
-    } else if (!zero_x0) {  // (A x)_row, one warp, lane per block (consecutive 72-B blocks)
+      finish_row(row, y0, y1, y2);
+    }
+  } else {
+    for (int64_t row = (int64_t)blockIdx.x * PCG_WARPS + w; row < n; row += (int64_t)gridDim.x * PCG_WARPS) {
+      // (A x)_row, one warp, lane per block (consecutive 72-B blocks)
+      double y0 = 0.0, y1 = 0.0, y2 = 0.0;
       for (int64_t k = rp[row] + l; k < rp[row + 1]; k += 32) {
         const double *B = val + 9 * k;
         const int64_t c = 3 * (int64_t)col[k];
@@ -418,21 +482,7 @@ __global__ void __launch_bounds__(PCG_THREADS) k_init(int64_t n, const int64_t *
       y0 = warp_sum(y0);
       y1 = warp_sum(y1);
       y2 = warp_sum(y2);
-    }
-    if (l == 0) {
-      if (zero_x0) {
-        x[3 * row] = 0.0; x[3 * row + 1] = 0.0; x[3 * row + 2] = 0.0;
-      }
-      double b0 = b[3 * row], b1 = b[3 * row + 1], b2 = b[3 * row + 2];
-      double r0 = b0 - y0, r1 = b1 - y1, r2 = b2 - y2;
-      double z0, z1, z2;
-      dinv_apply(Dinv + 9 * row, r0, r1, r2, z0, z1, z2);
-      r[3 * row] = r0; r[3 * row + 1] = r1; r[3 * row + 2] = r2;
-      z[3 * row] = z0; z[3 * row + 1] = z1; z[3 * row + 2] = z2;
-      p[3 * row] = 0.0; p[3 * row + 1] = 0.0; p[3 * row + 2] = 0.0;
-      rz += r0 * z0 + r1 * z1 + r2 * z2;
-      rr += r0 * r0 + r1 * r1 + r2 * r2;
-      bb += b0 * b0 + b1 * b1 + b2 * b2;
+      if (l == 0) finish_row(row, y0, y1, y2);
     }
   }
   const int G = gridDim.x;
