@@ -1402,42 +1402,53 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
     const int first12 = A.f12[a];
-    double acc[QN][9];
-#pragma unroll
-    for (int q = 0; q < QN; ++q)
-#pragma unroll
-      for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
+    const int cpa = A.dpos[a];
     for (int base = 0; base < T; base += LSTAGE_A) {
       const int n = min(LSTAGE_A, T - base);
       int cnt = 0, icnt = 0;
-      // software pipeline: the column of the next batch is loaded while this batch's column
-      // aggregate, class and X_bar (all independent of each other) are in flight
-      int c_nx = 0, j_nx = 0;
-      long long k_nx = 0;
+      // two-stage software pipeline: while the entries e0 + l are classified, the column
+      // aggregate / class / X_bar of e0 + 32 + l and the column of e0 + 64 + l are in flight
+      int c1 = 0, j1 = 0;
+      long long k1 = 0;
+      int c0 = 0, j0 = 0, b0v = -1;
+      long long k0 = 0;
+      bool sm0 = true;
+      double x0a = 0.0, x0b = 0.0, x0c = 0.0;
       if (l < n) {
-        entry_of(tab, s, base + l, c_nx, k_nx);
-        j_nx = A.col[k_nx];
+        entry_of(tab, s, base + l, c0, k0);
+        j0 = A.col[k0];
+      }
+      if (32 + l < n) {
+        entry_of(tab, s, base + 32 + l, c1, k1);
+        j1 = A.col[k1];
+      }
+      if (l < n) {
+        b0v = A.nm[j0];
+        sm0 = A.fcls[j0];
+        x0a = __ldg(A.X + 3 * (int64_t)j0);
+        x0b = __ldg(A.X + 3 * (int64_t)j0 + 1);
+        x0c = __ldg(A.X + 3 * (int64_t)j0 + 2);
       }
       for (int e0 = 0; e0 < n; e0 += 32) {
         const bool valid = e0 + l < n;
-        bool diag = false;
-        const long long k = k_nx;
-        const int c = c_nx, j = j_nx;
-        int b = -1;
-        bool small_col = true;
-        double xj0 = 0.0, xj1 = 0.0, xj2 = 0.0;
-        if (valid) {
-          b = A.nm[j];
-          small_col = A.fcls[j];
-          xj0 = __ldg(A.X + 3 * (int64_t)j);
-          xj1 = __ldg(A.X + 3 * (int64_t)j + 1);
-          xj2 = __ldg(A.X + 3 * (int64_t)j + 2);
+        const long long k = k0;
+        const int c = c0, b = valid ? b0v : -1;
+        const bool small_col = valid ? sm0 : true;
+        const double xj0 = x0a, xj1 = x0b, xj2 = x0c;
+        if (e0 + 32 + l < n) {  // stage 1 -> stage 0
+          b0v = A.nm[j1];
+          sm0 = A.fcls[j1];
+          x0a = __ldg(A.X + 3 * (int64_t)j1);
+          x0b = __ldg(A.X + 3 * (int64_t)j1 + 1);
+          x0c = __ldg(A.X + 3 * (int64_t)j1 + 2);
         }
-        if (e0 + 32 + l < n) {
-          entry_of(tab, s, base + e0 + 32 + l, c_nx, k_nx);
-          j_nx = A.col[k_nx];
+        c0 = c1;
+        k0 = k1;
+        if (e0 + 64 + l < n) {  // new stage 1
+          entry_of(tab, s, base + e0 + 64 + l, c1, k1);
+          j1 = A.col[k1];
         }
-        diag = valid && b == a;
+        const bool diag = valid && b == a;
         const unsigned m = __ballot_sync(FULL_MASK, diag);
         if (diag) {
           const int pos = cnt + __popc(m & ((1u << l) - 1u));
@@ -1458,6 +1469,11 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
         }
         icnt += __popc(mi);
       }
+      double acc[QN][9];
+#pragma unroll
+      for (int q = 0; q < QN; ++q)
+#pragma unroll
+        for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
       __syncwarp();
       // phase 2: every lane stages one diagonal block (32 independent 72-B loads in flight per
       // warp), then lane (group, p, q half) accumulates the staged blocks d = gq, gq + G, ...
@@ -1483,6 +1499,21 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
         __syncwarp();
       }
       __syncwarp();
+      if (cnt > 0) {  // reduce over the block groups (lanes with the same p, q half), flush the batch's part
+#pragma unroll
+        for (int o = LPB; o < 32; o <<= 1)
+#pragma unroll
+          for (int qq = 0; qq < QN; ++qq)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) acc[qq][x] += __shfl_xor_sync(FULL_MASK, acc[qq][x], o);
+        if (gq == 0 && cpa >= 0) {
+          const long long rs = A.crp[slot_of(a, p, n3)];
+#pragma unroll
+          for (int qq = 0; qq < QN; ++qq)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q0 + qq) + x, acc[qq][x]);
+        }
+      }
       // interface entries [LSTAGE_A - icnt, LSTAGE_A): one pass per distinct column aggregate b0,
       // lanes (block group, p, q half) accumulate its entries, one set of atomics per (a, b0)
       const int i0 = LSTAGE_A - icnt;
@@ -1559,21 +1590,6 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
             }
         }
       }
-    }
-    // reduce over the block groups (lanes with the same p, q half) and flush the diagonal block
-#pragma unroll
-    for (int o = LPB; o < 32; o <<= 1)
-#pragma unroll
-      for (int qq = 0; qq < QN; ++qq)
-#pragma unroll
-        for (int x = 0; x < 9; ++x) acc[qq][x] += __shfl_xor_sync(FULL_MASK, acc[qq][x], o);
-    const int cpa = A.dpos[a];
-    if (gq == 0 && cpa >= 0) {
-      const long long rs = A.crp[slot_of(a, p, n3)];
-#pragma unroll
-      for (int qq = 0; qq < QN; ++qq)
-#pragma unroll
-        for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q0 + qq) + x, acc[qq][x]);
     }
     if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
       for (int pp = 0; pp < NCB; ++pp) {
