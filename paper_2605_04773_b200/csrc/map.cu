@@ -352,15 +352,29 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // occupancy query before launch): a monotone arrival counter, barrier i completes when it reaches
 // (i + 1) * gridDim.x.  Lets k_tail go out as an ordinary launch (the host-side cost of
 // cudaLaunchCooperativeKernel is paid while the GPU waits, once per Newton step).
+#ifndef TAIL_BAR_ACQREL
+#define TAIL_BAR_ACQREL 1
+#endif
 __device__ __forceinline__ void sw_grid_sync(unsigned *bar, unsigned &epoch) {
   __syncthreads();
   epoch += 1;
   if (threadIdx.x == 0) {
     const unsigned target = epoch * gridDim.x;
+#if TAIL_BAR_ACQREL
+    // release-add of the arrival (orders this CTA's writes, made visible to thread 0 by the
+    // __syncthreads above, before it), acquire-load spin (orders every later read after the
+    // other CTAs' releases): no full fences
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+#else
     __threadfence();
     atomicAdd(bar, 1u);
     while (*(volatile unsigned *)bar < target) __nanosleep(32);
     __threadfence();
+#endif
   }
   __syncthreads();
 }
