@@ -44,6 +44,8 @@ struct AsmScal {
   long long n_tasks;     // large-row chunks
   int err_map;           // map value outside [0, n_c)
   int err_overflow;      // a buffer capacity was exceeded
+  int err_cap;           // the numeric pass must not write: an error above, a slot count past
+                         // int32 or outputs larger than the caller's capacity (k_final_scalars)
 };
 
 __device__ __forceinline__ int slot_of(int c, int p, long long n3) {
@@ -648,10 +650,21 @@ __global__ void k_slot_rowlen(int64_t n_c, const AsmScal *sc, const int32_t *__r
 }
 
 __global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr, const int64_t *__restrict__ task_ptr,
-                                int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound) {
+                                int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound,
+                                int64_t cap_slots, int64_t cap_nnzb) {
   sc->nnzb = row_ptr[sc->n_slots];
   sc->n_tasks = task_ptr[n_c];
   sc->rec_total = rec_off[task_bound];
+  sc->err_cap = sc->err_map || sc->err_overflow || sc->n_slots >= INT32_MAX || sc->n_slots > cap_slots ||
+                sc->nnzb > cap_nnzb;
+}
+
+// out row pointer = the slot row pointer (n_slots + 1 entries; nothing if the outputs do not fit)
+__global__ void k_copy_rowptr(const AsmScal *sc, const int64_t *__restrict__ src, int64_t *__restrict__ dst) {
+  if (sc->err_cap) return;
+  const long long n = sc->n_slots + 1;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------------------------
@@ -694,6 +707,11 @@ __device__ __forceinline__ double seg_sum(double v) {
 
 struct WarpArgs {
   int64_t n_w;
+  // list sizes on the device (no host round trip after the classification): n16 = cnt16[0],
+  // n32 = cnt32[0], nmid = cntmid[0]; kind 0 / 1 / 2 = this kernel's list (16-entry, 32-entry,
+  // mid); n_w, mir_base and the 32-entry key offset are derived from them (warp_args_resolve)
+  const int64_t *cnt16, *cnt32, *cntmid;
+  int kind;
   long long *msrc;             // small nodes: (fine block << 5 | child index) per sorted key
   long long *mkeys;            // mid nodes: sorted (column, entry) keys, written by the symbolic
   const int64_t *e_off;        //   pass at e_off[wi], reused by the numeric pass (no second sort)
@@ -726,8 +744,27 @@ struct WarpArgs {
   double *g_c;
 };
 
+__device__ __forceinline__ void warp_args_resolve(WarpArgs &A) {
+  if (!A.cnt16) return;
+  const long long n16 = *A.cnt16, n32 = *A.cnt32;
+  if (A.kind == 0) {
+    A.n_w = n16;
+    A.mir_base = 0;
+  } else if (A.kind == 1) {
+    A.n_w = n32;
+    A.mir_base = 16 * n16;
+    A.mkeys += 16 * n16;
+    A.msrc += 16 * n16;
+  } else {
+    A.n_w = *A.cntmid;
+    A.mir_base = 16 * n16 + 32 * n32;
+  }
+}
+
 template <int SEG, bool NUMERIC>
 __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
+  if (NUMERIC && A.sc->err_cap) return;  // outputs do not fit / bad input: write nothing
+  warp_args_resolve(A);
   constexpr int NSEG = 32 / SEG;
   __shared__ ChildTab s_tab[NUMERIC ? 1 : 8 * NSEG];
   // numeric: per-lane parked block B_ij (9), X_bar of its row child (3) and of its column node (3)
@@ -1020,6 +1057,8 @@ __device__ __forceinline__ void mid_keys_sorted(const WarpArgs &A, const ChildTa
 
 template <bool NUMERIC>
 __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
+  if (NUMERIC && A.sc->err_cap) return;
+  warp_args_resolve(A);
   __shared__ ChildTab s_tab[MID_WARPS];
   __shared__ long long s_key[MID_WARPS][MID_CAP];
   __shared__ double s_carry[MID_WARPS][4][9];  // partial sums of a run continuing into the next window
@@ -1288,6 +1327,7 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
                                   const int32_t *__restrict__ nb_cnt, const int32_t *__restrict__ rowlen,
                                   const int64_t *__restrict__ crp, int32_t *__restrict__ ccol, double *__restrict__ cval,
                                   int32_t *__restrict__ dpos) {
+  if (sc->err_cap) return;  // outputs do not fit / bad input: write nothing
   const int w = threadIdx.x >> 5, l = lane_id();
   const int wpb = blockDim.x >> 5;
   const long long n3 = sc->n3;
@@ -1348,6 +1388,7 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 
 template <int NCB, int NB>
 __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atomic(LargeArgs A) {
+  if (A.sc->err_cap || (NCB == 1 && A.sc->n_large3 == 0)) return;
   __shared__ ChildTab s_tab[4];
   __shared__ long long s_k[4][LSTAGE_A];
   __shared__ int s_i[4][LSTAGE_A];     // child slot c of the entry's row (weights in s_wc)
@@ -1677,6 +1718,7 @@ __device__ __forceinline__ void itf_flush(LargeArgs &A, int w, int l, int icnt, 
 
 template <int NCB>
 __global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
+  if (A.sc->err_cap) return;
   __shared__ ChildTab s_tab[4];
   __shared__ int s_ce[4][LSTAGE];     // diagonal entries: (child c << 16) | entry offset in its row
   __shared__ int s_j[4][LSTAGE];      //   column node j (w_j = X_bar_j)
@@ -1824,6 +1866,7 @@ __global__ void __launch_bounds__(128, 6) k_num_large(LargeArgs A) {
 // of its records in record order -- every coarse value is written once, no read-modify-write.
 #define RED_REC 256  // records of one node handled in shared memory (more: a second pass)
 __global__ void __launch_bounds__(128) k_large_reduce(LargeArgs A, const int32_t *__restrict__ f12) {
+  if (A.sc->err_cap) return;
   __shared__ int s_rb[RED_REC];
   __shared__ int s_first[RED_REC];  // record index of the first record of each distinct b0
   __shared__ int s_cp[RED_REC];     // column position of that b0 in row a
@@ -1915,6 +1958,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (N == 0) return AGIPC_OK;
   if (!map || !mesh->x_rest || !H->row_ptr || !H->col || !H->val || !out->new_map)
     return set_err(h, AGIPC_EINVAL, "assemble_coarse: null pointer");
+  if (out->cap_slots < 0 || out->cap_nnzb < 0 || (out->cap_slots > 0 && !out->row_ptr) ||
+      (out->cap_nnzb > 0 && (!out->col || !out->val)))
+    return set_err(h, AGIPC_EINVAL, "assemble_coarse: null output arrays");
   CU_TRY(h, cudaSetDevice(h->device));
   ProfScope prof_scope(h, PROF_ASSEMBLE, h->stream);
   cudaStream_t st_ = h->stream;
@@ -1992,16 +2038,14 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f16, n_c, i16)) != AGIPC_OK) return st;
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f32, n_c, i32)) != AGIPC_OK) return st;
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, small_i32, n_c, sidx)) != AGIPC_OK) return st;
+  CU_TRY(h, cudaMemsetAsync(ecount, 0, sizeof(int64_t) * n_c, st_));
   LAUNCH(h, k_small_lists, gC, 256, 0, n_c, f16, f32, small_i32, i16, i32, sidx, rowsum, w16, w32, small_list, ecount);
   AsmScal *hsc = (AsmScal *)pinned_get(h, sizeof(AsmScal) + 64, &st);
   if (st != AGIPC_OK) return st;
-  long long *h_small = (long long *)(hsc + 1);
-  CU_TRY(h, cudaMemcpyAsync(h_small, sidx + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
-  CU_TRY(h, cudaMemcpyAsync(h_small + 1, i16 + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
-  CU_TRY(h, cudaMemcpyAsync(h_small + 2, i32 + n_c, sizeof(long long), cudaMemcpyDeviceToHost, st_));
-  CU_TRY(h, cudaStreamSynchronize(st_));
-  const int64_t n_small = h_small[0], n_w16 = h_small[1], n_w32 = h_small[2];
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I64, ecount, n_small, e_off)) != AGIPC_OK) return st;
+  // the list sizes stay on the device (i16[n_c], i32[n_c], sidx[n_c]): the symbolic and numeric
+  // kernels read them (warp_args_resolve); buffers and grids use the bound n_c.  ecount is zero
+  // past the mid list, so its scan over n_c entries is exact on the first n_small + 1.
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_I64, ecount, n_c, e_off)) != AGIPC_OK) return st;
 
   ps_classify.reset();
   std::unique_ptr<ProfScope> ps_sym(new ProfScope(h, PROF_ASM_SYMBOLIC, st_));
@@ -2024,49 +2068,49 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemsetAsync(recmax, 0, sizeof(int32_t) * (task_bound + 1), st_));
   const double *gfp = (g_fine && out->g_c) ? g_fine : nullptr;
   WarpArgs WA;
-  WA.n_w = n_w16; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
+  WA.n_w = 0; WA.wlist = w16; WA.child_list = child_list; WA.child_ptr = child_ptr; WA.size_new = size_new;
   WA.is_small = is_small; WA.rp = H->row_ptr; WA.col = H->col; WA.val = H->val; WA.nm = out->new_map;
   WA.X = mesh->x_rest; WA.g_f = gfp; WA.sc = sc; WA.rowlen = rowlen; WA.pairs = pairs; WA.pair_cap = pair_cap;
   WA.porig = porig; WA.mirpos = nullptr; WA.mirrl = nullptr; WA.mir_base = 0;
   WA.scw = sc; WA.gbuf = gbuf; WA.nb_off = nb_off; WA.nb_cnt = nb_cnt; WA.crp = nullptr; WA.ccol = nullptr;
   WA.cval = nullptr; WA.g_c = out->g_c;
   WA.mkeys = nullptr; WA.e_off = nullptr; WA.msrc = nullptr;
+  WA.cnt16 = i16 + n_c; WA.cnt32 = i32 + n_c; WA.cntmid = sidx + n_c; WA.kind = 0;
   WarpArgs WB = WA, WM;
-  WB.n_w = n_w32; WB.wlist = w32;
-  // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys
-  const long long mir_mid = 16 * n_w16 + 32 * n_w32;
-  WS(h, mirpos, long long, "asm_mirror_pos", mir_mid + nnzb_f + 1);
-  WS(h, mirrl, int32_t, "asm_mirror_rl", mir_mid + nnzb_f + 1);
+  WB.wlist = w32; WB.kind = 1;
+  // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys (the
+  // list sizes are on the device: buffers use 16 n_w16 + 32 n_w32 <= 32 n_c)
+  WS(h, mirpos, long long, "asm_mirror_pos", 32 * n_c + nnzb_f + 1);
+  WS(h, mirrl, int32_t, "asm_mirror_rl", 32 * n_c + nnzb_f + 1);
   {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
-    WS(h, skeys, long long, "asm_small_keys", 16 * n_w16 + 32 * n_w32 + 1);
-    WS(h, ssrc, long long, "asm_small_src", 16 * n_w16 + 32 * n_w32 + 1);
+    WS(h, skeys, long long, "asm_small_keys", 32 * n_c + 1);
+    WS(h, ssrc, long long, "asm_small_src", 32 * n_c + 1);
     WA.mkeys = skeys;
-    WB.mkeys = skeys + 16 * n_w16;
+    WB.mkeys = skeys;  // + 16 n_w16 (warp_args_resolve)
     WA.msrc = ssrc;
-    WB.msrc = ssrc + 16 * n_w16;
+    WB.msrc = ssrc;
     WA.mirpos = mirpos;
     WA.mirrl = mirrl;
     WB.mirpos = mirpos;
     WB.mirrl = mirrl;
-    WB.mir_base = 16 * n_w16;
   }
-  const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w16, 16), 32 * h->sm_count));
-  const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_w32, 8), 32 * h->sm_count));
+  // grid-stride kernels; the 32-entry list is usually short or empty (persistent grid)
+  const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, 16), 32 * h->sm_count));
+  const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, 8), 4 * h->sm_count));
   // the large-row symbolic pass runs on the aux stream next to the small / mid rows' (both
   // latency-bound at partial occupancy; they only share the atomic pair counter)
   if ((st = aux_fork(h)) != AGIPC_OK) return st;
-  if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
-  if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
+  LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
+  LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
   WM = WA;
-  WM.n_w = n_small; WM.wlist = small_list;
+  WM.wlist = small_list; WM.kind = 2;
   {  // mid-node entries: sum of their candidate entries <= the fine blocks
     WS(h, mkeys, long long, "asm_mid_keys", nnzb_f + 1);
     WM.mkeys = mkeys;
     WM.e_off = e_off;
-    WM.mir_base = mir_mid;
   }
-  const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_small, MID_WARPS), 32 * h->sm_count));
-  if (n_small > 0) LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
+  const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, MID_WARPS), 12 * h->sm_count));
+  LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
@@ -2097,10 +2141,16 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_slot_rowlen, gC, 256, 0, n_c, sc, rowlen, rl);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, rl, slot_bound, crp_ws)) != AGIPC_OK) return st;
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, recmax, task_bound, rec_off)) != AGIPC_OK) return st;
-  LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound);
+  LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound,
+         out->cap_slots, out->cap_nnzb);
   LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, (const AsmScal *)sc, pair_cap, (const int2 *)pairs,
          (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
          (const int32_t *)f12, (const int32_t *)rowlen, (const int64_t *)crp_ws, mirpos, mirrl);
+  // one host round trip per call, here: the sizes and error flags come back while the numeric
+  // pass is still to be enqueued (it then runs asynchronously to the caller); the capacity check
+  // is also on the device (k_final_scalars sets err_cap: every numeric kernel writes nothing)
+  LAUNCH(h, k_copy_rowptr, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(slot_bound + 1, 256), 4 * h->sm_count)),
+         256, 0, (const AsmScal *)sc, (const int64_t *)crp_ws, out->row_ptr);
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
   CU_TRY(h, cudaStreamSynchronize(st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
@@ -2113,9 +2163,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if (out->cap_slots < out->n_slots || out->cap_nnzb < out->nnzb)
     return set_err(h, AGIPC_ENOSPACE, "assemble_coarse: need %lld slots / %lld blocks", (long long)out->n_slots,
                    (long long)out->nnzb);
-  if (!out->row_ptr || (out->nnzb > 0 && (!out->col || !out->val)))
-    return set_err(h, AGIPC_EINVAL, "assemble_coarse: null output arrays");
-  CU_TRY(h, cudaMemcpyAsync(out->row_ptr, crp_ws, sizeof(int64_t) * (out->n_slots + 1), cudaMemcpyDeviceToDevice, st_));
 
   ps_sym.reset();
   if (h->values_event) {  // H_fine / g_fine values uploaded on another stream (one-shot)
@@ -2164,12 +2211,12 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   };
   if (num_mode == 1 && (st = launch_large()) != AGIPC_OK) return st;
   WM.crp = out->row_ptr; WM.ccol = out->col; WM.cval = out->val;
-  if (n_small > 0) LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
+  LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
   WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
   WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
   // (5 CTAs/SM at 48 registers measured slower: 1.35 vs 1.26 ms numeric at C3, profiles/r02k)
-  if (n_w16 > 0) LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
-  if (n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
+  LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
+  LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   if (num_mode != 1 && (st = launch_large()) != AGIPC_OK) return st;
   return fork ? aux_join(h) : AGIPC_OK;
 }
