@@ -283,3 +283,22 @@ agipc_status scan_exclusive_i64(agipc_handle h, int kind, const void *src, int64
 // kinds of source for scan_exclusive_i64: value(i) = mul * src[i] + add  (int32 or int64 source)
 #define SCAN_SRC_I32 0
 #define SCAN_SRC_I64 1
+#define SCAN_SRC_GT 2      // int32 src[i] > add ? 1 : 0
+#define SCAN_SRC_POW2 3    // int32 src[i] > 0 ? next power of two : 0
+#define SCAN_SRC_SLOTRL 4  // slot i < *dev_nslots: int32 src[node of slot i] (12-DoF nodes: 4 slots)
+#define SCAN_MAX_JOBS 4
+struct ScanJob {
+  const void *src;
+  const long long *dev_n3, *dev_nslots;  // SCAN_SRC_SLOTRL
+  int64_t n, mul, add;
+  int64_t *out;
+  int kind;
+  int tile0;  // set by scan_multi
+};
+struct ScanJobs {
+  ScanJob j[SCAN_MAX_JOBS];
+  int njobs;
+};
+ScanJob scan_job(int kind, const void *src, int64_t n, int64_t *out, int64_t mul = 1, int64_t add = 0);
+// up to SCAN_MAX_JOBS independent exclusive scans in one launch (out[k][n_k] = total)
+agipc_status scan_multi(agipc_handle h, ScanJobs jobs);

@@ -353,22 +353,47 @@ int agipc_profile_read(agipc_handle h, agipc_profile_entry *out, int cap) {
 #define SCAN_ITEMS 8
 #define SCAN_TILE (SCAN_THREADS * SCAN_ITEMS)
 
-template <typename TS>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(const TS *__restrict__ src, int64_t n, int64_t mul,
-                                                        int64_t add, int64_t *__restrict__ out,
-                                                        unsigned long long *status, int *counter) {
+// Several independent scans in ONE launch (scan_multi): tiles are claimed from one counter in
+// job order, so every predecessor tile of a job belongs to a resident CTA; each job has its own
+// look-back status region.  The item value is a functor of the job's kind (SCAN_SRC_*).
+__device__ __forceinline__ long long scan_item(const ScanJob &J, int64_t i, long long n3, long long nslots) {
+  switch (J.kind) {
+    case SCAN_SRC_I32: return (long long)(J.mul * (int64_t)((const int32_t *)J.src)[i] + J.add);
+    case SCAN_SRC_I64: return (long long)(J.mul * ((const int64_t *)J.src)[i] + J.add);
+    case SCAN_SRC_GT: return ((const int32_t *)J.src)[i] > J.add ? 1 : 0;
+    case SCAN_SRC_POW2: {
+      const int x = ((const int32_t *)J.src)[i];
+      return x > 0 ? (1ll << (32 - __clz(x - 1))) : 0;  // next power of two (1 -> 1)
+    }
+    default: {  // SCAN_SRC_SLOTRL: row length of slot i (a 12-DoF node's 4 slots share its row)
+      if (i >= nslots) return 0;
+      const long long c = i < n3 ? i : n3 + (i - n3) / 4;
+      return ((const int32_t *)J.src)[c];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_multi(ScanJobs Jobs, unsigned long long *status, int *counter) {
   __shared__ int s_tile;
   __shared__ long long s_warp[SCAN_THREADS / 32];
   __shared__ long long s_prefix;
   __shared__ long long s_items[SCAN_TILE];
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
   __syncthreads();
-  const int tile = s_tile;
+  int jb = 0;
+  while (jb + 1 < Jobs.njobs && s_tile >= Jobs.j[jb + 1].tile0) ++jb;
+  const ScanJob &J = Jobs.j[jb];
+  const int tile = s_tile - J.tile0;
+  long long n3 = 0, nslots = 0;
+  if (J.kind == SCAN_SRC_SLOTRL) {
+    n3 = *J.dev_n3;
+    nslots = *J.dev_nslots;
+  }
+  const int64_t n = J.n;
   const int64_t base = (int64_t)tile * SCAN_TILE;
-  // striped coalesced load into shared memory
-  for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_THREADS) {
+  for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_THREADS) {  // striped coalesced load
     int64_t i = base + k;
-    s_items[k] = i < n ? (long long)(mul * (int64_t)src[i] + add) : 0;
+    s_items[k] = i < n ? scan_item(J, i, n3, nslots) : 0;
   }
   __syncthreads();
   long long v[SCAN_ITEMS];
@@ -387,7 +412,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const TS *__restrict__ sr
     long long wi = warp_incl_scan(ws);
     long long agg = __shfl_sync(FULL_MASK, wi, SCAN_THREADS / 32 - 1);
     if (l < SCAN_THREADS / 32) s_warp[l] = wi - ws;  // exclusive warp offsets
-    long long pfx = lb_exclusive(status, tile, agg);
+    long long pfx = lb_exclusive(status + J.tile0, tile, agg);
     if (l == 0) s_prefix = pfx;
   }
   __syncthreads();
@@ -398,24 +423,48 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(const TS *__restrict__ sr
     run += v[k];
   }
   __syncthreads();
+  int64_t *out = J.out;
   for (int k = threadIdx.x; k < SCAN_TILE; k += SCAN_THREADS) {
     int64_t i = base + k;
-    if (i < n) out[i] = s_items[k];
-    if (i == n) out[n] = s_items[k];  // exclusive value at n == total
+    if (i <= n) out[i] = s_items[k];  // out[n] (the total) is the exclusive value at n
   }
+}
+
+agipc_status scan_multi(agipc_handle h, ScanJobs jobs) {
+  if (jobs.njobs < 1 || jobs.njobs > SCAN_MAX_JOBS) return set_err(h, AGIPC_EINVAL, "scan_multi: bad job count");
+  int64_t tiles = 0;
+  for (int k = 0; k < jobs.njobs; ++k) {
+    if (jobs.j[k].n < 0) return set_err(h, AGIPC_EINVAL, "scan of negative size");
+    // one extra item so that out[n] (the total) is produced by the tile containing index n
+    const int64_t t = cdiv(jobs.j[k].n + 1, SCAN_TILE);
+    if (tiles + t >= INT32_MAX) return set_err(h, AGIPC_ERANGE, "scan too large");
+    jobs.j[k].tile0 = (int)tiles;
+    tiles += t;
+  }
+  WS(h, status, unsigned long long, "scan_status", tiles + 1);
+  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), h->stream));
+  int *counter = (int *)(status + tiles);
+  LAUNCH(h, k_scan_multi, (unsigned)tiles, SCAN_THREADS, 0, jobs, status, counter);
+  return AGIPC_OK;
+}
+
+ScanJob scan_job(int kind, const void *src, int64_t n, int64_t *out, int64_t mul, int64_t add) {
+  ScanJob J;
+  memset(&J, 0, sizeof(J));
+  J.kind = kind;
+  J.src = src;
+  J.n = n;
+  J.out = out;
+  J.mul = mul;
+  J.add = add;
+  return J;
 }
 
 agipc_status scan_exclusive_i64(agipc_handle h, int kind, const void *src, int64_t n, int64_t *out,
                                 int64_t mul, int64_t add) {
-  if (n < 0) return set_err(h, AGIPC_EINVAL, "scan of negative size");
-  // one extra item so that out[n] (the total) is produced by the tile containing index n
-  int64_t tiles = cdiv(n + 1, SCAN_TILE);
-  WS(h, status, unsigned long long, "scan_status", tiles + 1);
-  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), h->stream));
-  int *counter = (int *)(status + tiles);
-  if (kind == SCAN_SRC_I32)
-    LAUNCH(h, k_scan<int32_t>, (int)tiles, SCAN_THREADS, 0, (const int32_t *)src, n, mul, add, out, status, counter);
-  else
-    LAUNCH(h, k_scan<int64_t>, (int)tiles, SCAN_THREADS, 0, (const int64_t *)src, n, mul, add, out, status, counter);
-  return AGIPC_OK;
+  ScanJobs jobs;
+  memset(&jobs, 0, sizeof(jobs));
+  jobs.njobs = 1;
+  jobs.j[0] = scan_job(kind, src, n, out, mul, add);
+  return scan_multi(h, jobs);
 }

@@ -85,13 +85,8 @@ __global__ void k_size_hist(int64_t N, const int32_t *__restrict__ map, int64_t 
   if (key >= 0 && (__ffs(peers) - 1) == lane_id()) atomicAdd(size + key, __popc(peers));
 }
 
-__global__ void k_is12(int64_t n_c, const int32_t *__restrict__ size, int64_t thr, int32_t *__restrict__ is12) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_c) is12[c] = (int64_t)size[c] > thr;  // "exceeds 32", strict
-}
-
 // stable partition: 3-DoF nodes keep ascending order first, then 12-DoF (Alg S3 l.10-13)
-__global__ void k_newid(int64_t n_c, const int64_t *__restrict__ ex12, const int32_t *__restrict__ is12,
+__global__ void k_newid(int64_t n_c, const int64_t *__restrict__ ex12, int64_t thr,
                         const int32_t *__restrict__ size, int32_t *__restrict__ newid,
                         int32_t *__restrict__ size_new, AsmScal *sc) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -103,7 +98,7 @@ __global__ void k_newid(int64_t n_c, const int64_t *__restrict__ ex12, const int
     sc->n_slots = n3 + 4 * n12;
   }
   if (c < n_c) {
-    long long id = is12[c] ? n3 + ex12[c] : c - ex12[c];
+    long long id = (int64_t)size[c] > thr ? n3 + ex12[c] : c - ex12[c];  // is12 (k_is12 semantics)
     newid[c] = (int32_t)id;
     size_new[id] = size[c];
   }
@@ -185,13 +180,20 @@ __global__ void k_children(int64_t N, const int32_t *__restrict__ nm, const int6
 
 __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
                            const unsigned long long *__restrict__ rowsum, uint8_t *__restrict__ is_small,
-                           int32_t *__restrict__ ntasks, AsmScal *sc) {
+                           int32_t *__restrict__ ntasks, AsmScal *sc, int32_t *__restrict__ f16,
+                           int32_t *__restrict__ f32, int32_t *__restrict__ ft, int64_t *__restrict__ ecount) {
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < n_c) {
-    bool s = size_new[c] <= SMALL_CHILDREN && rowsum[c] <= SMALL_T;
+    const unsigned long long rs = rowsum[c];
+    bool s = size_new[c] <= SMALL_CHILDREN && rs <= SMALL_T;
     is_small[c] = s;
     ntasks[c] = s ? 0 : (int32_t)((size_new[c] + LARGE_CHUNK - 1) / LARGE_CHUNK);
     if (!s && c < sc->n3) atomicAdd((unsigned long long *)&sc->n_large3, 1ull);
+    // small nodes: the 16- / 32-entry warp lists and the mid list (k_small_flags semantics)
+    f16[c] = s && rs <= 16;
+    f32[c] = s && rs > 16 && rs <= 32;
+    ft[c] = s && rs > 32;
+    ecount[c] = 0;  // k_small_lists fills the first n_small (the e_off scan runs over n_c)
   }
 }
 
@@ -520,11 +522,6 @@ __global__ void k_pair_count(const AsmScal *sc, long long cap, const int2 *__res
 }
 
 // padded group sizes: next power of two (so every group can be sorted in place)
-__global__ void k_pow2(int64_t n, const int32_t *__restrict__ cnt, int32_t *__restrict__ out) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n) out[c] = cnt[c] ? next_pow2(cnt[c]) : 0;
-}
-
 __global__ void k_pair_scatter(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
                                unsigned long long *__restrict__ cursor, int32_t *__restrict__ gbuf) {
   const long long np = min(sc->pair_count, cap);
@@ -639,16 +636,6 @@ __global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__res
 // ------------------------------------------------------------------------------------
 // C. slot row lengths
 // ------------------------------------------------------------------------------------
-__global__ void k_slot_rowlen(int64_t n_c, const AsmScal *sc, const int32_t *__restrict__ rowlen,
-                              int32_t *__restrict__ rl) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long n3 = sc->n3;
-  if (c < n_c) {
-    int ncb = ncb_of((int)c, n3);
-    for (int p = 0; p < ncb; ++p) rl[slot_of((int)c, p, n3)] = rowlen[c];
-  }
-}
-
 __global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr, const int64_t *__restrict__ task_ptr,
                                 int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound,
                                 int64_t cap_slots, int64_t cap_nnzb) {
@@ -1286,18 +1273,6 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
 }
 
 // split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
-__global__ void k_small_flags(int64_t n_c, const uint8_t *__restrict__ is_small,
-                              const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ f16,
-                              int32_t *__restrict__ f32, int32_t *__restrict__ ft) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_c) {
-    const bool sm = is_small[c];
-    f16[c] = sm && rowsum[c] <= 16;
-    f32[c] = sm && rowsum[c] > 16 && rowsum[c] <= 32;
-    ft[c] = sm && rowsum[c] > 32;
-  }
-}
-
 __global__ void k_small_lists(int64_t n_c, const int32_t *__restrict__ f16, const int32_t *__restrict__ f32,
                               const int32_t *__restrict__ ft, const int64_t *__restrict__ i16,
                               const int64_t *__restrict__ i32, const int64_t *__restrict__ it,
@@ -1984,7 +1959,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemsetAsync(sc, 0, sizeof(AsmScal), st_));
   // ---- A. classification ----
   WS(h, size, int32_t, "asm_size", n_c);
-  WS(h, is12, int32_t, "asm_is12", n_c);
   WS(h, ex12, int64_t, "asm_ex12", n_c + 1);
   WS(h, newid, int32_t, "asm_newid", n_c);
   WS(h, size_new, int32_t, "asm_size_new", n_c);
@@ -2004,9 +1978,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   CU_TRY(h, cudaMemsetAsync(rowsum, 0, sizeof(unsigned long long) * n_c, st_));
   const unsigned gN = (unsigned)cdiv(N, 256), gC = (unsigned)cdiv(n_c, 256);
   LAUNCH(h, k_size_hist, gN, 256, 0, N, map, n_c, size, sc);
-  LAUNCH(h, k_is12, gC, 256, 0, n_c, size, affine_threshold, is12);
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, is12, n_c, ex12)) != AGIPC_OK) return st;
-  LAUNCH(h, k_newid, gC, 256, 0, n_c, ex12, is12, size, newid, size_new, sc);
+  // ex12 = exclusive count of 12-DoF nodes: the scan evaluates size > threshold itself
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_GT, size, n_c, ex12, 1, affine_threshold)) != AGIPC_OK) return st;
+  LAUNCH(h, k_newid, gC, 256, 0, n_c, ex12, affine_threshold, size, newid, size_new, sc);
   LAUNCH(h, k_new_map, gN, 256, 0, N, n_c, map, newid, out->new_map);
   if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, size_new, n_c, child_ptr)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(cursor, child_ptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
@@ -2020,12 +1994,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
            (const int64_t *)child_ptr, child_list, sscr);
     CU_TRY(h, cudaMemsetAsync(&sc->big_groups, 0, sizeof(long long), st_));  // reused by the symbolic phase
   }
-  LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks, sc);
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, ntasks, n_c, task_ptr)) != AGIPC_OK) return st;
-  WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
-  LAUNCH(h, k_task_node, gC, 256, 0, n_c, (const int64_t *)task_ptr, task_node);
-  WS(h, fcls, uint8_t, "asm_fcls", N);
-  LAUNCH(h, k_fine_class, gN, 256, 0, N, (const int32_t *)out->new_map, (const uint8_t *)is_small, fcls);
   // small nodes: the warp list (<= 32 candidate entries) and the tile list (> 32, with the
   // prefix of their entries)
   WS(h, f16, int32_t, "asm_f16", n_c);
@@ -2034,11 +2002,21 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, i32, int64_t, "asm_i32", n_c + 1);
   WS(h, w16, int32_t, "asm_w16", n_c);
   WS(h, w32, int32_t, "asm_w32", n_c);
-  LAUNCH(h, k_small_flags, gC, 256, 0, n_c, is_small, rowsum, f16, f32, small_i32);
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f16, n_c, i16)) != AGIPC_OK) return st;
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, f32, n_c, i32)) != AGIPC_OK) return st;
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, small_i32, n_c, sidx)) != AGIPC_OK) return st;
-  CU_TRY(h, cudaMemsetAsync(ecount, 0, sizeof(int64_t) * n_c, st_));
+  LAUNCH(h, k_classify, gC, 256, 0, n_c, size_new, rowsum, is_small, ntasks, sc, f16, f32, small_i32, ecount);
+  {  // chunk offsets and the three small-node list positions: one launch
+    ScanJobs jobs;
+    memset(&jobs, 0, sizeof(jobs));
+    jobs.njobs = 4;
+    jobs.j[0] = scan_job(SCAN_SRC_I32, ntasks, n_c, task_ptr);
+    jobs.j[1] = scan_job(SCAN_SRC_I32, f16, n_c, i16);
+    jobs.j[2] = scan_job(SCAN_SRC_I32, f32, n_c, i32);
+    jobs.j[3] = scan_job(SCAN_SRC_I32, small_i32, n_c, sidx);
+    if ((st = scan_multi(h, jobs)) != AGIPC_OK) return st;
+  }
+  WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
+  LAUNCH(h, k_task_node, gC, 256, 0, n_c, (const int64_t *)task_ptr, task_node);
+  WS(h, fcls, uint8_t, "asm_fcls", N);
+  LAUNCH(h, k_fine_class, gN, 256, 0, N, (const int32_t *)out->new_map, (const uint8_t *)is_small, fcls);
   LAUNCH(h, k_small_lists, gC, 256, 0, n_c, f16, f32, small_i32, i16, i32, sidx, rowsum, w16, w32, small_list, ecount);
   AsmScal *hsc = (AsmScal *)pinned_get(h, sizeof(AsmScal) + 64, &st);
   if (st != AGIPC_OK) return st;
@@ -2058,7 +2036,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, porig, long long, "asm_pair_orig", pair_cap);
   WS(h, f12, int32_t, "asm_first12", n_c);
   WS(h, gcnt, int32_t, "asm_gcnt", n_c);
-  WS(h, gpad, int32_t, "asm_gpad", n_c);
   WS(h, gptr, int64_t, "asm_gptr", n_c + 1);
   WS(h, gbuf, int32_t, "asm_gbuf", 2 * pair_cap);
   WS(h, big_list, int32_t, "asm_big_list", n_c);
@@ -2122,8 +2099,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   if ((st = aux_join(h)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
   LAUNCH(h, k_pair_count, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, gcnt);
-  LAUNCH(h, k_pow2, gC, 256, 0, n_c, gcnt, gpad);
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, gpad, n_c, gptr)) != AGIPC_OK) return st;
+  // bucket offsets: power-of-two padded counts (k_group_unique sorts in place), evaluated by the scan
+  if ((st = scan_exclusive_i64(h, SCAN_SRC_POW2, gcnt, n_c, gptr)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(cursor, gptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
   LAUNCH(h, k_pair_scatter, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, cursor, gbuf);
   const unsigned gsym = (unsigned)std::min<int64_t>(cdiv(n_c, SYM_WARPS), 64 * h->sm_count);
@@ -2135,12 +2112,17 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
 
   // ---- C. slot row pointer (upper bound 4 n_c slots; entries past n_slots are 0) ----
   const int64_t slot_bound = 4 * n_c;
-  WS(h, rl, int32_t, "asm_rl", slot_bound);
   WS(h, crp_ws, int64_t, "asm_crp", slot_bound + 1);
-  CU_TRY(h, cudaMemsetAsync(rl, 0, sizeof(int32_t) * slot_bound, st_));
-  LAUNCH(h, k_slot_rowlen, gC, 256, 0, n_c, sc, rowlen, rl);
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, rl, slot_bound, crp_ws)) != AGIPC_OK) return st;
-  if ((st = scan_exclusive_i64(h, SCAN_SRC_I32, recmax, task_bound, rec_off)) != AGIPC_OK) return st;
+  {  // slot row pointer (the scan reads each slot's node row length) and the chunk record offsets
+    ScanJobs jobs;
+    memset(&jobs, 0, sizeof(jobs));
+    jobs.njobs = 2;
+    jobs.j[0] = scan_job(SCAN_SRC_SLOTRL, rowlen, slot_bound, crp_ws);
+    jobs.j[0].dev_n3 = &sc->n3;
+    jobs.j[0].dev_nslots = &sc->n_slots;
+    jobs.j[1] = scan_job(SCAN_SRC_I32, recmax, task_bound, rec_off);
+    if ((st = scan_multi(h, jobs)) != AGIPC_OK) return st;
+  }
   LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound,
          out->cap_slots, out->cap_nnzb);
   LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, (const AsmScal *)sc, pair_cap, (const int2 *)pairs,
