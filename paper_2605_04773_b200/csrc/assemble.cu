@@ -37,6 +37,7 @@
 struct AsmScal {
   long long n3, n12, n_slots, nnzb;
   long long nbs_count;   // entries used in the small-node neighbour buffer
+  long long list_top;    // entries allocated in the large-row entry lists (k_sym_large)
   long long pair_count;  // (large, x) pairs
   long long big_groups;  // large lists that need the CTA sort
   long long n_large3;    // large nodes with 3 DoF (affine threshold > 32)
@@ -426,6 +427,14 @@ struct LargeArgs {
   double *cval;
   double *g_c;
   int32_t *recmax;         // symbolic: interface records a chunk may write (distinct large columns x batches)
+  // large-row entry lists written by k_sym_large, read by k_num_large_list: per chunk t the
+  // diagonal entries (column aggregate == a) at [lbase[t], lbase[t] + lnd[t]) and the large-large
+  // interface entries at [lib[t], lib[t] + lni[t]); per entry (fine block << 5 | child slot) and
+  // the column node j (interface entries also the column aggregate b)
+  long long *lent;
+  int32_t *lj, *lb;
+  long long *lbase, *lib;
+  int32_t *lnd, *lni;
   const int64_t *rec_off;  // numeric: exclusive scan of recmax
   int32_t *rec_b;          // [rec_total] column aggregate of each record (-1: unused)
   double *rec_v;           // [rec_total][144] record values, (p*4+q)*9+x
@@ -472,19 +481,41 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
     if (l == 0) tab.off[0] = 0;
     __syncwarp();
     const int T = __shfl_sync(FULL_MASK, incl_c, 31);
-    int nseen = 0, nitf = 0;
+    int nseen = 0, nitf = 0, ndg = 0;
+    long long lbase = 0;
+    if (A.lent) {  // T list slots for this chunk: diagonal entries from the front, interface from the back
+      if (l == 0) lbase = (long long)atomicAdd((unsigned long long *)&A.scw->list_top, (unsigned long long)T);
+      lbase = __shfl_sync(FULL_MASK, lbase, 0);
+    }
     for (int e0 = 0; e0 < T; e0 += 32) {
       const int e = e0 + l;
       int key = -1;
+      bool dg = false;
+      int c = 0, j = 0;
+      long long k = 0;
       if (e < T) {
-        int c;
-        long long k;
         entry_of(tab, s, e, c, k);
-        const int j = A.col[k];
+        j = A.col[k];
         if (!A.fcls[j]) {
           const int b = A.nm[j];
           if (b != a) key = b;
+          else dg = true;
         }
+      }
+      if (A.lent) {
+        const unsigned md = __ballot_sync(FULL_MASK, dg), mi = __ballot_sync(FULL_MASK, key >= 0);
+        const unsigned below = (1u << l) - 1u;
+        if (dg) {
+          const long long o = lbase + ndg + __popc(md & below);
+          A.lent[o] = (k << 5) | c;
+          A.lj[o] = j;
+        } else if (key >= 0) {
+          const long long o = lbase + T - 1 - (nitf + __popc(mi & below));
+          A.lent[o] = (k << 5) | c;
+          A.lj[o] = j;
+          A.lb[o] = key;
+        }
+        ndg += __popc(md);
       }
       nitf += __popc(__ballot_sync(FULL_MASK, key >= 0));
       const unsigned peers = __match_any_sync(FULL_MASK, key);
@@ -507,6 +538,12 @@ __global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
     // interface records the numeric chunk may write: one per (flush of its interface list,
     // distinct large column); the list holds ITF_CAP entries and is flushed before it overflows
     if (l == 0) A.recmax[t] = nseen * (1 + nitf / (ITF_CAP - 31));
+    if (A.lent && l == 0) {
+      A.lbase[t] = lbase;
+      A.lnd[t] = ndg;
+      A.lib[t] = lbase + T - nitf;
+      A.lni[t] = nitf;
+    }
     // the diagonal block (a, a) always exists
     pairs_push(chunk == 0 && l == 0, make_int2(a, a), -1, s_pb[w], npb, A.pairs, A.porig, A.pair_cap, A.scw);
     __syncwarp();
@@ -1632,6 +1669,218 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
   }
 }
 
+// Large rows from the entry lists of k_sym_large (default numeric path): one warp per 32-children
+// chunk as k_num_large_atomic, but no classification pass -- the chunk's diagonal entries come as
+// a list (fine block, child slot, column node), read 32 per round one round ahead, so a round has
+// ONE dependent latency (its 72-B blocks and X_bar of the column nodes); the interface entries
+// are staged from their list and reduced per column aggregate as before.
+template <int NCB>
+__global__ void __launch_bounds__(128, 4) k_num_large_list(LargeArgs A) {
+  if (A.sc->err_cap || (NCB == 1 && A.sc->n_large3 == 0)) return;
+  __shared__ long long s_k[4][LSTAGE_A];
+  __shared__ int s_i[4][LSTAGE_A];
+  __shared__ int s_b[4][LSTAGE_A];
+  __shared__ double s_xj[4][LSTAGE_A][3];
+  __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
+  __shared__ double s_B[4][32][9];       // 32 blocks staged per warp (one per lane)
+  __shared__ int s_ix[4][LSTAGE_A];
+  const int w = threadIdx.x >> 5, l = lane_id();
+  constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
+  const int gq = l / LPB, p = NCB == 4 ? (l >> 1) & 3 : 0, q0 = NCB == 4 ? (l & 1) * 2 : 0;
+  const long long n3 = A.sc->n3;
+  const int64_t n_tasks = A.task_ptr[A.n_c];
+  const int64_t tstride = (int64_t)gridDim.x * 4;
+  int a_nx = 0, s_nx = 0, ci_nx = 0;
+  auto prefetch = [&](int64_t tn) {
+    if (tn < n_tasks) {
+      a_nx = A.task_node[tn];
+      const int ch = (int)(tn - A.task_ptr[a_nx]);
+      s_nx = min(LARGE_CHUNK, A.size_new[a_nx] - ch * LARGE_CHUNK);
+      ci_nx = l < s_nx ? A.child_list[A.child_ptr[a_nx] + (int64_t)ch * LARGE_CHUNK + l] : 0;
+    }
+  };
+  prefetch((int64_t)blockIdx.x * 4 + w);
+  for (int64_t t = (int64_t)blockIdx.x * 4 + w; t < n_tasks; t += tstride) {
+    const int a = a_nx, s = s_nx, ci_c = ci_nx;
+    prefetch(t + tstride);
+    if (ncb_of(a, n3) != NCB) continue;
+    const long long lbase = A.lbase[t], lib = A.lib[t];
+    const int nd = A.lnd[t], ni = A.lni[t];
+    // first round of the diagonal list in flight with the children's X_bar
+    long long ek_nx = 0;
+    int ej_nx = 0;
+    if (l < nd) {
+      ek_nx = A.lent[lbase + l];
+      ej_nx = A.lj[lbase + l];
+    }
+    if (l < s) {
+      s_wc[w][l][0] = __ldg(A.X + 3 * (int64_t)ci_c);
+      s_wc[w][l][1] = __ldg(A.X + 3 * (int64_t)ci_c + 1);
+      s_wc[w][l][2] = __ldg(A.X + 3 * (int64_t)ci_c + 2);
+    }
+    const int first12 = A.f12[a];
+    const int cpa = A.dpos[a];
+    double acc[QN][9];
+#pragma unroll
+    for (int q = 0; q < QN; ++q)
+#pragma unroll
+      for (int x = 0; x < 9; ++x) acc[q][x] = 0.0;
+    for (int d0 = 0; d0 < nd; d0 += 32) {
+      const long long ek = ek_nx;
+      const int ej = ej_nx;
+      if (d0 + 32 + l < nd) {  // next round's entries
+        ek_nx = A.lent[lbase + d0 + 32 + l];
+        ej_nx = A.lj[lbase + d0 + 32 + l];
+      }
+      if (d0 + l < nd) {
+        const long long kk = ek >> 5;
+#pragma unroll
+        for (int x = 0; x < 9; ++x) s_B[w][l][x] = __ldg(A.val + 9 * kk + x);
+        s_i[w][l] = (int)(ek & 31);
+        s_xj[w][l][0] = __ldg(A.X + 3 * (int64_t)ej);
+        s_xj[w][l][1] = __ldg(A.X + 3 * (int64_t)ej + 1);
+        s_xj[w][l][2] = __ldg(A.X + 3 * (int64_t)ej + 2);
+      }
+      __syncwarp();
+      const int dn = min(32, nd - d0);
+      for (int dd = gq; dd < dn; dd += G) {
+        const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][dd]][p];
+#pragma unroll
+        for (int qq = 0; qq < QN; ++qq) {
+          const int q = q0 + qq;
+          const double c = wi * ((NCB == 1 || q == 3) ? 1.0 : s_xj[w][dd][q]);
+#pragma unroll
+          for (int x = 0; x < 9; ++x) acc[qq][x] += c * s_B[w][dd][x];
+        }
+      }
+      __syncwarp();
+    }
+    if (nd > 0) {  // reduce over the block groups (lanes with the same p, q half) and flush
+#pragma unroll
+      for (int o = LPB; o < 32; o <<= 1)
+#pragma unroll
+        for (int qq = 0; qq < QN; ++qq)
+#pragma unroll
+          for (int x = 0; x < 9; ++x) acc[qq][x] += __shfl_xor_sync(FULL_MASK, acc[qq][x], o);
+      if (gq == 0 && cpa >= 0) {
+        const long long rs = A.crp[slot_of(a, p, n3)];
+#pragma unroll
+        for (int qq = 0; qq < QN; ++qq)
+#pragma unroll
+          for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q0 + qq) + x, acc[qq][x]);
+      }
+    }
+    // interface entries: batches of LSTAGE_A staged from the list, one pass per distinct column
+    // aggregate b0 (its entries compacted, their blocks staged 32 at a time), one set of atomics
+    // per (a, b0, batch)
+    const int32_t *lst = A.gbuf + A.nb_off[a];
+    const int U = A.nb_cnt[a];
+    for (int ibase = 0; ibase < ni; ibase += LSTAGE_A) {
+      const int icnt = min(LSTAGE_A, ni - ibase);
+      for (int e = l; e < icnt; e += 32) {
+        const long long o = lib + ibase + e;
+        const long long ek = A.lent[o];
+        const int ej = A.lj[o];
+        s_k[w][e] = ek >> 5;
+        s_i[w][e] = (int)(ek & 31);
+        s_b[w][e] = A.lb[o];
+        s_xj[w][e][0] = __ldg(A.X + 3 * (int64_t)ej);
+        s_xj[w][e][1] = __ldg(A.X + 3 * (int64_t)ej + 1);
+        s_xj[w][e][2] = __ldg(A.X + 3 * (int64_t)ej + 2);
+      }
+      __syncwarp();
+      int left = icnt;
+      while (left > 0) {
+        int f = -1;
+        for (int d0 = 0; d0 < icnt && f < 0; d0 += 32) {
+          const unsigned mb = __ballot_sync(FULL_MASK, d0 + l < icnt && s_b[w][d0 + l] >= 0);
+          if (mb) f = d0 + __ffs(mb) - 1;
+        }
+        const int b0 = s_b[w][f];
+        const int ncb_b = ncb_of(b0, n3);
+        constexpr int QI = NCB == 4 ? 2 : 4;  // q values per lane (a 3-DoF row meets 12-DoF columns)
+        double ac[QI][9];
+#pragma unroll
+        for (int qq = 0; qq < QI; ++qq)
+#pragma unroll
+          for (int x = 0; x < 9; ++x) ac[qq][x] = 0.0;
+        int nb = 0;
+        for (int d0 = f; d0 < icnt; d0 += 32) {
+          const bool mine = d0 + l < icnt && s_b[w][d0 + l] == b0;
+          const unsigned mm = __ballot_sync(FULL_MASK, mine);
+          if (mine) s_ix[w][nb + __popc(mm & ((1u << l) - 1u))] = d0 + l;
+          nb += __popc(mm);
+        }
+        __syncwarp();
+        for (int s0 = 0; s0 < nb; s0 += 32) {
+          if (s0 + l < nb) {
+            const long long kk = s_k[w][s_ix[w][s0 + l]];
+#pragma unroll
+            for (int x = 0; x < 9; ++x) s_B[w][l][x] = __ldg(A.val + 9 * kk + x);
+          }
+          __syncwarp();
+          const int dn = min(32, nb - s0);
+          for (int dd = gq; dd < dn; dd += G) {
+            const int d = s_ix[w][s0 + dd];
+            const double wi = (NCB == 1 || p == 3) ? 1.0 : s_wc[w][s_i[w][d]][p];
+#pragma unroll
+            for (int qq = 0; qq < QI; ++qq) {
+              const int q = q0 + qq;
+              const double c = q < ncb_b ? wi * ((ncb_b == 1 || q == 3) ? 1.0 : s_xj[w][d][q]) : 0.0;
+#pragma unroll
+              for (int x = 0; x < 9; ++x) ac[qq][x] += c * s_B[w][dd][x];
+            }
+          }
+          __syncwarp();
+        }
+        for (int d0 = f; d0 < icnt; d0 += 32)
+          if (d0 + l < icnt && s_b[w][d0 + l] == b0) s_b[w][d0 + l] = -1;
+        __syncwarp();
+        left -= nb;
+#pragma unroll
+        for (int o = LPB; o < 32; o <<= 1)
+#pragma unroll
+          for (int qq = 0; qq < QI; ++qq)
+#pragma unroll
+            for (int x = 0; x < 9; ++x) ac[qq][x] += __shfl_xor_sync(FULL_MASK, ac[qq][x], o);
+        const int cp = colpos(lower_bound_dev<int32_t>(lst, U, b0), first12);
+        if (gq == 0) {
+          const long long rs = A.crp[slot_of(a, p, n3)];
+#pragma unroll
+          for (int qq = 0; qq < QI; ++qq)
+            if (q0 + qq < ncb_b) {
+              double *dst = A.cval + 9 * (rs + cp + q0 + qq);
+#pragma unroll
+              for (int x = 0; x < 9; ++x) atomicAdd(dst + x, ac[qq][x]);
+            }
+        }
+      }
+      __syncwarp();
+    }
+    if (A.g_f) {  // g_c[slot(a,pp)] += sum over the chunk of w_i[pp] g_f[i]
+      for (int pp = 0; pp < NCB; ++pp) {
+        double g0 = 0, g1 = 0, g2 = 0;
+        if (l < s) {
+          const double wi = (NCB == 1 || pp == 3) ? 1.0 : s_wc[w][l][pp];
+          g0 = wi * A.g_f[3 * (int64_t)ci_c];
+          g1 = wi * A.g_f[3 * (int64_t)ci_c + 1];
+          g2 = wi * A.g_f[3 * (int64_t)ci_c + 2];
+        }
+        g0 = warp_sum(g0);
+        g1 = warp_sum(g1);
+        g2 = warp_sum(g2);
+        if (l == 0) {
+          double *gc = A.g_c + 3 * (int64_t)slot_of(a, pp, n3);
+          atomicAdd(gc, g0);
+          atomicAdd(gc + 1, g1);
+          atomicAdd(gc + 2, g2);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Interface flush: one record per distinct column aggregate b0 of the staged interface list
 // (lanes (g, p, q) accumulate the entries of b0, the two groups are reduced, group 0 writes).
 template <int NCB>
@@ -2095,6 +2344,21 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LA.gbuf = gbuf; LA.nb_off = nb_off; LA.nb_cnt = nb_cnt; LA.crp = nullptr; LA.cval = nullptr; LA.g_c = out->g_c;
   LA.recmax = recmax; LA.rec_off = rec_off; LA.rec_b = nullptr; LA.rec_v = nullptr; LA.part = nullptr;
   const unsigned glarge = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), 64 * h->sm_count);
+  // large-row entry lists for the numeric pass (default, non-deterministic mode; AGIPC_LARGE_LIST=0
+  // selects the classifying k_num_large_atomic for experiments)
+  static const bool large_list = !(getenv("AGIPC_LARGE_LIST") && atoi(getenv("AGIPC_LARGE_LIST")) == 0);
+  LA.lent = nullptr; LA.lj = nullptr; LA.lb = nullptr; LA.lbase = nullptr; LA.lib = nullptr;
+  LA.lnd = nullptr; LA.lni = nullptr;
+  if (large_list && !h->opt_deterministic) {
+    WS(h, lent, long long, "asm_lent", nnzb_f + 1);
+    WS(h, lj, int32_t, "asm_lj", nnzb_f + 1);
+    WS(h, lb, int32_t, "asm_lb", nnzb_f + 1);
+    WS(h, lbase, long long, "asm_lbase", task_bound + 1);
+    WS(h, lib, long long, "asm_lib", task_bound + 1);
+    WS(h, lnd, int32_t, "asm_lnd", task_bound + 1);
+    WS(h, lni, int32_t, "asm_lni", task_bound + 1);
+    LA.lent = lent; LA.lj = lj; LA.lb = lb; LA.lbase = lbase; LA.lib = lib; LA.lnd = lnd; LA.lni = lni;
+  }
   LAUNCH_S(h, h->aux, k_sym_large, glarge, 128, 0, LA);
   if ((st = aux_join(h)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
@@ -2174,8 +2438,13 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     // cuts the FMAs 4x but measured 2.03 vs 0.54 ms at C3: divergent per-lane row walks, 17% warps
     // active; profiles/r02f)
     if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
-      LAUNCH_S(h, ls, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
-      if (hsc->n_large3 > 0) LAUNCH_S(h, ls, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
+      if (LA.lent) {
+        LAUNCH_S(h, ls, k_num_large_list<4>, glarge, 128, 0, LA);
+        if (hsc->n_large3 > 0) LAUNCH_S(h, ls, k_num_large_list<1>, glarge, 128, 0, LA);
+      } else {
+        LAUNCH_S(h, ls, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
+        if (hsc->n_large3 > 0) LAUNCH_S(h, ls, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
+      }
     } else {  // large rows: per-chunk partials + records, then the fixed-order reduction (no atomics)
       // sizes vary between Newton steps: ask for 1.5x so that the buffers rarely grow
       WS(h, part, double, "asm_large_part", PART_STRIDE * (3 * hsc->n_tasks / 2 + 64));
