@@ -38,6 +38,7 @@ struct AsmScal {
   long long n3, n12, n_slots, nnzb;
   long long nbs_count;   // entries used in the small-node neighbour buffer
   long long list_top;    // entries allocated in the large-row entry lists (k_sym_large)
+  long long n_w32;       // nodes of the 32-entry small list (k_final_scalars)
   long long pair_count;  // (large, x) pairs
   long long big_groups;  // large lists that need the CTA sort
   long long n_large3;    // large nodes with 3 DoF (affine threshold > 32)
@@ -296,6 +297,64 @@ __device__ __forceinline__ void warp_bitonic_sort(int *buf, int P) {
       __syncwarp();
     }
   }
+}
+
+// Bitonic sort (ascending) of 32 R keys held lane-major in registers: key i = lane R + r.
+// Partner distances j < R stay inside a lane (compile-time register pairs), j >= R are one
+// shuffle with lane ^ (j / R) -- no shared-memory round trips or warp barriers per stage.
+template <int R, typename T>
+__device__ __forceinline__ void warp_reg_bitonic(T (&k)[R]) {
+  const int l = lane_id();
+#pragma unroll
+  for (int kq = 2; kq <= 32 * R; kq <<= 1) {
+#pragma unroll
+    for (int j = kq >> 1; j > 0; j >>= 1) {
+      if (j >= R) {
+        const int lj = j / R;
+        const bool lower = (l & lj) == 0;  // my element is the lower index of its pair
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool up = ((l * R + r) & kq) == 0;
+          const T o = __shfl_xor_sync(FULL_MASK, k[r], lj);
+          k[r] = (lower == up) ? min(k[r], o) : max(k[r], o);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if ((r & j) == 0) {
+            const bool up = ((l * R + r) & kq) == 0;
+            const T x = k[r], y = k[r | j];
+            const bool sw = (x > y) == up;
+            k[r] = sw ? y : x;
+            k[r | j] = sw ? x : y;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Sort P (power of two) ints of a warp's shared-memory buffer: in registers for 64 <= P <= 512,
+// the shared-memory network otherwise.
+template <int R>
+__device__ __forceinline__ void warp_sort_int_reg(int *buf) {
+  const int l = lane_id();
+  int k[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) k[r] = buf[l * R + r];
+  warp_reg_bitonic<R>(k);
+#pragma unroll
+  for (int r = 0; r < R; ++r) buf[l * R + r] = k[r];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void warp_sort_int(int *buf, int P) {
+  __syncwarp();
+  if (P == 64) warp_sort_int_reg<2>(buf);
+  else if (P == 128) warp_sort_int_reg<4>(buf);
+  else if (P == 256) warp_sort_int_reg<8>(buf);
+  else if (P == 512) warp_sort_int_reg<16>(buf);
+  else warp_bitonic_sort(buf, P);
 }
 
 __device__ __forceinline__ int next_pow2(int x) {
@@ -589,7 +648,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_group_unique(int64_t n_c, co
     }
     for (int e = l; e < P; e += 32) buf[e] = e < n ? g[e] : INT_MAX;
     __syncwarp();
-    warp_bitonic_sort(buf, P);
+    warp_sort_int(buf, P);
     int u12;
     int U = warp_unique_store(buf, n, g, n3, u12);
     if (l == 0) {
@@ -675,8 +734,9 @@ __global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__res
 // ------------------------------------------------------------------------------------
 __global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr, const int64_t *__restrict__ task_ptr,
                                 int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound,
-                                int64_t cap_slots, int64_t cap_nnzb) {
+                                int64_t cap_slots, int64_t cap_nnzb, const int64_t *__restrict__ cnt32) {
   sc->nnzb = row_ptr[sc->n_slots];
+  sc->n_w32 = *cnt32;
   sc->n_tasks = task_ptr[n_c];
   sc->rec_total = rec_off[task_bound];
   sc->err_cap = sc->err_map || sc->err_overflow || sc->n_slots >= INT32_MAX || sc->n_slots > cap_slots ||
@@ -1015,41 +1075,6 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
 // ------------------------------------------------------------------------------------
 #define MID_WARPS 4
 #define MID_CAP 1024
-
-// Bitonic sort (ascending) of 32 R 64-bit keys held lane-major in registers: key i = lane R + r.
-// Partner distances j < R stay inside a lane (compile-time register pairs), j >= R are one
-// shuffle with lane ^ (j / R) -- no shared-memory round trips or warp barriers per stage.
-template <int R>
-__device__ __forceinline__ void warp_reg_bitonic(long long (&k)[R]) {
-  const int l = lane_id();
-#pragma unroll
-  for (int kq = 2; kq <= 32 * R; kq <<= 1) {
-#pragma unroll
-    for (int j = kq >> 1; j > 0; j >>= 1) {
-      if (j >= R) {
-        const int lj = j / R;
-        const bool lower = (l & lj) == 0;  // my element is the lower index of its pair
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const bool up = ((l * R + r) & kq) == 0;
-          const long long o = __shfl_xor_sync(FULL_MASK, k[r], lj);
-          k[r] = (lower == up) ? min(k[r], o) : max(k[r], o);
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if ((r & j) == 0) {
-            const bool up = ((l * R + r) & kq) == 0;
-            const long long x = k[r], y = k[r | j];
-            const bool sw = (x > y) == up;
-            k[r] = sw ? y : x;
-            k[r | j] = sw ? x : y;
-          }
-        }
-      }
-    }
-  }
-}
 
 // Mid-node symbolic keys ((column << 10) | entry) of T <= 32 R entries, sorted in registers and
 // stored to shared memory (run counting) and to global memory (reused by the numeric pass).
@@ -2326,8 +2351,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   // the large-row symbolic pass runs on the aux stream next to the small / mid rows' (both
   // latency-bound at partial occupancy; they only share the atomic pair counter)
   if ((st = aux_fork(h)) != AGIPC_OK) return st;
-  LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
+  // the 32-entry list first: usually short or empty, it then does not wait for free SM slots
+  // behind the large-row symbolic pass
   LAUNCH(h, (k_small_warp<32, false>), g32, 256, 0, WB);
+  LAUNCH(h, (k_small_warp<16, false>), g16, 256, 0, WA);
   WM = WA;
   WM.wlist = small_list; WM.kind = 2;
   {  // mid-node entries: sum of their candidate entries <= the fine blocks
@@ -2388,7 +2415,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     if ((st = scan_multi(h, jobs)) != AGIPC_OK) return st;
   }
   LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound,
-         out->cap_slots, out->cap_nnzb);
+         out->cap_slots, out->cap_nnzb, (const int64_t *)(i32 + n_c));
   LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, (const AsmScal *)sc, pair_cap, (const int2 *)pairs,
          (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
          (const int32_t *)f12, (const int32_t *)rowlen, (const int64_t *)crp_ws, mirpos, mirrl);
@@ -2467,7 +2494,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
   // (5 CTAs/SM at 48 registers measured slower: 1.35 vs 1.26 ms numeric at C3, profiles/r02k)
   LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
-  LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
+  if (hsc->n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   if (num_mode != 1 && (st = launch_large()) != AGIPC_OK) return st;
   return fork ? aux_join(h) : AGIPC_OK;
 }
