@@ -758,15 +758,15 @@ __global__ void k_copy_rowptr(const AsmScal *sc, const int64_t *__restrict__ src
 // shuffle bitonic sort of (column, lane) keys, run heads by ballot, run sums by a segmented
 // shuffle scan.  No shared-memory staging of values, no barriers.
 // ------------------------------------------------------------------------------------
-template <int SEG>
-__device__ __forceinline__ long long seg_sort(long long key, int sl) {
+template <int SEG, typename T = long long>
+__device__ __forceinline__ T seg_sort(T key, int sl) {
 #pragma unroll
   for (int k = 2; k <= SEG; k <<= 1)
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      const long long other = __shfl_xor_sync(FULL_MASK, key, j, SEG);
+      const T other = __shfl_xor_sync(FULL_MASK, key, j, SEG);
       const bool up = (sl & k) == 0, lower = (sl & j) == 0;
-      const long long mn = min(key, other), mx = max(key, other);
+      const T mn = min(key, other), mx = max(key, other);
       key = (lower == up) ? mn : mx;
     }
   return key;
@@ -796,6 +796,8 @@ struct WarpArgs {
   // mid); n_w, mir_base and the 32-entry key offset are derived from them (warp_args_resolve)
   const int64_t *cnt16, *cnt32, *cntmid;
   int kind;
+  int key32;  // n_c < 2^26 - 1: symbolic sort keys (column << 5 | lane) fit in 31 bits
+  int32_t *mchild;  // small nodes: child of lane sl at wi * SEG + sl (symbolic -> numeric prefetch)
   long long *msrc;             // small nodes: (fine block << 5 | child index) per sorted key
   long long *mkeys;            // mid nodes: sorted (column, entry) keys, written by the symbolic
   const int64_t *e_off;        //   pass at e_off[wi], reused by the numeric pass (no second sort)
@@ -839,6 +841,7 @@ __device__ __forceinline__ void warp_args_resolve(WarpArgs &A) {
     A.mir_base = 16 * n16;
     A.mkeys += 16 * n16;
     A.msrc += 16 * n16;
+    A.mchild += 16 * n16;
   } else {
     A.n_w = *A.cntmid;
     A.mir_base = 16 * n16 + 32 * n32;
@@ -881,11 +884,12 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
     if (u0 < n_units && wi0 < A.n_w) {
       a_nx = A.wlist[wi0];
       s_nx = A.size_new[a_nx];
-      if (sl < s_nx) ci_nx = A.child_list[A.child_ptr[a_nx] + sl];
+      if (!NUMERIC && sl < s_nx) ci_nx = A.child_list[A.child_ptr[a_nx] + sl];
       if (NUMERIC) {
         key_nx = A.mkeys[wi0 * SEG + sl];
         m_nx = A.msrc[wi0 * SEG + sl];
       }
+      if (NUMERIC) ci_nx = max(A.mchild[wi0 * SEG + sl], 0);
     }
   }
   for (int64_t u = (int64_t)blockIdx.x * 8 + w; u < n_units; u += ustride) {
@@ -900,10 +904,12 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       if (u + ustride < n_units && wn < A.n_w) {
         a_nx = A.wlist[wn];
         s_nx = A.size_new[a_nx];
-        ci_nx = sl < s_nx ? A.child_list[A.child_ptr[a_nx] + sl] : 0;
-        if (NUMERIC) {
+        if (NUMERIC) {  // the child list as the symbolic pass left it: no child_ptr -> child_list chain
           key_nx = A.mkeys[wn * SEG + sl];
           m_nx = A.msrc[wn * SEG + sl];
+          ci_nx = max(A.mchild[wn * SEG + sl], 0);
+        } else {
+          ci_nx = sl < s_nx ? A.child_list[A.child_ptr[a_nx] + sl] : 0;
         }
       }
     }
@@ -931,11 +937,15 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
       }
       // sorted (column, entry) keys and, per sorted position, its fine block and child index:
       // kept at wi * SEG + sl for the numeric pass (no second new_map gather, sort or row walk)
-      const long long key = seg_sort<SEG>(((long long)b << 5) | sl, sl);
+      // 32-bit keys while every column id fits in 26 bits (one-instruction shuffles and min / max);
+      // the same order as the 64-bit keys, the invalid lanes last in lane order
+      const long long key = A.key32 ? (long long)seg_sort<SEG, int>(sl < T ? (b << 5) | sl : (0x7FFFFFE0 | sl), sl)
+                                    : seg_sort<SEG>(((long long)b << 5) | sl, sl);
       const int src = (int)(key & 31);
       const long long ksrc = __shfl_sync(FULL_MASK, k, src, SEG);
       const int csrc = __shfl_sync(FULL_MASK, c, src, SEG);
       if (segv) {
+        A.mchild[wi * SEG + sl] = sl < s ? ci_cur : -1;
         A.mkeys[wi * SEG + sl] = key;
         A.msrc[wi * SEG + sl] = sl < T ? ((ksrc << 5) | csrc) : -1;
       }
@@ -2327,6 +2337,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WA.cval = nullptr; WA.g_c = out->g_c;
   WA.mkeys = nullptr; WA.e_off = nullptr; WA.msrc = nullptr;
   WA.cnt16 = i16 + n_c; WA.cnt32 = i32 + n_c; WA.cntmid = sidx + n_c; WA.kind = 0;
+  WA.key32 = n_c < (1 << 26) - 1;
   WarpArgs WB = WA, WM;
   WB.wlist = w32; WB.kind = 1;
   // mirror positions: [16 n_w16 | 32 n_w32 | mid entries], indexed like the sorted keys (the
@@ -2336,6 +2347,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   {  // small nodes: SEG key slots per node of the 16- and 32-entry lists
     WS(h, skeys, long long, "asm_small_keys", 32 * n_c + 1);
     WS(h, ssrc, long long, "asm_small_src", 32 * n_c + 1);
+    WS(h, schild, int32_t, "asm_small_child", 32 * n_c + 1);
+    WA.mchild = schild;
+    WB.mchild = schild;  // + 16 n_w16 (warp_args_resolve)
     WA.mkeys = skeys;
     WB.mkeys = skeys;  // + 16 n_w16 (warp_args_resolve)
     WA.msrc = ssrc;
