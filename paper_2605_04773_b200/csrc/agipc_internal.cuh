@@ -87,6 +87,7 @@ struct agipc_handle_s {
   struct Comm *comm = nullptr;  // NCCL communicator (comm.cu, agipc_comm_init)
   cudaStream_t aux = nullptr;   // second stream for independent kernels of one call (fork / join)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_wait = nullptr;  // host_wait
   // profiling (CUDA events on the launching stream; off by default)
   bool prof = false;
   std::vector<ProfPending> prof_pending;
@@ -191,6 +192,11 @@ void trace_post(agipc_handle h, cudaStream_t s);
                        cudaGetErrorString(_e));                                              \
     }                                                                                        \
   } while (0)
+
+// Host wait for everything enqueued on s so far by spinning on an event (cudaEventQuery) instead
+// of cudaStreamSynchronize: the calls that must return device-computed sizes pay no blocking-sync
+// wake-up latency (the GPU idles until the host enqueues the next work).
+cudaError_t host_wait(agipc_handle h, cudaStream_t s);
 
 // Fork: work enqueued on h->aux after this starts once everything before on h->stream is done.
 agipc_status aux_fork(agipc_handle h);

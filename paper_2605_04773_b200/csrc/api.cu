@@ -71,6 +71,18 @@ agipc_status aux_fork(agipc_handle h) {
   return AGIPC_OK;
 }
 
+cudaError_t host_wait(agipc_handle h, cudaStream_t s) {
+  if (!h->ev_wait) {
+    cudaError_t e = cudaEventCreateWithFlags(&h->ev_wait, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(h->ev_wait, s);
+  if (e != cudaSuccess) return e;
+  while ((e = cudaEventQuery(h->ev_wait)) == cudaErrorNotReady) {
+  }
+  return e;
+}
+
 agipc_status aux_join(agipc_handle h) {
   CU_TRY(h, cudaEventRecord(h->ev_join, h->aux));
   CU_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
@@ -220,6 +232,7 @@ agipc_status agipc_destroy(agipc_handle h) {
     cudaEventDestroy(h->ev_join);
   }
   if (h->dpcg) dpcg_free(h->dpcg);
+  if (h->ev_wait) cudaEventDestroy(h->ev_wait);
   trace_dump(h);
   prof_flush(h);
   for (auto e : h->prof_pool) cudaEventDestroy(e);

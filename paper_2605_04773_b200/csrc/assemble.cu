@@ -2439,7 +2439,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   LAUNCH(h, k_copy_rowptr, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(slot_bound + 1, 256), 4 * h->sm_count)),
          256, 0, (const AsmScal *)sc, (const int64_t *)crp_ws, out->row_ptr);
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
-  CU_TRY(h, cudaStreamSynchronize(st_));
+  CU_TRY(h, host_wait(h, st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
   if (hsc->err_overflow) return set_err(h, AGIPC_ECUDA, "assemble_coarse: internal buffer overflow");
   out->n3 = hsc->n3;

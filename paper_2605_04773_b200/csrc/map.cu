@@ -730,7 +730,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   MapScalars *hs = (MapScalars *)pinned_get(h, sizeof(MapScalars), &st);
   if (st != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(hs, sc, sizeof(MapScalars), cudaMemcpyDeviceToHost, s0));
-  CU_TRY(h, cudaStreamSynchronize(s0));
+  CU_TRY(h, host_wait(h, s0));
   if (getenv("AGIPC_TAIL_TRACE") && max_levels != 1) {  // per-phase time of the tail levels (CTA 0)
     unsigned long long t[8 * 64];
     if (cudaMemcpy(t, h->ws["map_tail_trace"].ptr, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {

@@ -1349,7 +1349,7 @@ static agipc_status pcg_solve_impl(agipc_handle h, const agipc_bsr *A, int stora
         CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
         launched += chunk;
         CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
-        CU_TRY(h, cudaStreamSynchronize(g->stream));
+        CU_TRY(h, host_wait(h, g->stream));
         const int ran = hst->it - it_before;  // iterations whose K1/K2 did work in this chunk
         h->launches += 2 * (int64_t)ran;
         if (h->prof) {
@@ -1781,7 +1781,7 @@ extern "C" agipc_status agipc_dpcg_solve(agipc_handle h, const agipc_bsr *A, con
         CU_TRY(h, cudaGraphLaunch(g->exec, g->stream));
         launched += chunk;
         CU_TRY(h, cudaMemcpyAsync(hst, B.st, sizeof(PcgState), cudaMemcpyDeviceToHost, g->stream));
-        CU_TRY(h, cudaStreamSynchronize(g->stream));
+        CU_TRY(h, host_wait(h, g->stream));
         const int ran = hst->it - it_before;
         h->launches += (2 + (d->n_gs > 0) + (X.n_send > 0) + 2) * (int64_t)ran;
         it_before = hst->it;
