@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
         for (int gg = 0; gg < NSEG - 1; ++gg)
           if (g == gg && oo >= s_seg[w][gg][2]) { oo -= s_seg[w][gg][2]; g = gg + 1; }
         const int ag = s_seg[w][g][0], Rg = s_seg[w][g][1];
-        const int p = oo / Rg, r = oo - p * Rg;
+        const int p = (oo >= Rg) + (oo >= 2 * Rg) + (oo >= 3 * Rg), r = oo - p * Rg;  // p < 4: no division
         const int d = s_desc[w][g * 4 * SEG + r];
         const int h0 = g * SEG + (d & 63), t1 = g * SEG + ((d >> 6) & 63), q = d >> 12;
         const int b = s_rbs[w][h0];

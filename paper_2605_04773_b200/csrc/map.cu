@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
         hit = true;
       }
       Ew[e] = keep ? o : make_int2(-1, -1);
+      if (A.trace && keep && level <= 64) atomicAdd(A.trace + 8 * (level - 1) + 7, 1ull);  // live edges
     }
     if (__any_sync(FULL_MASK, hit) && lane == 0) atomicOr(A.ctrl + (1 - fl), 1);
     if (tr) tr[4] = gtimer();
@@ -742,6 +743,10 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
         ++nl;
         for (int k = 0; k < 6; ++k) acc[k] += 1e-3 * (double)(r[k + 1] - r[k]);
       }
+      fprintf(stderr, "libagipc[tail-trace] live edges per level:");
+      for (int lv = 0; lv < 64; ++lv)
+        if (t[8 * lv + 6]) fprintf(stderr, " %llu", t[8 * lv + 7]);
+      fprintf(stderr, "\n");
       fprintf(stderr, "libagipc[tail-trace] levels %d, mean us per level: P2 closure %.2f | barrier %.2f | "
               "tile scan %.2f | edges %.2f | compose %.2f | barrier %.2f\n", nl, acc[0] / nl, acc[1] / nl,
               acc[2] / nl, acc[3] / nl, acc[4] / nl, acc[5] / nl);
