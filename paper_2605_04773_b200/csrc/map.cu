@@ -134,8 +134,7 @@ __device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles
 __global__ void __launch_bounds__(MAP_THREADS)
     k_level0(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
              const uint8_t *__restrict__ tags, int32_t *__restrict__ map_out, int2 *__restrict__ cross,
-             unsigned long long *__restrict__ cross_count, unsigned long long *status, int *tile_counter,
-             long long *n_out) {
+             unsigned long long *__restrict__ cross_count, int32_t *__restrict__ tile_cnt, int *tile_counter) {
   __shared__ TileSmem S;
   __shared__ long long s_ptr[MAP_WARPS][33];
   __shared__ uint32_t s_h[MAP_WARPS][32];
@@ -232,19 +231,18 @@ __global__ void __launch_bounds__(MAP_THREADS)
     const long long ci = warp_incl_scan(cc);
     const long long agg = __shfl_sync(FULL_MASK, ci, MAP_WARPS - 1);
     if (lane < MAP_WARPS) S.warp[lane] = ci - cc;
-    const long long pfx = lb_exclusive(status, tile, agg);  // ExclusiveSum over groups
-    if (lane == 0) {
-      S.prefix = pfx;
-      if (tile == gridDim.x - 1) *n_out = pfx + agg;
-    }
+    // the ExclusiveSum over groups is split: this tile's count now, the tile prefix by one
+    // scan afterwards, added by the map's consumers (k_cross_to_level1, k_apply) -- no look-back
+    // chain on this kernel's critical path (it cost ~40 of 140 us at C3, profiles/r02v)
+    if (lane == 0) tile_cnt[tile] = (int32_t)agg;
   }
   __syncthreads();
-  const long long wb = S.prefix + S.warp[w];
+  const long long wb = S.warp[w];  // tile-relative map
 #pragma unroll
   for (int c = 0; c < L0_CHUNKS; ++c) {
     const int64_t q = ((int64_t)tile * MAP_WARPS + w) * L0_CHUNKS + c;
     const int64_t v = q * cn + lane;
-    if (lane < cn && v < n) map_out[v] = (int32_t)(wb + off[c] + local[c]);  // O[g] + P
+    if (lane < cn && v < n) map_out[v] = (int32_t)(wb + off[c] + local[c]);  // O[g] + P, minus the tile prefix
   }
 }
 
@@ -276,7 +274,9 @@ __device__ __forceinline__ unsigned long long cta_compact(bool keep, unsigned lo
 __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned long long *__restrict__ ne_ptr,
                                   const int32_t *__restrict__ m0, unsigned long long *__restrict__ table,
                                   unsigned long long tmask, int2 *__restrict__ E_out,
-                                  unsigned long long *__restrict__ ne_out, unsigned long long *__restrict__ used) {
+                                  unsigned long long *__restrict__ ne_out, unsigned long long *__restrict__ used,
+                                  const int64_t *__restrict__ tpref, int tn0, int64_t tiles0, long long *n1_out) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n1_out = tpref[tiles0];  // level-1 node count
   __shared__ int s_w[32];
   __shared__ unsigned long long s_base;
   const int64_t ne = (int64_t)*ne_ptr;
@@ -289,7 +289,7 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
     unsigned long long key = 0ull;  // 0: no edge
     if (e < ne) {
       const int2 uv = E[e];
-      o = make_int2(m0[uv.x], m0[uv.y]);
+      o = make_int2((int)(m0[uv.x] + tpref[uv.x / tn0]), (int)(m0[uv.y] + tpref[uv.y / tn0]));
       key = (((unsigned long long)(unsigned)o.x << 32) | (unsigned)o.y) + 1ull;
     }
     // neighbouring list entries mostly map to the same coarse pair: one probe per distinct key
@@ -578,11 +578,16 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
 }
 
 // map[f] = comp[map[f]] if any tail level merged
+// map[f] = level-0 id (tile-relative value + tile prefix), then comp[] if any tail level merged
 __global__ void k_apply(int64_t n, int32_t *__restrict__ map, const int32_t *__restrict__ comp,
-                        const int *__restrict__ ctrl) {
-  if (!ctrl[3]) return;
+                        const int *__restrict__ ctrl, const int64_t *__restrict__ tpref, int tn0, int64_t tiles0,
+                        long long *n1_out) {
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < n) map[f] = comp[map[f]];
+  if (n1_out && f == 0) *n1_out = tpref[tiles0];  // no tail launched (max_levels == 1)
+  if (f < n) {
+    const int g = (int)(map[f] + tpref[f / tn0]);
+    map[f] = ctrl[3] ? comp[g] : g;
+  }
 }
 
 // Aggregate sizes: histogram of the final map with warp-aggregated atomics.
@@ -631,16 +636,20 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   const int64_t ecap = mesh->nnz_adj / 2 + 1;
 
   WS(h, sc, MapScalars, "map_scalars", 1);
-  WS(h, status, unsigned long long, "map_status", tiles0 + 2);
+  WS(h, tcnt, int32_t, "map_tile_cnt", tiles0 + 2);
+  WS(h, tpref, int64_t, "map_tile_pref", tiles0 + 1);
   WS(h, cross, int2, "map_cross", ecap);
   CU_TRY(h, cudaMemsetAsync(sc, 0, sizeof(MapScalars), s0));
-  CU_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles0 + 2), s0));
-  int *tile_counter = (int *)(status + tiles0 + 1);
+  int *tile_counter = (int *)(tcnt + tiles0 + 1);
+  CU_TRY(h, cudaMemsetAsync(tile_counter, 0, sizeof(int), s0));
+  const int tn0 = MAP_WARPS * L0_CHUNKS * geo.gpw * geo.gs;  // fine nodes per k_level0 tile
 
   // ---- level 0: warp-per-group hashing over the fine mesh (fused look-back scan) ----
   std::unique_ptr<ProfScope> ps_l0(new ProfScope(h, PROF_MAP_LEVEL0, s0));
   LAUNCH(h, k_level0, (unsigned)tiles0, MAP_THREADS, 0, N, geo, mesh->adj_ptr, mesh->adj_nbr, slot_tags, map, cross,
-         &sc->cross, status, tile_counter, &sc->nvals[0]);
+         &sc->cross, tcnt, tile_counter);
+  agipc_status sst = scan_exclusive_i64(h, SCAN_SRC_I32, tcnt, tiles0, tpref);  // O[g] over the tiles
+  if (sst != AGIPC_OK) return sst;
 
   ps_l0.reset();
   // ---- levels >= 1: one cooperative persistent kernel ----
@@ -669,7 +678,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     CU_TRY(h, cudaMemsetAsync(hh, 0, sizeof(uint32_t) * N, s0));
     const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), 8 * h->sm_count));
     LAUNCH(h, k_cross_to_level1, gedge, 256, 0, cross, &sc->cross, map, table, (unsigned long long)(tsize - 1), EA,
-           &sc->ne[0], used);
+           &sc->ne[0], used, (const int64_t *)tpref, tn0, tiles0, &sc->nvals[0]);
     LAUNCH(h, k_clear_slots, gedge, 256, 0, &sc->ne[0], used, table);
     TailArgs A;
     A.geo = geo;
@@ -721,7 +730,11 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
       LAUNCH(h, k_tail, (unsigned)grid, TAIL_THREADS, smem, A);
     }
     ps_tail.reset();
-    LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl);
+    LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl, (const int64_t *)tpref, tn0, tiles0,
+           (long long *)nullptr);
+  } else {  // level 0 only: the tile prefixes still have to be added
+    LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, (const int32_t *)nullptr, sc->ctrl,
+           (const int64_t *)tpref, tn0, tiles0, &sc->nvals[0]);
   }
   if (agg_size) {
     CU_TRY(h, cudaMemsetAsync(agg_size, 0, sizeof(int32_t) * N, s0));
