@@ -2377,7 +2377,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     WM.e_off = e_off;
   }
   const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, MID_WARPS), 12 * h->sm_count));
-  LAUNCH(h, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
@@ -2401,6 +2400,8 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     LA.lent = lent; LA.lj = lj; LA.lb = lb; LA.lbase = lbase; LA.lib = lib; LA.lnd = lnd; LA.lni = lni;
   }
   LAUNCH_S(h, h->aux, k_sym_large, glarge, 128, 0, LA);
+  // the mid nodes follow the large rows on the aux stream: the small rows alone are the longer stream
+  LAUNCH_S(h, h->aux, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   if ((st = aux_join(h)) != AGIPC_OK) return st;
   CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
   LAUNCH(h, k_pair_count, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, gcnt);
@@ -2503,12 +2504,12 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   };
   if (num_mode == 1 && (st = launch_large()) != AGIPC_OK) return st;
   WM.crp = out->row_ptr; WM.ccol = out->col; WM.cval = out->val;
-  LAUNCH(h, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);
   WA.crp = out->row_ptr; WA.ccol = out->col; WA.cval = out->val;
   WB.crp = out->row_ptr; WB.ccol = out->col; WB.cval = out->val;
   // (5 CTAs/SM at 48 registers measured slower: 1.35 vs 1.26 ms numeric at C3, profiles/r02k)
   LAUNCH(h, (k_small_warp<16, true>), g16, 256, 0, WA);
   if (hsc->n_w32 > 0) LAUNCH(h, (k_small_warp<32, true>), g32, 256, 0, WB);
   if (num_mode != 1 && (st = launch_large()) != AGIPC_OK) return st;
+  LAUNCH_S(h, ls, k_mid_warp<true>, gmid, MID_WARPS * 32, 0, WM);  // after the large rows (aux stream)
   return fork ? aux_join(h) : AGIPC_OK;
 }
