@@ -62,7 +62,14 @@ void *ws_get(agipc_handle h, const char *name, size_t bytes, agipc_status *st, b
 
 agipc_status aux_fork(agipc_handle h) {
   if (!h->aux) {
-    CU_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    // the aux stream carries the longer half of each fork (large-row + mid-node passes): it gets
+    // the highest priority, so its CTAs take the SM slots first (AGIPC_AUX_PRIO=0: default priority)
+    int lo = 0, hi = 0;
+    static const bool prio = !(getenv("AGIPC_AUX_PRIO") && atoi(getenv("AGIPC_AUX_PRIO")) == 0);
+    if (prio && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess)
+      CU_TRY(h, cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, hi));
+    else
+      CU_TRY(h, cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
     CU_TRY(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     CU_TRY(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   }
