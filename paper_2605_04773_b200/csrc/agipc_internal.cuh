@@ -160,6 +160,7 @@ void *pinned_get(agipc_handle h, size_t bytes, agipc_status *st);
 
 void trace_pre(agipc_handle h, const char *name, cudaStream_t s);
 void trace_post(agipc_handle h, cudaStream_t s);
+void trace_mark(agipc_handle h, const char *name);  // host-time marker (no GPU events)
 
 // Every kernel launch goes through LAUNCH so that the handle counts it and errors surface.
 // (one cudaGetLastError after the launch: it also reports an error left pending by an earlier

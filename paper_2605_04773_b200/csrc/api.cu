@@ -169,6 +169,10 @@ void trace_pre(agipc_handle h, const char *name, cudaStream_t s) {
   if (r.a) cudaEventRecord(r.a, s);
   h->trace_recs.push_back(r);
 }
+void trace_mark(agipc_handle h, const char *name) {
+  if (h->trace_recs.size() >= 200000) return;
+  h->trace_recs.push_back(agipc_handle_s::TraceRec{name, nullptr, nullptr, nullptr, host_now_us()});
+}
 void trace_post(agipc_handle h, cudaStream_t s) {
   if (h->trace_recs.empty() || h->trace_recs.back().b || h->trace_recs.back().s != s) return;
   auto &r = h->trace_recs.back();

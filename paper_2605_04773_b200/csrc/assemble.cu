@@ -2207,6 +2207,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
                                               int64_t n_coarse, int64_t affine_threshold, const agipc_bsr *H,
                                               const double *g_fine, agipc_coarse *out) {
   if (!h) return AGIPC_EINVAL;
+  if (h->trace) trace_mark(h, "@assemble_enter");
   if (!mesh || !H || !out) return set_err(h, AGIPC_EINVAL, "assemble_coarse: null argument");
   const int64_t N = mesh->n_nodes, n_c = n_coarse;
   if (N < 0 || n_c < 0 || (N > 0 && n_c < 1) || n_c > N) return set_err(h, AGIPC_EINVAL, "assemble_coarse: bad sizes");

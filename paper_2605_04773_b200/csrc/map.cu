@@ -312,13 +312,6 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
   }
 }
 
-__global__ void k_clear_slots(const unsigned long long *__restrict__ ne_ptr, const unsigned long long *__restrict__ used,
-                              unsigned long long *__restrict__ table) {
-  const int64_t ne = (int64_t)*ne_ptr;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
-    table[used[e]] = 0ull;
-}
-
 #define TAIL_THREADS 1024
 #define TAIL_WARPS (TAIL_THREADS / 32)
 #define TAIL_SUB 2  // group blocks per warp per tile (a tile = TAIL_WARPS * TAIL_SUB * gpw * gs nodes)
@@ -340,6 +333,14 @@ struct TailArgs {
   unsigned *bar;           // software grid barrier counter (zeroed before launch); nullptr =
                            // cooperative launch + cg grid.sync()
   unsigned long long *trace;  // AGIPC_TAIL_TRACE: CTA 0's %globaltimer at 7 points of each level
+  // folded launches: the level-1 hash-set slots are cleared at the start (k_clear_slots) and the
+  // fine map is finished at the end (k_apply: level-0 tile prefix, then the composed map)
+  unsigned long long *table;
+  const unsigned long long *used;
+  int32_t *map;
+  int64_t n_fine;
+  const int64_t *tpref;
+  int tn0;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -407,12 +408,25 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
   int64_t n = n1;
   int level = 1, cur = 0;
   if (gtid == 0) A.level_n[0] = n1;
+  {  // the level-1 de-duplication's hash slots, cleared for the next call (k_clear_slots)
+    const int64_t ne0 = (int64_t)*(volatile unsigned long long *)A.ne;
+    for (int64_t e = gtid; e < ne0; e += gstride) A.table[A.used[e]] = 0ull;
+  }
+  // fine map = level-0 id (tile-relative value + tile prefix), then the composed tail map (k_apply)
+  auto apply = [&](bool composed) {
+    for (int64_t f = gtid; f < A.n_fine; f += gstride) {
+      const int g = (int)(A.map[f] + A.tpref[f / A.tn0]);
+      A.map[f] = composed ? A.comp[g] : g;
+    }
+  };
   if (n1 == A.N) {  // level 0 merged nothing: fixpoint after one pass
     if (gtid == 0) A.ctrl[2] = 1;
+    apply(false);
     return;
   }
   const int gin = lane / gs, lig = lane - gin * gs, base_lane = gin * gs;
   bool first_pass = true;
+  bool composed = false;  // some level's P3 composed the level maps (ctrl[3])
   while (true) {
     ++level;
     const int fl = level & 1;
@@ -558,6 +572,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       A.comp[c] = s_pref[u0 / TN] + m0;
       if (two) A.comp[c1] = s_pref[u1 / TN] + m1;
     }
+    composed = true;
     if (gtid == 0) {
       A.ctrl[fl] = 0;
       A.ctrl[3] = 1;
@@ -575,6 +590,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) k_tail(TailArgs A) {
       break;
     }
   }
+  apply(composed);  // the last composition is behind a grid barrier
 }
 
 // map[f] = comp[map[f]] if any tail level merged
@@ -679,7 +695,6 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
     const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), 8 * h->sm_count));
     LAUNCH(h, k_cross_to_level1, gedge, 256, 0, cross, &sc->cross, map, table, (unsigned long long)(tsize - 1), EA,
            &sc->ne[0], used, (const int64_t *)tpref, tn0, tiles0, &sc->nvals[0]);
-    LAUNCH(h, k_clear_slots, gedge, 256, 0, &sc->ne[0], used, table);
     TailArgs A;
     A.geo = geo;
     A.max_levels = max_levels;
@@ -703,6 +718,12 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
       trace = trw;
     }
     A.trace = trace;
+    A.table = table;
+    A.used = used;
+    A.map = map;
+    A.n_fine = N;
+    A.tpref = tpref;
+    A.tn0 = tn0;
     const size_t smem = sizeof(int32_t) * (size_t)tiles_max;
     if (smem > 200 * 1024) return set_err(h, AGIPC_ERANGE, "build_map: %lld nodes exceed the tail kernel", (long long)N);
     if (smem > h->tail_smem) {  // host-side attribute + residency check once per size (they cost
@@ -729,9 +750,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
       ps_tail.reset(new ProfScope(h, PROF_MAP_TAIL, s0));
       LAUNCH(h, k_tail, (unsigned)grid, TAIL_THREADS, smem, A);
     }
-    ps_tail.reset();
-    LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, comp, sc->ctrl, (const int64_t *)tpref, tn0, tiles0,
-           (long long *)nullptr);
+    ps_tail.reset();  // (k_tail also cleared the hash slots and finished the fine map)
   } else {  // level 0 only: the tile prefixes still have to be added
     LAUNCH(h, k_apply, (unsigned)cdiv(N, 256), 256, 0, N, map, (const int32_t *)nullptr, sc->ctrl,
            (const int64_t *)tpref, tn0, tiles0, &sc->nvals[0]);
@@ -745,6 +764,7 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
   if (st != AGIPC_OK) return st;
   CU_TRY(h, cudaMemcpyAsync(hs, sc, sizeof(MapScalars), cudaMemcpyDeviceToHost, s0));
   CU_TRY(h, host_wait(h, s0));
+  if (h->trace) trace_mark(h, "@build_map_synced");
   if (getenv("AGIPC_TAIL_TRACE") && max_levels != 1) {  // per-phase time of the tail levels (CTA 0)
     unsigned long long t[8 * 64];
     if (cudaMemcpy(t, h->ws["map_tail_trace"].ptr, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {

@@ -19,6 +19,9 @@ busy_end = base
 tot_gap = tot_k = 0.0
 print(f"{'kernel':40s} {'start':>9s} {'dur':>8s} {'gap':>7s} {'host':>9s} stream")
 for name, s, t0, t1, hs in seq:
+    if name.startswith("@"):  # host-time marker
+        print(f"{name[:40]:40s} {'':>9s} {'':>8s} {'':>7s} {hs-hbase:9.1f} host")
+        continue
     gap = max(0.0, t0 - busy_end)
     tot_gap += gap
     tot_k += t1 - t0
