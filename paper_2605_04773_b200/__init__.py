@@ -300,8 +300,14 @@ class DeviceMesh:
         return self.x_rest.shape[0] if self.n_own is None else self.n_own
 
     def c_struct(self):
-        return _Mesh(self.n_nodes, self.tets.shape[0], self.adj_nbr.shape[0], _p(self.tets), _p(self.adj_ptr),
-                     _p(self.adj_nbr), _p(self.tet_slots), _p(self.x_rest))
+        # cached per tensor identity: the struct is marshalled once, not at every call of a step
+        key = (id(self.tets), id(self.adj_ptr), id(self.adj_nbr), id(self.tet_slots), id(self.x_rest), self.n_own)
+        c = self.__dict__.get("_cstruct")
+        if c is None or c[0] != key:
+            c = (key, _Mesh(self.n_nodes, self.tets.shape[0], self.adj_nbr.shape[0], _p(self.tets), _p(self.adj_ptr),
+                            _p(self.adj_nbr), _p(self.tet_slots), _p(self.x_rest)))
+            self.__dict__["_cstruct"] = c
+        return c[1]
 
     @staticmethod
     def from_arrays(tets, adj_ptr, adj_nbr, tet_slots, x_rest, device="cuda", n_own=None):
@@ -337,7 +343,7 @@ def build_map(h: Handle, mesh: DeviceMesh, slot_tags, group_size: int = 32, max_
                                    _p(agg_size), C.byref(info)))
     L = info.n_levels
     return map, dict(n_coarse=int(info.n_coarse), n_levels=int(L),
-                     level_n=[int(info.level_n[i]) for i in range(min(L, 64))],
+                     level_n=list(info.level_n[:min(L, 64)]),
                      n_cross_edges=int(info.n_cross_edges))
 
 
