@@ -74,10 +74,14 @@ __device__ __forceinline__ void green(const double Ds[3][3], const double M[3][3
     }
 }
 
-#ifndef TAG_MINB
-#define TAG_MINB 4  // 64 registers: 3 (80 regs) and 5 (48 regs + spills) measured slower (profiles/r02v)
+// (launch bounds without a minimum: 64 registers, no spills; 3 / 4 / 5 CTAs per SM pinned gave
+// 80 / 64 + spill / 48 + spill registers and were slower, profiles/r02v)
+#ifdef TAG_MINB
+__global__ void __launch_bounds__(TAG_THREADS, TAG_MINB) k_tag(int64_t n_tets,
+#else
+__global__ void __launch_bounds__(TAG_THREADS) k_tag(int64_t n_tets,
 #endif
-__global__ void __launch_bounds__(TAG_THREADS, TAG_MINB) k_tag(int64_t n_tets, const int4 *__restrict__ tets,
+                                                     const int4 *__restrict__ tets,
                                                      const int4 *__restrict__ tet_slots,
                                                      const double *__restrict__ X,
                                                      const double *__restrict__ xp,
