@@ -38,7 +38,7 @@ struct AsmScal {
   long long n3, n12, n_slots, nnzb;
   long long nbs_count;   // entries used in the small-node neighbour buffer
   long long list_top;    // entries allocated in the large-row entry lists (k_sym_large)
-  long long n_w32;       // nodes of the 32-entry small list (k_final_scalars)
+  long long n_w32;       // nodes of the 32-entry small list (k_sym_finish)
   long long pair_count;  // (large, x) pairs
   long long big_groups;  // large lists that need the CTA sort
   long long n_large3;    // large nodes with 3 DoF (affine threshold > 32)
@@ -47,7 +47,7 @@ struct AsmScal {
   int err_map;           // map value outside [0, n_c)
   int err_overflow;      // a buffer capacity was exceeded
   int err_cap;           // the numeric pass must not write: an error above, a slot count past
-                         // int32 or outputs larger than the caller's capacity (k_final_scalars)
+                         // int32 or outputs larger than the caller's capacity (k_sym_finish)
 };
 
 __device__ __forceinline__ int slot_of(int c, int p, long long n3) {
@@ -207,7 +207,7 @@ __global__ void k_classify(int64_t n_c, const int32_t *__restrict__ size_new,
 #define PAIR_BUF 128
 // Each (large row, column) pair may carry an ORIGIN: the index of a mirror-position slot
 // (A.mir) of the small row that emitted it; after the large rows' lists are final,
-// k_mirror_pos writes there the column position of the small row inside the large row, so the
+// k_sym_finish writes there the column position of the small row inside the large row, so the
 // numeric pass mirrors B_ij^T (R22) without a binary search (-1: no origin).
 struct PairBuf {
   int2 v[PAIR_BUF];
@@ -619,11 +619,12 @@ __global__ void k_pair_count(const AsmScal *sc, long long cap, const int2 *__res
 
 // padded group sizes: next power of two (so every group can be sorted in place)
 __global__ void k_pair_scatter(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
-                               unsigned long long *__restrict__ cursor, int32_t *__restrict__ gbuf) {
+                               const int64_t *__restrict__ gptr, int32_t *__restrict__ gcur,
+                               int32_t *__restrict__ gbuf) {
   const long long np = min(sc->pair_count, cap);
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
     int2 q = pairs[p];
-    gbuf[atomicAdd(cursor + q.x, 1ull)] = q.y;
+    gbuf[gptr[q.x] + atomicAdd(gcur + q.x, 1)] = q.y;  // gcur zeroed with gcnt
   }
 }
 
@@ -705,21 +706,36 @@ __global__ void __launch_bounds__(1024) k_group_unique_big(const AsmScal *sc, co
   }
 }
 
-// Mirror positions: for every pair with an origin (a small row a meeting the large column b),
-// the BLOCK INDEX of (slot(b, 0), a) in the final coarse BSR -- row start + column position of a
-// inside b's row -- and b's slot-row length, so the numeric pass writes the mirrored block
-// (slot(b, q), slot(a, p)) at mirpos + q * rowlen(b) + p with no further lookup (independent
-// binary searches, thread per pair; runs after the slot row pointer scan).  Heads of runs with a
-// small column keep the -1 written by the symbolic pass.
-__global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
-                             const long long *__restrict__ porig, const int32_t *__restrict__ gbuf,
-                             const long long *__restrict__ nb_off, const int32_t *__restrict__ nb_cnt,
-                             const int32_t *__restrict__ f12, const int32_t *__restrict__ rowlen,
-                             const int64_t *__restrict__ crp, long long *__restrict__ mirpos,
+// ------------------------------------------------------------------------------------
+// C. slot row lengths
+// ------------------------------------------------------------------------------------
+// End of the symbolic pass in ONE launch (was k_final_scalars + k_mirror_pos + k_copy_rowptr):
+// every block derives the capacity / error verdict itself (block 0 also stores the scalars), then
+// grid-stride loops copy the slot row pointer out and place the small rows' mirror positions.
+__global__ void k_sym_finish(AsmScal *sc, const int64_t *__restrict__ crp, const int64_t *__restrict__ task_ptr,
+                             int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound, int64_t cap_slots,
+                             int64_t cap_nnzb, const int64_t *__restrict__ cnt32, int64_t *__restrict__ row_ptr_out,
+                             long long cap, const int2 *__restrict__ pairs, const long long *__restrict__ porig,
+                             const int32_t *__restrict__ gbuf, const long long *__restrict__ nb_off,
+                             const int32_t *__restrict__ nb_cnt, const int32_t *__restrict__ f12,
+                             const int32_t *__restrict__ rowlen, long long *__restrict__ mirpos,
                              int32_t *__restrict__ mirrl) {
+  const long long n_slots = sc->n_slots, n3 = sc->n3;
+  const long long nnzb = crp[n_slots];
+  const bool bad = sc->err_map || sc->err_overflow || n_slots >= INT32_MAX || n_slots > cap_slots || nnzb > cap_nnzb;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->nnzb = nnzb;
+    sc->n_tasks = task_ptr[n_c];
+    sc->rec_total = rec_off[task_bound];
+    sc->n_w32 = *cnt32;
+    sc->err_cap = bad;
+  }
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (!bad)
+    for (long long i = tid; i <= n_slots; i += stride) row_ptr_out[i] = crp[i];
   const long long np = min(sc->pair_count, cap);
-  const long long n3 = sc->n3;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
+  for (long long p = tid; p < np; p += stride) {
     const long long o = porig[p];
     if (o < 0) continue;
     const int2 q = pairs[p];
@@ -727,28 +743,6 @@ __global__ void k_mirror_pos(const AsmScal *sc, long long cap, const int2 *__res
     mirpos[o] = crp[slot_of(q.x, 0, n3)] + colpos(idx, f12[q.x]);
     mirrl[o] = rowlen[q.x];
   }
-}
-
-// ------------------------------------------------------------------------------------
-// C. slot row lengths
-// ------------------------------------------------------------------------------------
-__global__ void k_final_scalars(AsmScal *sc, const int64_t *__restrict__ row_ptr, const int64_t *__restrict__ task_ptr,
-                                int64_t n_c, const int64_t *__restrict__ rec_off, int64_t task_bound,
-                                int64_t cap_slots, int64_t cap_nnzb, const int64_t *__restrict__ cnt32) {
-  sc->nnzb = row_ptr[sc->n_slots];
-  sc->n_w32 = *cnt32;
-  sc->n_tasks = task_ptr[n_c];
-  sc->rec_total = rec_off[task_bound];
-  sc->err_cap = sc->err_map || sc->err_overflow || sc->n_slots >= INT32_MAX || sc->n_slots > cap_slots ||
-                sc->nnzb > cap_nnzb;
-}
-
-// out row pointer = the slot row pointer (n_slots + 1 entries; nothing if the outputs do not fit)
-__global__ void k_copy_rowptr(const AsmScal *sc, const int64_t *__restrict__ src, int64_t *__restrict__ dst) {
-  if (sc->err_cap) return;
-  const long long n = sc->n_slots + 1;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------------------------
@@ -816,7 +810,7 @@ struct WarpArgs {
   int32_t *rowlen;
   int2 *pairs;
   long long *porig;
-  long long *mirpos;           // mirror block positions (k_mirror_pos), indexed like mkeys from
+  long long *mirpos;           // mirror block positions (k_sym_finish), indexed like mkeys from
   int32_t *mirrl;              //   mir_base; -1 = the run's column is small (no mirror)
   long long mir_base;
   long long pair_cap;
@@ -999,7 +993,7 @@ __global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
         for (int q = 0; q < ncb_b; ++q) s_desc[w][sg * 4 * SEG + cp + q] = sl | (tl << 6) | (q << 12);
         s_rbs[w][l] = bs;
         // mirrored block (slot(bs, q), slot(a, p)) at mb + q * mrl + p (B_ji = B_ij^T, reading R22)
-        s_rmb[w][l] = A.mirpos[A.mir_base + wi * SEG + sl];  // k_mirror_pos (-1: small column)
+        s_rmb[w][l] = A.mirpos[A.mir_base + wi * SEG + sl];  // k_sym_finish (-1: small column)
         s_rml[w][l] = A.mirrl[A.mir_base + wi * SEG + sl];
       }
       if (sl == 0) {
@@ -1261,7 +1255,7 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
         const int ncb_b = valid ? ncb_of(b, n3) : 1;
         const int Q = __ballot_sync(FULL_MASK, valid && ncb_b == 4) ? 4 : 1;
         const int he = hl < 0 ? carry_he : e0 + hl;  // sorted position of my run's head
-        long long mbase = -1;  // mirrored block of (b, a): mbase + q * mrl + p (R22, k_mirror_pos)
+        long long mbase = -1;  // mirrored block of (b, a): mbase + q * mrl + p (R22, k_sym_finish)
         int mrl = 0;
         if (tail) {
           mbase = A.mirpos[mir0 + he];
@@ -2320,7 +2314,7 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   WS(h, pairs, int2, "asm_pairs", pair_cap);
   WS(h, porig, long long, "asm_pair_orig", pair_cap);
   WS(h, f12, int32_t, "asm_first12", n_c);
-  WS(h, gcnt, int32_t, "asm_gcnt", n_c);
+  WS(h, gcnt, int32_t, "asm_gcnt", 2 * n_c);  // [count | scatter cursor]
   WS(h, gptr, int64_t, "asm_gptr", n_c + 1);
   WS(h, gbuf, int32_t, "asm_gbuf", 2 * pair_cap);
   WS(h, big_list, int32_t, "asm_big_list", n_c);
@@ -2404,12 +2398,12 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   // the mid nodes follow the large rows on the aux stream: the small rows alone are the longer stream
   LAUNCH_S(h, h->aux, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   if ((st = aux_join(h)) != AGIPC_OK) return st;
-  CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * n_c, st_));
+  CU_TRY(h, cudaMemsetAsync(gcnt, 0, sizeof(int32_t) * 2 * n_c, st_));
   LAUNCH(h, k_pair_count, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, gcnt);
   // bucket offsets: power-of-two padded counts (k_group_unique sorts in place), evaluated by the scan
   if ((st = scan_exclusive_i64(h, SCAN_SRC_POW2, gcnt, n_c, gptr)) != AGIPC_OK) return st;
-  CU_TRY(h, cudaMemcpyAsync(cursor, gptr, sizeof(int64_t) * n_c, cudaMemcpyDeviceToDevice, st_));
-  LAUNCH(h, k_pair_scatter, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, cursor, gbuf);
+  LAUNCH(h, k_pair_scatter, (unsigned)(8 * h->sm_count), 256, 0, sc, pair_cap, pairs, (const int64_t *)gptr,
+         gcnt + n_c, gbuf);
   const unsigned gsym = (unsigned)std::min<int64_t>(cdiv(n_c, SYM_WARPS), 64 * h->sm_count);
   LAUNCH(h, k_group_unique, gsym, SYM_WARPS * 32, 0, n_c, is_small, gptr, gbuf, gcnt, nb_off, nb_cnt, rowlen,
          big_list, sc, f12);
@@ -2430,16 +2424,14 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     jobs.j[1] = scan_job(SCAN_SRC_I32, recmax, task_bound, rec_off);
     if ((st = scan_multi(h, jobs)) != AGIPC_OK) return st;
   }
-  LAUNCH(h, k_final_scalars, 1, 1, 0, sc, crp_ws, (const int64_t *)task_ptr, n_c, (const int64_t *)rec_off, task_bound,
-         out->cap_slots, out->cap_nnzb, (const int64_t *)(i32 + n_c));
-  LAUNCH(h, k_mirror_pos, (unsigned)(8 * h->sm_count), 256, 0, (const AsmScal *)sc, pair_cap, (const int2 *)pairs,
-         (const long long *)porig, (const int32_t *)gbuf, (const long long *)nb_off, (const int32_t *)nb_cnt,
-         (const int32_t *)f12, (const int32_t *)rowlen, (const int64_t *)crp_ws, mirpos, mirrl);
-  // one host round trip per call, here: the sizes and error flags come back while the numeric
-  // pass is still to be enqueued (it then runs asynchronously to the caller); the capacity check
-  // is also on the device (k_final_scalars sets err_cap: every numeric kernel writes nothing)
-  LAUNCH(h, k_copy_rowptr, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(slot_bound + 1, 256), 4 * h->sm_count)),
-         256, 0, (const AsmScal *)sc, (const int64_t *)crp_ws, out->row_ptr);
+  // one host round trip per call, after this: the sizes and error flags come back while the
+  // numeric pass is still to be enqueued (it then runs asynchronously to the caller); the capacity
+  // check is also on the device (err_cap: every numeric kernel writes nothing)
+  LAUNCH(h, k_sym_finish, (unsigned)(8 * h->sm_count), 256, 0, sc, (const int64_t *)crp_ws, (const int64_t *)task_ptr,
+         n_c, (const int64_t *)rec_off, task_bound, out->cap_slots, out->cap_nnzb, (const int64_t *)(i32 + n_c),
+         out->row_ptr, pair_cap, (const int2 *)pairs, (const long long *)porig, (const int32_t *)gbuf,
+         (const long long *)nb_off, (const int32_t *)nb_cnt, (const int32_t *)f12, (const int32_t *)rowlen, mirpos,
+         mirrl);
   CU_TRY(h, cudaMemcpyAsync(hsc, sc, sizeof(AsmScal), cudaMemcpyDeviceToHost, st_));
   CU_TRY(h, host_wait(h, st_));
   if (hsc->err_map) return set_err(h, AGIPC_EINVAL, "assemble_coarse: map value outside [0, n_coarse)");
