@@ -1420,6 +1420,12 @@ __global__ void k_large_rows_init(int64_t n_c, const AsmScal *sc, const uint8_t 
 // by the small row, reading R22).  Phase 2: lane = (block group g, p) streams the diagonal list
 // two blocks per group in flight and accumulates acc[q][x] += w_i[p] w_j[q] B_ij[x] (Eq 4) in
 // registers; a final reduction over g and one fp64 atomic per entry per chunk.
+#ifndef LIST_ISTAGE
+#define LIST_ISTAGE 192  // k_num_large_list: interface entries staged per batch
+#endif
+#ifndef LIST_MINB
+#define LIST_MINB 4  // k_num_large_list CTAs per SM (128 registers)
+#endif
 #ifndef LSTAGE_A
 #define LSTAGE_A 192
 #endif
@@ -1704,15 +1710,15 @@ __global__ void __launch_bounds__(128, NB > 2 ? 3 : LARGE_MINB) k_num_large_atom
 // ONE dependent latency (its 72-B blocks and X_bar of the column nodes); the interface entries
 // are staged from their list and reduced per column aggregate as before.
 template <int NCB>
-__global__ void __launch_bounds__(128, 4) k_num_large_list(LargeArgs A) {
+__global__ void __launch_bounds__(128, LIST_MINB) k_num_large_list(LargeArgs A) {
   if (A.sc->err_cap || (NCB == 1 && A.sc->n_large3 == 0)) return;
-  __shared__ long long s_k[4][LSTAGE_A];
-  __shared__ int s_i[4][LSTAGE_A];
-  __shared__ int s_b[4][LSTAGE_A];
-  __shared__ double s_xj[4][LSTAGE_A][3];
+  __shared__ long long s_k[4][LIST_ISTAGE];
+  __shared__ int s_i[4][LIST_ISTAGE];
+  __shared__ int s_b[4][LIST_ISTAGE];
+  __shared__ double s_xj[4][LIST_ISTAGE][3];
   __shared__ double s_wc[4][32][3];      // X_bar of the chunk's children (w_i)
   __shared__ double s_B[4][32][9];       // 32 blocks staged per warp (one per lane)
-  __shared__ int s_ix[4][LSTAGE_A];
+  __shared__ int s_ix[4][LIST_ISTAGE];
   const int w = threadIdx.x >> 5, l = lane_id();
   constexpr int LPB = NCB == 4 ? 8 : 1, QN = NCB == 4 ? 2 : 1, G = 32 / LPB;
   const int gq = l / LPB, p = NCB == 4 ? (l >> 1) & 3 : 0, q0 = NCB == 4 ? (l & 1) * 2 : 0;
@@ -1799,13 +1805,13 @@ __global__ void __launch_bounds__(128, 4) k_num_large_list(LargeArgs A) {
           for (int x = 0; x < 9; ++x) atomicAdd(A.cval + 9 * (rs + cpa + q0 + qq) + x, acc[qq][x]);
       }
     }
-    // interface entries: batches of LSTAGE_A staged from the list, one pass per distinct column
+    // interface entries: batches of LIST_ISTAGE staged from the list, one pass per distinct column
     // aggregate b0 (its entries compacted, their blocks staged 32 at a time), one set of atomics
     // per (a, b0, batch)
     const int32_t *lst = A.gbuf + A.nb_off[a];
     const int U = A.nb_cnt[a];
-    for (int ibase = 0; ibase < ni; ibase += LSTAGE_A) {
-      const int icnt = min(LSTAGE_A, ni - ibase);
+    for (int ibase = 0; ibase < ni; ibase += LIST_ISTAGE) {
+      const int icnt = min(LIST_ISTAGE, ni - ibase);
       for (int e = l; e < icnt; e += 32) {
         const long long o = lib + ibase + e;
         const long long ek = A.lent[o];
