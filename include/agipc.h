@@ -27,7 +27,11 @@
  *    caller pointer between calls.
  *  - Every kernel is enqueued on the handle's stream (agipc_set_stream; default: the
  *    legacy default stream).  Calls that return a data-dependent size in a [host] argument
- *    synchronise that stream before returning; the others are asynchronous.
+ *    synchronise that stream before returning; the others are asynchronous.  build_map,
+ *    assemble_coarse and the PCG status polls wait by spinning on a CUDA event (the calling
+ *    thread stays busy; no blocking-sync wake-up latency while the GPU idles).
+ *    assemble_coarse returns once the sizes are known; its numeric pass is still running on
+ *    the stream (and on an internal second stream joined back into it).
  *  - Errors are returned as agipc_status, never thrown or aborted; agipc_last_error()
  *    returns a human-readable message for the last failing call on that handle.
  *  - Index types: node, slot and column ids are int32 (sizes >= 2^31-1 return
