@@ -33,6 +33,13 @@
 #define ACC_CAP 1024
 #define LARGE_CHUNK 32
 #define SMALL_T 1024           // small nodes: <= 32 children and <= 1024 candidate entries
+// CTAs per SM requested by the launch bounds (experiment knobs, defaults = measured best)
+#ifndef SMALL_MINB_S
+#define SMALL_MINB_S 6  // symbolic small rows: 40 registers, 6 x 8 warps per SM (profiles/r02v)
+#endif
+#ifndef MID_MINB_S
+#define MID_MINB_S 6    // symbolic mid nodes: 80 registers (the register sort), 6 x 4 warps per SM
+#endif
 
 struct AsmScal {
   long long n3, n12, n_slots, nnzb;
@@ -843,7 +850,7 @@ __device__ __forceinline__ void warp_args_resolve(WarpArgs &A) {
 }
 
 template <int SEG, bool NUMERIC>
-__global__ void __launch_bounds__(256, 4) k_small_warp(WarpArgs A) {
+__global__ void __launch_bounds__(256, NUMERIC ? 4 : SMALL_MINB_S) k_small_warp(WarpArgs A) {
   if (NUMERIC && A.sc->err_cap) return;  // outputs do not fit / bad input: write nothing
   warp_args_resolve(A);
   constexpr int NSEG = 32 / SEG;
@@ -1109,7 +1116,11 @@ __device__ __forceinline__ void mid_keys_sorted(const WarpArgs &A, const ChildTa
 }
 
 template <bool NUMERIC>
+#ifdef MID_MINB_S  // the numeric mid pass keeps the plain bounds (126 registers)
+__global__ void __launch_bounds__(MID_WARPS * 32, NUMERIC ? 1 : MID_MINB_S) k_mid_warp(WarpArgs A) {
+#else
 __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
+#endif
   if (NUMERIC && A.sc->err_cap) return;
   warp_args_resolve(A);
   __shared__ ChildTab s_tab[MID_WARPS];
