@@ -34,6 +34,12 @@
 #define LARGE_CHUNK 32
 #define SMALL_T 1024           // small nodes: <= 32 children and <= 1024 candidate entries
 // CTAs per SM requested by the launch bounds (experiment knobs, defaults = measured best)
+#ifndef SMALL_MINB_N
+#define SMALL_MINB_N 4  // numeric small rows: 64 registers
+#endif
+#ifndef MID_MINB_N
+#define MID_MINB_N 1    // numeric mid nodes: 128 registers
+#endif
 #ifndef SMALL_MINB_S
 #define SMALL_MINB_S 6  // symbolic small rows: 40 registers, 6 x 8 warps per SM (profiles/r02v)
 #endif
@@ -850,7 +856,7 @@ __device__ __forceinline__ void warp_args_resolve(WarpArgs &A) {
 }
 
 template <int SEG, bool NUMERIC>
-__global__ void __launch_bounds__(256, NUMERIC ? 4 : SMALL_MINB_S) k_small_warp(WarpArgs A) {
+__global__ void __launch_bounds__(256, NUMERIC ? SMALL_MINB_N : SMALL_MINB_S) k_small_warp(WarpArgs A) {
   if (NUMERIC && A.sc->err_cap) return;  // outputs do not fit / bad input: write nothing
   warp_args_resolve(A);
   constexpr int NSEG = 32 / SEG;
@@ -1117,7 +1123,7 @@ __device__ __forceinline__ void mid_keys_sorted(const WarpArgs &A, const ChildTa
 
 template <bool NUMERIC>
 #ifdef MID_MINB_S  // the numeric mid pass keeps the plain bounds (126 registers)
-__global__ void __launch_bounds__(MID_WARPS * 32, NUMERIC ? 1 : MID_MINB_S) k_mid_warp(WarpArgs A) {
+__global__ void __launch_bounds__(MID_WARPS * 32, NUMERIC ? MID_MINB_N : MID_MINB_S) k_mid_warp(WarpArgs A) {
 #else
 __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
 #endif
