@@ -312,9 +312,13 @@ __global__ void k_cross_to_level1(const int2 *__restrict__ E, const unsigned lon
   }
 }
 
+#ifndef TAIL_THREADS
 #define TAIL_THREADS 1024
+#endif
 #define TAIL_WARPS (TAIL_THREADS / 32)
+#ifndef TAIL_SUB
 #define TAIL_SUB 2  // group blocks per warp per tile (a tile = TAIL_WARPS * TAIL_SUB * gpw * gs nodes)
+#endif
 
 struct TailArgs {
   GroupGeom geo;
