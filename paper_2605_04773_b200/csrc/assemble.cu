@@ -519,7 +519,10 @@ struct LargeArgs {
 #define ITF_CAP 160      // staged large-large interface entries of a chunk (flushed when full)
 
 #define SEEN_CAP 128
-__global__ void __launch_bounds__(128) k_sym_large(LargeArgs A) {
+#ifndef SYML_MINB
+#define SYML_MINB 16  // 32 registers, 64 warps per SM: symbolic -27 us vs 48 registers (profiles/r02v)
+#endif
+__global__ void __launch_bounds__(128, SYML_MINB) k_sym_large(LargeArgs A) {
   __shared__ ChildTab s_tab[4];
   __shared__ int s_seen[4][SEEN_CAP];  // large columns already emitted by this chunk
   __shared__ PairBuf s_pb[4];

@@ -131,7 +131,11 @@ __device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles
 #define L0_CHUNKS 4
 #define L0_XCAP 256
 
+#ifdef L0_MINB  // (6 / 8 CTAs per SM measured slower: 40 / 32 registers with spills, profiles/r02v)
+__global__ void __launch_bounds__(MAP_THREADS, L0_MINB)
+#else
 __global__ void __launch_bounds__(MAP_THREADS)
+#endif
     k_level0(int64_t n, GroupGeom geo, const int64_t *__restrict__ adj_ptr, const int32_t *__restrict__ adj_nbr,
              const uint8_t *__restrict__ tags, int32_t *__restrict__ map_out, int2 *__restrict__ cross,
              unsigned long long *__restrict__ cross_count, int32_t *__restrict__ tile_cnt, int *tile_counter) {
