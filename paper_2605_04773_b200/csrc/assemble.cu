@@ -2481,8 +2481,6 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   // ---- D. numeric ----
   if (gfp) CU_TRY(h, cudaMemsetAsync(out->g_c, 0, sizeof(double) * 3 * out->n_slots, st_));
   WS(h, dpos, int32_t, "asm_dpos", n_c);
-  LAUNCH(h, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr, out->col,
-         out->val, dpos);
   LA.f12 = f12;
   LA.dpos = dpos;
   // the 12-DoF chunks and the small / mid rows write disjoint blocks -- (large, large) by the
@@ -2493,6 +2491,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
   const bool fork = num_mode == 0;
   cudaStream_t ls = fork ? h->aux : st_;
   if (fork && (st = aux_fork(h)) != AGIPC_OK) return st;
+  // the large rows' column ids / zeroed blocks only gate the 12-DoF chunks: on their stream, so the
+  // small rows start at once (the small rows' mirrored values go to other words of those rows)
+  LAUNCH_S(h, ls, k_large_rows_init, gsym, 128, 0, n_c, sc, is_small, gbuf, nb_off, nb_cnt, rowlen, out->row_ptr,
+           out->col, out->val, dpos);
   auto launch_large = [&]() -> agipc_status {
     LA.crp = out->row_ptr; LA.cval = out->val;
     // (a factorised variant -- lane per child, C_i[q] = sum_j w_j[q] B_ij, then sum_i w_i[p] C_i[q] --
