@@ -460,16 +460,28 @@ __device__ __forceinline__ int warp_unique_store(const int *buf, int n, int32_t 
 // ------------------------------------------------------------------------------------
 // Large nodes: 32-children chunks emit (a, b) for every large column b != a (warp de-dup with
 // __match_any_sync; duplicates across chunks are removed by the per-node sort), and (a, a).
-__global__ void k_fine_class(int64_t N, const int32_t *__restrict__ nm, const uint8_t *__restrict__ is_small,
-                             uint8_t *__restrict__ fcls) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f < N) fcls[f] = is_small[nm[f]];
-}
-
-__global__ void k_task_node(int64_t n_c, const int64_t *__restrict__ task_ptr, int32_t *__restrict__ task_node) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_c)
+// k_task_node + k_fine_class + k_small_lists in one launch (independent once the scans are done):
+// thread c < n_c writes the owner of its chunks and its small-list entries, thread f < N the
+// class of fine node f
+__global__ void k_class_lists(int64_t N, int64_t n_c, const int64_t *__restrict__ task_ptr, int32_t *__restrict__ task_node,
+                              const int32_t *__restrict__ nm, const uint8_t *__restrict__ is_small,
+                              uint8_t *__restrict__ fcls, const int32_t *__restrict__ f16,
+                              const int32_t *__restrict__ f32, const int32_t *__restrict__ ft,
+                              const int64_t *__restrict__ i16, const int64_t *__restrict__ i32,
+                              const int64_t *__restrict__ it, const unsigned long long *__restrict__ rowsum,
+                              int32_t *__restrict__ w16, int32_t *__restrict__ w32, int32_t *__restrict__ tlist,
+                              int64_t *__restrict__ ecount) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < N) fcls[c] = is_small[nm[c]];
+  if (c < n_c) {
     for (int64_t t = task_ptr[c]; t < task_ptr[c + 1]; ++t) task_node[t] = (int32_t)c;
+    if (f16[c]) w16[i16[c]] = (int32_t)c;
+    if (f32[c]) w32[i32[c]] = (int32_t)c;
+    if (ft[c]) {
+      tlist[it[c]] = (int32_t)c;
+      ecount[it[c]] = (int64_t)rowsum[c];
+    }
+  }
 }
 
 struct LargeArgs {
@@ -1359,22 +1371,6 @@ __global__ void __launch_bounds__(MID_WARPS * 32) k_mid_warp(WarpArgs A) {
 }
 
 // split the small nodes into the warp list (<= 32 entries) and the tile list (> 32)
-__global__ void k_small_lists(int64_t n_c, const int32_t *__restrict__ f16, const int32_t *__restrict__ f32,
-                              const int32_t *__restrict__ ft, const int64_t *__restrict__ i16,
-                              const int64_t *__restrict__ i32, const int64_t *__restrict__ it,
-                              const unsigned long long *__restrict__ rowsum, int32_t *__restrict__ w16,
-                              int32_t *__restrict__ w32, int32_t *__restrict__ tlist, int64_t *__restrict__ ecount) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_c) {
-    if (f16[c]) w16[i16[c]] = (int32_t)c;
-    if (f32[c]) w32[i32[c]] = (int32_t)c;
-    if (ft[c]) {
-      tlist[it[c]] = (int32_t)c;
-      ecount[it[c]] = (int64_t)rowsum[c];
-    }
-  }
-}
-
 // ------------------------------------------------------------------------------------
 // D. numeric
 // ------------------------------------------------------------------------------------
@@ -2319,10 +2315,9 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     if ((st = scan_multi(h, jobs)) != AGIPC_OK) return st;
   }
   WS(h, task_node, int32_t, "asm_task_node", N / LARGE_CHUNK + n_c + 1);
-  LAUNCH(h, k_task_node, gC, 256, 0, n_c, (const int64_t *)task_ptr, task_node);
   WS(h, fcls, uint8_t, "asm_fcls", N);
-  LAUNCH(h, k_fine_class, gN, 256, 0, N, (const int32_t *)out->new_map, (const uint8_t *)is_small, fcls);
-  LAUNCH(h, k_small_lists, gC, 256, 0, n_c, f16, f32, small_i32, i16, i32, sidx, rowsum, w16, w32, small_list, ecount);
+  LAUNCH(h, k_class_lists, gN, 256, 0, N, n_c, (const int64_t *)task_ptr, task_node, (const int32_t *)out->new_map,
+         (const uint8_t *)is_small, fcls, f16, f32, small_i32, i16, i32, sidx, rowsum, w16, w32, small_list, ecount);
   AsmScal *hsc = (AsmScal *)pinned_get(h, sizeof(AsmScal) + 64, &st);
   if (st != AGIPC_OK) return st;
   // the list sizes stay on the device (i16[n_c], i32[n_c], sidx[n_c]): the symbolic and numeric
