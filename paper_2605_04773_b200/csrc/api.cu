@@ -374,7 +374,9 @@ int agipc_profile_read(agipc_handle h, agipc_profile_entry *out, int cap) {
 // Generic single-pass exclusive scan (decoupled look-back), 2048 items per CTA tile.
 // ------------------------------------------------------------------------------------
 #define SCAN_THREADS 256
-#define SCAN_ITEMS 8
+#ifndef SCAN_ITEMS
+#define SCAN_ITEMS 4  // 1024-item tiles (8: 2048 and 16: 4096 measured slower, profiles/r02v)
+#endif
 #define SCAN_TILE (SCAN_THREADS * SCAN_ITEMS)
 
 // Several independent scans in ONE launch (scan_multi): tiles are claimed from one counter in

@@ -641,8 +641,13 @@ __global__ void __launch_bounds__(128, SYML_MINB) k_sym_large(LargeArgs A) {
 __global__ void k_pair_count(const AsmScal *sc, long long cap, const int2 *__restrict__ pairs,
                              int32_t *__restrict__ gcnt) {
   const long long np = min(sc->pair_count, cap);
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x)
-    atomicAdd(gcnt + pairs[p].x, 1);
+  // consecutive pairs mostly share their large row: one atomic per distinct row of the warp
+  for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < np; b0 += (long long)gridDim.x * blockDim.x) {
+    const long long p = b0 + threadIdx.x;
+    const int key = p < np ? pairs[p].x : -1;
+    const unsigned peers = __match_any_sync(FULL_MASK, key);
+    if (key >= 0 && (__ffs(peers) - 1) == lane_id()) atomicAdd(gcnt + key, __popc(peers));
+  }
 }
 
 // padded group sizes: next power of two (so every group can be sorted in place)
@@ -650,9 +655,15 @@ __global__ void k_pair_scatter(const AsmScal *sc, long long cap, const int2 *__r
                                const int64_t *__restrict__ gptr, int32_t *__restrict__ gcur,
                                int32_t *__restrict__ gbuf) {
   const long long np = min(sc->pair_count, cap);
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (long long)gridDim.x * blockDim.x) {
-    int2 q = pairs[p];
-    gbuf[gptr[q.x] + atomicAdd(gcur + q.x, 1)] = q.y;  // gcur zeroed with gcnt
+  for (long long b0 = (long long)blockIdx.x * blockDim.x; b0 < np; b0 += (long long)gridDim.x * blockDim.x) {
+    const long long p = b0 + threadIdx.x;
+    const int2 q = p < np ? pairs[p] : make_int2(-1, 0);
+    const unsigned peers = __match_any_sync(FULL_MASK, q.x);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (q.x >= 0 && leader == lane_id()) base = atomicAdd(gcur + q.x, __popc(peers));  // gcur zeroed with gcnt
+    base = __shfl_sync(FULL_MASK, base, leader);
+    if (q.x >= 0) gbuf[gptr[q.x] + base + __popc(peers & ((1u << lane_id()) - 1u))] = q.y;
   }
 }
 
