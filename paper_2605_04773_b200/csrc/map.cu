@@ -128,7 +128,9 @@ __device__ __forceinline__ void group_tile(TileSmem &S, int tile, int64_t ntiles
 // hash bit with a shared atomicOr (Alg S1 l.10-13), tagged cross-group edges (u > v) are
 // compacted warp-wide (one global atomic per 32 entries).  Then the register closure /
 // election of group_tile per chunk, and one decoupled look-back per CTA tile.
-#define L0_CHUNKS 4
+#ifndef L0_CHUNKS
+#define L0_CHUNKS 1  // chunks of groups per warp per tile (2 / 4 / 8 measured slower: 98 / 105 / 164 vs 94.5 us at C3, profiles/r02v)
+#endif
 #define L0_XCAP 256
 
 #ifdef L0_MINB  // (6 / 8 CTAs per SM measured slower: 40 / 32 registers with spills, profiles/r02v)
@@ -700,7 +702,10 @@ extern "C" agipc_status agipc_build_map(agipc_handle h, const agipc_mesh *mesh, 
       if (fresh) CU_TRY(h, cudaMemsetAsync(table, 0, h->ws["map_hash"].bytes, s0));
     }
     CU_TRY(h, cudaMemsetAsync(hh, 0, sizeof(uint32_t) * N, s0));
-    const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), 8 * h->sm_count));
+#ifndef CROSS_GRID
+#define CROSS_GRID 8  // CTAs per SM of the level-1 edge de-duplication
+#endif
+    const unsigned gedge = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(ecap, 256), CROSS_GRID * h->sm_count));
     LAUNCH(h, k_cross_to_level1, gedge, 256, 0, cross, &sc->cross, map, table, (unsigned long long)(tsize - 1), EA,
            &sc->ne[0], used, (const int64_t *)tpref, tn0, tiles0, &sc->nvals[0]);
     TailArgs A;
