@@ -2387,7 +2387,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     WB.mirrl = mirrl;
   }
   // grid-stride kernels; the 32-entry list is usually short or empty (persistent grid)
-  const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, 16), 32 * h->sm_count));
+#ifndef SMALL_GRID
+#define SMALL_GRID 32  // CTAs per SM of the 16-entry small-row kernels
+#endif
+  const unsigned g16 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, 16), SMALL_GRID * h->sm_count));
   const unsigned g32 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, 8), 4 * h->sm_count));
   // the large-row symbolic pass runs on the aux stream next to the small / mid rows' (both
   // latency-bound at partial occupancy; they only share the atomic pair counter)
@@ -2426,7 +2429,11 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     WS(h, lni, int32_t, "asm_lni", task_bound + 1);
     LA.lent = lent; LA.lj = lj; LA.lb = lb; LA.lbase = lbase; LA.lib = lib; LA.lnd = lnd; LA.lni = lni;
   }
-  LAUNCH_S(h, h->aux, k_sym_large, glarge, 128, 0, LA);
+#ifndef SYML_GRID
+#define SYML_GRID 64  // CTAs per SM of the large-row symbolic pass
+#endif
+  LAUNCH_S(h, h->aux, k_sym_large, (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), SYML_GRID * h->sm_count),
+           128, 0, LA);
   // the mid nodes follow the large rows on the aux stream: the small rows alone are the longer stream
   LAUNCH_S(h, h->aux, k_mid_warp<false>, gmid, MID_WARPS * 32, 0, WM);
   if ((st = aux_join(h)) != AGIPC_OK) return st;
@@ -2508,8 +2515,12 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     // active; profiles/r02f)
     if (!h->opt_deterministic) {  // 2 diagonal blocks per group in flight: 3 or 4 measured slower (r01h)
       if (LA.lent) {
-        LAUNCH_S(h, ls, k_num_large_list<4>, glarge, 128, 0, LA);
-        if (hsc->n_large3 > 0) LAUNCH_S(h, ls, k_num_large_list<1>, glarge, 128, 0, LA);
+#ifndef LIST_GRID
+#define LIST_GRID 8  // CTAs per SM: persistent warps with the next-chunk prefetch (64 / 16 / 4 measured slower, profiles/r02v)
+#endif
+        const unsigned glist = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(task_bound, 4)), LIST_GRID * h->sm_count);
+        LAUNCH_S(h, ls, k_num_large_list<4>, glist, 128, 0, LA);
+        if (hsc->n_large3 > 0) LAUNCH_S(h, ls, k_num_large_list<1>, glist, 128, 0, LA);
       } else {
         LAUNCH_S(h, ls, (k_num_large_atomic<4, 2>), glarge, 128, 0, LA);
         if (hsc->n_large3 > 0) LAUNCH_S(h, ls, (k_num_large_atomic<1, 2>), glarge, 128, 0, LA);
