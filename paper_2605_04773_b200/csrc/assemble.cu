@@ -2406,7 +2406,10 @@ extern "C" agipc_status agipc_assemble_coarse(agipc_handle h, const agipc_mesh *
     WM.mkeys = mkeys;
     WM.e_off = e_off;
   }
-  const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, MID_WARPS), 12 * h->sm_count));
+#ifndef MID_GRID
+#define MID_GRID 12  // CTAs per SM of the mid-node kernels
+#endif
+  const unsigned gmid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_c, MID_WARPS), MID_GRID * h->sm_count));
   LargeArgs LA;
   LA.n_c = n_c; LA.child_list = child_list; LA.child_ptr = child_ptr; LA.size_new = size_new; LA.is_small = is_small;
   LA.rp = H->row_ptr; LA.col = H->col; LA.val = H->val; LA.nm = out->new_map; LA.X = mesh->x_rest;
