@@ -3,7 +3,7 @@
 # warm C3 coarsen, ncu launch list + --set full of the dominant kernels
 set -x
 python __graft_entry__.py build 2>&1 | tail -2
-O=gpurun_out/r02z3
+O=gpurun_out/r02z7
 mkdir -p $O
 timeout 1800 python -m pytest tests -m gpu -q --timeout 900 --timeout-method thread --durations=10 2>&1 | tail -22 > $O/pytest_gpu.txt
 tail -4 $O/pytest_gpu.txt
